@@ -1,0 +1,187 @@
+/*
+ * ppo5.h -- C ABI of libppo5.so: the data-parallel PPO optimizer step of OpenAI Five
+ * (arXiv 1912.06680), B200-native (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n [section]; Qn / On = DESIGN.md readings / oracle
+ * equations.  The step (§3.2):
+ *     ppo_gae -> lstm_bptt_fwd -> ppo_loss_grad -> lstm_bptt_bwd -> grad_allreduce -> adam_step
+ *
+ * Conventions (all calls):
+ *   - Pointers are DEVICE pointers unless marked (host).  The caller (PyTorch) owns every
+ *     buffer; the library never allocates in a hot call.  Buffers must be 16-byte aligned
+ *     (PPO_E_ALIGN otherwise); workspaces 1024-byte aligned.
+ *   - Calls are asynchronous on the given stream (NULL = legacy default stream).  Host-
+ *     checkable errors return immediately with a message in ppo_last_error()
+ *     (thread-local).  Data errors found on the device (non-finite loss, unavailable taken
+ *     action, empty availability row) set bits in stats[PPO_STAT_FLAGS]; the caller checks
+ *     them after synchronising and aborts the step.
+ *   - Results are deterministic for fixed inputs and world size (no float atomics).
+ *   - bf16 values are passed as uint16_t bit patterns.
+ */
+#ifndef PPO5_H
+#define PPO5_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ppo_stream_t; /* == cudaStream_t */
+
+enum {
+  PPO_OK = 0,
+  PPO_E_ARG = -1,         /* bad pointer / value */
+  PPO_E_SHAPE = -2,       /* unsupported or inconsistent sizes */
+  PPO_E_ALIGN = -3,       /* misaligned pointer */
+  PPO_E_CUDA = -4,        /* CUDA runtime/driver error (message has the CUDA string) */
+  PPO_E_NCCL = -5,        /* NCCL error */
+  PPO_E_UNSUPPORTED = -6  /* e.g. no sm_100 device for the tcgen05 path */
+};
+
+enum { PPO_PREC_BF16 = 0, PPO_PREC_FP32 = 1 };
+
+#define PPO_MAX_HEADS 8
+
+/* Network shape.  D = LSTM input width (DESIGN Q1: 4032), H = hidden units (4096),
+ * T = TBPTT length (16), heads = factorised action heads (P:303-368:
+ * 30,4,189,189,81,81,81).  A = sum(head_sizes) + 1 (value).
+ * D and H must be multiples of 64; T >= 1; 1 <= n_heads <= 8; head_sizes[0] <= 64
+ * (the primary head carries the availability mask).
+ * precision: PPO_PREC_BF16 = tcgen05 tensor cores, bf16 operands, fp32 accumulate;
+ *            PPO_PREC_FP32 = SIMT fp32 reference path (parity 1e-4). */
+typedef struct {
+  int32_t D, H, T;
+  int32_t n_heads;
+  int32_t head_sizes[PPO_MAX_HEADS];
+  int32_t precision;
+} ppo_dims;
+
+/* Flat parameter vector theta (fp32 master; grads, Adam m and v share the layout).
+ *   W_xh_aug [4H][Kx], Kx = D + H + 64: row r holds gate (r%256)/64 of hidden unit
+ *            64*(r/256) + r%64 (gate-interleaved, gates i,f,g,o);
+ *            cols [0,D) = W_x, [D,D+H) = W_h, col D+H = LSTM bias b, rest 0.
+ *   W_o_aug  [A][Ko],  Ko = H + 64: cols [0,H) = W_o, col H = b_o, rest 0.
+ * The zero pad columns receive exactly zero gradient and stay zero under Adam. */
+typedef struct {
+  int64_t Kx, Ko, A;
+  int64_t off_wxh, n_wxh;
+  int64_t off_wo, n_wo;
+  int64_t n_total;
+} ppo_param_layout;
+
+typedef struct {
+  float clip_eps; /* PPO clip epsilon, 0.2 */
+  float c_v;      /* value loss weight, 1.0 */
+  float c_e;      /* entropy coefficient, 0.01 */
+  float denom;    /* loss denominator; <= 0 means T*B (DESIGN Q9) */
+} ppo_loss_cfg;
+
+/* stats[] layout written by ppo_loss_grad (all Σ_rows w·x / denom unless noted) */
+enum {
+  PPO_STAT_LOSS = 0, PPO_STAT_PG = 1, PPO_STAT_VF = 2, PPO_STAT_ENT = 3,
+  PPO_STAT_KL = 4,        /* approx KL: mean(logp_old - logp) */
+  PPO_STAT_CLIPFRAC = 5,  /* rows on the clipped (zero-gradient) side */
+  PPO_STAT_NVALID = 6,    /* Σ w */
+  PPO_STAT_FLAGS = 7,     /* bit0 non-finite, bit1 taken primary unavailable, bit2 empty avail */
+  PPO_STATS = 8
+};
+#define PPO_LOSS_BLOCKS 1184                       /* 148 SMs x 8 */
+#define PPO_STATS_BUF (PPO_STATS * (1 + PPO_LOSS_BLOCKS)) /* floats; [0,8) = result */
+
+/* ---- library / errors ---------------------------------------------------------------- */
+const char* ppo_last_error(void);                  /* thread-local message of the last error */
+const char* ppo_version(void);
+
+/* Host-only: parameter layout for dims (no device access). */
+int ppo_get_param_layout(const ppo_dims* dims, ppo_param_layout* out /* host */);
+
+/* Canonical fp32 params (gate blocks [i;f;g;o], PyTorch order, Q14) -> flat theta.
+ * Wx [4H][D], Wh [4H][H], b [4H], Wo [A][H], bo [A]; theta [n_total] (fully written). */
+int ppo_pack_params(const ppo_dims* dims, const float* Wx, const float* Wh, const float* b,
+                    const float* Wo, const float* bo, float* theta, ppo_stream_t s);
+/* Inverse of ppo_pack_params (also used to read gradients in canonical layout). */
+int ppo_unpack_params(const ppo_dims* dims, const float* theta, float* Wx, float* Wh, float* b,
+                      float* Wo, float* bo, ppo_stream_t s);
+/* fp32 -> bf16 (round to nearest even) copy of n elements: the tensor-core shadow of theta. */
+int ppo_cast_bf16(const float* src, uint16_t* dst, size_t n, ppo_stream_t s);
+
+/* ---- a1: GAE (oracle O2, reading Q10) --------------------------
+ * rew [R][L], val [R][L+1] (val[r][L] = bootstrap), done [R][L] (1 = episode ended after
+ * step t; zeroes bootstrap and carry).  gamma = 1 - T_step/H_horizon, lam 0.95.
+ *   delta_t = r_t + gamma (1-d_t) V_{t+1} - V_t ;  A_t = delta_t + gamma lam (1-d_t) A_{t+1}
+ *   R_t = A_t + V_t.
+ * seq_T = 0: adv/ret are [R][L].  seq_T = T > 0 (L % T == 0): adv/ret are written time-major
+ * for the minibatch, [T][R*L/T], sequence b = r*(L/T) + k covers steps kT..kT+T-1 (O3).
+ * fp32 arithmetic.  R*L = 0 is a no-op. */
+int ppo_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
+            float gamma, float lam, int32_t seq_T, float* adv, float* ret, ppo_stream_t s);
+
+/* ---- a2-a4: forward (P:1210 LSTM, P:1254 TBPTT-16, P:606/618 heads; O4, O5) ------------
+ * Workspace holding the saved activations for lstm_bptt_bwd; caller-owned. */
+int lstm_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes /* host */);
+/* w: weights in the flat theta layout -- the bf16 shadow (uint16) for PPO_PREC_BF16, the fp32
+ *    theta itself for PPO_PREC_FP32.
+ * x: [T][B][D] LSTM inputs (bf16 bits for BF16, fp32 for FP32); h0, c0: [B][H] fp32 stored
+ *    rollout states.  out: [T][B][A] fp32 head outputs (655 logits + value).
+ * Computes z_t = [x_t | h_{t-1} | 1] W_xh_aug^T with the cell (i,f,o sigmoid, g tanh,
+ * c_t = f c_{t-1} + i g, h_t = o tanh c_t) fused into the GEMM epilogue, then
+ * y = [h_t | 1] W_o_aug^T.  1 <= B; ws_bytes >= lstm_ws_bytes(). */
+int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const float* h0,
+                  const float* c0, int64_t B, void* ws, size_t ws_bytes, float* out,
+                  ppo_stream_t s);
+
+/* ---- a5: PPO loss and its gradient (O6, O7) --
+ * out [T·B][A] fp32 (row = t*B + b); act [T·B][n_heads] int32; head_on [T·B][n_heads] u8
+ * (heads read by the taken primary action, Table target types P:350-368); avail
+ * [T·B][head_sizes[0]] u8 (action filter); logp_old, adv, ret [T·B] fp32;
+ * valid [T·B] u8 or NULL (= all rows valid).
+ * dout [T·B][A]: dL/dout, in the path's activation type (bf16 bits / fp32), consumed by
+ * lstm_bptt_bwd.  logp [T·B] fp32 or NULL: current log pi(a).  stats [PPO_STATS_BUF]. */
+int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,
+                  const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
+                  const float* adv, const float* ret, const uint8_t* valid, int64_t B,
+                  const ppo_loss_cfg* cfg, void* dout, float* logp, float* stats,
+                  ppo_stream_t s);
+
+/* ---- a6-a8: backward (TBPTT, no gradient into h0/c0; O8) ------------------------
+ * ws: the workspace filled by lstm_bptt_fwd for the same (w, B) (it is modified: saved gates
+ * are overwritten by dz).  dout: from ppo_loss_grad.  grad: [n_total] fp32, OVERWRITTEN with
+ * dL/dtheta in the theta layout (bias gradients fall out of the augmented columns). */
+int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
+                  const void* dout, int64_t B, float* grad, ppo_stream_t s);
+
+/* ---- a9: data-parallel gradient average (P:1251 NCCL allreduce; O9) --------------------- */
+typedef struct ppo_comm ppo_comm;
+#define PPO_COMM_ID_BYTES 128
+int ppo_comm_unique_id(uint8_t id[PPO_COMM_ID_BYTES] /* host */);
+/* Collective over `world` ranks; call once per rank with the same id (broadcast by the
+ * caller, e.g. over a torch process group).  Uses the current CUDA device. */
+int ppo_comm_init(const uint8_t id[PPO_COMM_ID_BYTES] /* host */, int rank, int world,
+                  ppo_comm** comm /* host out */);
+/* In-place average g <- (1/world) sum_ranks g over n fp32 elements, split into n_buckets
+ * equal buckets issued in order (n_buckets <= 0 -> 1).  world == 1 is a no-op. */
+int grad_allreduce(ppo_comm* comm, float* g, size_t n, int32_t n_buckets, ppo_stream_t s);
+int ppo_comm_destroy(ppo_comm* comm);
+
+/* ---- a10: Adam with the +-clip_sigma sqrt(v) clip (O10, Q3, Q4) --
+ *   v <- b2 v + (1-b2) g^2;  g_c = clamp(g, +-clip_sigma sqrt(v));  m <- b1 m + (1-b1) g_c
+ *   p <- p - lr sqrt(1-b2^t)/(1-b1^t) * m / (sqrt(v) + eps)
+ * t >= 1 (step number); clip_sigma <= 0 or inf disables the clip.  p_bf16 (nullable) receives
+ * the bf16 shadow of the updated p.  All arrays n fp32 elements (p_bf16: n uint16). */
+int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, size_t n,
+              int64_t t, float lr, float b1, float b2, float eps, float clip_sigma,
+              ppo_stream_t s);
+
+/* ---- testing hook (not part of the step) -------------------------------------------------
+ * One standalone tcgen05 GEMM C[M][N] (fp32) = sum_k A(m,k) B(n,k) on bf16 operands, used by
+ * the kernel unit tests.  mode bit0: B stored MN-major [K][N] (else K-major [N][K]);
+ * bit1: A stored MN-major [K][M] (else [M][K]); bit2: N-tile 224 instead of 256. */
+int ppo_test_tc_gemm(int mode, const uint16_t* A, const uint16_t* B, float* C, int M, int N,
+                     int K, ppo_stream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPO5_H */

@@ -1,0 +1,204 @@
+"""Thin ctypes binding of libppo5.so (include/ppo5.h).  Argument marshalling only: every step
+of the PPO path runs in the library's CUDA kernels.  Names follow the C ABI.
+
+Raises ImportError at import time if the in-tree library has not been built -- there is no
+fallback of any kind.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_size_t, c_uint8, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libppo5.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_1912_06680_b200.build` "
+                      "(or __graft_entry__.build()).  There is no CPU fallback.")
+
+import torch  # noqa: E402,F401  -- load torch (and its NCCL) before libppo5 links against it
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+PPO_OK, PPO_E_ARG, PPO_E_SHAPE, PPO_E_ALIGN, PPO_E_CUDA, PPO_E_NCCL, PPO_E_UNSUPPORTED = (
+    0, -1, -2, -3, -4, -5, -6)
+PPO_PREC_BF16, PPO_PREC_FP32 = 0, 1
+PPO_MAX_HEADS = 8
+PPO_STATS = 8
+PPO_LOSS_BLOCKS = 1184
+PPO_STATS_BUF = PPO_STATS * (1 + PPO_LOSS_BLOCKS)
+PPO_COMM_ID_BYTES = 128
+STAT_NAMES = ("loss", "pg", "vf", "ent", "approx_kl", "clipfrac", "n_valid", "flags")
+
+
+class ppo_dims(ctypes.Structure):
+    _fields_ = [("D", c_int32), ("H", c_int32), ("T", c_int32), ("n_heads", c_int32),
+                ("head_sizes", c_int32 * PPO_MAX_HEADS), ("precision", c_int32)]
+
+
+class ppo_param_layout(ctypes.Structure):
+    _fields_ = [("Kx", c_int64), ("Ko", c_int64), ("A", c_int64), ("off_wxh", c_int64),
+                ("n_wxh", c_int64), ("off_wo", c_int64), ("n_wo", c_int64), ("n_total", c_int64)]
+
+
+class ppo_loss_cfg(ctypes.Structure):
+    _fields_ = [("clip_eps", c_float), ("c_v", c_float), ("c_e", c_float), ("denom", c_float)]
+
+
+class PPOError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libppo5 error {code}: {msg}")
+        self.code = code
+
+
+def _sig(name, args, res=c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_D = POINTER(ppo_dims)
+_lib_fns = dict(
+    ppo_last_error=([], c_char_p),
+    ppo_version=([], c_char_p),
+    ppo_get_param_layout=([_D, POINTER(ppo_param_layout)], c_int),
+    ppo_pack_params=([_D] + [c_void_p] * 7, c_int),
+    ppo_unpack_params=([_D] + [c_void_p] * 7, c_int),
+    ppo_cast_bf16=([c_void_p, c_void_p, c_size_t, c_void_p], c_int),
+    ppo_gae=([c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_float, c_int32, c_void_p,
+              c_void_p, c_void_p], c_int),
+    lstm_ws_bytes=([_D, c_int64, POINTER(c_size_t)], c_int),
+    lstm_bptt_fwd=([_D, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_size_t,
+                    c_void_p, c_void_p], c_int),
+    ppo_loss_grad=([_D] + [c_void_p] * 9 + [c_int64, POINTER(ppo_loss_cfg), c_void_p, c_void_p,
+                                             c_void_p, c_void_p], c_int),
+    lstm_bptt_bwd=([_D, c_void_p, c_void_p, c_size_t, c_void_p, c_int64, c_void_p, c_void_p], c_int),
+    ppo_comm_unique_id=([POINTER(c_uint8)], c_int),
+    ppo_comm_init=([POINTER(c_uint8), c_int, c_int, POINTER(c_void_p)], c_int),
+    grad_allreduce=([c_void_p, c_void_p, c_size_t, c_int32, c_void_p], c_int),
+    ppo_comm_destroy=([c_void_p], c_int),
+    adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_float,
+                c_float, c_float, c_float, c_float, c_void_p], c_int),
+    ppo_test_tc_gemm=([c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p], c_int),
+)
+EXPORTED = tuple(_lib_fns)
+for _n, (_a, _r) in _lib_fns.items():
+    _sig(_n, _a, _r)
+
+
+def last_error() -> str:
+    return _lib.ppo_last_error().decode()
+
+
+def version() -> str:
+    return _lib.ppo_version().decode()
+
+
+def _check(rc):
+    if rc != PPO_OK:
+        raise PPOError(rc, last_error())
+
+
+# ------------------------------------------------------------------ marshalling helpers
+def _p(t):
+    """device/host pointer of a torch tensor (or None -> NULL)."""
+    return None if t is None else c_void_p(t.data_ptr())
+
+
+def _s(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return c_void_p(stream.cuda_stream)
+
+
+def make_dims(D, H, T, head_sizes, precision=PPO_PREC_BF16) -> ppo_dims:
+    d = ppo_dims()
+    d.D, d.H, d.T = D, H, T
+    d.n_heads = len(head_sizes)
+    for i, h in enumerate(head_sizes):
+        d.head_sizes[i] = h
+    d.precision = precision
+    return d
+
+
+def param_layout(dims: ppo_dims) -> ppo_param_layout:
+    out = ppo_param_layout()
+    _check(_lib.ppo_get_param_layout(ctypes.byref(dims), ctypes.byref(out)))
+    return out
+
+
+def ws_bytes(dims: ppo_dims, B: int) -> int:
+    n = c_size_t()
+    _check(_lib.lstm_ws_bytes(ctypes.byref(dims), B, ctypes.byref(n)))
+    return n.value
+
+
+# ------------------------------------------------------------------ the hot-path calls
+def ppo_pack_params(dims, Wx, Wh, b, Wo, bo, theta, stream=None):
+    _check(_lib.ppo_pack_params(ctypes.byref(dims), _p(Wx), _p(Wh), _p(b), _p(Wo), _p(bo),
+                                _p(theta), _s(stream)))
+
+
+def ppo_unpack_params(dims, theta, Wx, Wh, b, Wo, bo, stream=None):
+    _check(_lib.ppo_unpack_params(ctypes.byref(dims), _p(theta), _p(Wx), _p(Wh), _p(b), _p(Wo),
+                                  _p(bo), _s(stream)))
+
+
+def ppo_cast_bf16(src, dst, stream=None):
+    _check(_lib.ppo_cast_bf16(_p(src), _p(dst), src.numel(), _s(stream)))
+
+
+def ppo_gae(rew, val, done, gamma, lam, adv, ret, seq_T=0, stream=None):
+    R, L = rew.shape
+    _check(_lib.ppo_gae(_p(rew), _p(val), _p(done), R, L, gamma, lam, seq_T, _p(adv), _p(ret),
+                        _s(stream)))
+
+
+def lstm_bptt_fwd(dims, w, x, h0, c0, B, ws, out, stream=None):
+    _check(_lib.lstm_bptt_fwd(ctypes.byref(dims), _p(w), _p(x), _p(h0), _p(c0), B, _p(ws),
+                              ws.numel() * ws.element_size(), _p(out), _s(stream)))
+
+
+def ppo_loss_grad(dims, out, act, head_on, avail, logp_old, adv, ret, valid, B, cfg, dout, logp,
+                  stats, stream=None):
+    _check(_lib.ppo_loss_grad(ctypes.byref(dims), _p(out), _p(act), _p(head_on), _p(avail),
+                              _p(logp_old), _p(adv), _p(ret), _p(valid), B, ctypes.byref(cfg),
+                              _p(dout), _p(logp), _p(stats), _s(stream)))
+
+
+def lstm_bptt_bwd(dims, w, ws, dout, B, grad, stream=None):
+    _check(_lib.lstm_bptt_bwd(ctypes.byref(dims), _p(w), _p(ws), ws.numel() * ws.element_size(),
+                              _p(dout), B, _p(grad), _s(stream)))
+
+
+def adam_step(p, p_bf16, g, m, v, t, lr, b1, b2, eps, clip_sigma, stream=None):
+    _check(_lib.adam_step(_p(p), _p(p_bf16), _p(g), _p(m), _p(v), p.numel(), t, lr, b1, b2, eps,
+                          clip_sigma, _s(stream)))
+
+
+def comm_unique_id() -> bytes:
+    buf = (c_uint8 * PPO_COMM_ID_BYTES)()
+    _check(_lib.ppo_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def comm_init(uid: bytes, rank: int, world: int) -> c_void_p:
+    buf = (c_uint8 * PPO_COMM_ID_BYTES).from_buffer_copy(uid)
+    h = c_void_p()
+    _check(_lib.ppo_comm_init(buf, rank, world, ctypes.byref(h)))
+    return h
+
+
+def grad_allreduce(comm, g, n_buckets=1, stream=None):
+    _check(_lib.grad_allreduce(comm, _p(g), g.numel(), n_buckets, _s(stream)))
+
+
+def comm_destroy(comm):
+    _check(_lib.ppo_comm_destroy(comm))
+
+
+def test_tc_gemm(mode, A, B, C, M, N, K, stream=None):
+    _check(_lib.ppo_test_tc_gemm(mode, _p(A), _p(B), _p(C), M, N, K, _s(stream)))

@@ -1,0 +1,333 @@
+// api.cu -- the extern "C" boundary of libppo5.so (include/ppo5.h): argument checking,
+// workspace layout and the composition of each hot-path call from the kernels.
+#include <math.h>
+
+#include <algorithm>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace ppo {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return PPO_E_CUDA;
+}
+
+int num_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    return 148;
+  return n;
+}
+
+int check_dims(const ppo_dims* d, Shape* s) {
+  if (!d) return fail(PPO_E_ARG, "dims is NULL");
+  if (d->D <= 0 || d->H <= 0 || d->T <= 0 || d->D % 64 || d->H % 64)
+    return fail(PPO_E_SHAPE, "D and H must be positive multiples of 64, T >= 1");
+  if (d->n_heads < 1 || d->n_heads > PPO_MAX_HEADS)
+    return fail(PPO_E_SHAPE, "n_heads must be in [1, 8]");
+  if (d->precision != PPO_PREC_BF16 && d->precision != PPO_PREC_FP32)
+    return fail(PPO_E_ARG, "unknown precision");
+  s->D = d->D;
+  s->H = d->H;
+  s->T = d->T;
+  s->G4 = 4LL * d->H;
+  s->Kx = (int64_t)d->D + d->H + 64;
+  s->Ko = (int64_t)d->H + 64;
+  s->n_heads = d->n_heads;
+  s->head_off[0] = 0;
+  for (int k = 0; k < d->n_heads; ++k) {
+    if (d->head_sizes[k] <= 0) return fail(PPO_E_SHAPE, "head sizes must be positive");
+    s->head_off[k + 1] = s->head_off[k] + d->head_sizes[k];
+  }
+  if (d->head_sizes[0] > 64) return fail(PPO_E_SHAPE, "primary head must have <= 64 actions");
+  s->A = s->head_off[d->n_heads] + 1;
+  s->bf16 = d->precision == PPO_PREC_BF16;
+  if (s->bf16 && (s->A * 2) % 16)
+    return fail(PPO_E_SHAPE, "bf16 path needs A*2 to be a multiple of 16 bytes (TMA stride)");
+  return PPO_OK;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+WsLayout ws_layout(const Shape& s, int64_t B) {
+  const size_t esz = s.bf16 ? 2 : 4;
+  WsLayout L{};
+  size_t off = 0;
+  L.xh = off;
+  off = align_up(off + (size_t)(s.T + 1) * B * s.Kx * esz, 1024);
+  L.g = off;
+  off = align_up(off + (size_t)s.T * B * s.G4 * esz, 1024);
+  L.c = off;
+  off = align_up(off + (size_t)(s.T + 1) * B * s.H * 4, 1024);
+  L.dc = off;
+  off = align_up(off + (size_t)B * s.H * 4, 1024);
+  L.raw = off;
+  if (!s.bf16) off = align_up(off + (size_t)B * s.G4 * 4, 1024);
+  L.total = off;
+  return L;
+}
+
+static int param_layout(const Shape& s, ppo_param_layout* o) {
+  o->Kx = s.Kx;
+  o->Ko = s.Ko;
+  o->A = s.A;
+  o->off_wxh = 0;
+  o->n_wxh = s.G4 * s.Kx;
+  o->off_wo = o->n_wxh;
+  o->n_wo = s.A * s.Ko;
+  o->n_total = o->n_wxh + o->n_wo;
+  return PPO_OK;
+}
+
+static int need(const void* p, const char* name) {
+  if (!p) return fail(PPO_E_ARG, std::string(name) + " is NULL");
+  if (!aligned(p, 16)) return fail(PPO_E_ALIGN, std::string(name) + " is not 16-byte aligned");
+  return PPO_OK;
+}
+#define NEED(p)                          \
+  do {                                   \
+    int _r = need((p), #p);              \
+    if (_r) return _r;                   \
+  } while (0)
+
+static int check_tc_device() {
+  int dev = 0, major = 0;
+  PPO_CUDA_CHECK(cudaGetDevice(&dev));
+  PPO_CUDA_CHECK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) return fail(PPO_E_UNSUPPORTED, "bf16 tcgen05 path needs an sm_100 device");
+  return PPO_OK;
+}
+
+}  // namespace ppo
+
+using namespace ppo;
+
+extern "C" {
+
+const char* ppo_last_error(void) { return g_err.c_str(); }
+const char* ppo_version(void) { return "libppo5 0.1 (sm_100a; tcgen05 bf16 + SIMT fp32 paths)"; }
+
+int ppo_get_param_layout(const ppo_dims* dims, ppo_param_layout* out) {
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (!out) return fail(PPO_E_ARG, "out is NULL");
+  return param_layout(s, out);
+}
+
+int ppo_pack_params(const ppo_dims* dims, const float* Wx, const float* Wh, const float* b,
+                    const float* Wo, const float* bo, float* theta, ppo_stream_t st) {
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (!Wx || !Wh || !b || !Wo || !bo || !theta) return fail(PPO_E_ARG, "NULL pointer");
+  ppo_param_layout L;
+  param_layout(s, &L);
+  return launch_pack_params(s, Wx, Wh, b, Wo, bo, theta, L.n_wxh, L.n_total, (cudaStream_t)st);
+}
+
+int ppo_unpack_params(const ppo_dims* dims, const float* theta, float* Wx, float* Wh, float* b,
+                      float* Wo, float* bo, ppo_stream_t st) {
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (!Wx || !Wh || !b || !Wo || !bo || !theta) return fail(PPO_E_ARG, "NULL pointer");
+  ppo_param_layout L;
+  param_layout(s, &L);
+  return launch_unpack_params(s, theta, Wx, Wh, b, Wo, bo, L.n_wxh, (cudaStream_t)st);
+}
+
+int ppo_cast_bf16(const float* src, uint16_t* dst, size_t n, ppo_stream_t st) {
+  if (n == 0) return PPO_OK;
+  if (!src || !dst) return fail(PPO_E_ARG, "NULL pointer");
+  return launch_cast_bf16(src, dst, n, (cudaStream_t)st);
+}
+
+int ppo_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
+            float gamma, float lam, int32_t seq_T, float* adv, float* ret, ppo_stream_t st) {
+  if (R < 0 || L < 0) return fail(PPO_E_SHAPE, "R and L must be >= 0");
+  if (R == 0 || L == 0) return PPO_OK;
+  if (!rew || !val || !done || !adv || !ret) return fail(PPO_E_ARG, "NULL pointer");
+  if (seq_T < 0 || (seq_T > 0 && L % seq_T)) return fail(PPO_E_SHAPE, "L must be a multiple of seq_T");
+  if (!(gamma >= 0.f && gamma <= 1.f && lam >= 0.f && lam <= 1.f))
+    return fail(PPO_E_ARG, "gamma and lam must be in [0, 1]");
+  return launch_gae(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, (cudaStream_t)st);
+}
+
+int lstm_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes) {
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
+  if (!bytes) return fail(PPO_E_ARG, "bytes is NULL");
+  *bytes = ws_layout(s, B).total;
+  return PPO_OK;
+}
+
+int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const float* h0,
+                  const float* c0, int64_t B, void* ws, size_t ws_bytes, float* out,
+                  ppo_stream_t st_) {
+  cudaStream_t st = (cudaStream_t)st_;
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
+  if (s.bf16 && B * s.T > (int64_t)INT32_MAX / 2) return fail(PPO_E_SHAPE, "T*B too large");
+  NEED(w);
+  NEED(x);
+  NEED(h0);
+  NEED(c0);
+  NEED(out);
+  if (!ws || !aligned(ws, 1024)) return fail(PPO_E_ALIGN, "ws must be 1024-byte aligned");
+  WsLayout L = ws_layout(s, B);
+  if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small");
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  float* C = reinterpret_cast<float*>(wsb + L.c);
+  if ((rc = launch_pack_x(s, B, x, h0, c0, wsb + L.xh, C, st))) return rc;
+  if (s.bf16) {
+    if ((rc = check_tc_device())) return rc;
+    return tc_forward(s, B, w, ws, out, st);
+  }
+  // ---- SIMT fp32 reference path
+  const float* W = static_cast<const float*>(w);
+  const float* Wo = W + s.G4 * s.Kx;
+  float* XH = reinterpret_cast<float*>(wsb + L.xh);
+  float* G = reinterpret_cast<float*>(wsb + L.g);
+  float* raw = reinterpret_cast<float*>(wsb + L.raw);
+  for (int64_t t = 0; t < s.T; ++t) {
+    SimtOp a{{XH + t * B * s.Kx, nullptr}, {s.Kx, 0}, {B, 0}, {s.Kx, 0}, s.Kx, false};
+    SimtOp b{{W, nullptr}, {s.Kx, 0}, {s.G4, 0}, {s.Kx, 0}, s.Kx, false};
+    if ((rc = launch_simt_gemm(a, b, B, s.G4, s.Kx, raw, s.G4, st))) return rc;
+    if ((rc = launch_simt_cell_fwd(s, B, raw, C + t * B * s.H, C + (t + 1) * B * s.H,
+                                   XH + (t + 1) * B * s.Kx + s.D, s.Kx, G + t * B * s.G4, st)))
+      return rc;
+  }
+  SimtOp a{{XH + B * s.Kx + s.D, nullptr}, {s.Kx, 0}, {s.T * B, 0}, {s.Ko, 0}, s.Ko, false};
+  SimtOp b{{Wo, nullptr}, {s.Ko, 0}, {s.A, 0}, {s.Ko, 0}, s.Ko, false};
+  return launch_simt_gemm(a, b, s.T * B, s.A, s.Ko, out, s.A, st);
+}
+
+int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,
+                  const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
+                  const float* adv, const float* ret, const uint8_t* valid, int64_t B,
+                  const ppo_loss_cfg* cfg, void* dout, float* logp, float* stats,
+                  ppo_stream_t st) {
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
+  if (!out || !act || !head_on || !avail || !logp_old || !adv || !ret || !cfg || !dout || !stats)
+    return fail(PPO_E_ARG, "NULL pointer");
+  LossParams p{};
+  p.N = s.T * B;
+  p.A = (int)s.A;
+  p.A_pad = (int)((s.A + 31) / 32 * 32);
+  p.nh = s.n_heads;
+  for (int k = 0; k <= s.n_heads; ++k) p.off[k] = s.head_off[k];
+  p.clip_eps = cfg->clip_eps;
+  p.c_v = cfg->c_v;
+  p.c_e = cfg->c_e;
+  const double denom = cfg->denom > 0 ? cfg->denom : (double)p.N;
+  p.inv_denom = (float)(1.0 / denom);
+  if ((size_t)p.A_pad * 8 * sizeof(float) > 48 * 1024) return fail(PPO_E_SHAPE, "A too large");
+  return launch_loss(p, s.bf16, out, act, head_on, avail, logp_old, adv, ret, valid, dout, logp,
+                     stats, (cudaStream_t)st);
+}
+
+int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
+                  const void* dout, int64_t B, float* grad, ppo_stream_t st_) {
+  cudaStream_t st = (cudaStream_t)st_;
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
+  NEED(w);
+  NEED(dout);
+  NEED(grad);
+  if (!ws || !aligned(ws, 1024)) return fail(PPO_E_ALIGN, "ws must be 1024-byte aligned");
+  WsLayout L = ws_layout(s, B);
+  if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small");
+  if (s.bf16) {
+    if ((rc = check_tc_device())) return rc;
+    return tc_backward(s, B, w, ws, dout, grad, st);
+  }
+  // ---- SIMT fp32 reference path
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  const float* W = static_cast<const float*>(w);
+  const float* Wo = W + s.G4 * s.Kx;
+  const float* dY = static_cast<const float*>(dout);
+  float* XH = reinterpret_cast<float*>(wsb + L.xh);
+  float* G = reinterpret_cast<float*>(wsb + L.g);
+  float* C = reinterpret_cast<float*>(wsb + L.c);
+  float* dc = reinterpret_cast<float*>(wsb + L.dc);
+  float* raw = reinterpret_cast<float*>(wsb + L.raw);
+  PPO_CUDA_CHECK(cudaMemsetAsync(dc, 0, B * s.H * sizeof(float), st));
+  for (int64_t t = s.T - 1; t >= 0; --t) {
+    const bool last = t == s.T - 1;
+    const float* dYt = dY + t * B * s.A;
+    SimtOp a, b;
+    int64_t K;
+    if (last) {  // dh_{T-1} = dy_{T-1} W_o only
+      a = SimtOp{{dYt, nullptr}, {s.A, 0}, {B, 0}, {s.A, 0}, s.A, false};
+      b = SimtOp{{Wo, nullptr}, {s.Ko, 0}, {s.H, 0}, {s.A, 0}, s.A, true};
+      K = s.A;
+    } else {     // dh_t = dz_{t+1} W_h + dy_t W_o
+      a = SimtOp{{G + (t + 1) * B * s.G4, dYt}, {s.G4, s.A}, {B, B}, {s.G4, s.A}, s.G4, false};
+      b = SimtOp{{W + s.D, Wo}, {s.Kx, s.Ko}, {s.H, s.H}, {s.G4, s.A}, s.G4, true};
+      K = s.G4 + s.A;
+    }
+    if ((rc = launch_simt_gemm(a, b, B, s.H, K, raw, s.H, st))) return rc;
+    if ((rc = launch_simt_cell_bwd(s, B, raw, G + t * B * s.G4, C + (t + 1) * B * s.H,
+                                   C + t * B * s.H, dc, st)))
+      return rc;
+  }
+  const int64_t rows = s.T * B;
+  {
+    SimtOp a{{G, nullptr}, {s.G4, 0}, {s.G4, 0}, {rows, 0}, rows, true};
+    SimtOp b{{XH, nullptr}, {s.Kx, 0}, {s.Kx, 0}, {rows, 0}, rows, true};
+    if ((rc = launch_simt_gemm(a, b, s.G4, s.Kx, rows, grad, s.Kx, st))) return rc;
+  }
+  {
+    SimtOp a{{dY, nullptr}, {s.A, 0}, {s.A, 0}, {rows, 0}, rows, true};
+    SimtOp b{{XH + B * s.Kx + s.D, nullptr}, {s.Kx, 0}, {s.Ko, 0}, {rows, 0}, rows, true};
+    if ((rc = launch_simt_gemm(a, b, s.A, s.Ko, rows, grad + s.G4 * s.Kx, s.Ko, st))) return rc;
+  }
+  return PPO_OK;
+}
+
+int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, size_t n,
+              int64_t t, float lr, float b1, float b2, float eps, float clip_sigma,
+              ppo_stream_t st) {
+  if (n == 0) return PPO_OK;
+  NEED(p);
+  NEED(g);
+  NEED(m);
+  NEED(v);
+  if (p_bf16 && !aligned(p_bf16, 16)) return fail(PPO_E_ALIGN, "p_bf16 is not 16-byte aligned");
+  if (t < 1) return fail(PPO_E_ARG, "t must be >= 1");
+  if (!(b1 >= 0.f && b1 < 1.f && b2 >= 0.f && b2 < 1.f)) return fail(PPO_E_ARG, "bad betas");
+  const double alpha =
+      (double)lr * sqrt(1.0 - pow((double)b2, (double)t)) / (1.0 - pow((double)b1, (double)t));
+  const float clip = (clip_sigma > 0.f && isfinite(clip_sigma)) ? clip_sigma : 0.f;
+  return launch_adam(p, p_bf16, g, m, v, n, (float)alpha, b1, b2, eps, clip, (cudaStream_t)st);
+}
+
+// ---- testing hook (not part of the step): one tcgen05 GEMM, see tc_path.cu -------------
+int ppo_test_tc_gemm(int mode, const uint16_t* A, const uint16_t* B, float* C, int M, int N, int K,
+                     ppo_stream_t st) {
+  if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0) return fail(PPO_E_ARG, "bad test GEMM args");
+  int rc = check_tc_device();
+  if (rc) return rc;
+  return tc_test_gemm(mode, A, B, C, M, N, K, (cudaStream_t)st);
+}
+
+}  // extern "C"

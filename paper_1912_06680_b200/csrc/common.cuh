@@ -1,0 +1,92 @@
+// common.cuh -- internal helpers shared by the libppo5 translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/ppo5.h"
+
+namespace ppo {
+
+// ---- error plumbing (ppo_last_error is thread-local) -----------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define PPO_CUDA_CHECK(expr)                                   \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return ::ppo::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define PPO_LAUNCH_CHECK(what)                                  \
+  do {                                                          \
+    cudaError_t _e = cudaGetLastError();                        \
+    if (_e != cudaSuccess) return ::ppo::cuda_fail(_e, what);   \
+  } while (0)
+
+inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int num_sms();
+
+// ---- derived shapes ----------------------------------------------------------------------
+struct Shape {
+  int64_t D, H, T, A, G4, Kx, Ko;  // G4 = 4H gate rows
+  int n_heads;
+  int head_off[PPO_MAX_HEADS + 1];
+  bool bf16;
+};
+int check_dims(const ppo_dims* d, Shape* s);
+
+// Workspace regions (byte offsets from ws base); esz = activation element size.
+struct WsLayout {
+  size_t xh, g, c, dc, raw, total;
+};
+WsLayout ws_layout(const Shape& s, int64_t B);
+
+// ---- activation storage type ---------------------------------------------------------------
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <class T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// ---- the LSTM cell (Gers et al. forget-gate LSTM; oracle O4 / O8) -------------------
+__device__ __forceinline__ float sigmoidf_acc(float z) { return 1.0f / (1.0f + expf(-z)); }
+
+// Forward: pre-activations -> gates (i,f,g,o), new cell and hidden state.
+__device__ __forceinline__ void cell_fwd(float zi, float zf, float zg, float zo, float c_prev,
+                                         float& i, float& f, float& g, float& o, float& c,
+                                         float& h) {
+  i = sigmoidf_acc(zi);
+  f = sigmoidf_acc(zf);
+  g = tanhf(zg);
+  o = sigmoidf_acc(zo);
+  c = f * c_prev + i * g;
+  h = o * tanhf(c);
+}
+
+// Backward through one cell: dh (total), carried dc, saved gates, c_t, c_{t-1}
+// -> pre-activation grads dz (i,f,g,o) and the carry dc_next = dc * f.
+__device__ __forceinline__ void cell_bwd(float dh, float dc_carry, float i, float f, float g,
+                                         float o, float c, float c_prev, float& dzi, float& dzf,
+                                         float& dzg, float& dzo, float& dc_next) {
+  float tc = tanhf(c);
+  float dc = dc_carry + dh * o * (1.0f - tc * tc);
+  float d_o = dh * tc;
+  float di = dc * g;
+  float dg = dc * i;
+  float df = dc * c_prev;
+  dc_next = dc * f;
+  dzi = di * i * (1.0f - i);
+  dzf = df * f * (1.0f - f);
+  dzg = dg * (1.0f - g * g);
+  dzo = d_o * o * (1.0f - o);
+}
+
+}  // namespace ppo

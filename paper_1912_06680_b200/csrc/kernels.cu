@@ -1,0 +1,560 @@
+// kernels.cu -- HBM-bound kernels of the PPO step (GAE, loss, Adam, layout) and the SIMT
+// fp32 reference GEMM path.  See DESIGN.md for the roofline of each.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ppo {
+
+// ============================================================================ layout
+// theta layout (ppo5.h): W_xh_aug [4H][Kx] gate-interleaved, W_o_aug [A][Ko].
+__device__ __forceinline__ int64_t canon_gate_row(int64_t r, int64_t H) {
+  const int64_t q = r >> 8, gate = (r & 255) >> 6, u = r & 63;
+  return gate * H + q * 64 + u;
+}
+
+__global__ void pack_params_kernel(Shape s, const float* __restrict__ Wx, const float* __restrict__ Wh,
+                                   const float* __restrict__ b, const float* __restrict__ Wo,
+                                   const float* __restrict__ bo, float* __restrict__ theta,
+                                   int64_t n_wxh, int64_t n_total) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n_total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    if (idx < n_wxh) {
+      const int64_t r = idx / s.Kx, c = idx - r * s.Kx;
+      const int64_t cr = canon_gate_row(r, s.H);
+      if (c < s.D) v = Wx[cr * s.D + c];
+      else if (c < s.D + s.H) v = Wh[cr * s.H + (c - s.D)];
+      else if (c == s.D + s.H) v = b[cr];
+    } else {
+      const int64_t i = idx - n_wxh, a = i / s.Ko, c = i - a * s.Ko;
+      if (c < s.H) v = Wo[a * s.H + c];
+      else if (c == s.H) v = bo[a];
+    }
+    theta[idx] = v;
+  }
+}
+
+__global__ void unpack_params_kernel(Shape s, const float* __restrict__ theta, float* __restrict__ Wx,
+                                     float* __restrict__ Wh, float* __restrict__ b,
+                                     float* __restrict__ Wo, float* __restrict__ bo, int64_t n_wxh) {
+  // iterate over theta rows (gate rows of W_xh_aug, then rows of W_o_aug)
+  const int64_t nrows = s.G4 + s.A;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+       idx < nrows * s.Kx; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / s.Kx, c = idx - r * s.Kx;
+    if (r < s.G4) {
+      const int64_t cr = canon_gate_row(r, s.H);
+      const float v = theta[r * s.Kx + c];
+      if (c < s.D) Wx[cr * s.D + c] = v;
+      else if (c < s.D + s.H) Wh[cr * s.H + (c - s.D)] = v;
+      else if (c == s.D + s.H) b[cr] = v;
+    } else {
+      const int64_t a = r - s.G4;
+      if (c >= s.Ko) continue;
+      const float v = theta[n_wxh + a * s.Ko + c];
+      if (c < s.H) Wo[a * s.H + c] = v;
+      else if (c == s.H) bo[a] = v;
+    }
+  }
+}
+
+__global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                 size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+// XH[t][b] = [x_t | h_{t-1} | 1 | 0...] for t = 0..T (x_T := 0), h_{-1} = h0; C[0] = c0.
+template <class TA>
+__global__ void pack_x_kernel(Shape s, int64_t B, const TA* __restrict__ x,
+                              const float* __restrict__ h0, const float* __restrict__ c0,
+                              TA* __restrict__ xh, float* __restrict__ c) {
+  const int64_t total = (s.T + 1) * B * s.Kx;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / s.Kx, col = idx - row * s.Kx;
+    const int64_t t = row / B, b = row - t * B;
+    if (col < s.D) {
+      xh[idx] = t < s.T ? x[(t * B + b) * s.D + col] : from_f<TA>(0.f);
+    } else if (col < s.D + s.H) {
+      if (t == 0) {
+        xh[idx] = from_f<TA>(h0[b * s.H + (col - s.D)]);
+        c[b * s.H + (col - s.D)] = c0[b * s.H + (col - s.D)];
+      }
+    } else {
+      xh[idx] = from_f<TA>(col == s.D + s.H ? 1.f : 0.f);
+    }
+  }
+}
+
+// ============================================================================ GAE
+// One warp per rollout stream; 256-step windows from the end; each lane owns 8 steps and
+// the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
+// across lanes with a reverse shuffle scan of affine maps (oracle O2).
+__global__ void gae_kernel(const float* __restrict__ rew, const float* __restrict__ val,
+                           const uint8_t* __restrict__ done, int64_t R, int64_t L, float gamma,
+                           float lam, int seq_T, float* __restrict__ adv, float* __restrict__ ret) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float gl = gamma * lam;
+  const int64_t spr = seq_T > 0 ? L / seq_T : 0;  // sequences per rollout
+  const int64_t nseq = R * spr;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
+    const float* rr = rew + r * L;
+    const float* vv = val + r * (L + 1);
+    const uint8_t* dd = done + r * L;
+    float carry = 0.f;
+    for (int64_t w_end = L; w_end > 0; w_end -= 256) {
+      const int64_t w_start = w_end > 256 ? w_end - 256 : 0;
+      const int64_t t0 = w_start + 8 * lane;
+      const int n = (int)max((int64_t)0, min((int64_t)8, w_end - t0));
+      float delta[8], cf[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < n) {
+          const int64_t t = t0 + i;
+          const float nd = dd[t] ? 0.f : 1.f;
+          delta[i] = rr[t] + gamma * nd * vv[t + 1] - vv[t];
+          cf[i] = gl * nd;
+        } else {
+          delta[i] = 0.f;
+          cf[i] = 1.f;
+        }
+      }
+      float P = 0.f, Q = 1.f;  // A_first = P + Q * A_after
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        P = delta[i] + cf[i] * P;
+        Q = cf[i] * Q;
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float P2 = __shfl_down_sync(0xffffffffu, P, off);
+        const float Q2 = __shfl_down_sync(0xffffffffu, Q, off);
+        if (lane + off < 32) {
+          P = P + Q * P2;
+          Q = Q * Q2;
+        }
+      }
+      const float a_first = P + Q * carry;
+      float a = __shfl_down_sync(0xffffffffu, a_first, 1);
+      if (lane == 31) a = carry;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        if (i < n) {
+          const int64_t t = t0 + i;
+          a = delta[i] + cf[i] * a;
+          int64_t o;
+          if (seq_T > 0) {
+            const int64_t k = t / seq_T, tt = t - k * seq_T;
+            o = tt * nseq + r * spr + k;
+          } else {
+            o = r * L + t;
+          }
+          adv[o] = a;
+          ret[o] = a + vv[t];
+        }
+      }
+      carry = __shfl_sync(0xffffffffu, a_first, 0);
+    }
+  }
+}
+
+// ============================================================================ PPO loss
+// One warp per row (row = t*B + b); the row is staged in shared memory; per head a masked
+// log-sum-exp, the entropy, then the analytic gradient (oracle O6/O7).  Statistics go to
+// fixed per-block partial slots and a second kernel reduces them in a fixed order.
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <class TD>
+__global__ void __launch_bounds__(256) loss_kernel(
+    const float* __restrict__ out, const int32_t* __restrict__ act,
+    const uint8_t* __restrict__ head_on, const uint8_t* __restrict__ avail,
+    const float* __restrict__ logp_old, const float* __restrict__ adv,
+    const float* __restrict__ ret, const uint8_t* __restrict__ valid, LossParams p,
+    TD* __restrict__ dout, float* __restrict__ logp, float* __restrict__ partials) {
+  extern __shared__ float smem_y[];
+  __shared__ float red[8][PPO_STATS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* y = smem_y + warp * p.A_pad;
+  const int A = p.A, nh = p.nh, n0 = p.off[1];
+  float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  uint32_t flags = 0;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.N; row += (int64_t)gridDim.x * 8) {
+    const float* yr = out + row * A;
+    for (int j = lane; j < A; j += 32) y[j] = yr[j];
+    const uint8_t* av = avail + row * n0;
+    const uint32_t m_lo = __ballot_sync(0xffffffffu, lane < n0 && av[lane] != 0);
+    const uint32_t m_hi = __ballot_sync(0xffffffffu, lane + 32 < n0 && av[min(lane + 32, n0 - 1)] != 0);
+    const uint64_t amask = (uint64_t)m_lo | ((uint64_t)m_hi << 32);
+    __syncwarp();
+    const float w = valid ? (float)valid[row] : 1.f;
+    float lse[PPO_MAX_HEADS], Hk[PPO_MAX_HEADS];
+    float lpi = 0.f, ent = 0.f;
+    for (int k = 0; k < nh; ++k) {
+      const int s0 = p.off[k], e0 = p.off[k + 1];
+      float mx = -INFINITY;
+      for (int j = s0 + lane; j < e0; j += 32)
+        if (k != 0 || ((amask >> (j - s0)) & 1ull)) mx = fmaxf(mx, y[j]);
+      mx = warp_max(mx);
+      float se = 0.f;
+      if (mx != -INFINITY)
+        for (int j = s0 + lane; j < e0; j += 32)
+          if (k != 0 || ((amask >> (j - s0)) & 1ull)) se += expf(y[j] - mx);
+      se = warp_sum(se);
+      const float l = mx == -INFINITY ? 0.f : mx + logf(se);
+      float pl = 0.f;
+      if (mx != -INFINITY)
+        for (int j = s0 + lane; j < e0; j += 32)
+          if (k != 0 || ((amask >> (j - s0)) & 1ull)) {
+            const float lp = y[j] - l;
+            pl += expf(lp) * lp;
+          }
+      pl = warp_sum(pl);
+      lse[k] = l;
+      Hk[k] = -pl;
+      const int a = act[row * nh + k];
+      if (head_on[row * nh + k]) {
+        const int ac = min(max(a, 0), e0 - s0 - 1);
+        lpi += y[s0 + ac] - l;
+        ent += Hk[k];
+      }
+      if (k == 0 && w != 0.f) {
+        if (amask == 0) flags |= 4u;
+        if (a < 0 || a >= n0 || !((amask >> a) & 1ull)) flags |= 2u;
+      }
+    }
+    const float lo = logp_old[row];
+    const float rho = expf(lpi - lo);
+    const float At = adv[row];
+    const float s1 = rho * At;
+    const float s2 = fminf(fmaxf(rho, 1.f - p.clip_eps), 1.f + p.clip_eps) * At;
+    const bool unclipped = s1 <= s2;
+    const float pg = -fminf(s1, s2);
+    const float V = y[A - 1];
+    const float Rt = ret[row];
+    const float vf = (V - Rt) * (V - Rt);
+    const float lrow = pg + p.c_v * vf - p.c_e * ent;
+    const float gpi = unclipped ? -At * rho * w * p.inv_denom : 0.f;
+    const float ce = p.c_e * w * p.inv_denom;
+    TD* dr = dout + row * A;
+    for (int k = 0; k < nh; ++k) {
+      const int s0 = p.off[k], e0 = p.off[k + 1];
+      const bool on = head_on[row * nh + k] != 0;
+      const int a = act[row * nh + k];
+      for (int j = s0 + lane; j < e0; j += 32) {
+        float d = 0.f;
+        if (on && (k != 0 || ((amask >> (j - s0)) & 1ull))) {
+          const float lp = y[j] - lse[k];
+          const float pj = expf(lp);
+          d = gpi * ((j - s0 == a ? 1.f : 0.f) - pj) + ce * pj * (lp + Hk[k]);
+        }
+        dr[j] = from_f<TD>(d);
+      }
+    }
+    if (lane == 0) {
+      dr[A - 1] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
+      if (logp) logp[row] = lpi;
+      if (w != 0.f) {
+        if (!isfinite(lrow)) flags |= 1u;
+        acc[0] += w * lrow;
+        acc[1] += w * pg;
+        acc[2] += w * vf;
+        acc[3] += w * ent;
+        acc[4] += w * (lo - lpi);
+        acc[5] += unclipped ? 0.f : w;
+        acc[6] += w;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 7; ++i) red[warp][i] = acc[i];
+    red[warp][7] = __uint_as_float(flags);
+  }
+  __syncthreads();
+  if (threadIdx.x < PPO_STATS) {
+    const int i = threadIdx.x;
+    float v = 0.f;
+    uint32_t f = 0;
+    for (int wi = 0; wi < 8; ++wi) {
+      if (i < 7) v += red[wi][i];
+      else f |= __float_as_uint(red[wi][7]);
+    }
+    partials[blockIdx.x * PPO_STATS + i] = i < 7 ? v : __uint_as_float(f);
+  }
+}
+
+__global__ void loss_finalize_kernel(const float* __restrict__ partials, int nblocks,
+                                     float inv_denom, float* __restrict__ stats) {
+  __shared__ float sv[256];
+  __shared__ uint32_t sf[256];
+  for (int i = 0; i < PPO_STATS; ++i) {
+    float v = 0.f;
+    uint32_t f = 0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+      if (i < 7) v += partials[b * PPO_STATS + i];
+      else f |= __float_as_uint(partials[b * PPO_STATS + i]);
+    }
+    sv[threadIdx.x] = v;
+    sf[threadIdx.x] = f;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) {
+        sv[threadIdx.x] += sv[threadIdx.x + s];
+        sf[threadIdx.x] |= sf[threadIdx.x + s];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      if (i < 6) stats[i] = sv[0] * inv_denom;
+      else if (i == 6) stats[i] = sv[0];
+      else stats[i] = (float)sf[0];
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================================ Adam + clip
+// 30 B/param: read p, g, m, v; write p, m, v, bf16 shadow (oracle O10).
+__global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p16,
+                            const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, size_t n, float alpha, float b1, float b2,
+                            float eps, float clip) {
+  const size_t n4 = n / 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float* pe = &pp.x;
+    const float* ge = &gg.x;
+    float* me = &mm.x;
+    float* ve = &vv.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float gi = ge[e];
+      const float vi = b2 * ve[e] + (1.f - b2) * gi * gi;
+      const float sv = sqrtf(vi);
+      const float gc = clip > 0.f ? fminf(fmaxf(gi, -clip * sv), clip * sv) : gi;
+      const float mi = b1 * me[e] + (1.f - b1) * gc;
+      pe[e] = pe[e] - alpha * mi / (sv + eps);
+      me[e] = mi;
+      ve[e] = vi;
+    }
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    if (p16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(pp.x, pp.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(pp.z, pp.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(p16)[i] = u;
+    }
+  }
+  for (size_t i = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float gi = g[i];
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    const float sv = sqrtf(vi);
+    const float gc = clip > 0.f ? fminf(fmaxf(gi, -clip * sv), clip * sv) : gi;
+    const float mi = b1 * m[i] + (1.f - b1) * gc;
+    p[i] = p[i] - alpha * mi / (sv + eps);
+    m[i] = mi;
+    v[i] = vi;
+    if (p16) p16[i] = __float2bfloat16_rn(p[i]);
+  }
+}
+
+// ============================================================================ SIMT fp32 path
+// Reference GEMM C[m][n] = sum_k A(m,k) B(n,k) with FFMA (no tf32), 64x64 tiles.
+__device__ __forceinline__ float op_get(const SimtOp& o, int64_t i, int64_t k) {
+  int s = k < o.kseg0 ? 0 : 1;
+  const int64_t kk = s ? k - o.kseg0 : k;
+  if (i >= o.rows[s] || kk >= o.kext[s]) return 0.f;
+  const float* p = o.p[s];
+  return o.mn ? p[kk * o.ld[s] + i] : p[i * o.ld[s] + kk];
+}
+
+__global__ void __launch_bounds__(256) simt_gemm_kernel(SimtOp a, SimtOp b, int64_t M, int64_t N,
+                                                        int64_t K, float* __restrict__ C,
+                                                        int64_t ldc) {
+  __shared__ float As[16][65];
+  __shared__ float Bs[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e / 64, ii = e % 64;
+      const int64_t k = k0 + kk;
+      As[kk][ii] = (k < K && m0 + ii < M) ? op_get(a, m0 + ii, k) : 0.f;
+      Bs[kk][ii] = (k < K && n0 + ii < N) ? op_get(b, n0 + ii, k) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        av[i] = As[kk][ty * 4 + i];
+        bv[i] = Bs[kk][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < M && n < N) C[m * ldc + n] = acc[i][j];
+    }
+}
+
+// Cell epilogues for the SIMT path (same cell math as the fused tcgen05 epilogues).
+__global__ void simt_cell_fwd_kernel(Shape s, int64_t B, const float* __restrict__ z,
+                                     const float* __restrict__ c_prev, float* __restrict__ c_out,
+                                     float* __restrict__ h_out, int64_t ldxh,
+                                     float* __restrict__ gates) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < B * s.H;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / s.H, j = idx - b * s.H;
+    const int64_t base = b * s.G4 + (j >> 6) * 256 + (j & 63);
+    float i, f, g, o, c, h;
+    cell_fwd(z[base], z[base + 64], z[base + 128], z[base + 192], c_prev[idx], i, f, g, o, c, h);
+    c_out[idx] = c;
+    h_out[b * ldxh + j] = h;
+    gates[base] = i;
+    gates[base + 64] = f;
+    gates[base + 128] = g;
+    gates[base + 192] = o;
+  }
+}
+
+__global__ void simt_cell_bwd_kernel(Shape s, int64_t B, const float* __restrict__ dh,
+                                     float* __restrict__ gz, const float* __restrict__ c_t,
+                                     const float* __restrict__ c_prev, float* __restrict__ dc) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < B * s.H;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / s.H, j = idx - b * s.H;
+    const int64_t base = b * s.G4 + (j >> 6) * 256 + (j & 63);
+    float a, bb, c, d, dn;
+    cell_bwd(dh[idx], dc[idx], gz[base], gz[base + 64], gz[base + 128], gz[base + 192], c_t[idx],
+             c_prev[idx], a, bb, c, d, dn);
+    gz[base] = a;
+    gz[base + 64] = bb;
+    gz[base + 128] = c;
+    gz[base + 192] = d;
+    dc[idx] = dn;
+  }
+}
+
+// ============================================================================ launchers
+static int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int launch_pack_params(const Shape& s, const float* Wx, const float* Wh, const float* b,
+                       const float* Wo, const float* bo, float* theta, int64_t n_wxh,
+                       int64_t n_total, cudaStream_t st) {
+  pack_params_kernel<<<grid_for(n_total), 256, 0, st>>>(s, Wx, Wh, b, Wo, bo, theta, n_wxh, n_total);
+  PPO_LAUNCH_CHECK("pack_params_kernel");
+  return PPO_OK;
+}
+int launch_unpack_params(const Shape& s, const float* theta, float* Wx, float* Wh, float* b,
+                         float* Wo, float* bo, int64_t n_wxh, cudaStream_t st) {
+  unpack_params_kernel<<<grid_for((s.G4 + s.A) * s.Kx), 256, 0, st>>>(s, theta, Wx, Wh, b, Wo, bo, n_wxh);
+  PPO_LAUNCH_CHECK("unpack_params_kernel");
+  return PPO_OK;
+}
+int launch_cast_bf16(const float* src, void* dst, size_t n, cudaStream_t st) {
+  cast_bf16_kernel<<<grid_for((int64_t)n), 256, 0, st>>>(src, (__nv_bfloat16*)dst, n);
+  PPO_LAUNCH_CHECK("cast_bf16_kernel");
+  return PPO_OK;
+}
+int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, const float* c0,
+                  void* xh, float* c, cudaStream_t st) {
+  const int64_t n = (s.T + 1) * B * s.Kx;
+  if (s.bf16)
+    pack_x_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(
+        s, B, (const __nv_bfloat16*)x, h0, c0, (__nv_bfloat16*)xh, c);
+  else
+    pack_x_kernel<float><<<grid_for(n), 256, 0, st>>>(s, B, (const float*)x, h0, c0, (float*)xh, c);
+  PPO_LAUNCH_CHECK("pack_x_kernel");
+  return PPO_OK;
+}
+int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
+               float gamma, float lam, int seq_T, float* adv, float* ret, cudaStream_t st) {
+  const int64_t threads = R * 32;
+  gae_kernel<<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret);
+  PPO_LAUNCH_CHECK("gae_kernel");
+  return PPO_OK;
+}
+int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t* act,
+                const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
+                const float* adv, const float* ret, const uint8_t* valid, void* dout, float* logp,
+                float* stats, cudaStream_t st) {
+  const size_t smem = 8 * (size_t)p.A_pad * sizeof(float);
+  float* partials = stats + PPO_STATS;
+  if (bf16)
+    loss_kernel<__nv_bfloat16><<<PPO_LOSS_BLOCKS, 256, smem, st>>>(
+        out, act, head_on, avail, logp_old, adv, ret, valid, p, (__nv_bfloat16*)dout, logp, partials);
+  else
+    loss_kernel<float><<<PPO_LOSS_BLOCKS, 256, smem, st>>>(
+        out, act, head_on, avail, logp_old, adv, ret, valid, p, (float*)dout, logp, partials);
+  PPO_LAUNCH_CHECK("loss_kernel");
+  loss_finalize_kernel<<<1, 256, 0, st>>>(partials, PPO_LOSS_BLOCKS, p.inv_denom, stats);
+  PPO_LAUNCH_CHECK("loss_finalize_kernel");
+  return PPO_OK;
+}
+int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n, float alpha,
+                float b1, float b2, float eps, float clip, cudaStream_t st) {
+  adam_kernel<<<grid_for((int64_t)(n / 4 + 1)), 256, 0, st>>>(p, (__nv_bfloat16*)p16, g, m, v, n,
+                                                               alpha, b1, b2, eps, clip);
+  PPO_LAUNCH_CHECK("adam_kernel");
+  return PPO_OK;
+}
+int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int64_t K, float* C,
+                     int64_t ldc, cudaStream_t st) {
+  dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64));
+  simt_gemm_kernel<<<grid, 256, 0, st>>>(a, b, M, N, K, C, ldc);
+  PPO_LAUNCH_CHECK("simt_gemm_kernel");
+  return PPO_OK;
+}
+int launch_simt_cell_fwd(const Shape& s, int64_t B, const float* z, const float* c_prev,
+                         float* c_out, float* h_out, int64_t ldxh, float* gates, cudaStream_t st) {
+  simt_cell_fwd_kernel<<<grid_for(B * s.H), 256, 0, st>>>(s, B, z, c_prev, c_out, h_out, ldxh, gates);
+  PPO_LAUNCH_CHECK("simt_cell_fwd_kernel");
+  return PPO_OK;
+}
+int launch_simt_cell_bwd(const Shape& s, int64_t B, const float* dh, float* gz, const float* c_t,
+                         const float* c_prev, float* dc, cudaStream_t st) {
+  simt_cell_bwd_kernel<<<grid_for(B * s.H), 256, 0, st>>>(s, B, dh, gz, c_t, c_prev, dc);
+  PPO_LAUNCH_CHECK("simt_cell_bwd_kernel");
+  return PPO_OK;
+}
+
+}  // namespace ppo

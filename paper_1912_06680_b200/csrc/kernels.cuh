@@ -1,0 +1,55 @@
+// kernels.cuh -- launcher declarations (internal).
+#pragma once
+#include "common.cuh"
+
+namespace ppo {
+
+struct LossParams {
+  int64_t N;          // rows = T*B
+  int A, A_pad, nh;
+  int off[PPO_MAX_HEADS + 1];
+  float clip_eps, c_v, c_e, inv_denom;
+};
+
+// Operand of the SIMT reference GEMM (see common.cuh Operand); fp32 only.
+struct SimtOp {
+  const float* p[2];
+  int64_t ld[2];
+  int64_t rows[2];
+  int64_t kext[2];
+  int64_t kseg0;
+  bool mn;
+};
+
+int launch_pack_params(const Shape& s, const float* Wx, const float* Wh, const float* b,
+                       const float* Wo, const float* bo, float* theta, int64_t n_wxh,
+                       int64_t n_total, cudaStream_t st);
+int launch_unpack_params(const Shape& s, const float* theta, float* Wx, float* Wh, float* b,
+                         float* Wo, float* bo, int64_t n_wxh, cudaStream_t st);
+int launch_cast_bf16(const float* src, void* dst, size_t n, cudaStream_t st);
+int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, const float* c0,
+                  void* xh, float* c, cudaStream_t st);
+int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
+               float gamma, float lam, int seq_T, float* adv, float* ret, cudaStream_t st);
+int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t* act,
+                const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
+                const float* adv, const float* ret, const uint8_t* valid, void* dout, float* logp,
+                float* stats, cudaStream_t st);
+int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n, float alpha,
+                float b1, float b2, float eps, float clip, cudaStream_t st);
+int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int64_t K, float* C,
+                     int64_t ldc, cudaStream_t st);
+int launch_simt_cell_fwd(const Shape& s, int64_t B, const float* z, const float* c_prev,
+                         float* c_out, float* h_out, int64_t ldxh, float* gates, cudaStream_t st);
+int launch_simt_cell_bwd(const Shape& s, int64_t B, const float* dh, float* gz, const float* c_t,
+                         const float* c_prev, float* dc, cudaStream_t st);
+
+// tcgen05 bf16 path (tc_path.cu)
+int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, cudaStream_t st);
+int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
+                cudaStream_t st);
+// Standalone test GEMM (exported for tests): C = A B^T variants on bf16 inputs.
+int tc_test_gemm(int mode, const void* A, const void* B, float* C, int M, int N, int K,
+                 cudaStream_t st);
+
+}  // namespace ppo

@@ -1,0 +1,497 @@
+// tc_gemm.cuh -- persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[m][n] = sum_k A(m,k) B(n,k),  bf16 operands, fp32 accumulator in TMEM.
+//
+// Roles (192 threads, 1 CTA/SM):
+//   warp 0 lane 0 : TMA producer   (cp.async.bulk.tensor, 128B swizzle, mbarrier ring)
+//   warp 1        : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN, K=16)
+//   warps 2..5    : epilogue (tcgen05.ld -> registers -> fused functor -> global)
+// Two TMEM accumulators (2 x BN columns) so the epilogue of tile i overlaps the
+// mainloop of tile i+1.  A and B may each be the K-concatenation of two sources
+// (separate tensor maps), split at k-block nkb0; each operand is K-major or MN-major.
+#pragma once
+#include "common.cuh"
+
+namespace ppo {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;             // one 128-byte swizzle row of bf16
+constexpr int kThreads = 192;
+
+struct TileShape {
+  int M, N;          // logical output extent (tiles beyond are masked by the epilogue)
+  int nkb0, nkb1;    // k-blocks taken from source 0 / source 1
+  int za0, za1;      // 3rd TMA coordinate (time slot) for A sources
+  int zb0, zb1;      // ... for B sources
+  int group_m;       // rasterisation: m-tiles per group
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait for the phase with the given parity.  Watchdog: a wait longer than 20 s traps (a
+// pipeline bug then surfaces as a launch error instead of a hung GPU).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  uint32_t done;
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (!done && ((++spins & 0xFFFu) == 0)) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 20000000000ull) asm volatile("trap;");
+    }
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// SMEM matrix descriptor (tcgen05 "shared memory descriptor"): start>>4 [0,14),
+// LBO>>4 [16,30), SBO>>4 [32,46), version=1 [46,48), base offset 0, layout
+// SWIZZLE_128B (=2) in [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+// Instruction descriptor, kind::f16: D=f32 [4,6), A=bf16 [7,10), B=bf16 [10,13),
+// a_major [15], b_major [16] (1 = MN-major), N>>3 [17,23), M>>4 [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t ad, uint64_t bd,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// 32 lanes x 16 consecutive fp32 columns; waits for completion before returning.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  __syncwarp();  // .sync.aligned: the whole warp executes this convergently
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int BN, bool A_MN, bool B_MN, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group_m,
+                                            int& mb, int& nb) {
+  int per_group = group_m * num_n;
+  int g = tile / per_group;
+  int first_m = g * group_m;
+  int gsz = min(group_m, num_m - first_m);
+  int local = tile - g * per_group;
+  mb = first_m + local % gsz;
+  nb = local / gsz;
+}
+
+template <int BN, bool A_MN, bool B_MN, int STAGES, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
+                   const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
+                   const TileShape sh, const Epi epi) {
+  using L = Smem<BN, A_MN, B_MN, STAGES>;
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
+  static_assert(!B_MN || BN % 64 == 0, "MN-major B needs 64-wide panels");
+  extern __shared__ uint8_t smem_raw[];
+  // 128B-swizzled TMA/UMMA tiles need 1024-byte aligned shared addresses
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (sh.M + BM - 1) / BM;
+  const int num_n = (sh.N + BN - 1) / BN;
+  const int ntiles = num_m * num_n;
+  const int nkb = sh.nkb0 + sh.nkb1;
+
+  if (threadIdx.x == 0) {
+    prefetch_map(&ta0);
+    prefetch_map(&tb0);
+    if (sh.nkb1 > 0) {
+      prefetch_map(&ta1);
+      prefetch_map(&tb1);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer =====================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, sh.group_m, mb, nb);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], L::STAGE_BYTES);
+          const bool s1 = kb >= sh.nkb0;
+          const int kk = (s1 ? kb - sh.nkb0 : kb) * BK;
+          const CUtensorMap* ta = s1 ? &ta1 : &ta0;
+          const CUtensorMap* tb = s1 ? &tb1 : &tb0;
+          const int za = s1 ? sh.za1 : sh.za0;
+          const int zb = s1 ? sh.zb1 : sh.zb0;
+          uint8_t* a_dst = sA + stage * L::A_BYTES;
+          uint8_t* b_dst = sB + stage * L::B_BYTES;
+          if (!A_MN) {
+            tma_load_3d(ta, &full[stage], a_dst, kk, mb * BM, za);
+          } else {
+#pragma unroll
+            for (int p = 0; p < BM / 64; ++p)
+              tma_load_3d(ta, &full[stage], a_dst + p * (BK * 128), mb * BM + p * 64, kk, za);
+          }
+          if (!B_MN) {
+            tma_load_3d(tb, &full[stage], b_dst, kk, nb * BN, zb);
+          } else {
+#pragma unroll
+            for (int p = 0; p < BN / 64; ++p)
+              tma_load_3d(tb, &full[stage], b_dst + p * (BK * 128), nb * BN + p * 64, kk, zb);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===================== MMA issuer (single thread) =====================
+      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * L::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * L::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: +32 B per 16 elements inside the 128 B swizzle row.
+            // MN-major: +16 K-rows of 128 B.  LBO (MN-major) = stride between 64-wide panels.
+            const uint64_t ad = A_MN ? sdesc(a0 + k * 2048, BK * 128, 1024)
+                                     : sdesc(a0 + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc(b0 + k * 2048, BK * 128, 1024)
+                                     : sdesc(b0 + k * 32, 16, 1024);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5 =====================
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, sh.group_m, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr =
+          tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
+      epi.template apply<BN>(mb, nb, row, taddr);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- epilogues
+
+// Plain fp32 store: out[m*ldc + n] for m < M, n < N.
+struct EpiStoreF32 {
+  float* out;
+  int64_t ldc;
+  int M, N;
+  template <int BN>
+  __device__ __forceinline__ void apply(int mb, int nb, int row, uint32_t taddr) const {
+    const int m = mb * BM + row;
+    const bool vec = (N % 4 == 0) && (ldc % 4 == 0);
+#pragma unroll 1
+    for (int c = 0; c < BN / 16; ++c) {
+      float v[16];
+      tmem_ld16(taddr + c * 16, v);
+      const int n0 = nb * BN + c * 16;
+      if (m >= M || n0 >= N) continue;
+      float* dst = out + static_cast<int64_t>(m) * ldc + n0;
+      if (vec && n0 + 16 <= N) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (n0 + i < N) dst[i] = v[i];
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ void load_bf16x16(const __nv_bfloat16* p, float (&v)[16]) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4 a = q[0], b = q[1];
+  const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f0 = __bfloat1622float2(h0[i]);
+    float2 f1 = __bfloat1622float2(h1[i]);
+    v[2 * i] = f0.x;
+    v[2 * i + 1] = f0.y;
+    v[8 + 2 * i] = f1.x;
+    v[8 + 2 * i + 1] = f1.y;
+  }
+}
+__device__ __forceinline__ void store_bf16x16(__nv_bfloat16* p, const float (&v)[16]) {
+  uint4 a, b;
+  __nv_bfloat162* h0 = reinterpret_cast<__nv_bfloat162*>(&a);
+  __nv_bfloat162* h1 = reinterpret_cast<__nv_bfloat162*>(&b);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h0[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    h1[i] = __floats2bfloat162_rn(v[8 + 2 * i], v[8 + 2 * i + 1]);
+  }
+  uint4* q = reinterpret_cast<uint4*>(p);
+  q[0] = a;
+  q[1] = b;
+}
+__device__ __forceinline__ void load_f32x16(const float* p, float (&v)[16]) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float4 a = q[i];
+    v[4 * i] = a.x;
+    v[4 * i + 1] = a.y;
+    v[4 * i + 2] = a.z;
+    v[4 * i + 3] = a.w;
+  }
+}
+__device__ __forceinline__ void store_f32x16(float* p, const float (&v)[16]) {
+  float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) q[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+
+// LSTM forward step t (oracle O4).  Tile = 128 sequences x 256 gate rows = 4 gates of 64
+// hidden units (gate-interleaved W rows), so the whole cell update is tile-local.
+struct EpiLstmFwd {
+  __nv_bfloat16* h_out;   // XH[t+1] + D  (row stride ldxh)
+  int64_t ldxh;
+  const float* c_prev;    // C[t]   [B][H]
+  float* c_out;           // C[t+1] [B][H]
+  __nv_bfloat16* gates;   // G[t]   [B][4H], interleaved like the accumulator columns
+  int B, H;
+  template <int BN>
+  __device__ __forceinline__ void apply(int mb, int nb, int row, uint32_t taddr) const {
+    static_assert(BN == 256, "cell tile holds 4 gates x 64 units");
+    const int m = mb * BM + row;
+    const bool ok = m < B;
+    const int64_t G4 = 4 * static_cast<int64_t>(H);
+#pragma unroll 1
+    for (int u0 = 0; u0 < 64; u0 += 16) {
+      float zi[16], zf[16], zg[16], zo[16];
+      tmem_ld16(taddr + 0 + u0, zi);
+      tmem_ld16(taddr + 64 + u0, zf);
+      tmem_ld16(taddr + 128 + u0, zg);
+      tmem_ld16(taddr + 192 + u0, zo);
+      if (!ok) continue;
+      const int j0 = nb * 64 + u0;
+      float cp[16], c[16], h[16];
+      load_f32x16(c_prev + static_cast<int64_t>(m) * H + j0, cp);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        float i, f, g, o;
+        cell_fwd(zi[e], zf[e], zg[e], zo[e], cp[e], i, f, g, o, c[e], h[e]);
+        zi[e] = i;
+        zf[e] = f;
+        zg[e] = g;
+        zo[e] = o;
+      }
+      store_f32x16(c_out + static_cast<int64_t>(m) * H + j0, c);
+      store_bf16x16(h_out + static_cast<int64_t>(m) * ldxh + j0, h);
+      __nv_bfloat16* gp = gates + static_cast<int64_t>(m) * G4 + nb * 256 + u0;
+      store_bf16x16(gp + 0, zi);
+      store_bf16x16(gp + 64, zf);
+      store_bf16x16(gp + 128, zg);
+      store_bf16x16(gp + 192, zo);
+    }
+  }
+};
+
+// LSTM backward step t (oracle O8).  Accumulator = dh_t = dz_{t+1} W_h + dy_t W_o for 256
+// hidden units; the cell backward reads the saved gates of step t and overwrites them with dz_t.
+struct EpiLstmBwd {
+  __nv_bfloat16* gz;      // G[t]: gates in, dz out  [B][4H]
+  const float* c_t;       // C[t+1]
+  const float* c_prev;    // C[t]
+  float* dc;              // [B][H] carry (in/out)
+  int B, H;
+  template <int BN>
+  __device__ __forceinline__ void apply(int mb, int nb, int row, uint32_t taddr) const {
+    const int m = mb * BM + row;
+    const bool ok = m < B;
+    const int64_t G4 = 4 * static_cast<int64_t>(H);
+#pragma unroll 1
+    for (int cc = 0; cc < BN / 16; ++cc) {
+      float dh[16];
+      tmem_ld16(taddr + cc * 16, dh);
+      const int j0 = nb * BN + cc * 16;
+      if (!ok || j0 >= H) continue;
+      const int q = j0 >> 6, u0 = j0 & 63;
+      __nv_bfloat16* gp = gz + static_cast<int64_t>(m) * G4 + q * 256 + u0;
+      float gi[16], gf[16], gg[16], go[16], ct[16], cp[16], dcv[16];
+      load_bf16x16(gp + 0, gi);
+      load_bf16x16(gp + 64, gf);
+      load_bf16x16(gp + 128, gg);
+      load_bf16x16(gp + 192, go);
+      const int64_t o = static_cast<int64_t>(m) * H + j0;
+      load_f32x16(c_t + o, ct);
+      load_f32x16(c_prev + o, cp);
+      load_f32x16(dc + o, dcv);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        float a, b, c, d, dn;
+        cell_bwd(dh[e], dcv[e], gi[e], gf[e], gg[e], go[e], ct[e], cp[e], a, b, c, d, dn);
+        gi[e] = a;
+        gf[e] = b;
+        gg[e] = c;
+        go[e] = d;
+        dcv[e] = dn;
+      }
+      store_bf16x16(gp + 0, gi);
+      store_bf16x16(gp + 64, gf);
+      store_bf16x16(gp + 128, gg);
+      store_bf16x16(gp + 192, go);
+      store_f32x16(dc + o, dcv);
+    }
+  }
+};
+
+}  // namespace tc
+}  // namespace ppo

@@ -1,0 +1,190 @@
+// tc_path.cu -- the bf16 tcgen05 path of the step: TMA tensor maps over the workspace and
+// the GEMM launches for forward (a2-a4) and backward (a6-a8).  DESIGN.md "Data layout".
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "kernels.cuh"
+#include "tc_gemm.cuh"
+
+namespace ppo {
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 tensor map, dims innermost first; strides in bytes for dims 1 and 2.
+int make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+             uint64_t s1, uint64_t s2, uint32_t box0, uint32_t box1) {
+  auto fn = encode_fn();
+  if (!fn) return fail(PPO_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (d2 == 1) s2 = s1 * d1;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {s1, s2};
+  const cuuint32_t box[3] = {box0, box1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(PPO_E_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) +
+                                 ") d0=" + std::to_string(d0) + " d1=" + std::to_string(d1));
+  return PPO_OK;
+}
+
+// K-major operand [rows][K] (K contiguous): box {64, tile rows}.
+int map_kmajor(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint64_t ld_elems,
+               uint64_t Z, uint64_t zstride_elems, uint32_t box_rows) {
+  return make_map(m, base, K, rows, Z, ld_elems * 2, zstride_elems * 2, 64, box_rows);
+}
+// MN-major operand [K][MN] (MN contiguous): box {64 (MN panel), 64 (K)}.
+int map_mnmajor(CUtensorMap* m, const void* base, uint64_t MN, uint64_t K, uint64_t ld_elems) {
+  return make_map(m, base, MN, K, 1, ld_elems * 2, 0, 64, tc::BK);
+}
+
+template <int BN, bool A_MN, bool B_MN, class Epi>
+int launch(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
+           const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
+  constexpr int STAGES = 4;
+  using L = tc::Smem<BN, A_MN, B_MN, STAGES>;
+  auto kern = tc::tc_gemm_kernel<BN, A_MN, B_MN, STAGES, Epi>;
+  static bool configured = false;
+  if (!configured) {
+    PPO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
+  const int64_t ntiles = (int64_t)((sh.M + tc::BM - 1) / tc::BM) * ((sh.N + BN - 1) / BN);
+  const int grid = (int)std::min<int64_t>(ntiles, num_sms());
+  if (grid <= 0) return PPO_OK;
+  kern<<<grid, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, sh, epi);
+  PPO_LAUNCH_CHECK("tc_gemm_kernel");
+  return PPO_OK;
+}
+
+inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+struct WsPtrs {
+  __nv_bfloat16* xh;
+  __nv_bfloat16* g;
+  float* c;
+  float* dc;
+};
+WsPtrs ws_ptrs(const Shape& s, int64_t B, void* ws) {
+  WsLayout L = ws_layout(s, B);
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  return {reinterpret_cast<__nv_bfloat16*>(p + L.xh), reinterpret_cast<__nv_bfloat16*>(p + L.g),
+          reinterpret_cast<float*>(p + L.c), reinterpret_cast<float*>(p + L.dc)};
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- forward (a2-a4)
+int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, cudaStream_t st) {
+  WsPtrs P = ws_ptrs(s, B, ws);
+  const __nv_bfloat16* wxh = static_cast<const __nv_bfloat16*>(w);
+  const __nv_bfloat16* wo = wxh + s.G4 * s.Kx;
+  int rc;
+  // z_t = [x_t | h_{t-1} | 1] W_xh_aug^T : A = XH (3-D, slot t), B = W_xh_aug.
+  CUtensorMap mA, mB;
+  if ((rc = map_kmajor(&mA, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, tc::BM))) return rc;
+  if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
+  for (int t = 0; t < s.T; ++t) {
+    tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 16};
+    tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
+                       P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
+    if ((rc = launch<256, false, false>(mA, mA, mB, mB, sh, epi, st))) return rc;
+  }
+  // heads: y = [h_t | 1] W_o_aug^T over all T*B rows (XH slots 1..T, columns D..D+Ko).
+  CUtensorMap hA, hB;
+  if ((rc = map_kmajor(&hA, P.xh + B * s.Kx + s.D, s.Ko, s.T * B, s.Kx, 1, 0, tc::BM))) return rc;
+  if ((rc = map_kmajor(&hB, wo, s.Ko, s.A, s.Ko, 1, 0, 224))) return rc;
+  tc::TileShape sh{(int)(s.T * B), (int)s.A, cdiv(s.Ko, tc::BK), 0, 0, 0, 0, 0, 16};
+  tc::EpiStoreF32 epi{out, s.A, (int)(s.T * B), (int)s.A};
+  return launch<224, false, false>(hA, hA, hB, hB, sh, epi, st);
+}
+
+// ---------------------------------------------------------------- backward (a6-a8)
+int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
+                cudaStream_t st) {
+  WsPtrs P = ws_ptrs(s, B, ws);
+  const __nv_bfloat16* wxh = static_cast<const __nv_bfloat16*>(w);
+  const __nv_bfloat16* wo = wxh + s.G4 * s.Kx;
+  const __nv_bfloat16* dY = static_cast<const __nv_bfloat16*>(dout);
+  int rc;
+  PPO_CUDA_CHECK(cudaMemsetAsync(P.dc, 0, B * s.H * sizeof(float), st));
+  // dh_t = dz_{t+1} W_h + dy_t W_o : A = [G (3-D, slot t+1) | dY (3-D, slot t)] (K-major),
+  // B = [W_xh_aug[:, D:D+H] | W_o_aug[:, :H]] read MN-major (K = gate row / head output).
+  CUtensorMap a0, a1, b0, b1;
+  if ((rc = map_kmajor(&a0, P.g, s.G4, B, s.G4, s.T, B * s.G4, tc::BM))) return rc;
+  if ((rc = map_kmajor(&a1, dY, s.A, B, s.A, s.T, B * s.A, tc::BM))) return rc;
+  if ((rc = map_mnmajor(&b0, wxh + s.D, s.H, s.G4, s.Kx))) return rc;
+  if ((rc = map_mnmajor(&b1, wo, s.H, s.A, s.Ko))) return rc;
+  for (int t = (int)s.T - 1; t >= 0; --t) {
+    const bool last = t == s.T - 1;
+    tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A, tc::BK),
+                     t + 1, t, 0, 0, 16};
+    tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
+                       (int)B, (int)s.H};
+    if ((rc = launch<256, false, true>(a0, a1, b0, b1, sh, epi, st))) return rc;
+  }
+  // weight gradients: dW_xh_aug = dZ^T [x | h_prev | 1 | 0] over all T*B rows (db falls out
+  // of the ones column); dW_o_aug = dY^T [h | 1 | 0].
+  CUtensorMap wa, wb, oa, ob;
+  const int64_t rows = s.T * B;
+  if ((rc = map_mnmajor(&wa, P.g, s.G4, rows, s.G4))) return rc;
+  if ((rc = map_mnmajor(&wb, P.xh, s.Kx, rows, s.Kx))) return rc;
+  {
+    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16};
+    tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
+    if ((rc = launch<256, true, true>(wa, wa, wb, wb, sh, epi, st))) return rc;
+  }
+  if ((rc = map_mnmajor(&oa, dY, s.A, rows, s.A))) return rc;
+  if ((rc = map_mnmajor(&ob, P.xh + B * s.Kx + s.D, s.Ko, rows, s.Kx))) return rc;
+  {
+    tc::TileShape sh{(int)s.A, (int)s.Ko, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16};
+    tc::EpiStoreF32 epi{grad + s.G4 * s.Kx, s.Ko, (int)s.A, (int)s.Ko};
+    if ((rc = launch<256, true, true>(oa, oa, ob, ob, sh, epi, st))) return rc;
+  }
+  return PPO_OK;
+}
+
+// ---------------------------------------------------------------- standalone test GEMM
+// mode bit0: B is MN-major ([K][N]) else K-major ([N][K]); bit1: A is MN-major ([K][M]).
+// mode bit2: BN = 224 (only with K-major A and B).  C [M][N] fp32.
+int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N, int K,
+                 cudaStream_t st) {
+  const bool b_mn = mode & 1, a_mn = mode & 2, n224 = mode & 4;
+  CUtensorMap ma, mb;
+  int rc;
+  const int BN = n224 ? 224 : 256;
+  if (a_mn) rc = map_mnmajor(&ma, A, M, K, M);
+  else rc = map_kmajor(&ma, A, K, M, K, 1, 0, tc::BM);
+  if (rc) return rc;
+  if (b_mn) rc = map_mnmajor(&mb, Bm, N, K, N);
+  else rc = map_kmajor(&mb, Bm, K, N, K, 1, 0, BN);
+  if (rc) return rc;
+  tc::TileShape sh{M, N, cdiv(K, tc::BK), 0, 0, 0, 0, 0, 16};
+  tc::EpiStoreF32 epi{C, N, M, N};
+  if (n224) {
+    if (a_mn || b_mn) return fail(PPO_E_ARG, "BN=224 test only for K-major operands");
+    return launch<224, false, false>(ma, ma, mb, mb, sh, epi, st);
+  }
+  if (!a_mn && !b_mn) return launch<256, false, false>(ma, ma, mb, mb, sh, epi, st);
+  if (!a_mn && b_mn) return launch<256, false, true>(ma, ma, mb, mb, sh, epi, st);
+  if (a_mn && b_mn) return launch<256, true, true>(ma, ma, mb, mb, sh, epi, st);
+  return fail(PPO_E_ARG, "unsupported test mode");
+}
+
+}  // namespace ppo

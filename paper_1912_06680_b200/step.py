@@ -1,0 +1,141 @@
+"""PPOOptimizer: composes one PPO optimizer step (§3.2) from the C-ABI calls.
+
+    ppo_gae -> lstm_bptt_fwd -> ppo_loss_grad -> lstm_bptt_bwd -> grad_allreduce -> adam_step
+
+PyTorch only provides device memory, streams and the process group that carries the NCCL
+unique id; every step of the path runs in libppo5's kernels.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+
+#: factorised heads, P:303-368 [App. Action Space]
+HEAD_SIZES = (30, 4, 189, 189, 81, 81, 81)
+
+#: Baseline hyperparameters, Table hyperparams; DESIGN Q3/Q4.
+DEFAULT_HYPER = dict(T_step=4.0 / 30.0, horizon_s=180.0, lam=0.95, clip_eps=0.2, c_v=1.0,
+                     c_e=0.01, lr=5e-5, beta1=0.9, beta2=0.999, adam_eps=1e-8, clip_sigma=5.0)
+
+
+def _aligned_empty(nbytes: int, device, align: int = 1024) -> torch.Tensor:
+    raw = torch.empty(nbytes + align, dtype=torch.uint8, device=device)
+    off = (-raw.data_ptr()) % align
+    return raw[off:off + nbytes]
+
+
+class PPOOptimizer:
+    """Owns theta (fp32 master, flat layout of ppo5.h), its bf16 shadow, Adam moments, the
+    gradient buffer and the activation workspace for one rank's minibatch of B sequences."""
+
+    def __init__(self, D: int, H: int, B: int, T: int = 16, head_sizes=HEAD_SIZES,
+                 precision: str = "bf16", device="cuda", hyper: dict | None = None,
+                 comm=None, n_buckets: int = 1):
+        self.D, self.H, self.B, self.T = D, H, B, T
+        self.head_sizes = tuple(head_sizes)
+        self.A = sum(self.head_sizes) + 1
+        self.bf16 = precision == "bf16"
+        self.device = torch.device(device)
+        self.hyper = dict(DEFAULT_HYPER, **(hyper or {}))
+        self.dims = L.make_dims(D, H, T, self.head_sizes,
+                                L.PPO_PREC_BF16 if self.bf16 else L.PPO_PREC_FP32)
+        self.layout = L.param_layout(self.dims)
+        n = self.layout.n_total
+        dev = self.device
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.theta = torch.zeros(n, **f32)
+        self.m = torch.zeros(n, **f32)
+        self.v = torch.zeros(n, **f32)
+        self.grad = torch.zeros(n, **f32)
+        self.shadow = torch.zeros(n, dtype=torch.bfloat16, device=dev) if self.bf16 else None
+        self.ws = _aligned_empty(L.ws_bytes(self.dims, B), dev)
+        act_dtype = torch.bfloat16 if self.bf16 else torch.float32
+        rows = T * B
+        self.out = torch.empty(rows, self.A, **f32)
+        self.dout = torch.empty(rows, self.A, dtype=act_dtype, device=dev)
+        self.logp = torch.empty(rows, **f32)
+        self.stats = torch.zeros(L.PPO_STATS_BUF, **f32)
+        self.adv = torch.empty(T, B, **f32)
+        self.ret = torch.empty(T, B, **f32)
+        self.t = 0
+        self.comm = comm
+        self.n_buckets = n_buckets
+        h = self.hyper
+        self.gamma = 1.0 - h["T_step"] / h["horizon_s"]  # Eq. horizon
+        self.loss_cfg = L.ppo_loss_cfg(h["clip_eps"], h["c_v"], h["c_e"], 0.0)
+
+    # ---------------------------------------------------------------- parameters
+    @property
+    def weights(self):
+        """the tensor the GEMMs read: bf16 shadow or fp32 theta"""
+        return self.shadow if self.bf16 else self.theta
+
+    def load_canonical(self, Wx, Wh, b, Wo, bo, stream=None):
+        """canonical fp32 device tensors (gate blocks [i;f;g;o]) -> theta (+ bf16 shadow)"""
+        L.ppo_pack_params(self.dims, Wx, Wh, b, Wo, bo, self.theta, stream)
+        if self.bf16:
+            L.ppo_cast_bf16(self.theta, self.shadow, stream)
+
+    def unpack(self, flat: torch.Tensor, stream=None) -> dict:
+        """flat theta-layout vector (params or grads) -> canonical fp32 tensors"""
+        H, D, A = self.H, self.D, self.A
+        f32 = dict(dtype=torch.float32, device=self.device)
+        out = dict(Wx=torch.empty(4 * H, D, **f32), Wh=torch.empty(4 * H, H, **f32),
+                   b=torch.empty(4 * H, **f32), Wo=torch.empty(A, H, **f32), bo=torch.empty(A, **f32))
+        L.ppo_unpack_params(self.dims, flat, out["Wx"], out["Wh"], out["b"], out["Wo"], out["bo"],
+                            stream)
+        return out
+
+    # ---------------------------------------------------------------- the step
+    def gae(self, batch, stream=None):
+        """a1: advantages/returns written time-major [T][B] for the minibatch"""
+        h = self.hyper
+        L.ppo_gae(batch["rew"], batch["val"], batch["done"], self.gamma, h["lam"], self.adv,
+                  self.ret, seq_T=self.T, stream=stream)
+
+    def forward(self, batch, stream=None):
+        """a2-a4"""
+        L.lstm_bptt_fwd(self.dims, self.weights, batch["x"], batch["h0"], batch["c0"], self.B,
+                        self.ws, self.out, stream)
+
+    def loss(self, batch, logp_old=None, stream=None):
+        """a5"""
+        L.ppo_loss_grad(self.dims, self.out, batch["act"], batch["head_on"], batch["avail"],
+                        batch["logp_old"] if logp_old is None else logp_old, self.adv, self.ret,
+                        batch.get("valid"), self.B, self.loss_cfg, self.dout, self.logp,
+                        self.stats, stream)
+
+    def backward(self, stream=None):
+        """a6-a8"""
+        L.lstm_bptt_bwd(self.dims, self.weights, self.ws, self.dout, self.B, self.grad, stream)
+
+    def allreduce(self, stream=None):
+        """a9"""
+        if self.comm is not None:
+            L.grad_allreduce(self.comm, self.grad, self.n_buckets, stream)
+
+    def apply(self, stream=None):
+        """a10"""
+        h = self.hyper
+        self.t += 1
+        L.adam_step(self.theta, self.shadow, self.grad, self.m, self.v, self.t, h["lr"],
+                    h["beta1"], h["beta2"], h["adam_eps"], h["clip_sigma"], stream)
+
+    def step(self, batch, stream=None):
+        """One full optimizer step a1-a10 on this rank; returns the device stats tensor."""
+        self.gae(batch, stream)
+        self.forward(batch, stream)
+        self.loss(batch, stream=stream)
+        self.backward(stream)
+        self.allreduce(stream)
+        self.apply(stream)
+        return self.stats[:L.PPO_STATS]
+
+    def current_logp(self, batch, stream=None) -> torch.Tensor:
+        """log pi_theta(a) for the batch (forward + loss pass); used to synthesise behaviour
+        log-probs like the forward-pass GPUs'."""
+        self.gae(batch, stream)
+        self.forward(batch, stream)
+        self.loss(batch, logp_old=torch.zeros_like(self.logp), stream=stream)
+        return self.logp.view(self.T, self.B).clone()

@@ -195,3 +195,56 @@ def make_rollouts(R: int, L: int, seed: int, p_done: float = 1.0 / 20000) -> dic
 def make_logits(rows: int, A: int, seed: int, scale: float = 1.0) -> np.ndarray:
     """Head outputs for isolated loss tests: N(0, scale^2) float32 [rows][A]."""
     return (scale * _rng(seed).standard_normal((rows, A))).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# Device-side generation for large B (bench / full-size sampled parity).  Same recipe,
+# torch Philox generator on the device; still no method arithmetic.
+# ---------------------------------------------------------------------------
+
+def torch_sequences(cfg: Config, seed: int, device, x_dtype=None, tt_seed: int = 1234) -> dict:
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    T, B, H, D = cfg.T, cfg.B, cfg.H, cfg.D
+    x_dtype = x_dtype or torch.bfloat16
+    x = torch.empty((T, B, D), dtype=x_dtype, device=device)
+    for t in range(T):  # chunked to bound the fp32 temporary
+        x[t] = torch.randn((B, D), generator=g, device=device).clamp_(-5.0, 5.0).to(x_dtype)
+    c0 = torch.randn((B, H), generator=g, device=device)
+    h0 = torch.rand((B, H), generator=g, device=device) * (torch.rand((B, H), generator=g, device=device) * 2 - 1)
+    avail = (torch.rand((T, B, N_PRIMARY), generator=g, device=device) < 7.1 / 29.0).to(torch.uint8)
+    avail[..., 0] = 1
+    u = torch.rand((T, B, N_PRIMARY), generator=g, device=device) * avail
+    primary = torch.argmax(u, dim=-1).to(torch.int32)
+    act = torch.empty((T, B, len(cfg.head_sizes)), dtype=torch.int32, device=device)
+    act[..., 0] = primary
+    for k, n in enumerate(cfg.head_sizes[1:], start=1):
+        act[..., k] = torch.randint(0, n, (T, B), generator=g, device=device, dtype=torch.int32)
+    tab = torch.from_numpy(heads_on_table(cfg.head_sizes, tt_seed)).to(device)
+    head_on = tab[primary.long()]
+    logp_noise = 0.1 * torch.randn((T, B), generator=g, device=device)
+    return dict(x=x, h0=h0, c0=c0, act=act, head_on=head_on, avail=avail,
+                logp_noise=logp_noise)
+
+
+def torch_rollouts(R: int, L: int, seed: int, device, p_done: float = 1.0 / 20000) -> dict:
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 7)
+    return dict(rew=torch.randn((R, L), generator=g, device=device),
+                val=torch.randn((R, L + 1), generator=g, device=device),
+                done=(torch.rand((R, L), generator=g, device=device) < p_done).to(torch.uint8))
+
+
+def torch_params(cfg: Config, seed: int, device, bo_scale: float = 0.0) -> dict:
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 13)
+    H, D, A = cfg.H, cfg.D, cfg.A
+    s = 1.0 / float(np.sqrt(H))
+    def U(*shape):
+        return (torch.rand(shape, generator=g, device=device) * 2 - 1) * s
+    return dict(Wx=U(4 * H, D), Wh=U(4 * H, H), b=U(4 * H),
+                Wo=0.01 * torch.randn((A, H), generator=g, device=device),
+                bo=bo_scale * torch.randn((A,), generator=g, device=device))

@@ -1,0 +1,65 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol include/ppo5.h declares,
+and rejects bad arguments on the host without touching a device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ppo5.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\**(\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1912_06680_b200 import _lib
+    return _lib
+
+
+def test_header_declares_the_hot_path():
+    names = _declared()
+    for n in ("ppo_gae", "lstm_bptt_fwd", "lstm_bptt_bwd", "ppo_loss_grad", "grad_allreduce",
+              "adam_step", "lstm_ws_bytes", "ppo_comm_init"):
+        assert n in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    so = ctypes.CDLL(lib.LIB_PATH)
+    missing = [n for n in _declared() if not hasattr(so, n)]
+    assert not missing, missing
+    assert set(_declared()) == set(lib.EXPORTED)
+
+
+def test_host_side_errors(lib):
+    d = lib.make_dims(4032, 4096, 16, (30, 4, 189, 189, 81, 81, 81))
+    lay = lib.param_layout(d)
+    assert lay.Kx == 4032 + 4096 + 64 and lay.Ko == 4096 + 64 and lay.A == 656
+    assert lay.n_total == 4 * 4096 * lay.Kx + 656 * lay.Ko
+    bad = lib.make_dims(4000, 4096, 16, (30,))
+    with pytest.raises(lib.PPOError) as e:
+        lib.param_layout(bad)
+    assert e.value.code == lib.PPO_E_SHAPE
+    assert "multiples of 64" in lib.last_error()
+    with pytest.raises(lib.PPOError):
+        lib.ws_bytes(d, 0)
+    # workspace size matches the documented layout (bf16 activations)
+    B = 40
+    n = lib.ws_bytes(d, B)
+    assert n >= (17 * B * lay.Kx * 2 + 16 * B * 4 * 4096 * 2 + 17 * B * 4096 * 4 + B * 4096 * 4)
+    assert "sm_100a" in lib.version()
+
+
+def test_null_pointers_rejected(lib):
+    d = lib.make_dims(256, 128, 16, (30, 4, 189, 189, 81, 81, 81))
+    rc = lib._lib.adam_step(None, None, None, None, None, 10, 1, 1e-3, 0.9, 0.999, 1e-8, 5.0, None)
+    assert rc == lib.PPO_E_ARG
+    rc = lib._lib.ppo_gae(None, None, None, 2, 256, 0.99, 0.95, 0, None, None, None)
+    assert rc == lib.PPO_E_ARG
+    rc = lib._lib.ppo_gae(None, None, None, 0, 256, 0.99, 0.95, 0, None, None, None)
+    assert rc == lib.PPO_OK  # empty input is a no-op

@@ -1,0 +1,192 @@
+"""Isolated-kernel parity on the GPU (each ABI call fed identical inputs vs the oracle, or vs
+plain PyTorch fp32 for the GEMM core)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import dev, elementwise_ok
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1912_06680_b200 import _lib
+    return _lib
+
+
+# ------------------------------------------------------------------ tcgen05 GEMM core
+@pytest.mark.parametrize("mode,M,N,K", [
+    (0, 128, 256, 64), (0, 300, 520, 200), (0, 1000, 16384 // 8, 1024),
+    (1, 256, 512, 192), (1, 77, 264, 1000),
+    (3, 384, 768, 448), (3, 136, 320, 72),
+    (4, 300, 656, 4160), (4, 33, 100, 64),
+])
+def test_tc_gemm_vs_torch(L, mode, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    a_mn, b_mn = bool(mode & 2), bool(mode & 1)
+    A = torch.randn((K, M) if a_mn else (M, K), generator=g, device="cuda").bfloat16()
+    B = torch.randn((K, N) if b_mn else (N, K), generator=g, device="cuda").bfloat16()
+    C = torch.full((M, N), float("nan"), device="cuda")
+    L.test_tc_gemm(mode, A, B, C, M, N, K)
+    torch.cuda.synchronize()
+    Af = (A.t() if a_mn else A).float()
+    Bf = (B if b_mn else B.t()).float()
+    ref = (Af.double() @ Bf.double()).float()
+    err = ((C - ref).abs().max() / ref.abs().max()).item()
+    assert not torch.isnan(C).any()
+    assert err < 1e-5, err
+
+
+# ------------------------------------------------------------------ GAE
+@pytest.mark.parametrize("R,Lr,seq_T,p_done", [
+    (2, 256, 16, 0.01), (2400, 256, 16, 1 / 20000), (3, 1350, 0, 0.002), (5, 1, 0, 0.5),
+    (1, 6300, 0, 0.0), (7, 300, 0, 0.05), (4, 512, 16, 0.0),
+])
+def test_gae_parity(L, R, Lr, seq_T, p_done):
+    ro = synth.make_rollouts(R, Lr, seed=R + Lr, p_done=p_done)
+    gamma = float(np.float32(oracle.gamma_from_horizon(180.0)))
+    lam = float(np.float32(0.95))
+    A, Rt = oracle.gae(ro["r"], ro["V"], ro["done"], gamma, lam)
+    if seq_T:
+        A = oracle.segments_to_sequences(A, seq_T)
+        Rt = oracle.segments_to_sequences(Rt, seq_T)
+    adv = torch.full(A.shape, float("nan"), device="cuda")
+    ret = torch.full(A.shape, float("nan"), device="cuda")
+    L.ppo_gae(dev(ro["r"]), dev(ro["V"]), dev(ro["done"]), gamma, lam, adv, ret, seq_T=seq_T)
+    torch.cuda.synchronize()
+    ok, worst = elementwise_ok(adv.cpu().numpy(), A, 1e-5)
+    assert ok, worst
+    ok, worst = elementwise_ok(ret.cpu().numpy(), Rt, 1e-5)
+    assert ok, worst
+
+
+def test_gae_lambda_edge_cases(L):
+    """lambda = 0 -> TD residual; gamma = lambda = 1 with no dones -> return-to-go minus V."""
+    ro = synth.make_rollouts(3, 64, seed=9, p_done=0.0)
+    for gamma, lam in ((0.99, 0.0), (1.0, 1.0)):
+        A, _ = oracle.gae(ro["r"], ro["V"], ro["done"], gamma, lam)
+        adv = torch.empty(A.shape, device="cuda")
+        ret = torch.empty(A.shape, device="cuda")
+        L.ppo_gae(dev(ro["r"]), dev(ro["V"]), dev(ro["done"]), gamma, lam, adv, ret)
+        torch.cuda.synchronize()
+        ok, worst = elementwise_ok(adv.cpu().numpy(), A, 1e-5)
+        assert ok, (gamma, lam, worst)
+
+
+# ------------------------------------------------------------------ PPO loss
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("seed,pad", [(0, 0.0), (1, 0.5), (2, 0.0)])
+def test_loss_parity(L, precision, seed, pad):
+    T, B = 16, 40
+    cfg = synth.Config(H=64, D=64, B=B, T=T)
+    s = synth.make_sequences(cfg, seed, pad_frac=pad)
+    N = T * B
+    Y = synth.make_logits(N, cfg.A, seed, scale=1.5)
+    rng = np.random.default_rng(seed)
+    adv = rng.standard_normal(N).astype(np.float32)
+    ret = rng.standard_normal(N).astype(np.float32)
+    act, on, av, valid = (s[k].reshape(N, -1) for k in ("act", "head_on", "avail", "valid"))
+    valid = valid.reshape(N)
+    lp0 = oracle.ppo_loss(Y, act, on, av, np.zeros(N), adv, ret, None, cfg.head_sizes)[3]
+    logp_old = (lp0 + s["logp_noise"].reshape(N)).astype(np.float32)
+    Lref, dYref, st, lpref = oracle.ppo_loss(Y, act, on, av, logp_old, adv, ret, valid,
+                                             cfg.head_sizes, 0.2, 1.0, 0.01)
+    bf16 = precision == "bf16"
+    dims = L.make_dims(64, 64, T, cfg.head_sizes, L.PPO_PREC_BF16 if bf16 else L.PPO_PREC_FP32)
+    dout = torch.empty((N, cfg.A), device="cuda", dtype=torch.bfloat16 if bf16 else torch.float32)
+    logp = torch.empty(N, device="cuda")
+    stats = torch.zeros(L.PPO_STATS_BUF, device="cuda")
+    L.ppo_loss_grad(dims, dev(Y), dev(act), dev(on), dev(av), dev(logp_old), dev(adv), dev(ret),
+                    dev(valid), B, L.ppo_loss_cfg(0.2, 1.0, 0.01, 0.0), dout, logp, stats)
+    torch.cuda.synchronize()
+    ok, worst = elementwise_ok(logp.cpu().numpy(), lpref, 1e-5)
+    assert ok, worst
+    d = dout.float().cpu().numpy()
+    if bf16:
+        # bf16 storage of an fp32 result: one rounding (2^-9 relative)
+        assert np.all(np.abs(d - dYref) <= 2 ** -8 * np.abs(dYref) + 1e-12)
+    else:
+        ok, worst = elementwise_ok(d, dYref, 1e-5)
+        assert ok, worst
+    # masked entries are exactly zero
+    assert np.all(d[:, :30][av == 0] == 0.0)
+    assert np.all(d[valid == 0] == 0.0)
+    sv = stats[:8].cpu().numpy()
+    for i, k in enumerate(("loss", "pg", "vf", "ent", "approx_kl", "clipfrac", "n_valid")):
+        assert abs(sv[i] - st[k]) <= 1e-5 * (abs(st[k]) + 1.0), (k, sv[i], st[k])
+    assert int(sv[7]) == st["flags"] == 0
+
+
+def test_loss_flags(L):
+    T, B = 1, 64
+    cfg = synth.Config(H=64, D=64, B=B, T=T)
+    s = synth.make_sequences(cfg, 3)
+    N = T * B
+    act, on, av = (s[k].reshape(N, -1) for k in ("act", "head_on", "avail"))
+    av = av.copy()
+    act = act.copy()
+    av[5, act[5, 0]] = 0          # taken action unavailable
+    act[5, 0] = 7 if av[5, 7] == 0 else act[5, 0]
+    av[6, :] = 0                  # empty availability row
+    Y = synth.make_logits(N, cfg.A, 1)
+    dims = L.make_dims(64, 64, T, cfg.head_sizes, L.PPO_PREC_FP32)
+    stats = torch.zeros(L.PPO_STATS_BUF, device="cuda")
+    z = dev(np.zeros(N, np.float32))
+    L.ppo_loss_grad(dims, dev(Y), dev(act), dev(on), dev(av), z, z, z, None, B,
+                    L.ppo_loss_cfg(0.2, 1.0, 0.01, 0.0),
+                    torch.empty((N, cfg.A), device="cuda"), None, stats)
+    torch.cuda.synchronize()
+    flags = int(stats[7].item())
+    assert flags & 2 and flags & 4
+
+
+# ------------------------------------------------------------------ Adam + clip
+@pytest.mark.parametrize("n,t,clip", [(1000, 1, 5.0), (4097, 7, 5.0), (10001, 3, 0.0),
+                                      (1 << 20, 50, 5.0)])
+def test_adam_parity(L, n, t, clip):
+    rng = np.random.default_rng(n + t)
+    p = rng.standard_normal(n).astype(np.float32)
+    g = (rng.standard_normal(n) * np.exp(rng.uniform(-6, 2, n))).astype(np.float32)
+    m = (0.01 * rng.standard_normal(n)).astype(np.float32)
+    v = (np.abs(rng.standard_normal(n)) * 1e-4).astype(np.float32) if t > 1 else np.zeros(n, np.float32)
+    pr, mr, vr = oracle.adam_clip(p, g, m, v, t, 5e-5, 0.9, 0.999, 1e-8, clip if clip else math.inf)
+    P, Gt, Mt, Vt = dev(p), dev(g), dev(m), dev(v)
+    P16 = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    L.adam_step(P, P16, Gt, Mt, Vt, t, 5e-5, 0.9, 0.999, 1e-8, clip)
+    torch.cuda.synchronize()
+    for got, ref in ((P, pr), (Mt, mr), (Vt, vr)):
+        gg = got.cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(gg - ref) <= 1e-6 * np.abs(ref) + 1e-12), np.abs(gg - ref).max()
+    assert torch.equal(P16, P.bfloat16())
+
+
+# ------------------------------------------------------------------ layout
+def test_pack_unpack_roundtrip_bit_exact(L):
+    cfg = synth.Config(H=128, D=192, B=1)
+    prm = synth.make_params(cfg, 5, bo_scale=0.1)
+    dims = L.make_dims(cfg.D, cfg.H, 16, cfg.head_sizes, L.PPO_PREC_FP32)
+    lay = L.param_layout(dims)
+    theta = torch.full((lay.n_total,), float("nan"), device="cuda")
+    L.ppo_pack_params(dims, *(dev(prm[k]) for k in ("Wx", "Wh", "b", "Wo", "bo")), theta)
+    outs = {k: torch.empty(v.shape, device="cuda") for k, v in prm.items()}
+    L.ppo_unpack_params(dims, theta, *(outs[k] for k in ("Wx", "Wh", "b", "Wo", "bo")))
+    torch.cuda.synchronize()
+    th = theta.cpu().numpy()
+    assert not np.isnan(th).any()
+    for k in prm:
+        assert np.array_equal(outs[k].cpu().numpy(), prm[k]), k
+    # spot-check the documented interleave: row r -> gate (r%256)//64 of unit 64*(r//256)+r%64
+    W = th[:lay.n_wxh].reshape(4 * cfg.H, lay.Kx)
+    for r in (0, 63, 64, 200, 256, 511):
+        gate, unit = (r % 256) // 64, 64 * (r // 256) + r % 64
+        cr = gate * cfg.H + unit
+        assert np.array_equal(W[r, :cfg.D], prm["Wx"][cr])
+        assert np.array_equal(W[r, cfg.D:cfg.D + cfg.H], prm["Wh"][cr])
+        assert W[r, cfg.D + cfg.H] == prm["b"][cr]
+        assert np.all(W[r, cfg.D + cfg.H + 1:] == 0)
