@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""bench.py -- PPO optimizer-step throughput (OpenAI Five LSTM-4096, arXiv 1912.06680) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--B B]
+
+One step = one pass of the whole hot path a1-a10 (GAE, TBPTT-16 forward through the
+4096-unit LSTM + heads, PPO loss/grad, backward, DP gradient average, Adam with the
++-5 sqrt(v) clip) over one minibatch of B sequences per GPU.  Default
+workload = BASELINE configs[1]: H=4096, D=4032, T=16, B=38,400 sequences per GPU
+(= 7,680 paper samples of 5 hero replicas x 16 steps), weak scaling.
+metric: paper samples/s (whole job); sequences/s and timesteps/s are reported beside it.
+
+For N>1 launch with torchrun (one process per GPU, NCCL).  --impl reference times the
+float64 oracle (the reference arm of this tier) on a bounded sample on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PPO train samples/s, LSTM-4096 16-step BPTT, 1/2/4/8 B200; % of roofline"
+UNIT = "samples/s"
+SEQ_PER_SAMPLE = 5   # a paper sample = 5 hero replicas x 16 steps
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--B", type=int, default=38400, help="sequences per GPU")
+    ap.add_argument("--H", type=int, default=4096)
+    ap.add_argument("--D", type=int, default=4032)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seq", type=int, default=1, help="oracle sample: sequences per step")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ measured peaks
+def peaks():
+    p = {"hbm_gbs": 6551.0, "bf16_tflops": 1644.0, "bf16_tflops_sustained": 1362.1,
+         "source": "MEASURED_PEAKS.json"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained"):
+            if k in j:
+                p[k] = float(j[k])
+    except OSError:
+        p.update(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0,
+                 source="fallback (B200_PROFILING.md)")
+    return p
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle sample (CPU)
+def oracle_sample_step(ctx):
+    """One bounded sample of the step on the float64 oracle (test infrastructure): GAE over
+    the sample's 256-step stream, TBPTT-16 forward/backward of `nseq` full-width sequences,
+    PPO loss, and Adam over a 1/B share of the parameters (Adam runs once per B-sequence
+    minibatch in the real step, so its per-sequence cost is 1/B of a full update)."""
+    import numpy as np
+    import oracle
+    from oracle.step import loss_and_grads
+    A, R = oracle.gae(ctx["ro"]["r"], ctx["ro"]["V"], ctx["ro"]["done"], ctx["gamma"], 0.95)
+    T = ctx["cfg"].T
+    adv = oracle.segments_to_sequences(A, T)[:, :ctx["nseq"]]
+    ret = oracle.segments_to_sequences(R, T)[:, :ctx["nseq"]]
+    _, g, _, _ = loss_and_grads(ctx["p"], ctx["seq"], ctx["logp_old"], adv, ret,
+                                ctx["cfg"].head_sizes)
+    share = ctx["adam_share"]
+    for k in ("Wx", "Wh", "b", "Wo", "bo"):
+        n = max(1, int(round(g[k].size * share)))
+        p = ctx["p"][k].reshape(-1)[:n]
+        z = np.zeros(n)
+        oracle.adam_clip(p, g[k].reshape(-1)[:n], z, z, 1, 5e-5)
+
+
+def oracle_context(H, D, nseq, B_full):
+    import numpy as np
+    import oracle
+    import synth
+    cfg = synth.Config(H=H, D=D, B=nseq)
+    p = {k: v.astype(np.float64) for k, v in synth.make_params(cfg, 0).items()}
+    seq = synth.make_sequences(cfg, 0)
+    ro = synth.make_rollouts(1, 256, 0)
+    logp_old = seq["logp_noise"].astype(np.float64) - 5.0
+    return dict(cfg=cfg, p=p, seq=seq, ro=ro, logp_old=logp_old, nseq=nseq,
+                gamma=oracle.gamma_from_horizon(180.0), adam_share=nseq / B_full)
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max((d.get("num_threads", 1) for d in info), default=os.cpu_count())
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, rank 0 only, bounded samples."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ctx = oracle_context(args.H, args.D, args.ref_seq, args.B)
+    for _ in range(args.warmup):
+        oracle_sample_step(ctx)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle_sample_step(ctx)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = (args.ref_seq / SEQ_PER_SAMPLE) / t
+    sample = (f"{args.ref_seq} full-width sequence(s) (H={args.H}, D={args.D}, T=16) per step: "
+              f"GAE + TBPTT fwd/bwd + loss + Adam on a {args.ref_seq}/{args.B} share of theta")
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, n):
+    return {
+        "workload": (f"full OpenAI-Five LSTM-{args.H} PPO step: D={args.D}, T=16, "
+                     f"B={args.B} sequences/GPU ({args.B // SEQ_PER_SAMPLE} paper samples), "
+                     f"A=656 (7 factorised heads + value), GAE over 256-step segments"),
+        "H": args.H, "D": args.D, "T": 16, "B_per_gpu": args.B,
+        "global_batch_samples": args.B * n // SEQ_PER_SAMPLE,
+        "global_batch_timesteps": args.B * n * 16,
+        "parallelism": f"dp{n}",
+        "l2": "inputs larger than L2 (x alone is T*B*D*2 bytes per step)",
+    }
+
+
+# ------------------------------------------------------------------ our arm
+def algorithmic(H, D, T, B, A, nparam):
+    """Algorithmic work per launch-class: flops for GEMMs, bytes for
+    the HBM-bound kernels."""
+    G4 = 4 * H
+    rows = T * B
+    return {
+        "lstm_fwd_step": ("flop", 2.0 * B * G4 * (D + H) * T),
+        "heads_fwd": ("flop", 2.0 * rows * A * H),
+        "lstm_bwd_step": ("flop", 2.0 * B * H * G4 * (T - 1) + 2.0 * B * H * A * T),
+        "wgrad_xh": ("flop", 2.0 * G4 * (D + H) * rows),
+        "wgrad_o": ("flop", 2.0 * A * H * rows),
+        "gae": ("byte", 17.0 * rows + 4.0 * rows / 256),
+        "loss": ("byte", rows * (4.0 * A + 2.0 * A + 4 * 7 + 7 + 30 + 4 * 4 + 1)),
+        "adam": ("byte", 30.0 * nparam),
+        "pack_x": ("byte", rows * D * 2.0 + (T + 1) * B * (D + H + 64) * 2.0 + 8.0 * B * H),
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+
+    import synth
+    from paper_1912_06680_b200 import PPOOptimizer, _lib as L
+
+    comm = None
+    if world > 1:
+        uid = L.comm_unique_id() if rank == 0 else bytes(L.PPO_COMM_ID_BYTES)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=device)
+        dist.broadcast(t, 0)
+        comm = L.comm_init(bytes(t.cpu().tolist()), rank, world)
+
+    H, D, T, B = args.H, args.D, 16, args.B
+    cfg = synth.Config(H=H, D=D, B=B, T=T)
+    opt = PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16", device=device, comm=comm,
+                       n_buckets=8)
+    prm = synth.torch_params(cfg, 0, device)          # same init on every rank
+    opt.load_canonical(prm["Wx"], prm["Wh"], prm["b"], prm["Wo"], prm["bo"])
+    del prm
+    seq = synth.torch_sequences(cfg, 1000 + rank, device)
+    R = B * T // 256
+    ro = synth.torch_rollouts(R, 256, 1000 + rank, device)
+    batch = dict(x=seq["x"], h0=seq["h0"], c0=seq["c0"], act=seq["act"],
+                 head_on=seq["head_on"], avail=seq["avail"], rew=ro["rew"], val=ro["val"],
+                 done=ro["done"])
+    # behaviour log-probs = current policy + N(0, 0.1^2) (forward-pass GPUs)
+    batch["logp_old"] = opt.current_logp(batch) + seq["logp_noise"]
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        opt.step(batch)
+    torch.cuda.synchronize()
+    stats = opt.stats[:8].cpu().tolist()
+
+    clocks = Clocks(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    L.prof_start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        opt.step(batch)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    prof = L.prof_stop()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_step = ms / args.steps
+    seq_s = B * world / (ms_step / 1e3)
+    value = seq_s / SEQ_PER_SAMPLE
+
+    # ---- roofline of each kernel class, dominant one reported
+    pk = peaks()
+    alg = algorithmic(H, D, T, B, cfg.A, opt.layout.n_total)
+    kernels = {}
+    for tag, (n, tot) in prof.items():
+        per_step_ms = tot / args.steps
+        ent = {"launches_per_step": n // args.steps, "ms_per_step": per_step_ms,
+               "share": per_step_ms / ms_step}
+        if tag in alg:
+            kind, work = alg[tag]
+            if kind == "flop":
+                ach = work / (per_step_ms / 1e3) / 1e12
+                ent.update(bound="tensor", achieved=ach, unit="TFLOP/s",
+                           peak=pk["bf16_tflops_sustained"], frac=ach / pk["bf16_tflops_sustained"])
+            else:
+                ach = work / (per_step_ms / 1e3) / 1e9
+                ent.update(bound="hbm", achieved=ach, unit="GB/s", peak=pk["hbm_gbs"],
+                           frac=ach / pk["hbm_gbs"])
+        kernels[tag] = ent
+    dom = max((k for k in kernels if "achieved" in kernels[k]),
+              key=lambda k: kernels[k]["ms_per_step"])
+    d = kernels[dom]
+    n_launch = sum(n for n, _ in prof.values())
+    step_flop = sum(w for k, (kind, w) in alg.items() if kind == "flop")
+    roofline = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
+                "unit": d["unit"], "frac": d["frac"], "traffic": None, "kernel": dom,
+                "peak_source": pk["source"] + (" sustained" if d["bound"] == "tensor" else ""),
+                "step_tflops": step_flop / (ms_step / 1e3) / 1e12,
+                "step_frac_of_sustained_bf16": step_flop / (ms_step / 1e3) / 1e12 / pk["bf16_tflops_sustained"]}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        keys = ("x", "h0", "c0", "act", "head_on", "avail", "logp_old", "rew", "val", "done")
+        host = {k: batch[k].cpu().pin_memory() for k in keys}
+        h2d = sum(v.numel() * v.element_size() for v in host.values())
+        st_host = torch.empty(8, dtype=torch.float32).pin_memory()
+        d2h = st_host.numel() * 4
+
+        def e2e_step():
+            for k in keys:
+                batch[k].copy_(host[k], non_blocking=True)
+            opt.step(batch)
+            st_host.copy_(opt.stats[:8], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": B * world / (ems / args.steps / 1e3) / SEQ_PER_SAMPLE, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": ems / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ctx = oracle_context(H, D, args.ref_seq, B)
+        t0 = time.perf_counter()
+        oracle_sample_step(ctx)
+        tcpu = time.perf_counter() - t0
+        cpu = {"value": (args.ref_seq / SEQ_PER_SAMPLE) / tcpu, "unit": UNIT,
+               "cores": blas_threads(), "kind": "oracle",
+               "sample": (f"{args.ref_seq} full-width sequence(s) per step: GAE + TBPTT-16 "
+                          f"fwd/bwd + loss + Adam on a {args.ref_seq}/{B} share of theta; "
+                          f"{tcpu:.1f} s")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded; paper-shaped rollouts, random-init weights)",
+            "config": workload_config(args, world),
+            "sequences_per_s": seq_s, "timesteps_per_s": seq_s * T,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": n_launch, "clocks": clk, "kernels": kernels,
+            "loss_stats_warmup": dict(zip(L.STAT_NAMES, stats)),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        L.comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

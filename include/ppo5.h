@@ -169,10 +169,25 @@ int ppo_comm_destroy(ppo_comm* comm);
  *   v <- b2 v + (1-b2) g^2;  g_c = clamp(g, +-clip_sigma sqrt(v));  m <- b1 m + (1-b1) g_c
  *   p <- p - lr sqrt(1-b2^t)/(1-b1^t) * m / (sqrt(v) + eps)
  * t >= 1 (step number); clip_sigma <= 0 or inf disables the clip.  p_bf16 (nullable) receives
- * the bf16 shadow of the updated p.  All arrays n fp32 elements (p_bf16: n uint16). */
+ * the bf16 shadow of the updated p.  All arrays n fp32 elements (p_bf16: n uint16).
+ * Host scalars are double: alpha_t, 1-b1 and 1-b2 are formed in double and rounded once to
+ * fp32 (1-b2 from an fp32 b2 would be off by 1.3e-5 relative). */
 int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, size_t n,
-              int64_t t, float lr, float b1, float b2, float eps, float clip_sigma,
+              int64_t t, double lr, double b1, double b2, double eps, double clip_sigma,
               ppo_stream_t s);
+
+/* ---- tracing: CUDA events around every kernel launch ------------------------
+ * ppo_prof_start() enables recording (clears previous records); every library launch then
+ * records a start/end event pair on its stream.  ppo_prof_stop() synchronises those events,
+ * aggregates per kernel tag (launch count, total device ms, in first-seen order) into
+ * out[0..max_entries) (host), sets *n_out to the number of tags and disables recording. */
+typedef struct {
+  char name[32];
+  int32_t launches;
+  double total_ms;
+} ppo_prof_entry;
+int ppo_prof_start(void);
+int ppo_prof_stop(ppo_prof_entry* out /* host */, int32_t max_entries, int32_t* n_out /* host */);
 
 /* ---- testing hook (not part of the step) -------------------------------------------------
  * One standalone tcgen05 GEMM C[M][N] (fp32) = sum_k A(m,k) B(n,k) on bf16 operands, used by

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_size_t, c_uint8, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_uint8, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libppo5.so")
@@ -46,6 +46,10 @@ class ppo_loss_cfg(ctypes.Structure):
     _fields_ = [("clip_eps", c_float), ("c_v", c_float), ("c_e", c_float), ("denom", c_float)]
 
 
+class ppo_prof_entry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", c_int32), ("total_ms", c_double)]
+
+
 class PPOError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"libppo5 error {code}: {msg}")
@@ -72,15 +76,17 @@ _lib_fns = dict(
     lstm_ws_bytes=([_D, c_int64, POINTER(c_size_t)], c_int),
     lstm_bptt_fwd=([_D, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_size_t,
                     c_void_p, c_void_p], c_int),
-    ppo_loss_grad=([_D] + [c_void_p] * 9 + [c_int64, POINTER(ppo_loss_cfg), c_void_p, c_void_p,
+    ppo_loss_grad=([_D] + [c_void_p] * 8 + [c_int64, POINTER(ppo_loss_cfg), c_void_p, c_void_p,
                                              c_void_p, c_void_p], c_int),
     lstm_bptt_bwd=([_D, c_void_p, c_void_p, c_size_t, c_void_p, c_int64, c_void_p, c_void_p], c_int),
     ppo_comm_unique_id=([POINTER(c_uint8)], c_int),
     ppo_comm_init=([POINTER(c_uint8), c_int, c_int, POINTER(c_void_p)], c_int),
     grad_allreduce=([c_void_p, c_void_p, c_size_t, c_int32, c_void_p], c_int),
     ppo_comm_destroy=([c_void_p], c_int),
-    adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_float,
-                c_float, c_float, c_float, c_float, c_void_p], c_int),
+    adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_double,
+                c_double, c_double, c_double, c_double, c_void_p], c_int),
+    ppo_prof_start=([], c_int),
+    ppo_prof_stop=([POINTER(ppo_prof_entry), c_int32, POINTER(c_int32)], c_int),
     ppo_test_tc_gemm=([c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p], c_int),
 )
 EXPORTED = tuple(_lib_fns)
@@ -198,6 +204,19 @@ def grad_allreduce(comm, g, n_buckets=1, stream=None):
 
 def comm_destroy(comm):
     _check(_lib.ppo_comm_destroy(comm))
+
+
+def prof_start():
+    _check(_lib.ppo_prof_start())
+
+
+def prof_stop(max_entries: int = 64) -> dict:
+    """-> {kernel tag: (launches, total device ms)} recorded since prof_start()"""
+    arr = (ppo_prof_entry * max_entries)()
+    n = c_int32()
+    _check(_lib.ppo_prof_stop(arr, max_entries, ctypes.byref(n)))
+    return {arr[i].name.decode(): (arr[i].launches, arr[i].total_ms)
+            for i in range(min(n.value, max_entries))}
 
 
 def test_tc_gemm(mode, A, B, C, M, N, K, stream=None):

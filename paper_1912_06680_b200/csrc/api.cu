@@ -3,7 +3,10 @@
 #include <math.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -18,6 +21,53 @@ int fail(int code, const std::string& msg) {
 int cuda_fail(cudaError_t e, const char* what) {
   g_err = std::string(what) + ": " + cudaGetErrorString(e);
   return PPO_E_CUDA;
+}
+
+// ---- tracing ------------------------------------------------------------------------------
+namespace {
+struct ProfRec {
+  std::string tag;
+  cudaEvent_t a, b;
+};
+struct Prof {
+  std::mutex mu;
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<int> open;  // indices of records awaiting their end event
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Prof& prof() {
+  static Prof p;
+  return p;
+}
+}  // namespace
+
+void prof_begin(const char* tag, cudaStream_t s) {
+  Prof& P = prof();
+  if (!P.on) return;
+  std::lock_guard<std::mutex> g(P.mu);
+  ProfRec r{tag, P.get(), P.get()};
+  cudaEventRecord(r.a, s);
+  P.recs.push_back(r);
+  P.open.push_back((int)P.recs.size() - 1);
+}
+void prof_end(cudaStream_t s) {
+  Prof& P = prof();
+  if (!P.on) return;
+  std::lock_guard<std::mutex> g(P.mu);
+  if (P.open.empty()) return;
+  cudaEventRecord(P.recs[P.open.back()].b, s);
+  P.open.pop_back();
 }
 
 int num_sms() {
@@ -305,7 +355,7 @@ int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes
 }
 
 int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, size_t n,
-              int64_t t, float lr, float b1, float b2, float eps, float clip_sigma,
+              int64_t t, double lr, double b1, double b2, double eps, double clip_sigma,
               ppo_stream_t st) {
   if (n == 0) return PPO_OK;
   NEED(p);
@@ -314,11 +364,62 @@ int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, si
   NEED(v);
   if (p_bf16 && !aligned(p_bf16, 16)) return fail(PPO_E_ALIGN, "p_bf16 is not 16-byte aligned");
   if (t < 1) return fail(PPO_E_ARG, "t must be >= 1");
-  if (!(b1 >= 0.f && b1 < 1.f && b2 >= 0.f && b2 < 1.f)) return fail(PPO_E_ARG, "bad betas");
-  const double alpha =
-      (double)lr * sqrt(1.0 - pow((double)b2, (double)t)) / (1.0 - pow((double)b1, (double)t));
-  const float clip = (clip_sigma > 0.f && isfinite(clip_sigma)) ? clip_sigma : 0.f;
-  return launch_adam(p, p_bf16, g, m, v, n, (float)alpha, b1, b2, eps, clip, (cudaStream_t)st);
+  if (!(b1 >= 0.0 && b1 < 1.0 && b2 >= 0.0 && b2 < 1.0)) return fail(PPO_E_ARG, "bad betas");
+  AdamParams ap;
+  ap.alpha = (float)(lr * sqrt(1.0 - pow(b2, (double)t)) / (1.0 - pow(b1, (double)t)));
+  ap.b1 = (float)b1;
+  ap.omb1 = (float)(1.0 - b1);
+  ap.b2 = (float)b2;
+  ap.omb2 = (float)(1.0 - b2);
+  ap.eps = (float)eps;
+  ap.clip = (clip_sigma > 0.0 && isfinite(clip_sigma)) ? (float)clip_sigma : 0.f;
+  return launch_adam(p, p_bf16, g, m, v, n, ap, (cudaStream_t)st);
+}
+
+int ppo_prof_start(void) {
+  Prof& P = prof();
+  std::lock_guard<std::mutex> g(P.mu);
+  for (auto& r : P.recs) {
+    P.pool.push_back(r.a);
+    P.pool.push_back(r.b);
+  }
+  P.recs.clear();
+  P.open.clear();
+  P.on = true;
+  return PPO_OK;
+}
+
+int ppo_prof_stop(ppo_prof_entry* out, int32_t max_entries, int32_t* n_out) {
+  Prof& P = prof();
+  std::lock_guard<std::mutex> g(P.mu);
+  P.on = false;
+  std::map<std::string, std::pair<int, double>> agg;
+  std::vector<std::string> order;
+  for (auto& r : P.recs) {
+    PPO_CUDA_CHECK(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    PPO_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+    auto it = agg.find(r.tag);
+    if (it == agg.end()) {
+      order.push_back(r.tag);
+      agg[r.tag] = {1, ms};
+    } else {
+      it->second.first += 1;
+      it->second.second += ms;
+    }
+  }
+  int n = 0;
+  for (auto& tag : order) {
+    if (out && n < max_entries) {
+      memset(out[n].name, 0, sizeof(out[n].name));
+      strncpy(out[n].name, tag.c_str(), sizeof(out[n].name) - 1);
+      out[n].launches = agg[tag].first;
+      out[n].total_ms = agg[tag].second;
+    }
+    ++n;
+  }
+  if (n_out) *n_out = n;
+  return PPO_OK;
 }
 
 // ---- testing hook (not part of the step): one tcgen05 GEMM, see tc_path.cu -------------

@@ -51,6 +51,7 @@ int grad_allreduce(ppo_comm* c, float* g, size_t n, int32_t n_buckets, ppo_strea
   if (!g) return ppo::fail(PPO_E_ARG, "g is NULL");
   if (n_buckets <= 0) n_buckets = 1;
   const size_t per = (n + n_buckets - 1) / n_buckets;
+  ppo::ProfScope _prof("allreduce", (cudaStream_t)st);
   ncclResult_t r = ncclGroupStart();
   if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
   for (size_t off = 0; off < n; off += per) {

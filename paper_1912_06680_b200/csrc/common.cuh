@@ -32,6 +32,15 @@ inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_
 
 int num_sms();
 
+// ---- tracing: per-launch CUDA events on the launching stream (ppo_prof_start/stop) ---------
+void prof_begin(const char* tag, cudaStream_t s);
+void prof_end(cudaStream_t s);
+struct ProfScope {
+  cudaStream_t s;
+  ProfScope(const char* tag, cudaStream_t st) : s(st) { prof_begin(tag, st); }
+  ~ProfScope() { prof_end(s); }
+};
+
 // ---- derived shapes ----------------------------------------------------------------------
 struct Shape {
   int64_t D, H, T, A, G4, Kx, Ko;  // G4 = 4H gate rows

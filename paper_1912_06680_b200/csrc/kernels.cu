@@ -332,8 +332,9 @@ __global__ void loss_finalize_kernel(const float* __restrict__ partials, int nbl
 // 30 B/param: read p, g, m, v; write p, m, v, bf16 shadow (oracle O10).
 __global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p16,
                             const float* __restrict__ g, float* __restrict__ m,
-                            float* __restrict__ v, size_t n, float alpha, float b1, float b2,
-                            float eps, float clip) {
+                            float* __restrict__ v, size_t n, AdamParams ap) {
+  const float alpha = ap.alpha, b1 = ap.b1, b2 = ap.b2, omb1 = ap.omb1, omb2 = ap.omb2;
+  const float eps = ap.eps, clip = ap.clip;
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -348,10 +349,10 @@ __global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float gi = ge[e];
-      const float vi = b2 * ve[e] + (1.f - b2) * gi * gi;
+      const float vi = b2 * ve[e] + omb2 * gi * gi;
       const float sv = sqrtf(vi);
       const float gc = clip > 0.f ? fminf(fmaxf(gi, -clip * sv), clip * sv) : gi;
-      const float mi = b1 * me[e] + (1.f - b1) * gc;
+      const float mi = b1 * me[e] + omb1 * gc;
       pe[e] = pe[e] - alpha * mi / (sv + eps);
       me[e] = mi;
       ve[e] = vi;
@@ -370,10 +371,10 @@ __global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p
   }
   for (size_t i = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const float gi = g[i];
-    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    const float vi = b2 * v[i] + omb2 * gi * gi;
     const float sv = sqrtf(vi);
     const float gc = clip > 0.f ? fminf(fmaxf(gi, -clip * sv), clip * sv) : gi;
-    const float mi = b1 * m[i] + (1.f - b1) * gc;
+    const float mi = b1 * m[i] + omb1 * gc;
     p[i] = p[i] - alpha * mi / (sv + eps);
     m[i] = mi;
     v[i] = vi;
@@ -480,23 +481,27 @@ static int grid_for(int64_t n, int threads = 256) {
 int launch_pack_params(const Shape& s, const float* Wx, const float* Wh, const float* b,
                        const float* Wo, const float* bo, float* theta, int64_t n_wxh,
                        int64_t n_total, cudaStream_t st) {
+  ProfScope _prof("pack_params", st);
   pack_params_kernel<<<grid_for(n_total), 256, 0, st>>>(s, Wx, Wh, b, Wo, bo, theta, n_wxh, n_total);
   PPO_LAUNCH_CHECK("pack_params_kernel");
   return PPO_OK;
 }
 int launch_unpack_params(const Shape& s, const float* theta, float* Wx, float* Wh, float* b,
                          float* Wo, float* bo, int64_t n_wxh, cudaStream_t st) {
+  ProfScope _prof("unpack_params", st);
   unpack_params_kernel<<<grid_for((s.G4 + s.A) * s.Kx), 256, 0, st>>>(s, theta, Wx, Wh, b, Wo, bo, n_wxh);
   PPO_LAUNCH_CHECK("unpack_params_kernel");
   return PPO_OK;
 }
 int launch_cast_bf16(const float* src, void* dst, size_t n, cudaStream_t st) {
+  ProfScope _prof("cast_bf16", st);
   cast_bf16_kernel<<<grid_for((int64_t)n), 256, 0, st>>>(src, (__nv_bfloat16*)dst, n);
   PPO_LAUNCH_CHECK("cast_bf16_kernel");
   return PPO_OK;
 }
 int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, const float* c0,
                   void* xh, float* c, cudaStream_t st) {
+  ProfScope _prof("pack_x", st);
   const int64_t n = (s.T + 1) * B * s.Kx;
   if (s.bf16)
     pack_x_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(
@@ -508,6 +513,7 @@ int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, con
 }
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
                float gamma, float lam, int seq_T, float* adv, float* ret, cudaStream_t st) {
+  ProfScope _prof("gae", st);
   const int64_t threads = R * 32;
   gae_kernel<<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret);
   PPO_LAUNCH_CHECK("gae_kernel");
@@ -519,6 +525,8 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
                 float* stats, cudaStream_t st) {
   const size_t smem = 8 * (size_t)p.A_pad * sizeof(float);
   float* partials = stats + PPO_STATS;
+  {
+  ProfScope _prof("loss", st);
   if (bf16)
     loss_kernel<__nv_bfloat16><<<PPO_LOSS_BLOCKS, 256, smem, st>>>(
         out, act, head_on, avail, logp_old, adv, ret, valid, p, (__nv_bfloat16*)dout, logp, partials);
@@ -526,19 +534,22 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
     loss_kernel<float><<<PPO_LOSS_BLOCKS, 256, smem, st>>>(
         out, act, head_on, avail, logp_old, adv, ret, valid, p, (float*)dout, logp, partials);
   PPO_LAUNCH_CHECK("loss_kernel");
+  }
+  ProfScope _prof("loss_finalize", st);
   loss_finalize_kernel<<<1, 256, 0, st>>>(partials, PPO_LOSS_BLOCKS, p.inv_denom, stats);
   PPO_LAUNCH_CHECK("loss_finalize_kernel");
   return PPO_OK;
 }
-int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n, float alpha,
-                float b1, float b2, float eps, float clip, cudaStream_t st) {
-  adam_kernel<<<grid_for((int64_t)(n / 4 + 1)), 256, 0, st>>>(p, (__nv_bfloat16*)p16, g, m, v, n,
-                                                               alpha, b1, b2, eps, clip);
+int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n,
+                const AdamParams& ap, cudaStream_t st) {
+  ProfScope _prof("adam", st);
+  adam_kernel<<<grid_for((int64_t)(n / 4 + 1)), 256, 0, st>>>(p, (__nv_bfloat16*)p16, g, m, v, n, ap);
   PPO_LAUNCH_CHECK("adam_kernel");
   return PPO_OK;
 }
 int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int64_t K, float* C,
                      int64_t ldc, cudaStream_t st) {
+  ProfScope _prof("simt_gemm", st);
   dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64));
   simt_gemm_kernel<<<grid, 256, 0, st>>>(a, b, M, N, K, C, ldc);
   PPO_LAUNCH_CHECK("simt_gemm_kernel");
@@ -546,12 +557,14 @@ int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int
 }
 int launch_simt_cell_fwd(const Shape& s, int64_t B, const float* z, const float* c_prev,
                          float* c_out, float* h_out, int64_t ldxh, float* gates, cudaStream_t st) {
+  ProfScope _prof("simt_cell_fwd", st);
   simt_cell_fwd_kernel<<<grid_for(B * s.H), 256, 0, st>>>(s, B, z, c_prev, c_out, h_out, ldxh, gates);
   PPO_LAUNCH_CHECK("simt_cell_fwd_kernel");
   return PPO_OK;
 }
 int launch_simt_cell_bwd(const Shape& s, int64_t B, const float* dh, float* gz, const float* c_t,
                          const float* c_prev, float* dc, cudaStream_t st) {
+  ProfScope _prof("simt_cell_bwd", st);
   simt_cell_bwd_kernel<<<grid_for(B * s.H), 256, 0, st>>>(s, B, dh, gz, c_t, c_prev, dc);
   PPO_LAUNCH_CHECK("simt_cell_bwd_kernel");
   return PPO_OK;

@@ -35,8 +35,11 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
                 const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
                 const float* adv, const float* ret, const uint8_t* valid, void* dout, float* logp,
                 float* stats, cudaStream_t st);
-int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n, float alpha,
-                float b1, float b2, float eps, float clip, cudaStream_t st);
+struct AdamParams {
+  float alpha, b1, omb1, b2, omb2, eps, clip;
+};
+int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n,
+                const AdamParams& ap, cudaStream_t st);
 int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int64_t K, float* C,
                      int64_t ldc, cudaStream_t st);
 int launch_simt_cell_fwd(const Shape& s, int64_t B, const float* z, const float* c_prev,

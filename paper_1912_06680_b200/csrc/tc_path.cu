@@ -54,7 +54,7 @@ int map_mnmajor(CUtensorMap* m, const void* base, uint64_t MN, uint64_t K, uint6
 }
 
 template <int BN, bool A_MN, bool B_MN, class Epi>
-int launch(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
+int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
            const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
   constexpr int STAGES = 4;
   using L = tc::Smem<BN, A_MN, B_MN, STAGES>;
@@ -68,6 +68,7 @@ int launch(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
   const int64_t ntiles = (int64_t)((sh.M + tc::BM - 1) / tc::BM) * ((sh.N + BN - 1) / BN);
   const int grid = (int)std::min<int64_t>(ntiles, num_sms());
   if (grid <= 0) return PPO_OK;
+  ProfScope _prof(tag, st);
   kern<<<grid, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, sh, epi);
   PPO_LAUNCH_CHECK("tc_gemm_kernel");
   return PPO_OK;
@@ -104,7 +105,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
     tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 16};
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
-    if ((rc = launch<256, false, false>(mA, mA, mB, mB, sh, epi, st))) return rc;
+    if ((rc = launch<256, false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st))) return rc;
   }
   // heads: y = [h_t | 1] W_o_aug^T over all T*B rows (XH slots 1..T, columns D..D+Ko).
   CUtensorMap hA, hB;
@@ -112,7 +113,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   if ((rc = map_kmajor(&hB, wo, s.Ko, s.A, s.Ko, 1, 0, 224))) return rc;
   tc::TileShape sh{(int)(s.T * B), (int)s.A, cdiv(s.Ko, tc::BK), 0, 0, 0, 0, 0, 16};
   tc::EpiStoreF32 epi{out, s.A, (int)(s.T * B), (int)s.A};
-  return launch<224, false, false>(hA, hA, hB, hB, sh, epi, st);
+  return launch<224, false, false>("heads_fwd", hA, hA, hB, hB, sh, epi, st);
 }
 
 // ---------------------------------------------------------------- backward (a6-a8)
@@ -123,7 +124,10 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   const __nv_bfloat16* wo = wxh + s.G4 * s.Kx;
   const __nv_bfloat16* dY = static_cast<const __nv_bfloat16*>(dout);
   int rc;
-  PPO_CUDA_CHECK(cudaMemsetAsync(P.dc, 0, B * s.H * sizeof(float), st));
+  {
+    ProfScope _prof("memset_dc", st);
+    PPO_CUDA_CHECK(cudaMemsetAsync(P.dc, 0, B * s.H * sizeof(float), st));
+  }
   // dh_t = dz_{t+1} W_h + dy_t W_o : A = [G (3-D, slot t+1) | dY (3-D, slot t)] (K-major),
   // B = [W_xh_aug[:, D:D+H] | W_o_aug[:, :H]] read MN-major (K = gate row / head output).
   CUtensorMap a0, a1, b0, b1;
@@ -137,7 +141,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
                      t + 1, t, 0, 0, 16};
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
                        (int)B, (int)s.H};
-    if ((rc = launch<256, false, true>(a0, a1, b0, b1, sh, epi, st))) return rc;
+    if ((rc = launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st))) return rc;
   }
   // weight gradients: dW_xh_aug = dZ^T [x | h_prev | 1 | 0] over all T*B rows (db falls out
   // of the ones column); dW_o_aug = dY^T [h | 1 | 0].
@@ -148,14 +152,14 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   {
     tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16};
     tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
-    if ((rc = launch<256, true, true>(wa, wa, wb, wb, sh, epi, st))) return rc;
+    if ((rc = launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st))) return rc;
   }
   if ((rc = map_mnmajor(&oa, dY, s.A, rows, s.A))) return rc;
   if ((rc = map_mnmajor(&ob, P.xh + B * s.Kx + s.D, s.Ko, rows, s.Kx))) return rc;
   {
     tc::TileShape sh{(int)s.A, (int)s.Ko, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16};
     tc::EpiStoreF32 epi{grad + s.G4 * s.Kx, s.Ko, (int)s.A, (int)s.Ko};
-    if ((rc = launch<256, true, true>(oa, oa, ob, ob, sh, epi, st))) return rc;
+    if ((rc = launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st))) return rc;
   }
   return PPO_OK;
 }
@@ -179,11 +183,11 @@ int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N
   tc::EpiStoreF32 epi{C, N, M, N};
   if (n224) {
     if (a_mn || b_mn) return fail(PPO_E_ARG, "BN=224 test only for K-major operands");
-    return launch<224, false, false>(ma, ma, mb, mb, sh, epi, st);
+    return launch<224, false, false>("test_gemm", ma, ma, mb, mb, sh, epi, st);
   }
-  if (!a_mn && !b_mn) return launch<256, false, false>(ma, ma, mb, mb, sh, epi, st);
-  if (!a_mn && b_mn) return launch<256, false, true>(ma, ma, mb, mb, sh, epi, st);
-  if (a_mn && b_mn) return launch<256, true, true>(ma, ma, mb, mb, sh, epi, st);
+  if (!a_mn && !b_mn) return launch<256, false, false>("test_gemm", ma, ma, mb, mb, sh, epi, st);
+  if (!a_mn && b_mn) return launch<256, false, true>("test_gemm", ma, ma, mb, mb, sh, epi, st);
+  if (a_mn && b_mn) return launch<256, true, true>("test_gemm", ma, ma, mb, mb, sh, epi, st);
   return fail(PPO_E_ARG, "unsupported test mode");
 }
 

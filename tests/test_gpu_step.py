@@ -63,11 +63,13 @@ def _check_step(case, cfg, precision, tol_fwd, tol_grad):
         d_ref = ref - old[k]
         d_got = new[k] - old[k]
         if precision == "fp32":
+            # Adam's first step is ~ -alpha/2 sign(g) (eps/sqrt(v) matters only for tiny |g|):
+            # compare where the gradient itself agrees to 1e-4 relative (>= 90% of entries)
             gerr = np.abs(g[k] - case["grads"][k])
-            firm = np.abs(case["grads"][k]) > 100 * gerr + 1e-7
-            assert firm.mean() > 0.95, (k, firm.mean())
+            firm = np.abs(case["grads"][k]) > 1e4 * gerr
+            assert firm.mean() > 0.9, (k, firm.mean())
             e = normwise(d_got[firm], d_ref[firm])
-            assert e < 1e-4, (k, e)
+            assert e < 1e-4, (k, e, firm.mean())
         else:
             # first Adam step ~ -alpha/2 sign(g): compare where the sign is resolved
             gerr = np.abs(g[k] - case["grads"][k])
