@@ -68,25 +68,44 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* _
 }
 
 // XH[t][b] = [x_t | h_{t-1} | 1 | 0...] for t = 0..T (x_T := 0), h_{-1} = h0; C[0] = c0.
+// One warp per XH row, 16-byte vectors.  The h part of slots t >= 1 is left untouched: the
+// forward epilogue of step t-1 writes it.  D, H multiples of 64 keep every segment 16B-aligned.
 template <class TA>
-__global__ void pack_x_kernel(Shape s, int64_t B, const TA* __restrict__ x,
-                              const float* __restrict__ h0, const float* __restrict__ c0,
-                              TA* __restrict__ xh, float* __restrict__ c) {
-  const int64_t total = (s.T + 1) * B * s.Kx;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = idx / s.Kx, col = idx - row * s.Kx;
+__global__ void __launch_bounds__(256) pack_x_kernel(Shape s, int64_t B, const TA* __restrict__ x,
+                                                     const float* __restrict__ h0,
+                                                     const float* __restrict__ c0,
+                                                     TA* __restrict__ xh, float* __restrict__ c) {
+  constexpr int V = 16 / sizeof(TA);  // elements per 16-byte vector
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (s.T + 1) * B;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows;
+       row += nwarps) {
     const int64_t t = row / B, b = row - t * B;
-    if (col < s.D) {
-      xh[idx] = t < s.T ? x[(t * B + b) * s.D + col] : from_f<TA>(0.f);
-    } else if (col < s.D + s.H) {
-      if (t == 0) {
-        xh[idx] = from_f<TA>(h0[b * s.H + (col - s.D)]);
-        c[b * s.H + (col - s.D)] = c0[b * s.H + (col - s.D)];
-      }
+    TA* dst = xh + row * s.Kx;
+    uint4* dv = reinterpret_cast<uint4*>(dst);
+    if (t < s.T) {
+      const uint4* src = reinterpret_cast<const uint4*>(x + (t * B + b) * s.D);
+      for (int i = lane; i < s.D / V; i += 32) dv[i] = __ldcs(src + i);
     } else {
-      xh[idx] = from_f<TA>(col == s.D + s.H ? 1.f : 0.f);
+      for (int i = lane; i < s.D / V; i += 32) dv[i] = make_uint4(0, 0, 0, 0);
     }
+    if (t == 0) {
+      const float4* hs = reinterpret_cast<const float4*>(h0 + b * s.H);
+      const float4* cs = reinterpret_cast<const float4*>(c0 + b * s.H);
+      float4* cd = reinterpret_cast<float4*>(c + b * s.H);
+      for (int i = lane; i < s.H / 4; i += 32) {
+        const float4 h = hs[i];
+        TA* o = dst + s.D + 4 * i;
+        o[0] = from_f<TA>(h.x);
+        o[1] = from_f<TA>(h.y);
+        o[2] = from_f<TA>(h.z);
+        o[3] = from_f<TA>(h.w);
+        cd[i] = cs[i];
+      }
+    }
+    // [1 | 0 ... 0]: 64 pad columns
+    for (int i = lane; i < 64; i += 32) dst[s.D + s.H + i] = from_f<TA>(i == 0 ? 1.f : 0.f);
   }
 }
 
@@ -502,7 +521,7 @@ int launch_cast_bf16(const float* src, void* dst, size_t n, cudaStream_t st) {
 int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, const float* c0,
                   void* xh, float* c, cudaStream_t st) {
   ProfScope _prof("pack_x", st);
-  const int64_t n = (s.T + 1) * B * s.Kx;
+  const int64_t n = (s.T + 1) * B * 32;  // one warp per XH row
   if (s.bf16)
     pack_x_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(
         s, B, (const __nv_bfloat16*)x, h0, c0, (__nv_bfloat16*)xh, c);
