@@ -245,12 +245,8 @@ def main():
     import synth
     from paper_1912_06680_b200 import PPOOptimizer, _lib as L
 
-    comm = None
-    if world > 1:
-        uid = L.comm_unique_id() if rank == 0 else bytes(L.PPO_COMM_ID_BYTES)
-        t = torch.tensor(list(uid), dtype=torch.uint8, device=device)
-        dist.broadcast(t, 0)
-        comm = L.comm_init(bytes(t.cpu().tolist()), rank, world)
+    from paper_1912_06680_b200 import dist as pdist
+    comm = pdist.make_comm(device)
 
     H, D, T, B = args.H, args.D, 16, args.B
     cfg = synth.Config(H=H, D=D, B=B, T=T)
@@ -296,11 +292,7 @@ def main():
     prof = L.prof_stop()
     barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+    ms = pdist.max_over_ranks(e0.elapsed_time(e1), device)
     ms_step = ms / args.steps
     seq_s = B * world / (ms_step / 1e3)
     value = seq_s / SEQ_PER_SAMPLE
@@ -360,11 +352,7 @@ def main():
             e2e_step()
         f1.record(stream)
         torch.cuda.synchronize()
-        ems = f0.elapsed_time(f1)
-        if world > 1:
-            t = torch.tensor([ems], device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = t.item()
+        ems = pdist.max_over_ranks(f0.elapsed_time(f1), device)
         e2e = {"value": B * world / (ems / args.steps / 1e3) / SEQ_PER_SAMPLE, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / args.steps}

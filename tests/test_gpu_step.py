@@ -122,3 +122,34 @@ def test_determinism_bf16():
     o1 = _run(case, cfg, "bf16")[0]
     o2 = _run(case, cfg, "bf16")[0]
     assert torch.equal(o1.grad, o2.grad) and torch.equal(o1.theta, o2.theta)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_dp_equivalence_shards(precision):
+    """the average of N per-GPU gradients (each with its local denominator, Q9) equals
+    the gradient of the concatenated batch.  The N ranks are emulated serially on one GPU
+    (nothing waits on another launch); the average is the test's own reference arithmetic."""
+    from paper_1912_06680_b200 import PPOOptimizer
+    cfg = synth.Config(H=128, D=256, B=64)
+    case = make_case(cfg, 11, pad_frac=0.2, wo_scale=20.0)
+    full = device_batch(case, precision == "bf16")
+    ref = PPOOptimizer(cfg.D, cfg.H, cfg.B, cfg.T, cfg.head_sizes, precision=precision)
+    load_params(ref, case["params"])
+    ref.step(full)
+    N = 4
+    Bs = cfg.B // N
+    Rs = case["ro"]["r"].shape[0] // N
+    acc = torch.zeros_like(ref.grad)
+    for n in range(N):
+        sl, rs = slice(n * Bs, (n + 1) * Bs), slice(n * Rs, (n + 1) * Rs)
+        shard = {k: (v[:, sl] if k in ("x", "act", "head_on", "avail", "valid", "logp_old")
+                     else v[sl] if k in ("h0", "c0") else v[rs]).contiguous()
+                 for k, v in full.items()}
+        o = PPOOptimizer(cfg.D, cfg.H, Bs, cfg.T, cfg.head_sizes, precision=precision)
+        load_params(o, case["params"])
+        o.step(shard)
+        acc += o.grad
+    acc /= N
+    torch.cuda.synchronize()
+    e = (torch.linalg.vector_norm(acc - ref.grad) / torch.linalg.vector_norm(ref.grad)).item()
+    assert e < 1e-5, e
