@@ -137,6 +137,51 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+
+// ---- CTA-pair (cta_group::2) helpers ----------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's smem, completion counted on the leader CTA's mbarrier (cluster address).
+__device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* map, uint32_t bar_cluster,
+                                                 void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive (when all prior MMAs of this thread complete) on the barrier at the same smem
+// offset in both CTAs of the pair.
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
 // ---------------------------------------------------------------- the kernel
 template <int BN, bool A_MN, bool B_MN, int STAGES>
 struct Smem {
@@ -304,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t taddr =
           tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
-      epi.template apply<BN>(mb, nb, row, taddr);
+      epi.template apply<BN>(mb * BM, nb * BN, row, taddr);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       acc ^= 1;
@@ -322,6 +367,191 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------- the CTA-pair kernel
+// 256 x 256 output tile per cluster of 2 CTAs (cta_group::2, UMMA M=256 N=256): CTA r loads
+// rows [128r, 128r+128) of the A tile and rows [128r, 128r+128) of the B tile (N-half), the
+// leader (rank 0) issues the MMAs for both, each CTA's TMEM holds its 128 accumulator rows.
+// Halves per-SM operand traffic; 32 KB stages allow a 6-deep pipeline.
+template <bool A_MN, bool B_MN, int STAGES>
+struct Smem2 {
+  static constexpr int A_BYTES = BM * BK * 2;   // this CTA's 128 rows of A
+  static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's 128 rows (N-half) of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+};
+
+template <bool A_MN, bool B_MN, int STAGES, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_gemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
+                    const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
+                    const TileShape sh, const Epi epi) {
+  constexpr int BN = 256;
+  constexpr int TM = 2 * BM;  // rows per cluster tile
+  using L = Smem2<A_MN, B_MN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+  const int num_m = (sh.M + TM - 1) / TM;
+  const int num_n = (sh.N + BN - 1) / BN;
+  const int ntiles = num_m * num_n;
+  const int nkb = sh.nkb0 + sh.nkb1;
+
+  if (threadIdx.x == 0) {
+    prefetch_map(&ta0);
+    prefetch_map(&tb0);
+    if (sh.nkb1 > 0) {
+      prefetch_map(&ta1);
+      prefetch_map(&tb1);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader: one arrive.expect_tx for both CTAs' bytes
+      mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer (both CTAs) =====================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, sh.group_m, mb, nb);
+        const int m_row = mb * TM + rank * BM;     // this CTA's A rows
+        const int n_row = nb * BN + rank * 128;    // this CTA's B rows (N-half)
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fbar = mapa_shared(smem_u32(&full[stage]), 0);
+          if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
+          const bool s1 = kb >= sh.nkb0;
+          const int kk = (s1 ? kb - sh.nkb0 : kb) * BK;
+          const CUtensorMap* ta = s1 ? &ta1 : &ta0;
+          const CUtensorMap* tb = s1 ? &tb1 : &tb0;
+          const int za = s1 ? sh.za1 : sh.za0;
+          const int zb = s1 ? sh.zb1 : sh.zb0;
+          uint8_t* a_dst = sA + stage * L::A_BYTES;
+          uint8_t* b_dst = sB + stage * L::B_BYTES;
+          if (!A_MN) {
+            tma_load_3d_pair(ta, fbar, a_dst, kk, m_row, za);
+          } else {
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+              tma_load_3d_pair(ta, fbar, a_dst + p * (BK * 128), m_row + p * 64, kk, za);
+          }
+          if (!B_MN) {
+            tma_load_3d_pair(tb, fbar, b_dst, kk, n_row, zb);
+          } else {
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+              tma_load_3d_pair(tb, fbar, b_dst + p * (BK * 128), n_row + p * 64, kk, zb);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ===================== MMA issuer (leader CTA, single thread) =====================
+      constexpr uint32_t idesc = idesc_bf16(TM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * L::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * L::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? sdesc(a0 + k * 2048, BK * 128, 1024)
+                                     : sdesc(a0 + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc(b0 + k * 2048, BK * 128, 1024)
+                                     : sdesc(b0 + k * 32, 16, 1024);
+            umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5 (both CTAs) =====================
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, sh.group_m, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr =
+          tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
+      epi.template apply<BN>(mb * TM + rank * BM, nb * BN, row, taddr);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
+                 : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- epilogues
 
 // Plain fp32 store: out[m*ldc + n] for m < M, n < N.
@@ -330,14 +560,14 @@ struct EpiStoreF32 {
   int64_t ldc;
   int M, N;
   template <int BN>
-  __device__ __forceinline__ void apply(int mb, int nb, int row, uint32_t taddr) const {
-    const int m = mb * BM + row;
+  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr) const {
+    const int m = m_base + row;
     const bool vec = (N % 4 == 0) && (ldc % 4 == 0);
 #pragma unroll 1
     for (int c = 0; c < BN / 16; ++c) {
       float v[16];
       tmem_ld16(taddr + c * 16, v);
-      const int n0 = nb * BN + c * 16;
+      const int n0 = n_base + c * 16;
       if (m >= M || n0 >= N) continue;
       float* dst = out + static_cast<int64_t>(m) * ldc + n0;
       if (vec && n0 + 16 <= N) {
@@ -408,9 +638,9 @@ struct EpiLstmFwd {
   __nv_bfloat16* gates;   // G[t]   [B][4H], interleaved like the accumulator columns
   int B, H;
   template <int BN>
-  __device__ __forceinline__ void apply(int mb, int nb, int row, uint32_t taddr) const {
+  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr) const {
     static_assert(BN == 256, "cell tile holds 4 gates x 64 units");
-    const int m = mb * BM + row;
+    const int m = m_base + row;
     const bool ok = m < B;
     const int64_t G4 = 4 * static_cast<int64_t>(H);
 #pragma unroll 1
@@ -421,7 +651,7 @@ struct EpiLstmFwd {
       tmem_ld16(taddr + 128 + u0, zg);
       tmem_ld16(taddr + 192 + u0, zo);
       if (!ok) continue;
-      const int j0 = nb * 64 + u0;
+      const int j0 = n_base / 4 + u0;
       float cp[16], c[16], h[16];
       load_f32x16(c_prev + static_cast<int64_t>(m) * H + j0, cp);
 #pragma unroll
@@ -435,7 +665,7 @@ struct EpiLstmFwd {
       }
       store_f32x16(c_out + static_cast<int64_t>(m) * H + j0, c);
       store_bf16x16(h_out + static_cast<int64_t>(m) * ldxh + j0, h);
-      __nv_bfloat16* gp = gates + static_cast<int64_t>(m) * G4 + nb * 256 + u0;
+      __nv_bfloat16* gp = gates + static_cast<int64_t>(m) * G4 + n_base + u0;
       store_bf16x16(gp + 0, zi);
       store_bf16x16(gp + 64, zf);
       store_bf16x16(gp + 128, zg);
@@ -453,15 +683,15 @@ struct EpiLstmBwd {
   float* dc;              // [B][H] carry (in/out)
   int B, H;
   template <int BN>
-  __device__ __forceinline__ void apply(int mb, int nb, int row, uint32_t taddr) const {
-    const int m = mb * BM + row;
+  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr) const {
+    const int m = m_base + row;
     const bool ok = m < B;
     const int64_t G4 = 4 * static_cast<int64_t>(H);
 #pragma unroll 1
     for (int cc = 0; cc < BN / 16; ++cc) {
       float dh[16];
       tmem_ld16(taddr + cc * 16, dh);
-      const int j0 = nb * BN + cc * 16;
+      const int j0 = n_base + cc * 16;
       if (!ok || j0 >= H) continue;
       const int q = j0 >> 6, u0 = j0 & 63;
       __nv_bfloat16* gp = gz + static_cast<int64_t>(m) * G4 + q * 256 + u0;

@@ -74,6 +74,28 @@ int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const 
   return PPO_OK;
 }
 
+// CTA-pair launch: 256x256 tiles, grid = 2 x clusters (one CTA per SM, persistent).
+template <bool A_MN, bool B_MN, class Epi>
+int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
+            const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
+  constexpr int STAGES = 6;
+  using L = tc::Smem2<A_MN, B_MN, STAGES>;
+  auto kern = tc::tc_gemm2_kernel<A_MN, B_MN, STAGES, Epi>;
+  static bool configured = false;
+  if (!configured) {
+    PPO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
+  const int64_t ntiles = (int64_t)((sh.M + 255) / 256) * ((sh.N + 255) / 256);
+  const int clusters = (int)std::min<int64_t>(ntiles, num_sms() / 2);
+  if (clusters <= 0) return PPO_OK;
+  ProfScope _prof(tag, st);
+  kern<<<2 * clusters, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, sh, epi);
+  PPO_LAUNCH_CHECK("tc_gemm2_kernel");
+  return PPO_OK;
+}
+
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 struct WsPtrs {
@@ -100,12 +122,12 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   // z_t = [x_t | h_{t-1} | 1] W_xh_aug^T : A = XH (3-D, slot t), B = W_xh_aug.
   CUtensorMap mA, mB;
   if ((rc = map_kmajor(&mA, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, tc::BM))) return rc;
-  if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
+  if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 128))) return rc;
   for (int t = 0; t < s.T; ++t) {
-    tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 16};
+    tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8};
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
-    if ((rc = launch<256, false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st))) return rc;
+    if ((rc = launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st))) return rc;
   }
   // heads: y = [h_t | 1] W_o_aug^T over all T*B rows (XH slots 1..T, columns D..D+Ko).
   CUtensorMap hA, hB;
@@ -138,10 +160,10 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   for (int t = (int)s.T - 1; t >= 0; --t) {
     const bool last = t == s.T - 1;
     tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A, tc::BK),
-                     t + 1, t, 0, 0, 16};
+                     t + 1, t, 0, 0, 8};
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
                        (int)B, (int)s.H};
-    if ((rc = launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st))) return rc;
+    if ((rc = launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st))) return rc;
   }
   // weight gradients: dW_xh_aug = dZ^T [x | h_prev | 1 | 0] over all T*B rows (db falls out
   // of the ones column); dW_o_aug = dY^T [h | 1 | 0].
@@ -150,9 +172,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&wa, P.g, s.G4, rows, s.G4))) return rc;
   if ((rc = map_mnmajor(&wb, P.xh, s.Kx, rows, s.Kx))) return rc;
   {
-    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16};
+    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8};
     tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
-    if ((rc = launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st))) return rc;
+    if ((rc = launch2<true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st))) return rc;
   }
   if ((rc = map_mnmajor(&oa, dY, s.A, rows, s.A))) return rc;
   if ((rc = map_mnmajor(&ob, P.xh + B * s.Kx + s.D, s.Ko, rows, s.Kx))) return rc;
@@ -169,7 +191,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
 // mode bit2: BN = 224 (only with K-major A and B).  C [M][N] fp32.
 int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N, int K,
                  cudaStream_t st) {
-  const bool b_mn = mode & 1, a_mn = mode & 2, n224 = mode & 4;
+  const bool b_mn = mode & 1, a_mn = mode & 2, n224 = mode & 4, pair = mode & 8;
   CUtensorMap ma, mb;
   int rc;
   const int BN = n224 ? 224 : 256;
@@ -177,10 +199,16 @@ int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N
   else rc = map_kmajor(&ma, A, K, M, K, 1, 0, tc::BM);
   if (rc) return rc;
   if (b_mn) rc = map_mnmajor(&mb, Bm, N, K, N);
-  else rc = map_kmajor(&mb, Bm, K, N, K, 1, 0, BN);
+  else rc = map_kmajor(&mb, Bm, K, N, K, 1, 0, pair ? 128 : BN);
   if (rc) return rc;
   tc::TileShape sh{M, N, cdiv(K, tc::BK), 0, 0, 0, 0, 0, 16};
   tc::EpiStoreF32 epi{C, N, M, N};
+  if (pair) {
+    if (!a_mn && !b_mn) return launch2<false, false>("test_gemm2", ma, ma, mb, mb, sh, epi, st);
+    if (!a_mn && b_mn) return launch2<false, true>("test_gemm2", ma, ma, mb, mb, sh, epi, st);
+    if (a_mn && b_mn) return launch2<true, true>("test_gemm2", ma, ma, mb, mb, sh, epi, st);
+    return fail(PPO_E_ARG, "unsupported test mode");
+  }
   if (n224) {
     if (a_mn || b_mn) return fail(PPO_E_ARG, "BN=224 test only for K-major operands");
     return launch<224, false, false>("test_gemm", ma, ma, mb, mb, sh, epi, st);

@@ -26,10 +26,14 @@ def L():
     (1, 256, 512, 192), (1, 77, 264, 1000),
     (3, 384, 768, 448), (3, 136, 320, 72),
     (4, 300, 656, 4160), (4, 33, 100, 64),
+    # CTA-pair (cta_group::2) kernel, 256x256 tiles
+    (8, 256, 256, 64), (8, 300, 520, 200), (8, 1000, 2048, 1024),
+    (9, 512, 512, 192), (9, 77, 264, 1000),
+    (11, 384, 768, 448), (11, 136, 320, 72), (11, 2048, 1024, 4096),
 ])
 def test_tc_gemm_vs_torch(L, mode, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
-    a_mn, b_mn = bool(mode & 2), bool(mode & 1)
+    a_mn, b_mn = bool(mode & 2), bool(mode & 1)  # bit2: N=224 tile, bit3: CTA pair
     A = torch.randn((K, M) if a_mn else (M, K), generator=g, device="cuda").bfloat16()
     B = torch.randn((K, N) if b_mn else (N, K), generator=g, device="cuda").bfloat16()
     C = torch.full((M, N), float("nan"), device="cuda")
