@@ -98,6 +98,13 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
 
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// Kernel-variant knob for A/B measurements: PPO_TC_PAIR=0 selects the single-CTA 128x256
+// kernel for the recurrent and dW_xh GEMMs (default: CTA pair).  Both are tcgen05 paths.
+bool use_pair() {
+  const char* e = getenv("PPO_TC_PAIR");
+  return !e || atoi(e) != 0;
+}
+
 struct WsPtrs {
   __nv_bfloat16* xh;
   __nv_bfloat16* g;
@@ -122,12 +129,19 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   // z_t = [x_t | h_{t-1} | 1] W_xh_aug^T : A = XH (3-D, slot t), B = W_xh_aug.
   CUtensorMap mA, mB;
   if ((rc = map_kmajor(&mA, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, tc::BM))) return rc;
+  const bool pair = use_pair();
+  CUtensorMap mB1;
   if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 128))) return rc;
+  if ((rc = map_kmajor(&mB1, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
   for (int t = 0; t < s.T; ++t) {
     tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8};
+    tc::TileShape sh1 = sh;
+    sh1.group_m = 16;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
-    if ((rc = launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st))) return rc;
+    rc = pair ? launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st)
+              : launch<256, false, false>("lstm_fwd_step", mA, mA, mB1, mB1, sh1, epi, st);
+    if (rc) return rc;
   }
   // heads: y = [h_t | 1] W_o_aug^T over all T*B rows (XH slots 1..T, columns D..D+Ko).
   CUtensorMap hA, hB;
@@ -153,6 +167,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   // dh_t = dz_{t+1} W_h + dy_t W_o : A = [G (3-D, slot t+1) | dY (3-D, slot t)] (K-major),
   // B = [W_xh_aug[:, D:D+H] | W_o_aug[:, :H]] read MN-major (K = gate row / head output).
   CUtensorMap a0, a1, b0, b1;
+  const bool pair = use_pair();
   if ((rc = map_kmajor(&a0, P.g, s.G4, B, s.G4, s.T, B * s.G4, tc::BM))) return rc;
   if ((rc = map_kmajor(&a1, dY, s.A, B, s.A, s.T, B * s.A, tc::BM))) return rc;
   if ((rc = map_mnmajor(&b0, wxh + s.D, s.H, s.G4, s.Kx))) return rc;
@@ -163,7 +178,11 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
                      t + 1, t, 0, 0, 8};
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
                        (int)B, (int)s.H};
-    if ((rc = launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st))) return rc;
+    tc::TileShape sh1 = sh;
+    sh1.group_m = 16;
+    rc = pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
+              : launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh1, epi, st);
+    if (rc) return rc;
   }
   // weight gradients: dW_xh_aug = dZ^T [x | h_prev | 1 | 0] over all T*B rows (db falls out
   // of the ones column); dW_o_aug = dY^T [h | 1 | 0].
@@ -174,7 +193,11 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   {
     tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8};
     tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
-    if ((rc = launch2<true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st))) return rc;
+    tc::TileShape sh1 = sh;
+    sh1.group_m = 16;
+    rc = pair ? launch2<true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
+              : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh1, epi, st);
+    if (rc) return rc;
   }
   if ((rc = map_mnmajor(&oa, dY, s.A, rows, s.A))) return rc;
   if ((rc = map_mnmajor(&ob, P.xh + B * s.Kx + s.D, s.Ko, rows, s.Kx))) return rc;
