@@ -138,6 +138,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 
 
+// One lane of a converged warp (the lowest active one: always the same lane, so tcgen05.commit
+// tracks the MMAs that lane issued).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "+r"(pred));
+  return pred != 0;
+}
+
 // ---- CTA-pair (cta_group::2) helpers ----------------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -299,42 +311,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===================== MMA issuer (single thread) =====================
-      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // ===================== MMA issuer: the warp waits, one elected lane issues ===========
+    // Descriptors are built once for stage 0 and advanced by adding to the 14-bit start
+    // address field (stage: bytes>>4; UMMA_K step: 32 B K-major, 16 rows x 128 B MN-major).
+    constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+    const uint64_t a_desc0 = A_MN ? sdesc(smem_u32(sA), BK * 128, 1024) : sdesc(smem_u32(sA), 16, 1024);
+    const uint64_t b_desc0 = B_MN ? sdesc(smem_u32(sB), BK * 128, 1024) : sdesc(smem_u32(sB), 16, 1024);
+    constexpr uint64_t a_k = A_MN ? (2048 >> 4) : (32 >> 4);
+    constexpr uint64_t b_k = B_MN ? (2048 >> 4) : (32 >> 4);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * L::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * L::B_BYTES);
+        const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (L::A_BYTES >> 4));
+        const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (L::B_BYTES >> 4));
+        if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: +32 B per 16 elements inside the 128 B swizzle row.
-            // MN-major: +16 K-rows of 128 B.  LBO (MN-major) = stride between 64-wide panels.
-            const uint64_t ad = A_MN ? sdesc(a0 + k * 2048, BK * 128, 1024)
-                                     : sdesc(a0 + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sdesc(b0 + k * 2048, BK * 128, 1024)
-                                     : sdesc(b0 + k * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d_tmem, ad + k * a_k, bd + k * b_k, idesc, (kb | k) != 0 ? 1u : 0u);
           umma_commit(&empty[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        umma_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
   } else {
     // ===================== epilogue warps 2..5 =====================
@@ -484,9 +497,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
-      // ===================== MMA issuer (leader CTA, single thread) =====================
+    if (leader) {
+      // ===================== MMA issuer (leader): the warp waits, one lane issues ==========
       constexpr uint32_t idesc = idesc_bf16(TM, BN, A_MN, B_MN);
+      const uint64_t a_desc0 = A_MN ? sdesc(smem_u32(sA), BK * 128, 1024) : sdesc(smem_u32(sA), 16, 1024);
+      const uint64_t b_desc0 = B_MN ? sdesc(smem_u32(sB), BK * 128, 1024) : sdesc(smem_u32(sB), 16, 1024);
+      constexpr uint64_t a_k = A_MN ? (2048 >> 4) : (32 >> 4);
+      constexpr uint64_t b_k = B_MN ? (2048 >> 4) : (32 >> 4);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -498,23 +515,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * L::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * L::B_BYTES);
+          const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (L::A_BYTES >> 4));
+          const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (L::B_BYTES >> 4));
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? sdesc(a0 + k * 2048, BK * 128, 1024)
-                                     : sdesc(a0 + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sdesc(b0 + k * 2048, BK * 128, 1024)
-                                     : sdesc(b0 + k * 32, 16, 1024);
-            umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_pair(d_tmem, ad + k * a_k, bd + k * b_k, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_commit_pair(&empty[stage]);
           }
-          umma_commit_pair(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(&tfull[acc]);
+        if (elect_one()) umma_commit_pair(&tfull[acc]);
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
