@@ -24,7 +24,8 @@ struct TileShape {
   int nkb0, nkb1;    // k-blocks taken from source 0 / source 1
   int za0, za1;      // 3rd TMA coordinate (time slot) for A sources
   int zb0, zb1;      // ... for B sources
-  int group_m;       // rasterisation: m-tiles per group
+  int group;         // rasterisation: tiles per group along the grouped dimension
+  int group_n;       // 0: groups of `group` m-tiles sweep all n; 1: groups of n-tiles sweep m
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -204,15 +205,28 @@ struct Smem {
   static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
 };
 
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group_m,
-                                            int& mb, int& nb) {
-  int per_group = group_m * num_n;
-  int g = tile / per_group;
-  int first_m = g * group_m;
-  int gsz = min(group_m, num_m - first_m);
-  int local = tile - g * per_group;
-  mb = first_m + local % gsz;
-  nb = local / gsz;
+// Grouped rasterisation: consecutive tiles (which run concurrently) share a group of
+// `group` m-tiles (group_n = 0) or n-tiles (group_n = 1) and sweep the other dimension, so
+// the group's operand panels stay in L2 while the other operand streams through once.
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group,
+                                            int group_n, int& mb, int& nb) {
+  if (group_n) {
+    const int per_group = group * num_m;
+    const int g = tile / per_group;
+    const int first_n = g * group;
+    const int gsz = min(group, num_n - first_n);
+    const int local = tile - g * per_group;
+    nb = first_n + local % gsz;
+    mb = local / gsz;
+  } else {
+    const int per_group = group * num_n;
+    const int g = tile / per_group;
+    const int first_m = g * group;
+    const int gsz = min(group, num_m - first_m);
+    const int local = tile - g * per_group;
+    mb = first_m + local % gsz;
+    nb = local / gsz;
+  }
 }
 
 template <int BN, bool A_MN, bool B_MN, int STAGES, class Epi>
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, sh.group_m, mb, nb);
+        tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], L::STAGE_BYTES);
@@ -357,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       int mb, nb;
-      tile_coords(tile, num_m, num_n, sh.group_m, mb, nb);
+      tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr =
@@ -460,7 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, sh.group_m, mb, nb);
+        tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
         const int m_row = mb * TM + rank * BM;     // this CTA's A rows
         const int n_row = nb * BN + rank * 128;    // this CTA's B rows (N-half)
         for (int kb = 0; kb < nkb; ++kb) {
@@ -544,7 +558,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
       int mb, nb;
-      tile_coords(tile, num_m, num_n, sh.group_m, mb, nb);
+      tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr =

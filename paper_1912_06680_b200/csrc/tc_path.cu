@@ -98,6 +98,19 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
 
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// Raster override for experiments: PPO_RASTER_<KIND>=m<g> or n<g> (e.g. n16).
+void raster(tc::TileShape& sh, const char* kind, int def_group, int def_n) {
+  sh.group = def_group;
+  sh.group_n = def_n;
+  char name[64];
+  snprintf(name, sizeof(name), "PPO_RASTER_%s", kind);
+  const char* e = getenv(name);
+  if (e && (e[0] == 'm' || e[0] == 'n') && atoi(e + 1) > 0) {
+    sh.group_n = e[0] == 'n';
+    sh.group = atoi(e + 1);
+  }
+}
+
 // Kernel-variant knob for A/B measurements: PPO_TC_PAIR=0 selects the single-CTA 128x256
 // kernel for the recurrent and dW_xh GEMMs (default: CTA pair).  Both are tcgen05 paths.
 bool use_pair() {
@@ -134,9 +147,9 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 128))) return rc;
   if ((rc = map_kmajor(&mB1, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
   for (int t = 0; t < s.T; ++t) {
-    tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8};
+    tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 16, 1};
+    raster(sh, "FWD", 16, 1);
     tc::TileShape sh1 = sh;
-    sh1.group_m = 16;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
     rc = pair ? launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st)
@@ -147,7 +160,8 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   CUtensorMap hA, hB;
   if ((rc = map_kmajor(&hA, P.xh + B * s.Kx + s.D, s.Ko, s.T * B, s.Kx, 1, 0, tc::BM))) return rc;
   if ((rc = map_kmajor(&hB, wo, s.Ko, s.A, s.Ko, 1, 0, 224))) return rc;
-  tc::TileShape sh{(int)(s.T * B), (int)s.A, cdiv(s.Ko, tc::BK), 0, 0, 0, 0, 0, 16};
+  tc::TileShape sh{(int)(s.T * B), (int)s.A, cdiv(s.Ko, tc::BK), 0, 0, 0, 0, 0, 16, 0};
+  raster(sh, "HEADS", 16, 0);
   tc::EpiStoreF32 epi{out, s.A, (int)(s.T * B), (int)s.A};
   return launch<224, false, false>("heads_fwd", hA, hA, hB, hB, sh, epi, st);
 }
@@ -175,11 +189,11 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   for (int t = (int)s.T - 1; t >= 0; --t) {
     const bool last = t == s.T - 1;
     tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A, tc::BK),
-                     t + 1, t, 0, 0, 8};
+                     t + 1, t, 0, 0, 8, 1};
+    raster(sh, "BWD", 8, 1);
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
                        (int)B, (int)s.H};
     tc::TileShape sh1 = sh;
-    sh1.group_m = 16;
     rc = pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
               : launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh1, epi, st);
     if (rc) return rc;
@@ -191,10 +205,11 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&wa, P.g, s.G4, rows, s.G4))) return rc;
   if ((rc = map_mnmajor(&wb, P.xh, s.Kx, rows, s.Kx))) return rc;
   {
-    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8};
+    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8, 0};
+    raster(sh, "WGRAD", 8, 0);
     tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
     tc::TileShape sh1 = sh;
-    sh1.group_m = 16;
+    if (!getenv("PPO_RASTER_WGRAD")) sh1.group = 16;
     rc = pair ? launch2<true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
               : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh1, epi, st);
     if (rc) return rc;
@@ -202,7 +217,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&oa, dY, s.A, rows, s.A))) return rc;
   if ((rc = map_mnmajor(&ob, P.xh + B * s.Kx + s.D, s.Ko, rows, s.Kx))) return rc;
   {
-    tc::TileShape sh{(int)s.A, (int)s.Ko, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16};
+    tc::TileShape sh{(int)s.A, (int)s.Ko, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16, 0};
     tc::EpiStoreF32 epi{grad + s.G4 * s.Kx, s.Ko, (int)s.A, (int)s.Ko};
     if ((rc = launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st))) return rc;
   }
@@ -224,7 +239,8 @@ int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N
   if (b_mn) rc = map_mnmajor(&mb, Bm, N, K, N);
   else rc = map_kmajor(&mb, Bm, K, N, K, 1, 0, pair ? 128 : BN);
   if (rc) return rc;
-  tc::TileShape sh{M, N, cdiv(K, tc::BK), 0, 0, 0, 0, 0, 16};
+  tc::TileShape sh{M, N, cdiv(K, tc::BK), 0, 0, 0, 0, 0, 16, 0};
+  raster(sh, "TEST", 16, 0);
   tc::EpiStoreF32 epi{C, N, M, N};
   if (pair) {
     if (!a_mn && !b_mn) return launch2<false, false>("test_gemm2", ma, ma, mb, mb, sh, epi, st);

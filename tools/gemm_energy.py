@@ -74,8 +74,34 @@ def run(name, M, N, K, a_mn, b_mn):
     torch.cuda.empty_cache()
 
 
+SHAPES = {"square": (8192, 8192, 8192, False, False), "fwd": (38400, 16384, 8192, False, False),
+          "wgrad": (16384, 8192, 76800, True, True), "bwd": (38400, 4096, 16384, False, True)}
+
+
+def sweep(name, rasters, seconds=2.0):
+    """tcgen05 variants x rasterisations (PPO_RASTER_TEST) on one shape, plus cuBLAS"""
+    M, N, K, a_mn, b_mn = SHAPES[name]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    A = torch.randn((K, M) if a_mn else (M, K), generator=g, device="cuda").bfloat16()
+    B = torch.randn((K, N) if b_mn else (N, K), generator=g, device="cuda").bfloat16()
+    C = torch.empty((M, N), device="cuda")
+    flop = 2.0 * M * N * K
+    mode = (1 if b_mn else 0) | (2 if a_mn else 0)
+    Am = A.t() if a_mn else A
+    Bm = B if b_mn else B.t()
+    rows = [("cublas", "-", measure(lambda: torch.mm(Am, Bm), flop, seconds))]
+    for r in rasters:
+        os.environ["PPO_RASTER_TEST"] = r
+        rows.append(("tc_1cta", r, measure(lambda: L.test_tc_gemm(mode, A, B, C, M, N, K), flop, seconds)))
+        rows.append(("tc_pair", r, measure(lambda: L.test_tc_gemm(mode | 8, A, B, C, M, N, K), flop, seconds)))
+    for k, r, v in rows:
+        print(f"{name:7s} {k:8s} {r:4s} {v['tflops']:7.1f} TF/s  {v['watts']:6.0f} W  "
+              f"{v['tflop_per_j']:5.3f} TFLOP/J  sm {v['mhz']:5.0f} MHz  {v['ms']:8.3f} ms", flush=True)
+    del A, B, C
+    torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
-    run("square", 8192, 8192, 8192, False, False)
-    run("fwd", 38400, 16384, 8192, False, False)
-    run("wgrad", 16384, 8192, 76800, True, True)
-    run("bwd", 38400, 4096, 16384, False, True)
+    which = sys.argv[1:] or ["fwd"]
+    for nm in which:
+        sweep(nm, ["m8", "m16", "n8", "n16", "n32"])
