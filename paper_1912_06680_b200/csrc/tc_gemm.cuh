@@ -18,6 +18,10 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;             // one 128-byte swizzle row of bf16
 constexpr int kThreads = 192;
+#ifndef PPO_SUSPEND_HINT_NS
+#define PPO_SUSPEND_HINT_NS 1000000
+#endif
+constexpr uint32_t kSuspendHintNs = PPO_SUSPEND_HINT_NS;
 
 struct TileShape {
   int M, N;          // logical output extent (tiles beyond are masked by the epilogue)
@@ -48,8 +52,10 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// Wait for the phase with the given parity.  Watchdog: a wait longer than 20 s traps (a
-// pipeline bug then surfaces as a launch error instead of a hung GPU).
+// Wait for the phase with the given parity.  try_wait carries a suspend-time hint so a
+// waiting warp sleeps in hardware instead of re-issuing polls (energy: the step is
+// power-capped).  Watchdog: a wait longer than 20 s traps (a pipeline bug then surfaces as a
+// launch error instead of a hung GPU).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   uint32_t done;
@@ -58,12 +64,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(kSuspendHintNs)
         : "memory");
-    if (!done && ((++spins & 0xFFFu) == 0)) {
+    if (!done && ((++spins & 0xFFu) == 0)) {
       const uint64_t now = globaltimer_ns();
       if (t0 == 0) t0 = now;
       else if (now - t0 > 20000000000ull) asm volatile("trap;");

@@ -104,4 +104,4 @@ def sweep(name, rasters, seconds=2.0):
 if __name__ == "__main__":
     which = sys.argv[1:] or ["fwd"]
     for nm in which:
-        sweep(nm, ["m8", "m16", "n8", "n16", "n32"])
+        sweep(nm, os.environ.get("RASTERS", "m8,m16,n8,n16,n32").split(","))
