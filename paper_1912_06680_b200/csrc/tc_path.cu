@@ -111,11 +111,15 @@ void raster(tc::TileShape& sh, const char* kind, int def_group, int def_n) {
   }
 }
 
-// Kernel-variant knob for A/B measurements: PPO_TC_PAIR=0 selects the single-CTA 128x256
-// kernel for the recurrent and dW_xh GEMMs (default: CTA pair).  Both are tcgen05 paths.
-bool use_pair() {
-  const char* e = getenv("PPO_TC_PAIR");
-  return !e || atoi(e) != 0;
+// Kernel variant per GEMM kind (both are tcgen05 paths): CTA pair (256x256, cta_group::2)
+// or single CTA (128x256).  Defaults from the energy sweeps (tools/gemm_energy.py; the step
+// is power-capped, so TFLOP/J decides); PPO_VARIANT_<KIND>=pair|1cta overrides.
+bool use_pair(const char* kind, bool def) {
+  char name[64];
+  snprintf(name, sizeof(name), "PPO_VARIANT_%s", kind);
+  const char* e = getenv(name);
+  if (!e) return def;
+  return strcmp(e, "pair") == 0;
 }
 
 struct WsPtrs {
@@ -142,13 +146,13 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   // z_t = [x_t | h_{t-1} | 1] W_xh_aug^T : A = XH (3-D, slot t), B = W_xh_aug.
   CUtensorMap mA, mB;
   if ((rc = map_kmajor(&mA, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, tc::BM))) return rc;
-  const bool pair = use_pair();
+  const bool pair = use_pair("FWD", true);
   CUtensorMap mB1;
   if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 128))) return rc;
   if ((rc = map_kmajor(&mB1, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
   for (int t = 0; t < s.T; ++t) {
-    tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 16, 1};
-    raster(sh, "FWD", 16, 1);
+    tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8, 1};
+    raster(sh, "FWD", 8, 1);
     tc::TileShape sh1 = sh;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
@@ -181,7 +185,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   // dh_t = dz_{t+1} W_h + dy_t W_o : A = [G (3-D, slot t+1) | dY (3-D, slot t)] (K-major),
   // B = [W_xh_aug[:, D:D+H] | W_o_aug[:, :H]] read MN-major (K = gate row / head output).
   CUtensorMap a0, a1, b0, b1;
-  const bool pair = use_pair();
+  const bool pair = use_pair("BWD", false);
   if ((rc = map_kmajor(&a0, P.g, s.G4, B, s.G4, s.T, B * s.G4, tc::BM))) return rc;
   if ((rc = map_kmajor(&a1, dY, s.A, B, s.A, s.T, B * s.A, tc::BM))) return rc;
   if ((rc = map_mnmajor(&b0, wxh + s.D, s.H, s.G4, s.Kx))) return rc;
@@ -205,11 +209,11 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&wa, P.g, s.G4, rows, s.G4))) return rc;
   if ((rc = map_mnmajor(&wb, P.xh, s.Kx, rows, s.Kx))) return rc;
   {
-    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8, 0};
-    raster(sh, "WGRAD", 8, 0);
+    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8, 1};
+    raster(sh, "WGRAD", 8, 1);
     tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
     tc::TileShape sh1 = sh;
-    if (!getenv("PPO_RASTER_WGRAD")) sh1.group = 16;
+    const bool pair = use_pair("WGRAD", false);
     rc = pair ? launch2<true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
               : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh1, epi, st);
     if (rc) return rc;
