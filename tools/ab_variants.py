@@ -10,6 +10,7 @@ import sys
 import threading
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import pynvml  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
@@ -36,6 +37,10 @@ opt.step(batch)
 torch.cuda.synchronize()
 
 
+pynvml.nvmlInit()
+_nv = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+
+
 def smi():
     q = "clocks.sm,power.draw"
     proc = subprocess.Popen(["nvidia-smi", "-i", "0", f"--query-gpu={q}",
@@ -58,12 +63,14 @@ for r in range(a.rounds):
         torch.cuda.synchronize()
         proc, lines = smi()
         L.prof_start()
+        j0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(_nv)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(a.steps):
             opt.step(batch)
         e1.record()
         torch.cuda.synchronize()
+        j1 = pynvml.nvmlDeviceGetTotalEnergyConsumption(_nv)
         prof = L.prof_stop()
         proc.terminate()
         vals = []
@@ -77,5 +84,5 @@ for r in range(a.rounds):
         ms = e0.elapsed_time(e1) / a.steps
         ks = " ".join(f"{k}={prof[k][1] / a.steps:.1f}"
                       for k in ("lstm_fwd_step", "lstm_bwd_step", "wgrad_xh") if k in prof)
-        print(f"round {r} {a.var}={v}: step {ms:.1f} ms  sm_mhz~{med(clk):.0f} "
-              f"power~{med(pw):.0f}W  {ks}", flush=True)
+        print(f"round {r} {a.var}={v}: step {ms:.1f} ms  {(j1 - j0) / 1e3 / a.steps:.1f} J/step  "
+              f"sm_mhz~{med(clk):.0f} power~{med(pw):.0f}W  {ks}", flush=True)
