@@ -122,6 +122,8 @@ WsLayout ws_layout(const Shape& s, int64_t B) {
   off = align_up(off + (size_t)B * s.H * 4, 1024);
   L.raw = off;
   if (!s.bf16) off = align_up(off + (size_t)B * s.G4 * 4, 1024);
+  L.splitk = off;  // split-K partials of dW_o (bf16 path)
+  if (s.bf16) off = align_up(off + (size_t)kMaxSplitK * s.A * s.Ko * 4, 1024);
   L.total = off;
   return L;
 }

@@ -51,8 +51,9 @@ struct Shape {
 int check_dims(const ppo_dims* d, Shape* s);
 
 // Workspace regions (byte offsets from ws base); esz = activation element size.
+constexpr int kMaxSplitK = 16;
 struct WsLayout {
-  size_t xh, g, c, dc, raw, total;
+  size_t xh, g, c, dc, raw, splitk, total;
 };
 WsLayout ws_layout(const Shape& s, int64_t B);
 

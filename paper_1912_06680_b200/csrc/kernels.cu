@@ -213,7 +213,12 @@ __global__ void __launch_bounds__(256) loss_kernel(
   uint32_t flags = 0;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.N; row += (int64_t)gridDim.x * 8) {
     const float* yr = out + row * A;
-    for (int j = lane; j < A; j += 32) y[j] = yr[j];
+    if ((A & 3) == 0) {
+      const float4* y4 = reinterpret_cast<const float4*>(yr);
+      for (int j = lane; j < A / 4; j += 32) reinterpret_cast<float4*>(y)[j] = __ldcs(y4 + j);
+    } else {
+      for (int j = lane; j < A; j += 32) y[j] = __ldcs(yr + j);
+    }
     const uint8_t* av = avail + row * n0;
     const uint32_t m_lo = __ballot_sync(0xffffffffu, lane < n0 && av[lane] != 0);
     const uint32_t m_hi = __ballot_sync(0xffffffffu, lane + 32 < n0 && av[min(lane + 32, n0 - 1)] != 0);
@@ -228,20 +233,20 @@ __global__ void __launch_bounds__(256) loss_kernel(
       for (int j = s0 + lane; j < e0; j += 32)
         if (k != 0 || ((amask >> (j - s0)) & 1ull)) mx = fmaxf(mx, y[j]);
       mx = warp_max(mx);
-      float se = 0.f;
-      if (mx != -INFINITY)
-        for (int j = s0 + lane; j < e0; j += 32)
-          if (k != 0 || ((amask >> (j - s0)) & 1ull)) se += expf(y[j] - mx);
-      se = warp_sum(se);
-      const float l = mx == -INFINITY ? 0.f : mx + logf(se);
-      float pl = 0.f;
+      // one exp per element: sum e and sum e*y give lse and the entropy
+      // H = -sum p log p = lse - sum p y  (p = e / se, log p = y - lse)
+      float se = 0.f, sey = 0.f;
       if (mx != -INFINITY)
         for (int j = s0 + lane; j < e0; j += 32)
           if (k != 0 || ((amask >> (j - s0)) & 1ull)) {
-            const float lp = y[j] - l;
-            pl += expf(lp) * lp;
+            const float e = expf(y[j] - mx);
+            se += e;
+            sey = fmaf(e, y[j], sey);
           }
-      pl = warp_sum(pl);
+      se = warp_sum(se);
+      sey = warp_sum(sey);
+      const float l = mx == -INFINITY ? 0.f : mx + logf(se);
+      const float pl = mx == -INFINITY ? 0.f : sey / se - l;  // sum p log p
       lse[k] = l;
       Hk[k] = -pl;
       const int a = act[row * nh + k];
@@ -489,6 +494,23 @@ __global__ void simt_cell_bwd_kernel(Shape s, int64_t B, const float* __restrict
   }
 }
 
+// ============================================================================ split-K reduce
+__global__ void splitk_reduce_kernel(const float4* __restrict__ part, int nsplit, size_t n4,
+                                     float4* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float4 a = part[i];
+    for (int sidx = 1; sidx < nsplit; ++sidx) {
+      const float4 b = part[sidx * n4 + i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    out[i] = a;
+  }
+}
+
 // ============================================================================ launchers
 static int grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;
@@ -564,6 +586,13 @@ int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t 
   ProfScope _prof("adam", st);
   adam_kernel<<<grid_for((int64_t)(n / 4 + 1)), 256, 0, st>>>(p, (__nv_bfloat16*)p16, g, m, v, n, ap);
   PPO_LAUNCH_CHECK("adam_kernel");
+  return PPO_OK;
+}
+int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cudaStream_t st) {
+  ProfScope _prof("splitk_reduce", st);
+  splitk_reduce_kernel<<<grid_for((int64_t)(n / 4)), 256, 0, st>>>(
+      reinterpret_cast<const float4*>(part), nsplit, n / 4, reinterpret_cast<float4*>(out));
+  PPO_LAUNCH_CHECK("splitk_reduce_kernel");
   return PPO_OK;
 }
 int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int64_t K, float* C,

@@ -47,6 +47,9 @@ int launch_simt_cell_fwd(const Shape& s, int64_t B, const float* z, const float*
 int launch_simt_cell_bwd(const Shape& s, int64_t B, const float* dh, float* gz, const float* c_t,
                          const float* c_prev, float* dc, cudaStream_t st);
 
+// out[i] = sum_{s < nsplit} part[s * n + i] in fixed order (deterministic split-K reduction)
+int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cudaStream_t st);
+
 // tcgen05 bf16 path (tc_path.cu)
 int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, cudaStream_t st);
 int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,

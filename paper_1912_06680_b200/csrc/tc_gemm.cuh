@@ -30,6 +30,8 @@ struct TileShape {
   int zb0, zb1;      // ... for B sources
   int group;         // rasterisation: tiles per group along the grouped dimension
   int group_n;       // 0: groups of `group` m-tiles sweep all n; 1: groups of n-tiles sweep m
+  int ksplit;        // single-CTA kernel: split K into this many ranges (<= 1: no split); the
+                     // epilogue receives the split index and writes a partial result
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -260,6 +262,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_n = (sh.N + BN - 1) / BN;
   const int ntiles = num_m * num_n;
   const int nkb = sh.nkb0 + sh.nkb1;
+  const int nsplit = sh.ksplit > 1 ? sh.ksplit : 1;
+  const int nunits = ntiles * nsplit;
 
   if (threadIdx.x == 0) {
     prefetch_map(&ta0);
@@ -295,10 +299,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ===================== TMA producer =====================
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+        const int tile = unit / nsplit, split = unit - tile * nsplit;
         int mb, nb;
         tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], L::STAGE_BYTES);
           const bool s1 = kb >= sh.nkb0;
@@ -343,11 +349,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+      const int split = unit % nsplit;
+      const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = kb_lo; kb < kb_hi; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (L::A_BYTES >> 4));
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d_tmem, ad + k * a_k, bd + k * b_k, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16(d_tmem, ad + k * a_k, bd + k * b_k, idesc, ((kb - kb_lo) | k) != 0 ? 1u : 0u);
           umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -375,14 +383,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+      const int tile = unit / nsplit, split = unit - tile * nsplit;
       int mb, nb;
       tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr =
           tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
-      epi.template apply<BN>(mb * BM, nb * BN, row, taddr);
+      epi.template apply<BN>(mb * BM, nb * BN, row, taddr, split);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       acc ^= 1;
@@ -569,7 +578,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t taddr =
           tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
-      epi.template apply<BN>(mb * TM + rank * BM, nb * BN, row, taddr);
+      epi.template apply<BN>(mb * TM + rank * BM, nb * BN, row, taddr, 0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
@@ -595,8 +604,10 @@ struct EpiStoreF32 {
   float* out;
   int64_t ldc;
   int M, N;
+  int64_t split_stride;  // elements between split-K partial outputs
   template <int BN>
-  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr) const {
+  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
+                                        int split) const {
     const int m = m_base + row;
     const bool vec = (N % 4 == 0) && (ldc % 4 == 0);
 #pragma unroll 1
@@ -605,7 +616,7 @@ struct EpiStoreF32 {
       tmem_ld16(taddr + c * 16, v);
       const int n0 = n_base + c * 16;
       if (m >= M || n0 >= N) continue;
-      float* dst = out + static_cast<int64_t>(m) * ldc + n0;
+      float* dst = out + split * split_stride + static_cast<int64_t>(m) * ldc + n0;
       if (vec && n0 + 16 <= N) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -674,7 +685,8 @@ struct EpiLstmFwd {
   __nv_bfloat16* gates;   // G[t]   [B][4H], interleaved like the accumulator columns
   int B, H;
   template <int BN>
-  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr) const {
+  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
+                                        int split) const {
     static_assert(BN == 256, "cell tile holds 4 gates x 64 units");
     const int m = m_base + row;
     const bool ok = m < B;
@@ -719,7 +731,8 @@ struct EpiLstmBwd {
   float* dc;              // [B][H] carry (in/out)
   int B, H;
   template <int BN>
-  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr) const {
+  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
+                                        int split) const {
     const int m = m_base + row;
     const bool ok = m < B;
     const int64_t G4 = 4 * static_cast<int64_t>(H);

@@ -98,6 +98,24 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
 
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// Split-K factor in [1, kMaxSplitK] that best fills whole waves of `sms` CTAs (each split
+// keeps >= 64 k-blocks); 1 when the tiles alone fill the machine.
+int pick_split(int tiles, int sms, int nkb) {
+  if (tiles >= sms) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= kMaxSplitK && nkb / sp >= 64; ++sp) {
+    const int units = tiles * sp;
+    const int waves = (units + sms - 1) / sms;
+    const double eff = (double)units / ((double)waves * sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  return best;
+}
+
 // Raster override for experiments: PPO_RASTER_<KIND>=m<g> or n<g> (e.g. n16).
 void raster(tc::TileShape& sh, const char* kind, int def_group, int def_n) {
   sh.group = def_group;
@@ -221,9 +239,20 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&oa, dY, s.A, rows, s.A))) return rc;
   if ((rc = map_mnmajor(&ob, P.xh + B * s.Kx + s.D, s.Ko, rows, s.Kx))) return rc;
   {
+    // dW_o has only ceil(A/128) x ceil(Ko/256) = 102 tiles at full size (< 148 SMs) and
+    // K = T*B: split K so the grid fills the SMs; partials are reduced in a fixed order.
     tc::TileShape sh{(int)s.A, (int)s.Ko, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16, 0};
-    tc::EpiStoreF32 epi{grad + s.G4 * s.Kx, s.Ko, (int)s.A, (int)s.Ko};
+    const int tiles = cdiv(s.A, tc::BM) * cdiv(s.Ko, 256);
+    sh.ksplit = pick_split(tiles, num_sms(), cdiv(rows, tc::BK));
+    float* dwo = grad + s.G4 * s.Kx;
+    const int64_t n_o = s.A * s.Ko;
+    float* part = sh.ksplit > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) +
+                                                              ws_layout(s, B).splitk)
+                                : dwo;
+    tc::EpiStoreF32 epi{part, s.Ko, (int)s.A, (int)s.Ko, n_o};
     if ((rc = launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st))) return rc;
+    if (sh.ksplit > 1 && (rc = launch_splitk_reduce(part, sh.ksplit, (size_t)n_o, dwo, st)))
+      return rc;
   }
   return PPO_OK;
 }
