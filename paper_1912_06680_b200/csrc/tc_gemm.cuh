@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
-        const int tile = unit / nsplit, split = unit - tile * nsplit;
+        const int split = unit / ntiles, tile = unit - split * ntiles;
         int mb, nb;
         tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
         const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
-      const int split = unit % nsplit;
+      const int split = unit / ntiles;
       const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
-      const int tile = unit / nsplit, split = unit - tile * nsplit;
+      const int split = unit / ntiles, tile = unit - split * ntiles;
       int mb, nb;
       tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
