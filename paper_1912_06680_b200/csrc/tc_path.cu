@@ -66,7 +66,9 @@ int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const 
   }
   if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
   const int64_t ntiles = (int64_t)((sh.M + tc::BM - 1) / tc::BM) * ((sh.N + BN - 1) / BN);
-  const int grid = (int)std::min<int64_t>(ntiles, num_sms());
+  const bool all_tiles = getenv("PPO_GRID_ALL_TILES") && atoi(getenv("PPO_GRID_ALL_TILES"));
+  const int grid = (int)std::min<int64_t>(ntiles * std::max(sh.ksplit, 1),
+                                          all_tiles ? (int64_t)1 << 30 : num_sms());
   if (grid <= 0) return PPO_OK;
   ProfScope _prof(tag, st);
   kern<<<grid, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, sh, epi);
@@ -88,7 +90,9 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
   }
   if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
   const int64_t ntiles = (int64_t)((sh.M + 255) / 256) * ((sh.N + 255) / 256);
-  const int clusters = (int)std::min<int64_t>(ntiles, num_sms() / 2);
+  // PPO_GRID_ALL_TILES=1: one cluster per tile (hardware-ordered dispatch; experiment knob)
+  const bool all_tiles = getenv("PPO_GRID_ALL_TILES") && atoi(getenv("PPO_GRID_ALL_TILES"));
+  const int clusters = (int)std::min<int64_t>(ntiles, all_tiles ? (int64_t)1 << 30 : num_sms() / 2);
   if (clusters <= 0) return PPO_OK;
   ProfScope _prof(tag, st);
   kern<<<2 * clusters, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, sh, epi);
