@@ -32,7 +32,10 @@ struct TileShape {
   int group_n;       // 0: groups of `group` m-tiles sweep all n; 1: groups of n-tiles sweep m
   int ksplit;        // single-CTA kernel: split K into this many ranges (<= 1: no split); the
                      // epilogue receives the split index and writes a partial result
+  unsigned int* sched;  // dynamic tile scheduler: {next unit, exited fetchers}, zero at launch;
+                        // the last fetcher resets both (one launch per counter at a time)
 };
+constexpr int kSchedDepth = 4;  // tile-index ring between the fetcher and the consumers
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -200,7 +203,35 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_cluster(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Wait on a local barrier that a peer CTA arrives on (acquire at cluster scope).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "r"(kSuspendHintNs)
+        : "memory");
+  } while (!done);
+}
+// Fetch the next work unit from the global counter; the fetcher that observes the end last
+// resets the counter for the next launch.
+__device__ __forceinline__ int sched_fetch(unsigned int* ctr, int nunits, unsigned int nfetchers) {
+  const int u = static_cast<int>(atomicAdd(ctr, 1u));
+  if (u >= nunits && atomicAdd(ctr + 1, 1u) == nfetchers - 1) {
+    atomicExch(ctr, 0u);
+    atomicExch(ctr + 1, 0u);
+  }
+  return u;
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -210,7 +241,7 @@ struct Smem {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4 + 2 * kSchedDepth) * 8 + 32 + 1024;
 };
 
 // Grouped rasterisation: consecutive tiles (which run concurrently) share a group of
@@ -254,7 +285,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;              // tile-index ring: filled
+  uint64_t* sempty = sfull + kSchedDepth;    //                  consumed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + kSchedDepth);
+  int* ring = reinterpret_cast<int*>(tslot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -280,6 +314,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 128);
     }
+    for (int s = 0; s < kSchedDepth; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 5);  // MMA warp + 4 epilogue warps
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -297,9 +335,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ===================== TMA producer =====================
+      // also the tile-scheduler fetcher: units are handed out in order from a global
+      // counter, so the tiles in flight stay contiguous in raster order (L2 locality)
       int stage = 0;
       uint32_t phase = 0;
-      for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+      int sslot = 0;
+      uint32_t sphase = 0;
+      while (true) {
+        mbar_wait(&sempty[sslot], sphase ^ 1);
+        const int unit = sched_fetch(sh.sched, nunits, gridDim.x);
+        ring[sslot] = unit;
+        mbar_arrive(&sfull[sslot]);
+        if (++sslot == kSchedDepth) {
+          sslot = 0;
+          sphase ^= 1;
+        }
+        if (unit >= nunits) break;
         const int split = unit / ntiles, tile = unit - split * ntiles;
         int mb, nb;
         tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
@@ -349,7 +400,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+    int sslot = 0;
+    uint32_t sphase = 0;
+    while (true) {
+      mbar_wait(&sfull[sslot], sphase);
+      const int unit = ring[sslot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[sslot]);
+      if (++sslot == kSchedDepth) {
+        sslot = 0;
+        sphase ^= 1;
+      }
+      if (unit >= nunits) break;
       const int split = unit / ntiles;
       const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -383,7 +445,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+    int sslot = 0;
+    uint32_t sphase = 0;
+    while (true) {
+      mbar_wait(&sfull[sslot], sphase);
+      const int unit = ring[sslot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[sslot]);
+      if (++sslot == kSchedDepth) {
+        sslot = 0;
+        sphase ^= 1;
+      }
+      if (unit >= nunits) break;
       const int split = unit / ntiles, tile = unit - split * ntiles;
       int mb, nb;
       tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
@@ -421,7 +494,7 @@ struct Smem2 {
   static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's 128 rows (N-half) of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4 + 2 * kSchedDepth) * 8 + 32 + 1024;
 };
 
 template <bool A_MN, bool B_MN, int STAGES, class Epi>
@@ -440,13 +513,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;              // tile-index ring: filled
+  uint64_t* sempty = sfull + kSchedDepth;    //                  consumed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + kSchedDepth);
+  int* ring = reinterpret_cast<int*>(tslot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  const int cluster_id = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
   const int num_m = (sh.M + TM - 1) / TM;
   const int num_n = (sh.N + BN - 1) / BN;
@@ -468,6 +543,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
     }
+    for (int s = 0; s < kSchedDepth; ++s) {
+      mbar_init(&sfull[s], 1);
+      // leader copy: MMA warp + 4 + 4 epilogue warps + the follower's producer
+      mbar_init(&sempty[s], 10);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -485,9 +565,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ===================== TMA producer (both CTAs) =====================
+      // the leader's producer is the tile-scheduler fetcher for the pair; it publishes each
+      // tile index into both CTAs' rings
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+      int sslot = 0;
+      uint32_t sphase = 0;
+      const uint32_t sempty_l0 = mapa_shared(smem_u32(&sempty[0]), 0);
+      const uint32_t sfull_f0 = mapa_shared(smem_u32(&sfull[0]), 1);
+      const uint32_t ring_f0 = mapa_shared(smem_u32(&ring[0]), 1);
+      while (true) {
+        int tile;
+        if (leader) {
+          mbar_wait(&sempty[sslot], sphase ^ 1);
+          tile = sched_fetch(sh.sched, ntiles, nclusters);
+          ring[sslot] = tile;
+          st_shared_cluster(ring_f0 + 4 * sslot, tile);
+          mbar_arrive(&sfull[sslot]);
+          mbar_arrive_cluster(sfull_f0 + 8 * sslot);
+        } else {
+          mbar_wait_cluster(&sfull[sslot], sphase);
+          tile = ring[sslot];
+          mbar_arrive_cluster(sempty_l0 + 8 * sslot);
+        }
+        if (++sslot == kSchedDepth) {
+          sslot = 0;
+          sphase ^= 1;
+        }
+        if (tile >= ntiles) break;
         int mb, nb;
         tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
         const int m_row = mb * TM + rank * BM;     // this CTA's A rows
@@ -537,7 +642,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+      int sslot = 0;
+      uint32_t sphase = 0;
+      while (true) {
+        mbar_wait(&sfull[sslot], sphase);
+        const int tile = ring[sslot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[sslot]);
+        if (++sslot == kSchedDepth) {
+          sslot = 0;
+          sphase ^= 1;
+        }
+        if (tile >= ntiles) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
@@ -569,9 +685,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t sempty_l0 = mapa_shared(smem_u32(&sempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cluster_id; tile < ntiles; tile += nclusters) {
+    int sslot = 0;
+    uint32_t sphase = 0;
+    while (true) {
+      if (leader) mbar_wait(&sfull[sslot], sphase);
+      else mbar_wait_cluster(&sfull[sslot], sphase);
+      const int tile = ring[sslot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(sempty_l0 + 8 * sslot);
+      if (++sslot == kSchedDepth) {
+        sslot = 0;
+        sphase ^= 1;
+      }
+      if (tile >= ntiles) break;
       int mb, nb;
       tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);

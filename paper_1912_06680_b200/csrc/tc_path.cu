@@ -10,6 +10,24 @@
 namespace ppo {
 namespace {
 
+// Dynamic tile-scheduler counters (zero-initialised; each kernel resets its pair on exit).
+// One slot per GEMM call site, so stream-ordered launches never share a live counter.
+enum SchedSlot { kSchedFwd = 0, kSchedHeads, kSchedBwd, kSchedWgrad, kSchedWgradO, kSchedTest, kSchedSlots };
+__device__ unsigned int g_sched_ctr[2 * kSchedSlots];
+
+unsigned int* sched_counter(int slot) {
+  static unsigned int* base[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!base[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_sched_ctr) != cudaSuccess) return nullptr;
+    base[dev] = static_cast<unsigned int*>(p);
+  }
+  return base[dev] + 2 * slot;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -65,6 +83,7 @@ int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const 
     configured = true;
   }
   if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
+  if (!sh.sched) return fail(PPO_E_CUDA, "tile scheduler counter unavailable");
   const int64_t ntiles = (int64_t)((sh.M + tc::BM - 1) / tc::BM) * ((sh.N + BN - 1) / BN);
   const bool all_tiles = getenv("PPO_GRID_ALL_TILES") && atoi(getenv("PPO_GRID_ALL_TILES"));
   const int grid = (int)std::min<int64_t>(ntiles * std::max(sh.ksplit, 1),
@@ -89,6 +108,7 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
     configured = true;
   }
   if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
+  if (!sh.sched) return fail(PPO_E_CUDA, "tile scheduler counter unavailable");
   const int64_t ntiles = (int64_t)((sh.M + 255) / 256) * ((sh.N + 255) / 256);
   // PPO_GRID_ALL_TILES=1: one cluster per tile (hardware-ordered dispatch; experiment knob)
   const bool all_tiles = getenv("PPO_GRID_ALL_TILES") && atoi(getenv("PPO_GRID_ALL_TILES"));
@@ -175,6 +195,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   for (int t = 0; t < s.T; ++t) {
     tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8, 1};
     raster(sh, "FWD", 8, 1);
+    sh.sched = sched_counter(kSchedFwd);
     tc::TileShape sh1 = sh;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
@@ -188,6 +209,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   if ((rc = map_kmajor(&hB, wo, s.Ko, s.A, s.Ko, 1, 0, 224))) return rc;
   tc::TileShape sh{(int)(s.T * B), (int)s.A, cdiv(s.Ko, tc::BK), 0, 0, 0, 0, 0, 16, 0};
   raster(sh, "HEADS", 16, 0);
+  sh.sched = sched_counter(kSchedHeads);
   tc::EpiStoreF32 epi{out, s.A, (int)(s.T * B), (int)s.A};
   return launch<224, false, false>("heads_fwd", hA, hA, hB, hB, sh, epi, st);
 }
@@ -217,6 +239,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A, tc::BK),
                      t + 1, t, 0, 0, 8, 1};
     raster(sh, "BWD", 8, 1);
+    sh.sched = sched_counter(kSchedBwd);
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
                        (int)B, (int)s.H};
     tc::TileShape sh1 = sh;
@@ -233,6 +256,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   {
     tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8, 1};
     raster(sh, "WGRAD", 8, 1);
+    sh.sched = sched_counter(kSchedWgrad);
     tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
     tc::TileShape sh1 = sh;
     const bool pair = use_pair("WGRAD", false);
@@ -248,6 +272,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     tc::TileShape sh{(int)s.A, (int)s.Ko, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16, 0};
     const int tiles = cdiv(s.A, tc::BM) * cdiv(s.Ko, 256);
     sh.ksplit = pick_split(tiles, num_sms(), cdiv(rows, tc::BK));
+    sh.sched = sched_counter(kSchedWgradO);
     float* dwo = grad + s.G4 * s.Kx;
     const int64_t n_o = s.A * s.Ko;
     float* part = sh.ksplit > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) +
@@ -278,6 +303,7 @@ int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N
   if (rc) return rc;
   tc::TileShape sh{M, N, cdiv(K, tc::BK), 0, 0, 0, 0, 0, 16, 0};
   raster(sh, "TEST", 16, 0);
+  sh.sched = sched_counter(kSchedTest);
   tc::EpiStoreF32 epi{C, N, M, N};
   if (pair) {
     if (!a_mn && !b_mn) return launch2<false, false>("test_gemm2", ma, ma, mb, mb, sh, epi, st);
