@@ -853,6 +853,37 @@ struct EpiLstmFwd {
 
 // LSTM backward step t (oracle O8).  Accumulator = dh_t = dz_{t+1} W_h + dy_t W_o for 256
 // hidden units; the cell backward reads the saved gates of step t and overwrites them with dz_t.
+// Chunks of 8 units; the saved activations of chunk c+1 are loaded (raw 16-byte vectors) while
+// chunk c computes, so the HBM latency of the loads overlaps the math.
+struct BwdRaw {
+  uint4 g[4];            // gates i, f, g, o: 8 bf16 each
+  float4 ct[2], cp[2], dc[2];
+};
+__device__ __forceinline__ void bwd_load(BwdRaw& r, const __nv_bfloat16* gp, const float* ct,
+                                         const float* cp, const float* dc) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r.g[q] = *reinterpret_cast<const uint4*>(gp + q * 64);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    r.ct[q] = reinterpret_cast<const float4*>(ct)[q];
+    r.cp[q] = reinterpret_cast<const float4*>(cp)[q];
+    r.dc[q] = reinterpret_cast<const float4*>(dc)[q];
+  }
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  __syncwarp();
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 struct EpiLstmBwd {
   __nv_bfloat16* gz;      // G[t]: gates in, dz out  [B][4H]
   const float* c_t;       // C[t+1]
@@ -862,41 +893,68 @@ struct EpiLstmBwd {
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int split) const {
+    constexpr int CW = 8;  // units per chunk
     const int m = m_base + row;
     const bool ok = m < B;
     const int64_t G4 = 4 * static_cast<int64_t>(H);
+    const int nch = max(0, min(BN, H - n_base)) / CW;
+    const __nv_bfloat16* grow = gz + static_cast<int64_t>(m) * G4;
+    const int64_t crow = static_cast<int64_t>(m) * H + n_base;
+    auto goff = [&](int cc) {
+      const int j0 = n_base + cc * CW;
+      return (j0 >> 6) * 256 + (j0 & 63);
+    };
+    BwdRaw cur, nxt;
+    if (ok && nch > 0) bwd_load(cur, grow + goff(0), c_t + crow, c_prev + crow, dc + crow);
 #pragma unroll 1
-    for (int cc = 0; cc < BN / 16; ++cc) {
-      float dh[16];
-      tmem_ld16(taddr + cc * 16, dh);
-      const int j0 = n_base + cc * 16;
-      if (!ok || j0 >= H) continue;
-      const int q = j0 >> 6, u0 = j0 & 63;
-      __nv_bfloat16* gp = gz + static_cast<int64_t>(m) * G4 + q * 256 + u0;
-      float gi[16], gf[16], gg[16], go[16], ct[16], cp[16], dcv[16];
-      load_bf16x16(gp + 0, gi);
-      load_bf16x16(gp + 64, gf);
-      load_bf16x16(gp + 128, gg);
-      load_bf16x16(gp + 192, go);
-      const int64_t o = static_cast<int64_t>(m) * H + j0;
-      load_f32x16(c_t + o, ct);
-      load_f32x16(c_prev + o, cp);
-      load_f32x16(dc + o, dcv);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        float a, b, c, d, dn;
-        cell_bwd(dh[e], dcv[e], gi[e], gf[e], gg[e], go[e], ct[e], cp[e], a, b, c, d, dn);
-        gi[e] = a;
-        gf[e] = b;
-        gg[e] = c;
-        go[e] = d;
-        dcv[e] = dn;
+    for (int cc = 0; cc < BN / CW; ++cc) {
+      float dh[8];
+      tmem_ld8(taddr + cc * CW, dh);
+      if (cc >= nch) continue;
+      if (ok && cc + 1 < nch) {
+        const int64_t o = crow + (cc + 1) * CW;
+        bwd_load(nxt, grow + goff(cc + 1), c_t + o, c_prev + o, dc + o);
       }
-      store_bf16x16(gp + 0, gi);
-      store_bf16x16(gp + 64, gf);
-      store_bf16x16(gp + 128, gg);
-      store_bf16x16(gp + 192, go);
-      store_f32x16(dc + o, dcv);
+      if (ok) {
+        // in place: each 32-bit gate word holds units (2w, 2w+1); dz overwrites the gates
+        float* ct = reinterpret_cast<float*>(cur.ct);
+        float* cp = reinterpret_cast<float*>(cur.cp);
+        float* dcv = reinterpret_cast<float*>(cur.dc);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          float z[4][2];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t u = reinterpret_cast<const uint32_t*>(&cur.g[q])[w];
+            z[q][0] = __uint_as_float(u << 16);
+            z[q][1] = __uint_as_float(u & 0xFFFF0000u);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = 2 * w + h;
+            float a, b, c, d, dn;
+            cell_bwd(dh[e], dcv[e], z[0][h], z[1][h], z[2][h], z[3][h], ct[e], cp[e], a, b, c,
+                     d, dn);
+            z[0][h] = a;
+            z[1][h] = b;
+            z[2][h] = c;
+            z[3][h] = d;
+            dcv[e] = dn;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162 pk = __floats2bfloat162_rn(z[q][0], z[q][1]);
+            reinterpret_cast<uint32_t*>(&cur.g[q])[w] = *reinterpret_cast<const uint32_t*>(&pk);
+          }
+        }
+        __nv_bfloat16* gp = gz + static_cast<int64_t>(m) * G4 + goff(cc);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(gp + q * 64) = cur.g[q];
+        float4* d4 = reinterpret_cast<float4*>(dc + crow + cc * CW);
+        d4[0] = cur.dc[0];
+        d4[1] = cur.dc[1];
+      }
+      cur = nxt;
     }
   }
 };

@@ -229,7 +229,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   // dh_t = dz_{t+1} W_h + dy_t W_o : A = [G (3-D, slot t+1) | dY (3-D, slot t)] (K-major),
   // B = [W_xh_aug[:, D:D+H] | W_o_aug[:, :H]] read MN-major (K = gate row / head output).
   CUtensorMap a0, a1, b0, b1;
-  const bool pair = use_pair("BWD", false);
+  const bool pair = use_pair("BWD", true);
   if ((rc = map_kmajor(&a0, P.g, s.G4, B, s.G4, s.T, B * s.G4, tc::BM))) return rc;
   if ((rc = map_kmajor(&a1, dY, s.A, B, s.A, s.T, B * s.A, tc::BM))) return rc;
   if ((rc = map_mnmajor(&b0, wxh + s.D, s.H, s.G4, s.Kx))) return rc;
@@ -254,12 +254,12 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&wa, P.g, s.G4, rows, s.G4))) return rc;
   if ((rc = map_mnmajor(&wb, P.xh, s.Kx, rows, s.Kx))) return rc;
   {
-    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8, 1};
-    raster(sh, "WGRAD", 8, 1);
+    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8, 0};
+    raster(sh, "WGRAD", 8, 0);
     sh.sched = sched_counter(kSchedWgrad);
     tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
     tc::TileShape sh1 = sh;
-    const bool pair = use_pair("WGRAD", false);
+    const bool pair = use_pair("WGRAD", true);
     rc = pair ? launch2<true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
               : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh1, epi, st);
     if (rc) return rc;
