@@ -1,5 +1,5 @@
-"""One GEMM of a given shape through cuBLAS (torch.mm) and through the tcgen05 variants, for
-ncu side-by-side captures.   python tools/gemm_one.py fwd"""
+"""One GEMM of a given shape through cuBLAS (torch.mm) and through the tcgen05 variants
+(single CTA, CTA pair), for ncu side-by-side captures.   python tools/gemm_one.py wgrad"""
 import os
 import sys
 
@@ -18,9 +18,8 @@ C = torch.empty((M, N), device="cuda")
 mode = (1 if b_mn else 0) | (2 if a_mn else 0)
 Am = A.t() if a_mn else A
 Bm = B if b_mn else B.t()
-for _ in range(2):
-    torch.mm(Am, Bm)
-    L.test_tc_gemm(mode, A, B, C, M, N, K)
-    L.test_tc_gemm(mode | 8, A, B, C, M, N, K)
+torch.mm(Am, Bm)
+L.test_tc_gemm(mode, A, B, C, M, N, K)
+L.test_tc_gemm(mode | 8, A, B, C, M, N, K)
 torch.cuda.synchronize()
 print("ok")
