@@ -96,12 +96,12 @@ int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const 
 }
 
 // CTA-pair launch: 256x256 tiles, grid = 2 x clusters (one CTA per SM, persistent).
-template <bool A_MN, bool B_MN, class Epi>
+template <bool A_MN, bool B_MN, class Epi, int MB = 1>
 int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
             const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
-  constexpr int STAGES = 6;
-  using L = tc::Smem2<A_MN, B_MN, STAGES>;
-  auto kern = tc::tc_gemm2_kernel<A_MN, B_MN, STAGES, Epi>;
+  constexpr int STAGES = MB == 1 ? 6 : 4;
+  using L = tc::Smem2<A_MN, B_MN, STAGES, MB>;
+  auto kern = tc::tc_gemm2_kernel<A_MN, B_MN, STAGES, MB, Epi>;
   static bool configured = false;
   if (!configured) {
     PPO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
@@ -109,7 +109,7 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
   }
   if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
   if (!sh.sched) return fail(PPO_E_CUDA, "tile scheduler counter unavailable");
-  const int64_t ntiles = (int64_t)((sh.M + 255) / 256) * ((sh.N + 255) / 256);
+  const int64_t ntiles = (int64_t)((sh.M + 256 * MB - 1) / (256 * MB)) * ((sh.N + 255) / 256);
   // PPO_GRID_ALL_TILES=1: one cluster per tile (hardware-ordered dispatch; experiment knob)
   const bool all_tiles = getenv("PPO_GRID_ALL_TILES") && atoi(getenv("PPO_GRID_ALL_TILES"));
   const int clusters = (int)std::min<int64_t>(ntiles, all_tiles ? (int64_t)1 << 30 : num_sms() / 2);
@@ -260,7 +260,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
     tc::TileShape sh1 = sh;
     const bool pair = use_pair("WGRAD", true);
-    rc = pair ? launch2<true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
+    rc = pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
               : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh1, epi, st);
     if (rc) return rc;
   }
@@ -305,6 +305,12 @@ int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N
   raster(sh, "TEST", 16, 0);
   sh.sched = sched_counter(kSchedTest);
   tc::EpiStoreF32 epi{C, N, M, N};
+  const bool wide = mode & 16;
+  if (pair && wide) {
+    if (a_mn && b_mn)
+      return launch2<true, true, tc::EpiStoreF32, 2>("test_gemm2w", ma, ma, mb, mb, sh, epi, st);
+    return fail(PPO_E_ARG, "512-row pair tiles: test mode only for MN-major A and B");
+  }
   if (pair) {
     if (!a_mn && !b_mn) return launch2<false, false>("test_gemm2", ma, ma, mb, mb, sh, epi, st);
     if (!a_mn && b_mn) return launch2<false, true>("test_gemm2", ma, ma, mb, mb, sh, epi, st);

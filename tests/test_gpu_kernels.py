@@ -30,10 +30,12 @@ def L():
     (8, 256, 256, 64), (8, 300, 520, 200), (8, 1000, 2048, 1024),
     (9, 512, 512, 192), (9, 77, 264, 1000),
     (11, 384, 768, 448), (11, 136, 320, 72), (11, 2048, 1024, 4096),
+    # CTA pair with 512-row tiles (two MMAs per K step), MN-major operands (weight gradient)
+    (27, 512, 256, 64), (27, 600, 520, 200), (27, 2048, 1024, 4096),
 ])
 def test_tc_gemm_vs_torch(L, mode, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
-    a_mn, b_mn = bool(mode & 2), bool(mode & 1)  # bit2: N=224 tile, bit3: CTA pair
+    a_mn, b_mn = bool(mode & 2), bool(mode & 1)  # bit2: N=224, bit3: CTA pair, bit4: 512 rows
     A = torch.randn((K, M) if a_mn else (M, K), generator=g, device="cuda").bfloat16()
     B = torch.randn((K, N) if b_mn else (N, K), generator=g, device="cuda").bfloat16()
     C = torch.full((M, N), float("nan"), device="cuda")

@@ -94,6 +94,8 @@ def sweep(name, rasters, seconds=2.0):
         os.environ["PPO_RASTER_TEST"] = r
         rows.append(("tc_1cta", r, measure(lambda: L.test_tc_gemm(mode, A, B, C, M, N, K), flop, seconds)))
         rows.append(("tc_pair", r, measure(lambda: L.test_tc_gemm(mode | 8, A, B, C, M, N, K), flop, seconds)))
+        if a_mn and b_mn:
+            rows.append(("tc_pair2", r, measure(lambda: L.test_tc_gemm(mode | 24, A, B, C, M, N, K), flop, seconds)))
     for k, r, v in rows:
         print(f"{name:7s} {k:8s} {r:4s} {v['tflops']:7.1f} TF/s  {v['watts']:6.0f} W  "
               f"{v['tflop_per_j']:5.3f} TFLOP/J  sm {v['mhz']:5.0f} MHz  {v['ms']:8.3f} ms", flush=True)

@@ -21,5 +21,7 @@ Bm = B if b_mn else B.t()
 torch.mm(Am, Bm)
 L.test_tc_gemm(mode, A, B, C, M, N, K)
 L.test_tc_gemm(mode | 8, A, B, C, M, N, K)
+if a_mn and b_mn:
+    L.test_tc_gemm(mode | 8 | 16, A, B, C, M, N, K)
 torch.cuda.synchronize()
 print("ok")
