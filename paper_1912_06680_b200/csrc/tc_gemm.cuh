@@ -32,6 +32,7 @@ struct TileShape {
   int group_n;       // 0: groups of `group` m-tiles sweep all n; 1: groups of n-tiles sweep m
   int ksplit;        // single-CTA kernel: split K into this many ranges (<= 1: no split); the
                      // epilogue receives the split index and writes a partial result
+  int kb_off;        // k-block offset added to source-0 K coordinates (K-chunked launches)
   unsigned int* sched;  // dynamic tile scheduler: {next unit, exited fetchers}, zero at launch;
                         // the last fetcher resets both (one launch per counter at a time)
 };
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], L::STAGE_BYTES);
           const bool s1 = kb >= sh.nkb0;
-          const int kk = (s1 ? kb - sh.nkb0 : kb) * BK;
+          const int kk = (s1 ? kb - sh.nkb0 : kb + sh.kb_off) * BK;
           const CUtensorMap* ta = s1 ? &ta1 : &ta0;
           const CUtensorMap* tb = s1 ? &tb1 : &tb0;
           const int za = s1 ? sh.za1 : sh.za0;
@@ -607,7 +608,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t fbar = mapa_shared(smem_u32(&full[stage]), 0);
           if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
           const bool s1 = kb >= sh.nkb0;
-          const int kk = (s1 ? kb - sh.nkb0 : kb) * BK;
+          const int kk = (s1 ? kb - sh.nkb0 : kb + sh.kb_off) * BK;
           const CUtensorMap* ta = s1 ? &ta1 : &ta0;
           const CUtensorMap* tb = s1 ? &tb1 : &tb0;
           const int za = s1 ? sh.za1 : sh.za0;
@@ -749,6 +750,7 @@ struct EpiStoreF32 {
   int64_t ldc;
   int M, N;
   int64_t split_stride;  // elements between split-K partial outputs
+  int accumulate;        // 1: out += acc (K-chunked launches after the first)
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int split) const {
@@ -762,13 +764,23 @@ struct EpiStoreF32 {
       if (m >= M || n0 >= N) continue;
       float* dst = out + split * split_stride + static_cast<int64_t>(m) * ldc + n0;
       if (vec && n0 + 16 <= N) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int q = 0; q < 4; ++q) {
+          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          if (accumulate) {
+            const float4 p = d4[q];
+            o.x += p.x;
+            o.y += p.y;
+            o.z += p.z;
+            o.w += p.w;
+          }
+          d4[q] = o;
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          if (n0 + i < N) dst[i] = v[i];
+          if (n0 + i < N) dst[i] = accumulate ? dst[i] + v[i] : v[i];
       }
     }
   }

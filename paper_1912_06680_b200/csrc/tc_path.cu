@@ -254,15 +254,27 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&wa, P.g, s.G4, rows, s.G4))) return rc;
   if ((rc = map_mnmajor(&wb, P.xh, s.Kx, rows, s.Kx))) return rc;
   {
-    tc::TileShape sh{(int)s.G4, (int)s.Kx, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 8, 0};
-    raster(sh, "WGRAD", 8, 0);
-    sh.sched = sched_counter(kSchedWgrad);
-    tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx};
-    tc::TileShape sh1 = sh;
+    // K = T*B is long (614,400 at the full config): run it as K-chunks of ~76,800 rows, each
+    // a separate launch that accumulates into dW.  The tiles of one launch start together and
+    // drift apart little over a chunk, so the shared operand panels stay in L2 (DRAM traffic
+    // and hence power drop; the step is power-capped).  PPO_WGRAD_CHUNK overrides the rows.
+    const int nkb_all = cdiv(rows, tc::BK);
+    int chunk_kb = 1200;
+    if (const char* e = getenv("PPO_WGRAD_CHUNK")) chunk_kb = std::max(1, atoi(e) / tc::BK);
+    const int nchunks = std::max(1, (nkb_all + chunk_kb - 1) / chunk_kb);
     const bool pair = use_pair("WGRAD", true);
-    rc = pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
-              : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh1, epi, st);
-    if (rc) return rc;
+    for (int c = 0; c < nchunks; ++c) {
+      const int kb0 = (int)((int64_t)nkb_all * c / nchunks);
+      const int kb1 = (int)((int64_t)nkb_all * (c + 1) / nchunks);
+      tc::TileShape sh{(int)s.G4, (int)s.Kx, kb1 - kb0, 0, 0, 0, 0, 0, 8, 0};
+      raster(sh, "WGRAD", 8, 0);
+      sh.kb_off = kb0;
+      sh.sched = sched_counter(kSchedWgrad);
+      tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx, 0, c > 0 ? 1 : 0};
+      rc = pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
+                : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st);
+      if (rc) return rc;
+    }
   }
   if ((rc = map_mnmajor(&oa, dY, s.A, rows, s.A))) return rc;
   if ((rc = map_mnmajor(&ob, P.xh + B * s.Kx + s.D, s.Ko, rows, s.Kx))) return rc;
