@@ -71,8 +71,9 @@ _lib_fns = dict(
     ppo_pack_params=([_D] + [c_void_p] * 7, c_int),
     ppo_unpack_params=([_D] + [c_void_p] * 7, c_int),
     ppo_cast_bf16=([c_void_p, c_void_p, c_size_t, c_void_p], c_int),
+    ppo_gae_scratch_bytes=([c_int64, c_int64, POINTER(c_size_t)], c_int),
     ppo_gae=([c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_float, c_int32, c_void_p,
-              c_void_p, c_void_p], c_int),
+              c_void_p, c_void_p, c_size_t, c_void_p], c_int),
     lstm_ws_bytes=([_D, c_int64, POINTER(c_size_t)], c_int),
     lstm_bptt_fwd=([_D, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_size_t,
                     c_void_p, c_void_p], c_int),
@@ -157,10 +158,18 @@ def ppo_cast_bf16(src, dst, stream=None):
     _check(_lib.ppo_cast_bf16(_p(src), _p(dst), src.numel(), _s(stream)))
 
 
-def ppo_gae(rew, val, done, gamma, lam, adv, ret, seq_T=0, stream=None):
+def gae_scratch_bytes(R: int, L: int) -> int:
+    n = c_size_t()
+    _check(_lib.ppo_gae_scratch_bytes(R, L, ctypes.byref(n)))
+    return n.value
+
+
+def ppo_gae(rew, val, done, gamma, lam, adv, ret, seq_T=0, scratch=None, stream=None):
+    """scratch: uint8 device tensor of >= gae_scratch_bytes(R, L) (None if that is 0)"""
     R, L = rew.shape
+    nbytes = 0 if scratch is None else scratch.numel() * scratch.element_size()
     _check(_lib.ppo_gae(_p(rew), _p(val), _p(done), R, L, gamma, lam, seq_T, _p(adv), _p(ret),
-                        _s(stream)))
+                        _p(scratch), nbytes, _s(stream)))
 
 
 def lstm_bptt_fwd(dims, w, x, h0, c0, B, ws, out, stream=None):

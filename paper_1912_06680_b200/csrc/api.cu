@@ -204,15 +204,26 @@ int ppo_cast_bf16(const float* src, uint16_t* dst, size_t n, ppo_stream_t st) {
   return launch_cast_bf16(src, dst, n, (cudaStream_t)st);
 }
 
+int ppo_gae_scratch_bytes(int64_t R, int64_t L, size_t* bytes) {
+  if (R < 0 || L < 0) return fail(PPO_E_SHAPE, "R and L must be >= 0");
+  if (!bytes) return fail(PPO_E_ARG, "bytes is NULL");
+  *bytes = (R == 0 || L == 0) ? 0 : gae_scratch_bytes(R, L);
+  return PPO_OK;
+}
+
 int ppo_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
-            float gamma, float lam, int32_t seq_T, float* adv, float* ret, ppo_stream_t st) {
+            float gamma, float lam, int32_t seq_T, float* adv, float* ret, void* scratch,
+            size_t scratch_bytes, ppo_stream_t st) {
   if (R < 0 || L < 0) return fail(PPO_E_SHAPE, "R and L must be >= 0");
   if (R == 0 || L == 0) return PPO_OK;
   if (!rew || !val || !done || !adv || !ret) return fail(PPO_E_ARG, "NULL pointer");
   if (seq_T < 0 || (seq_T > 0 && L % seq_T)) return fail(PPO_E_SHAPE, "L must be a multiple of seq_T");
   if (!(gamma >= 0.f && gamma <= 1.f && lam >= 0.f && lam <= 1.f))
     return fail(PPO_E_ARG, "gamma and lam must be in [0, 1]");
-  return launch_gae(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, (cudaStream_t)st);
+  const size_t need = gae_scratch_bytes(R, L);
+  if (need > 0 && (!scratch || scratch_bytes < need || !aligned(scratch, 16)))
+    return fail(PPO_E_ARG, "long rollouts need ppo_gae_scratch_bytes() of 16-byte aligned scratch");
+  return launch_gae(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, scratch, (cudaStream_t)st);
 }
 
 int lstm_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes) {

@@ -182,6 +182,195 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
   }
 }
 
+
+// Long rollouts (L > kGaeShortL): chunk-parallel single pass with a decoupled look-back.
+// A block owns a chunk of kGaeChunk = 8192 steps of one stream (32 per thread, vectorised).
+// Chunks are numbered from the END of each stream and handed out in that order by a global
+// counter, so a chunk only waits on chunks dispatched before it.  Each block (1) reduces its
+// steps to an affine map A_first = P + Q A_after, (2) publishes it, (3) looks back over the
+// later chunks' published maps / inclusive values to get A_after, (4) recomputes its A_t in
+// registers, writes A and R, and publishes its inclusive A_first.  r, V, d are read once.
+struct GaeStatus {
+  float P, Q, A;
+  unsigned int flag;  // 0 = empty, 1 = aggregate (P,Q), 2 = inclusive (A)
+};
+
+__device__ __forceinline__ void gae_publish(GaeStatus* st, float P, float Q, float A,
+                                            unsigned int flag) {
+  st->P = P;
+  st->Q = Q;
+  st->A = A;
+  __threadfence();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&st->flag), "r"(flag) : "memory");
+}
+__device__ __forceinline__ unsigned int gae_flag(const GaeStatus* st) {
+  unsigned int f;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(&st->flag) : "memory");
+  return f;
+}
+
+__global__ void __launch_bounds__(256) gae_long_kernel(
+    const float* __restrict__ rew, const float* __restrict__ val, const uint8_t* __restrict__ done,
+    int64_t R, int64_t L, float gamma, float lam, int seq_T, float* __restrict__ adv,
+    float* __restrict__ ret, GaeStatus* __restrict__ status, unsigned int* __restrict__ counter) {
+  constexpr int PER = 32;
+  __shared__ int s_chunk;
+  __shared__ float sP[8], sQ[8];
+  __shared__ float s_after;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nck = (L + kGaeChunk - 1) / kGaeChunk;  // chunks per stream
+  if (tid == 0) s_chunk = (int)atomicAdd(counter, 1u);
+  __syncthreads();
+  const int64_t g = s_chunk;
+  const int64_t r = g / nck, j = g - r * nck;           // j-th chunk from the end
+  const int64_t c_end = L - j * kGaeChunk;
+  const int64_t c_begin = c_end > kGaeChunk ? c_end - kGaeChunk : 0;
+  const int64_t t0 = c_begin + (int64_t)tid * PER;
+  const int n = (int)max((int64_t)0, min((int64_t)PER, c_end - t0));
+  const float* rr = rew + r * L;
+  const float* vv = val + r * (L + 1);
+  const uint8_t* dd = done + r * L;
+  const float gl = gamma * lam;
+
+  float delta[PER], cf[PER];
+  const bool vec = n == PER && ((r * L + t0) & 3) == 0 && ((r * (L + 1) + t0) & 3) == 0;
+  if (vec) {
+    float rv[PER], v[PER + 1];
+    uint8_t d[PER];
+#pragma unroll
+    for (int q = 0; q < PER / 4; ++q) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(rr + t0) + q);
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(vv + t0) + q);
+      rv[4 * q] = a.x; rv[4 * q + 1] = a.y; rv[4 * q + 2] = a.z; rv[4 * q + 3] = a.w;
+      v[4 * q] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
+    }
+    v[PER] = vv[t0 + PER];
+    const uint4* dq = reinterpret_cast<const uint4*>(dd + t0);
+    uint4 d0 = dq[0], d1 = dq[1];
+    const uint8_t* b0 = reinterpret_cast<const uint8_t*>(&d0);
+    const uint8_t* b1 = reinterpret_cast<const uint8_t*>(&d1);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      d[i] = b0[i];
+      d[16 + i] = b1[i];
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const float nd = d[i] ? 0.f : 1.f;
+      delta[i] = rv[i] + gamma * nd * v[i + 1] - v[i];
+      cf[i] = gl * nd;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      if (i < n) {
+        const int64_t t = t0 + i;
+        const float nd = dd[t] ? 0.f : 1.f;
+        delta[i] = rr[t] + gamma * nd * vv[t + 1] - vv[t];
+        cf[i] = gl * nd;
+      } else {
+        delta[i] = 0.f;
+        cf[i] = 1.f;
+      }
+    }
+  }
+  // (1) thread map, then reverse inclusive scan over the block (later threads are later steps)
+  float P = 0.f, Q = 1.f;
+#pragma unroll
+  for (int i = PER - 1; i >= 0; --i) {
+    P = delta[i] + cf[i] * P;
+    Q = cf[i] * Q;
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float P2 = __shfl_down_sync(0xffffffffu, P, off);
+    const float Q2 = __shfl_down_sync(0xffffffffu, Q, off);
+    if (lane + off < 32) {
+      P = P + Q * P2;
+      Q = Q * Q2;
+    }
+  }
+  if (lane == 0) {
+    sP[warp] = P;
+    sQ[warp] = Q;
+  }
+  __syncthreads();
+  // suffix of the warps after this one
+  float wP = 0.f, wQ = 1.f;
+  for (int w = 7; w > warp; --w) {
+    wP = sP[w] + sQ[w] * wP;
+    wQ = sQ[w] * wQ;
+  }
+  if (tid == 0) {
+    // (2) chunk aggregate = warp 0's inclusive map composed with the rest
+    const float aP = P + Q * wP, aQ = Q * wQ;
+    GaeStatus* me = status + g;
+    float after = 0.f;  // A after the last step of the stream (A_L = 0)
+    if (j == 0) {
+      gae_publish(me, aP, aQ, aP, 2u);
+    } else {
+      gae_publish(me, aP, aQ, 0.f, 1u);
+      // (3) look back over later chunks: compose aggregates until an inclusive value
+      float cP = 0.f, cQ = 1.f;  // composed map of the chunks between
+      for (int64_t k = g - 1;; --k) {
+        unsigned int f;
+        do {
+          f = gae_flag(status + k);
+        } while (f == 0u);
+        const GaeStatus* o = status + k;
+        if (f == 2u) {
+          after = cP + cQ * *(volatile const float*)&o->A;
+          break;
+        }
+        const float oP = *(volatile const float*)&o->P, oQ = *(volatile const float*)&o->Q;
+        cP = cP + cQ * oP;
+        cQ = cQ * oQ;
+      }
+      gae_publish(me, aP, aQ, aP + aQ * after, 2u);
+    }
+    s_after = after;
+  }
+  __syncthreads();
+  // (4) A after this thread's steps = (warp suffix ∘ lane suffix) applied to the chunk's A_after
+  const float a_after_warp = wP + wQ * s_after;
+  const float Pn = __shfl_down_sync(0xffffffffu, P, 1), Qn = __shfl_down_sync(0xffffffffu, Q, 1);
+  float a = lane == 31 ? a_after_warp : Pn + Qn * a_after_warp;
+  float A_out[PER];
+#pragma unroll
+  for (int i = PER - 1; i >= 0; --i) {
+    a = delta[i] + cf[i] * a;
+    A_out[i] = a;
+  }
+  if (vec && seq_T == 0) {
+#pragma unroll
+    for (int q = 0; q < PER / 4; ++q) {
+      const float4 v4 = reinterpret_cast<const float4*>(vv + t0)[q];
+      reinterpret_cast<float4*>(adv + r * L + t0)[q] =
+          make_float4(A_out[4 * q], A_out[4 * q + 1], A_out[4 * q + 2], A_out[4 * q + 3]);
+      reinterpret_cast<float4*>(ret + r * L + t0)[q] =
+          make_float4(A_out[4 * q] + v4.x, A_out[4 * q + 1] + v4.y, A_out[4 * q + 2] + v4.z,
+                      A_out[4 * q + 3] + v4.w);
+    }
+  } else {
+    const int64_t spr = seq_T > 0 ? L / seq_T : 0, nseq = R * spr;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      if (i < n) {
+        const int64_t t = t0 + i;
+        int64_t o;
+        if (seq_T > 0) {
+          const int64_t k = t / seq_T, tt = t - k * seq_T;
+          o = tt * nseq + r * spr + k;
+        } else {
+          o = r * L + t;
+        }
+        adv[o] = A_out[i];
+        ret[o] = A_out[i] + vv[t];
+      }
+    }
+  }
+}
+
 // ============================================================================ PPO loss
 // One warp per row (row = t*B + b); the row is staged in shared memory; per head a masked
 // log-sum-exp, the entropy, then the analytic gradient (oracle O6/O7).  Statistics go to
@@ -552,12 +741,30 @@ int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, con
   PPO_LAUNCH_CHECK("pack_x_kernel");
   return PPO_OK;
 }
+size_t gae_scratch_bytes(int64_t R, int64_t L) {
+  if (L <= kGaeShortL) return 0;
+  const int64_t nck = (L + kGaeChunk - 1) / kGaeChunk;
+  return 256 + (size_t)(R * nck) * sizeof(GaeStatus);
+}
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
-               float gamma, float lam, int seq_T, float* adv, float* ret, cudaStream_t st) {
+               float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,
+               cudaStream_t st) {
   ProfScope _prof("gae", st);
-  const int64_t threads = R * 32;
-  gae_kernel<<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret);
-  PPO_LAUNCH_CHECK("gae_kernel");
+  if (L <= kGaeShortL) {
+    const int64_t threads = R * 32;
+    gae_kernel<<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret);
+    PPO_LAUNCH_CHECK("gae_kernel");
+    return PPO_OK;
+  }
+  const int64_t nck = (L + kGaeChunk - 1) / kGaeChunk;
+  const int64_t blocks = R * nck;
+  if (blocks > INT32_MAX) return fail(PPO_E_SHAPE, "too many GAE chunks");
+  PPO_CUDA_CHECK(cudaMemsetAsync(scratch, 0, gae_scratch_bytes(R, L), st));
+  unsigned int* counter = static_cast<unsigned int*>(scratch);
+  GaeStatus* status = reinterpret_cast<GaeStatus*>(static_cast<uint8_t*>(scratch) + 256);
+  gae_long_kernel<<<(unsigned)blocks, 256, 0, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv,
+                                                    ret, status, counter);
+  PPO_LAUNCH_CHECK("gae_long_kernel");
   return PPO_OK;
 }
 int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t* act,

@@ -29,8 +29,12 @@ int launch_unpack_params(const Shape& s, const float* theta, float* Wx, float* W
 int launch_cast_bf16(const float* src, void* dst, size_t n, cudaStream_t st);
 int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, const float* c0,
                   void* xh, float* c, cudaStream_t st);
+constexpr int64_t kGaeShortL = 8192;  // up to this length: one warp per stream
+constexpr int64_t kGaeChunk = 8192;   // longer: chunk-parallel look-back kernel
+size_t gae_scratch_bytes(int64_t R, int64_t L);
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
-               float gamma, float lam, int seq_T, float* adv, float* ret, cudaStream_t st);
+               float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,
+               cudaStream_t st);
 int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t* act,
                 const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
                 const float* adv, const float* ret, const uint8_t* valid, void* dout, float* logp,

@@ -59,7 +59,9 @@ def test_null_pointers_rejected(lib):
     d = lib.make_dims(256, 128, 16, (30, 4, 189, 189, 81, 81, 81))
     rc = lib._lib.adam_step(None, None, None, None, None, 10, 1, 1e-3, 0.9, 0.999, 1e-8, 5.0, None)
     assert rc == lib.PPO_E_ARG
-    rc = lib._lib.ppo_gae(None, None, None, 2, 256, 0.99, 0.95, 0, None, None, None)
+    rc = lib._lib.ppo_gae(None, None, None, 2, 256, 0.99, 0.95, 0, None, None, None, 0, None)
     assert rc == lib.PPO_E_ARG
-    rc = lib._lib.ppo_gae(None, None, None, 0, 256, 0.99, 0.95, 0, None, None, None)
+    rc = lib._lib.ppo_gae(None, None, None, 0, 256, 0.99, 0.95, 0, None, None, None, 0, None)
     assert rc == lib.PPO_OK  # empty input is a no-op
+    assert lib.gae_scratch_bytes(4, 256) == 0
+    assert lib.gae_scratch_bytes(1, 10 ** 6) >= 16 * (10 ** 6 // 8192)

@@ -53,6 +53,9 @@ def test_tc_gemm_vs_torch(L, mode, M, N, K):
 @pytest.mark.parametrize("R,Lr,seq_T,p_done", [
     (2, 256, 16, 0.01), (2400, 256, 16, 1 / 20000), (3, 1350, 0, 0.002), (5, 1, 0, 0.5),
     (1, 6300, 0, 0.0), (7, 300, 0, 0.05), (4, 512, 16, 0.0),
+    # long rollouts: chunk-parallel look-back kernel (chunks of 8192 steps), ragged tails
+    (1, 20000, 0, 1 / 20000), (3, 100001, 0, 1e-4), (2, 8193, 0, 0.0), (5, 40960, 16, 0.001),
+    (1, 1000000, 0, 1e-5),
 ])
 def test_gae_parity(L, R, Lr, seq_T, p_done):
     ro = synth.make_rollouts(R, Lr, seed=R + Lr, p_done=p_done)
@@ -64,7 +67,10 @@ def test_gae_parity(L, R, Lr, seq_T, p_done):
         Rt = oracle.segments_to_sequences(Rt, seq_T)
     adv = torch.full(A.shape, float("nan"), device="cuda")
     ret = torch.full(A.shape, float("nan"), device="cuda")
-    L.ppo_gae(dev(ro["r"]), dev(ro["V"]), dev(ro["done"]), gamma, lam, adv, ret, seq_T=seq_T)
+    nb = L.gae_scratch_bytes(R, Lr)
+    scratch = torch.empty(nb, dtype=torch.uint8, device="cuda") if nb else None
+    L.ppo_gae(dev(ro["r"]), dev(ro["V"]), dev(ro["done"]), gamma, lam, adv, ret, seq_T=seq_T,
+              scratch=scratch)
     torch.cuda.synchronize()
     ok, worst = elementwise_ok(adv.cpu().numpy(), A, 1e-5)
     assert ok, worst
