@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1, help="oracle sample: sequences per step")
+    ap.add_argument("--config", choices=["full", "gae"], default="full",
+                    help="full: the PPO step (default); gae: GAE-only HBM sweep (configs[3])")
     return ap.parse_args()
 
 
@@ -224,10 +226,58 @@ def algorithmic(H, D, T, B, A, nparam):
     }
 
 
+def run_gae_sweep(args):
+    """BASELINE configs[3]: GAE over long rollouts (segment 256 ... a whole game, 10^6 steps),
+    algorithmic 17 B/timestep (r, V, d in; A, R out) against the measured HBM peak."""
+    import torch
+    import synth
+    from paper_1912_06680_b200 import _lib as L
+    dev = torch.device("cuda", 0)
+    pk = peaks()
+    gamma = 1.0 - (4.0 / 30.0) / 180.0
+    rows = []
+    for steps in (10 ** 6, 10 ** 8, 10 ** 9):
+        for Lr in (256, 1350, 6300, 20000, 10 ** 6):
+            R = max(1, steps // Lr)
+            n = R * Lr
+            ro = synth.torch_rollouts(R, Lr, 1, dev)
+            adv = torch.empty((R, Lr), device=dev)
+            ret = torch.empty((R, Lr), device=dev)
+            nb = L.gae_scratch_bytes(R, Lr)
+            scratch = torch.empty(nb, dtype=torch.uint8, device=dev) if nb else None
+            for _ in range(args.warmup):
+                L.ppo_gae(ro["rew"], ro["val"], ro["done"], gamma, 0.95, adv, ret, scratch=scratch)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(args.steps):
+                L.ppo_gae(ro["rew"], ro["val"], ro["done"], gamma, 0.95, adv, ret, scratch=scratch)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            gbs = 17.0 * n / (ms / 1e3) / 1e9
+            rows.append({"L": Lr, "R": R, "timesteps": n, "ms": ms, "GB_s": gbs,
+                         "frac": gbs / pk["hbm_gbs"], "timesteps_per_s": n / (ms / 1e3)})
+            del ro, adv, ret, scratch
+            torch.cuda.empty_cache()
+    top = max((r for r in rows if r["timesteps"] >= 10 ** 9), key=lambda r: r["GB_s"])
+    print(json.dumps({
+        "metric": "GAE timesteps/s (configs[3] sweep)", "value": top["timesteps_per_s"],
+        "unit": "timesteps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "GAE-only, R streams x L steps, lambda 0.95, gamma(180 s)"},
+        "roofline": {"bound": "hbm", "achieved": top["GB_s"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": top["frac"], "traffic": None, "kernel": "gae"},
+        "sweep": rows}), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config == "gae":
+        run_gae_sweep(args)
         return
 
     import torch
