@@ -110,6 +110,48 @@ __global__ void __launch_bounds__(256) pack_x_kernel(Shape s, int64_t B, const T
 }
 
 // ============================================================================ GAE
+
+// NV consecutive floats from an arbitrarily aligned p, using aligned 16-byte loads (streaming,
+// evict-first); falls back to scalar loads where the aligned window would pass `end`.
+template <int NV>
+__device__ __forceinline__ void load_floats(const float* p, float (&v)[NV], const float* end) {
+  constexpr int NQ = (NV + 6) / 4;
+  const int m = static_cast<int>((reinterpret_cast<uintptr_t>(p) >> 2) & 3);
+  const float4* b = reinterpret_cast<const float4*>(p - m);
+  if (reinterpret_cast<const float*>(b + NQ) <= end) {
+    float buf[NQ * 4];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) reinterpret_cast<float4*>(buf)[q] = __ldcs(b + q);
+    switch (m) {
+#define PPO_SHIFT_CASE(M)                                  \
+  case M:                                                  \
+    _Pragma("unroll") for (int i = 0; i < NV; ++i) v[i] = buf[i + M]; \
+    break;
+      PPO_SHIFT_CASE(0)
+      PPO_SHIFT_CASE(1)
+      PPO_SHIFT_CASE(2)
+      PPO_SHIFT_CASE(3)
+#undef PPO_SHIFT_CASE
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = p[i];
+  }
+}
+template <int NV>
+__device__ __forceinline__ void store_floats(float* p, const float (&v)[NV]) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+    for (int q = 0; q < NV / 4; ++q)
+      reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+#pragma unroll
+    for (int i = (NV / 4) * 4; i < NV; ++i) p[i] = v[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) p[i] = v[i];
+  }
+}
+
 // One warp per rollout stream; 256-step windows from the end; each lane owns 8 steps and
 // the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
 // across lanes with a reverse shuffle scan of affine maps (oracle O2).
@@ -131,16 +173,28 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
       const int64_t t0 = w_start + 8 * lane;
       const int n = (int)max((int64_t)0, min((int64_t)8, w_end - t0));
       float delta[8], cf[8];
+      if (n == 8) {
+        float rv[8], v[9];
+        load_floats<8>(rr + t0, rv, rew + R * L);
+        load_floats<9>(vv + t0, v, val + R * (L + 1));
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (i < n) {
-          const int64_t t = t0 + i;
-          const float nd = dd[t] ? 0.f : 1.f;
-          delta[i] = rr[t] + gamma * nd * vv[t + 1] - vv[t];
+        for (int i = 0; i < 8; ++i) {
+          const float nd = dd[t0 + i] ? 0.f : 1.f;
+          delta[i] = rv[i] + gamma * nd * v[i + 1] - v[i];
           cf[i] = gl * nd;
-        } else {
-          delta[i] = 0.f;
-          cf[i] = 1.f;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < n) {
+            const int64_t t = t0 + i;
+            const float nd = dd[t] ? 0.f : 1.f;
+            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vv[t];
+            cf[i] = gl * nd;
+          } else {
+            delta[i] = 0.f;
+            cf[i] = 1.f;
+          }
         }
       }
       float P = 0.f, Q = 1.f;  // A_first = P + Q * A_after
@@ -161,20 +215,34 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
       const float a_first = P + Q * carry;
       float a = __shfl_down_sync(0xffffffffu, a_first, 1);
       if (lane == 31) a = carry;
+      float Aout[8];
 #pragma unroll
       for (int i = 7; i >= 0; --i) {
-        if (i < n) {
-          const int64_t t = t0 + i;
-          a = delta[i] + cf[i] * a;
-          int64_t o;
-          if (seq_T > 0) {
-            const int64_t k = t / seq_T, tt = t - k * seq_T;
-            o = tt * nseq + r * spr + k;
-          } else {
-            o = r * L + t;
+        a = delta[i] + cf[i] * a;
+        Aout[i] = a;
+      }
+      if (seq_T == 0 && n == 8) {
+        float vr[8], Rout[8];
+        load_floats<8>(vv + t0, vr, val + R * (L + 1));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Rout[i] = Aout[i] + vr[i];
+        store_floats<8>(adv + r * L + t0, Aout);
+        store_floats<8>(ret + r * L + t0, Rout);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < n) {
+            const int64_t t = t0 + i;
+            int64_t o;
+            if (seq_T > 0) {
+              const int64_t k = t / seq_T, tt = t - k * seq_T;
+              o = tt * nseq + r * spr + k;
+            } else {
+              o = r * L + t;
+            }
+            adv[o] = Aout[i];
+            ret[o] = Aout[i] + vv[t];
           }
-          adv[o] = a;
-          ret[o] = a + vv[t];
         }
       }
       carry = __shfl_sync(0xffffffffu, a_first, 0);
@@ -222,7 +290,9 @@ __global__ void __launch_bounds__(256) gae_long_kernel(
   if (tid == 0) s_chunk = (int)atomicAdd(counter, 1u);
   __syncthreads();
   const int64_t g = s_chunk;
-  const int64_t r = g / nck, j = g - r * nck;           // j-th chunk from the end
+  // chunk j (from the end) of every stream before chunk j+1 of any: a chunk's predecessor
+  // (chunk j-1 of the same stream, index g - R) was dispatched R blocks earlier
+  const int64_t j = g / R, r = g - j * R;
   const int64_t c_end = L - j * kGaeChunk;
   const int64_t c_begin = c_end > kGaeChunk ? c_end - kGaeChunk : 0;
   const int64_t t0 = c_begin + (int64_t)tid * PER;
@@ -233,26 +303,23 @@ __global__ void __launch_bounds__(256) gae_long_kernel(
   const float gl = gamma * lam;
 
   float delta[PER], cf[PER];
-  const bool vec = n == PER && ((r * L + t0) & 3) == 0 && ((r * (L + 1) + t0) & 3) == 0;
-  if (vec) {
+  const bool full = n == PER;
+  if (full) {
     float rv[PER], v[PER + 1];
+    load_floats<PER>(rr + t0, rv, rew + R * L);
+    load_floats<PER + 1>(vv + t0, v, val + R * (L + 1));
     uint8_t d[PER];
+    if (((reinterpret_cast<uintptr_t>(dd + t0)) & 15) == 0) {
+      const uint4* dq = reinterpret_cast<const uint4*>(dd + t0);
+      const uint4 d0 = dq[0], d1 = dq[1];
 #pragma unroll
-    for (int q = 0; q < PER / 4; ++q) {
-      const float4 a = __ldcs(reinterpret_cast<const float4*>(rr + t0) + q);
-      const float4 b = __ldcs(reinterpret_cast<const float4*>(vv + t0) + q);
-      rv[4 * q] = a.x; rv[4 * q + 1] = a.y; rv[4 * q + 2] = a.z; rv[4 * q + 3] = a.w;
-      v[4 * q] = b.x; v[4 * q + 1] = b.y; v[4 * q + 2] = b.z; v[4 * q + 3] = b.w;
-    }
-    v[PER] = vv[t0 + PER];
-    const uint4* dq = reinterpret_cast<const uint4*>(dd + t0);
-    uint4 d0 = dq[0], d1 = dq[1];
-    const uint8_t* b0 = reinterpret_cast<const uint8_t*>(&d0);
-    const uint8_t* b1 = reinterpret_cast<const uint8_t*>(&d1);
+      for (int i = 0; i < 16; ++i) {
+        d[i] = reinterpret_cast<const uint8_t*>(&d0)[i];
+        d[16 + i] = reinterpret_cast<const uint8_t*>(&d1)[i];
+      }
+    } else {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      d[i] = b0[i];
-      d[16 + i] = b1[i];
+      for (int i = 0; i < PER; ++i) d[i] = dd[t0 + i];
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
@@ -312,7 +379,7 @@ __global__ void __launch_bounds__(256) gae_long_kernel(
       gae_publish(me, aP, aQ, 0.f, 1u);
       // (3) look back over later chunks: compose aggregates until an inclusive value
       float cP = 0.f, cQ = 1.f;  // composed map of the chunks between
-      for (int64_t k = g - 1;; --k) {
+      for (int64_t k = g - R;; k -= R) {
         unsigned int f;
         do {
           f = gae_flag(status + k);
@@ -341,16 +408,13 @@ __global__ void __launch_bounds__(256) gae_long_kernel(
     a = delta[i] + cf[i] * a;
     A_out[i] = a;
   }
-  if (vec && seq_T == 0) {
+  if (full && seq_T == 0) {
+    float vr[PER];
+    load_floats<PER>(vv + t0, vr, val + R * (L + 1));
 #pragma unroll
-    for (int q = 0; q < PER / 4; ++q) {
-      const float4 v4 = reinterpret_cast<const float4*>(vv + t0)[q];
-      reinterpret_cast<float4*>(adv + r * L + t0)[q] =
-          make_float4(A_out[4 * q], A_out[4 * q + 1], A_out[4 * q + 2], A_out[4 * q + 3]);
-      reinterpret_cast<float4*>(ret + r * L + t0)[q] =
-          make_float4(A_out[4 * q] + v4.x, A_out[4 * q + 1] + v4.y, A_out[4 * q + 2] + v4.z,
-                      A_out[4 * q + 3] + v4.w);
-    }
+    for (int i = 0; i < PER; ++i) vr[i] += A_out[i];
+    store_floats<PER>(adv + r * L + t0, A_out);
+    store_floats<PER>(ret + r * L + t0, vr);
   } else {
     const int64_t spr = seq_T > 0 ? L / seq_T : 0, nseq = R * spr;
 #pragma unroll
