@@ -252,7 +252,7 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
 
 
 // Long rollouts (L > kGaeShortL): chunk-parallel single pass with a decoupled look-back.
-// A block owns a chunk of kGaeChunk = 8192 steps of one stream (32 per thread, vectorised).
+// A block owns a chunk of kGaeChunk = 4096 steps of one stream (16 per thread, vectorised).
 // Chunks are numbered from the END of each stream and handed out in that order by a global
 // counter, so a chunk only waits on chunks dispatched before it.  Each block (1) reduces its
 // steps to an affine map A_first = P + Q A_after, (2) publishes it, (3) looks back over the
@@ -277,11 +277,12 @@ __device__ __forceinline__ unsigned int gae_flag(const GaeStatus* st) {
   return f;
 }
 
-__global__ void __launch_bounds__(256) gae_long_kernel(
+__global__ void __launch_bounds__(256, 3) gae_long_kernel(
     const float* __restrict__ rew, const float* __restrict__ val, const uint8_t* __restrict__ done,
     int64_t R, int64_t L, float gamma, float lam, int seq_T, float* __restrict__ adv,
     float* __restrict__ ret, GaeStatus* __restrict__ status, unsigned int* __restrict__ counter) {
-  constexpr int PER = 32;
+  constexpr int PER = kGaeChunk / 256;
+  static_assert(PER % 16 == 0, "done bytes are loaded as 16-byte vectors");
   __shared__ int s_chunk;
   __shared__ float sP[8], sQ[8];
   __shared__ float s_after;
@@ -311,11 +312,11 @@ __global__ void __launch_bounds__(256) gae_long_kernel(
     uint8_t d[PER];
     if (((reinterpret_cast<uintptr_t>(dd + t0)) & 15) == 0) {
       const uint4* dq = reinterpret_cast<const uint4*>(dd + t0);
-      const uint4 d0 = dq[0], d1 = dq[1];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        d[i] = reinterpret_cast<const uint8_t*>(&d0)[i];
-        d[16 + i] = reinterpret_cast<const uint8_t*>(&d1)[i];
+      for (int q = 0; q < PER / 16; ++q) {
+        const uint4 dv = dq[q];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) d[16 * q + i] = reinterpret_cast<const uint8_t*>(&dv)[i];
       }
     } else {
 #pragma unroll
@@ -805,8 +806,11 @@ int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, con
   PPO_LAUNCH_CHECK("pack_x_kernel");
   return PPO_OK;
 }
+// Warp-per-stream kernel when streams are short or numerous enough to fill the GPU.
+static bool gae_use_short(int64_t R, int64_t L) { return L <= kGaeShortL || R >= 16384; }
+
 size_t gae_scratch_bytes(int64_t R, int64_t L) {
-  if (L <= kGaeShortL) return 0;
+  if (gae_use_short(R, L)) return 0;
   const int64_t nck = (L + kGaeChunk - 1) / kGaeChunk;
   return 256 + (size_t)(R * nck) * sizeof(GaeStatus);
 }
@@ -814,7 +818,7 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
                float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,
                cudaStream_t st) {
   ProfScope _prof("gae", st);
-  if (L <= kGaeShortL) {
+  if (gae_use_short(R, L)) {
     const int64_t threads = R * 32;
     gae_kernel<<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret);
     PPO_LAUNCH_CHECK("gae_kernel");

@@ -30,7 +30,7 @@ int launch_cast_bf16(const float* src, void* dst, size_t n, cudaStream_t st);
 int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, const float* c0,
                   void* xh, float* c, cudaStream_t st);
 constexpr int64_t kGaeShortL = 8192;  // up to this length: one warp per stream
-constexpr int64_t kGaeChunk = 8192;   // longer: chunk-parallel look-back kernel
+constexpr int64_t kGaeChunk = 4096;   // longer: chunk-parallel look-back kernel
 size_t gae_scratch_bytes(int64_t R, int64_t L);
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
                float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,

@@ -64,4 +64,5 @@ def test_null_pointers_rejected(lib):
     rc = lib._lib.ppo_gae(None, None, None, 0, 256, 0.99, 0.95, 0, None, None, None, 0, None)
     assert rc == lib.PPO_OK  # empty input is a no-op
     assert lib.gae_scratch_bytes(4, 256) == 0
-    assert lib.gae_scratch_bytes(1, 10 ** 6) >= 16 * (10 ** 6 // 8192)
+    assert lib.gae_scratch_bytes(1, 10 ** 6) >= 16 * (10 ** 6 // 4096)
+    assert lib.gae_scratch_bytes(20000, 20000) == 0  # enough streams: warp per stream

@@ -55,7 +55,7 @@ def test_tc_gemm_vs_torch(L, mode, M, N, K):
     (1, 6300, 0, 0.0), (7, 300, 0, 0.05), (4, 512, 16, 0.0),
     # long rollouts: chunk-parallel look-back kernel (chunks of 8192 steps), ragged tails
     (1, 20000, 0, 1 / 20000), (3, 100001, 0, 1e-4), (2, 8193, 0, 0.0), (5, 40960, 16, 0.001),
-    (1, 1000000, 0, 1e-5),
+    (1, 1000000, 0, 1e-5), (16384, 9000, 0, 1e-4),
 ])
 def test_gae_parity(L, R, Lr, seq_T, p_done):
     ro = synth.make_rollouts(R, Lr, seed=R + Lr, p_done=p_done)
