@@ -302,6 +302,7 @@ int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,
   const double denom = cfg->denom > 0 ? cfg->denom : (double)p.N;
   p.inv_denom = (float)(1.0 / denom);
   if ((size_t)p.A_pad * 8 * sizeof(float) > 48 * 1024) return fail(PPO_E_SHAPE, "A too large");
+  if (s.A > 6 * 128) return fail(PPO_E_SHAPE, "loss kernel supports A <= 768");
   return launch_loss(p, s.bf16, out, act, head_on, avail, logp_old, adv, ret, valid, dout, logp,
                      stats, (cudaStream_t)st);
 }

@@ -451,6 +451,15 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// Per-row inputs of the loss, loaded for row r+1 while row r computes (latency hiding).
+struct LossRowIn {
+  float4 y[6];                   // lane's share of the 656 head outputs (float4 index lane+32q)
+  int a;                         // act[row][lane]      (lane < n_heads)
+  uint32_t on;                   // head_on[row][lane]  (lane < n_heads)
+  uint32_t av_lo, av_hi;         // avail bytes lane, lane+32 (lane < n0)
+  float lo, At, Rt, w;           // lane 0: logp_old, adv, ret, valid
+};
+
 template <class TD>
 __global__ void __launch_bounds__(256) loss_kernel(
     const float* __restrict__ out, const int32_t* __restrict__ act,
@@ -463,48 +472,84 @@ __global__ void __launch_bounds__(256) loss_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* y = smem_y + warp * p.A_pad;
   const int A = p.A, nh = p.nh, n0 = p.off[1];
+  const int A4 = (A & 3) == 0 ? A / 4 : 0;  // vector path needs 16-byte rows
   float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   uint32_t flags = 0;
-  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.N; row += (int64_t)gridDim.x * 8) {
+  const int64_t stride = (int64_t)gridDim.x * 8;
+
+  auto fetch = [&](int64_t row, LossRowIn& in) {
+    if (row >= p.N) return;
     const float* yr = out + row * A;
-    if ((A & 3) == 0) {
+    if (A4) {
       const float4* y4 = reinterpret_cast<const float4*>(yr);
-      for (int j = lane; j < A / 4; j += 32) reinterpret_cast<float4*>(y)[j] = __ldcs(y4 + j);
-    } else {
-      for (int j = lane; j < A; j += 32) y[j] = __ldcs(yr + j);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int jj = lane + 32 * q;
+        if (jj < A4) in.y[q] = __ldcs(y4 + jj);
+      }
     }
+    in.a = lane < nh ? act[row * nh + lane] : 0;
+    in.on = lane < nh ? head_on[row * nh + lane] : 0u;
     const uint8_t* av = avail + row * n0;
-    const uint32_t m_lo = __ballot_sync(0xffffffffu, lane < n0 && av[lane] != 0);
-    const uint32_t m_hi = __ballot_sync(0xffffffffu, lane + 32 < n0 && av[min(lane + 32, n0 - 1)] != 0);
-    const uint64_t amask = (uint64_t)m_lo | ((uint64_t)m_hi << 32);
+    in.av_lo = lane < n0 ? av[lane] : 0u;
+    in.av_hi = lane + 32 < n0 ? av[lane + 32] : 0u;
+    if (lane == 0) {
+      in.lo = logp_old[row];
+      in.At = adv[row];
+      in.Rt = ret[row];
+      in.w = valid ? (float)valid[row] : 1.f;
+    }
+  };
+  auto stage = [&](int64_t row, const LossRowIn& in) {
+    if (A4) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int jj = lane + 32 * q;
+        if (jj < A4) reinterpret_cast<float4*>(y)[jj] = in.y[q];
+      }
+    } else {
+      const float* yr = out + row * A;
+      for (int jj = lane; jj < A; jj += 32) y[jj] = yr[jj];
+    }
+  };
+
+  int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  LossRowIn cur, nxt;
+  fetch(row, cur);
+  for (; row < p.N; row += stride) {
+    fetch(row + stride, nxt);  // next row's loads in flight while this one computes
+    stage(row, cur);
     __syncwarp();
-    const float w = valid ? (float)valid[row] : 1.f;
+    const uint64_t amask = (uint64_t)__ballot_sync(0xffffffffu, cur.av_lo != 0) |
+                           ((uint64_t)__ballot_sync(0xffffffffu, cur.av_hi != 0) << 32);
+    const float w = __shfl_sync(0xffffffffu, cur.w, 0);
     float lse[PPO_MAX_HEADS], Hk[PPO_MAX_HEADS];
     float lpi = 0.f, ent = 0.f;
+#pragma unroll 1
     for (int k = 0; k < nh; ++k) {
       const int s0 = p.off[k], e0 = p.off[k + 1];
       float mx = -INFINITY;
-      for (int j = s0 + lane; j < e0; j += 32)
-        if (k != 0 || ((amask >> (j - s0)) & 1ull)) mx = fmaxf(mx, y[j]);
+      for (int jj = s0 + lane; jj < e0; jj += 32)
+        if (k != 0 || ((amask >> (jj - s0)) & 1ull)) mx = fmaxf(mx, y[jj]);
       mx = warp_max(mx);
       // one exp per element: sum e and sum e*y give lse and the entropy
       // H = -sum p log p = lse - sum p y  (p = e / se, log p = y - lse)
       float se = 0.f, sey = 0.f;
       if (mx != -INFINITY)
-        for (int j = s0 + lane; j < e0; j += 32)
-          if (k != 0 || ((amask >> (j - s0)) & 1ull)) {
-            const float e = expf(y[j] - mx);
+        for (int jj = s0 + lane; jj < e0; jj += 32)
+          if (k != 0 || ((amask >> (jj - s0)) & 1ull)) {
+            const float e = expf(y[jj] - mx);
             se += e;
-            sey = fmaf(e, y[j], sey);
+            sey = fmaf(e, y[jj], sey);
           }
       se = warp_sum(se);
       sey = warp_sum(sey);
       const float l = mx == -INFINITY ? 0.f : mx + logf(se);
-      const float pl = mx == -INFINITY ? 0.f : sey / se - l;  // sum p log p
       lse[k] = l;
-      Hk[k] = -pl;
-      const int a = act[row * nh + k];
-      if (head_on[row * nh + k]) {
+      Hk[k] = mx == -INFINITY ? 0.f : l - sey / se;
+      const int a = __shfl_sync(0xffffffffu, cur.a, k);
+      const bool on = __shfl_sync(0xffffffffu, cur.on, k) != 0u;
+      if (on) {
         const int ac = min(max(a, 0), e0 - s0 - 1);
         lpi += y[s0 + ac] - l;
         ent += Hk[k];
@@ -514,32 +559,34 @@ __global__ void __launch_bounds__(256) loss_kernel(
         if (a < 0 || a >= n0 || !((amask >> a) & 1ull)) flags |= 2u;
       }
     }
-    const float lo = logp_old[row];
+    const float lo = __shfl_sync(0xffffffffu, cur.lo, 0);
+    const float At = __shfl_sync(0xffffffffu, cur.At, 0);
+    const float Rt = __shfl_sync(0xffffffffu, cur.Rt, 0);
     const float rho = expf(lpi - lo);
-    const float At = adv[row];
     const float s1 = rho * At;
     const float s2 = fminf(fmaxf(rho, 1.f - p.clip_eps), 1.f + p.clip_eps) * At;
     const bool unclipped = s1 <= s2;
     const float pg = -fminf(s1, s2);
     const float V = y[A - 1];
-    const float Rt = ret[row];
     const float vf = (V - Rt) * (V - Rt);
     const float lrow = pg + p.c_v * vf - p.c_e * ent;
     const float gpi = unclipped ? -At * rho * w * p.inv_denom : 0.f;
     const float ce = p.c_e * w * p.inv_denom;
     TD* dr = dout + row * A;
+#pragma unroll 1
     for (int k = 0; k < nh; ++k) {
       const int s0 = p.off[k], e0 = p.off[k + 1];
-      const bool on = head_on[row * nh + k] != 0;
-      const int a = act[row * nh + k];
-      for (int j = s0 + lane; j < e0; j += 32) {
+      const bool on = __shfl_sync(0xffffffffu, cur.on, k) != 0u;
+      const int a = __shfl_sync(0xffffffffu, cur.a, k);
+      const float lk = lse[k], hk = Hk[k];
+      for (int jj = s0 + lane; jj < e0; jj += 32) {
         float d = 0.f;
-        if (on && (k != 0 || ((amask >> (j - s0)) & 1ull))) {
-          const float lp = y[j] - lse[k];
+        if (on && (k != 0 || ((amask >> (jj - s0)) & 1ull))) {
+          const float lp = y[jj] - lk;
           const float pj = expf(lp);
-          d = gpi * ((j - s0 == a ? 1.f : 0.f) - pj) + ce * pj * (lp + Hk[k]);
+          d = gpi * ((jj - s0 == a ? 1.f : 0.f) - pj) + ce * pj * (lp + hk);
         }
-        dr[j] = from_f<TD>(d);
+        dr[jj] = from_f<TD>(d);
       }
     }
     if (lane == 0) {
@@ -557,6 +604,7 @@ __global__ void __launch_bounds__(256) loss_kernel(
       }
     }
     __syncwarp();
+    cur = nxt;
   }
   if (lane == 0) {
 #pragma unroll
