@@ -451,14 +451,12 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-// Per-row inputs of the loss, loaded for row r+1 while row r computes (latency hiding).
-struct LossRowIn {
-  float4 y[6];                   // lane's share of the 656 head outputs (float4 index lane+32q)
-  int a;                         // act[row][lane]      (lane < n_heads)
-  uint32_t on;                   // head_on[row][lane]  (lane < n_heads)
-  uint32_t av_lo, av_hi;         // avail bytes lane, lane+32 (lane < n0)
-  float lo, At, Rt, w;           // lane 0: logp_old, adv, ret, valid
-};
+// One warp per row (row = t*B + b).  Lane l holds elements j = l + 32 i (i < 24) of the row in
+// registers; the head of each element is precomputed per lane (fixed layout).  All per-head
+// reductions (max, sum e, sum e*y) run interleaved across the heads, so a row costs three
+// register passes and ~3 x 5 shuffle levels instead of 21 dependent reductions.  Stats go
+// to fixed per-block partial slots, reduced in a fixed order by loss_finalize_kernel.
+constexpr int kLossNE = 24;  // elements per lane (A <= 768)
 
 template <class TD>
 __global__ void __launch_bounds__(256) loss_kernel(
@@ -467,127 +465,165 @@ __global__ void __launch_bounds__(256) loss_kernel(
     const float* __restrict__ logp_old, const float* __restrict__ adv,
     const float* __restrict__ ret, const uint8_t* __restrict__ valid, LossParams p,
     TD* __restrict__ dout, float* __restrict__ logp, float* __restrict__ partials) {
-  extern __shared__ float smem_y[];
   __shared__ float red[8][PPO_STATS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* y = smem_y + warp * p.A_pad;
   const int A = p.A, nh = p.nh, n0 = p.off[1];
-  const int A4 = (A & 3) == 0 ? A / 4 : 0;  // vector path needs 16-byte rows
+  // head index of each of this lane's elements (4 bits each; 15 = value / past the end)
+  uint32_t hk_lo = 0, hk_hi = 0, hk_mid = 0;
+#pragma unroll
+  for (int i = 0; i < kLossNE; ++i) {
+    const int jj = lane + 32 * i;
+    int k = 15;
+    if (jj < A - 1) {
+      k = 0;
+#pragma unroll
+      for (int q = 1; q < PPO_MAX_HEADS; ++q) k += (q < nh && jj >= p.off[q]) ? 1 : 0;
+    }
+    if (i < 8) hk_lo |= (uint32_t)k << (4 * i);
+    else if (i < 16) hk_mid |= (uint32_t)k << (4 * (i - 8));
+    else hk_hi |= (uint32_t)k << (4 * (i - 16));
+  }
+  auto head_of = [&](int i) -> int {
+    return i < 8 ? (hk_lo >> (4 * i)) & 15 : i < 16 ? (hk_mid >> (4 * (i - 8))) & 15
+                                                   : (hk_hi >> (4 * (i - 16))) & 15;
+  };
   float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   uint32_t flags = 0;
-  const int64_t stride = (int64_t)gridDim.x * 8;
-
-  auto fetch = [&](int64_t row, LossRowIn& in) {
-    if (row >= p.N) return;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.N; row += (int64_t)gridDim.x * 8) {
     const float* yr = out + row * A;
-    if (A4) {
-      const float4* y4 = reinterpret_cast<const float4*>(yr);
+    float y[kLossNE];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        const int jj = lane + 32 * q;
-        if (jj < A4) in.y[q] = __ldcs(y4 + jj);
-      }
+    for (int i = 0; i < kLossNE; ++i) {
+      const int jj = lane + 32 * i;
+      y[i] = jj < A ? __ldcs(yr + jj) : 0.f;
     }
-    in.a = lane < nh ? act[row * nh + lane] : 0;
-    in.on = lane < nh ? head_on[row * nh + lane] : 0u;
+    const int a_l = lane < nh ? act[row * nh + lane] : 0;
+    const uint32_t on_l = lane < nh ? head_on[row * nh + lane] : 0u;
     const uint8_t* av = avail + row * n0;
-    in.av_lo = lane < n0 ? av[lane] : 0u;
-    in.av_hi = lane + 32 < n0 ? av[lane + 32] : 0u;
-    if (lane == 0) {
-      in.lo = logp_old[row];
-      in.At = adv[row];
-      in.Rt = ret[row];
-      in.w = valid ? (float)valid[row] : 1.f;
-    }
-  };
-  auto stage = [&](int64_t row, const LossRowIn& in) {
-    if (A4) {
+    const uint64_t amask =
+        (uint64_t)__ballot_sync(0xffffffffu, lane < n0 && av[lane] != 0) |
+        ((uint64_t)__ballot_sync(0xffffffffu, lane + 32 < n0 && av[min(lane + 32, n0 - 1)] != 0) << 32);
+    const float w = valid ? (float)valid[row] : 1.f;
+    const float lo = logp_old[row], At = adv[row], Rt = ret[row];
+    // allowed(i): element belongs to a head and, for the primary head, is available
+    auto allowed = [&](int i, int k) -> bool {
+      const int jj = lane + 32 * i;
+      return k < nh && (k != 0 || ((amask >> jj) & 1ull));
+    };
+    // pass 1: per-head max
+    float mx[PPO_MAX_HEADS];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        const int jj = lane + 32 * q;
-        if (jj < A4) reinterpret_cast<float4*>(y)[jj] = in.y[q];
-      }
-    } else {
-      const float* yr = out + row * A;
-      for (int jj = lane; jj < A; jj += 32) y[jj] = yr[jj];
+    for (int k = 0; k < PPO_MAX_HEADS; ++k) mx[k] = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kLossNE; ++i) {
+      const int k = head_of(i);
+#pragma unroll
+      for (int q = 0; q < PPO_MAX_HEADS; ++q)
+        if (q == k && allowed(i, k)) mx[q] = fmaxf(mx[q], y[i]);
     }
-  };
-
-  int64_t row = (int64_t)blockIdx.x * 8 + warp;
-  LossRowIn cur, nxt;
-  fetch(row, cur);
-  for (; row < p.N; row += stride) {
-    fetch(row + stride, nxt);  // next row's loads in flight while this one computes
-    stage(row, cur);
-    __syncwarp();
-    const uint64_t amask = (uint64_t)__ballot_sync(0xffffffffu, cur.av_lo != 0) |
-                           ((uint64_t)__ballot_sync(0xffffffffu, cur.av_hi != 0) << 32);
-    const float w = __shfl_sync(0xffffffffu, cur.w, 0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < PPO_MAX_HEADS; ++q) mx[q] = fmaxf(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], o));
+    // pass 2: sum e and sum e*y per head (one exp per element)
+    float se[PPO_MAX_HEADS], sey[PPO_MAX_HEADS];
+#pragma unroll
+    for (int q = 0; q < PPO_MAX_HEADS; ++q) se[q] = sey[q] = 0.f;
+#pragma unroll
+    for (int i = 0; i < kLossNE; ++i) {
+      const int k = head_of(i);
+      if (allowed(i, k)) {
+        float m = 0.f;
+#pragma unroll
+        for (int q = 0; q < PPO_MAX_HEADS; ++q) m = q == k ? mx[q] : m;
+        const float e = expf(y[i] - m);
+#pragma unroll
+        for (int q = 0; q < PPO_MAX_HEADS; ++q)
+          if (q == k) {
+            se[q] += e;
+            sey[q] = fmaf(e, y[i], sey[q]);
+          }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < PPO_MAX_HEADS; ++q) {
+        se[q] += __shfl_xor_sync(0xffffffffu, se[q], o);
+        sey[q] += __shfl_xor_sync(0xffffffffu, sey[q], o);
+      }
+    // per head: lse, entropy H = lse - sum p y; log pi(a) and entropy over the heads read
     float lse[PPO_MAX_HEADS], Hk[PPO_MAX_HEADS];
     float lpi = 0.f, ent = 0.f;
-#pragma unroll 1
-    for (int k = 0; k < nh; ++k) {
-      const int s0 = p.off[k], e0 = p.off[k + 1];
-      float mx = -INFINITY;
-      for (int jj = s0 + lane; jj < e0; jj += 32)
-        if (k != 0 || ((amask >> (jj - s0)) & 1ull)) mx = fmaxf(mx, y[jj]);
-      mx = warp_max(mx);
-      // one exp per element: sum e and sum e*y give lse and the entropy
-      // H = -sum p log p = lse - sum p y  (p = e / se, log p = y - lse)
-      float se = 0.f, sey = 0.f;
-      if (mx != -INFINITY)
-        for (int jj = s0 + lane; jj < e0; jj += 32)
-          if (k != 0 || ((amask >> (jj - s0)) & 1ull)) {
-            const float e = expf(y[jj] - mx);
-            se += e;
-            sey = fmaf(e, y[jj], sey);
-          }
-      se = warp_sum(se);
-      sey = warp_sum(sey);
-      const float l = mx == -INFINITY ? 0.f : mx + logf(se);
-      lse[k] = l;
-      Hk[k] = mx == -INFINITY ? 0.f : l - sey / se;
-      const int a = __shfl_sync(0xffffffffu, cur.a, k);
-      const bool on = __shfl_sync(0xffffffffu, cur.on, k) != 0u;
-      if (on) {
-        const int ac = min(max(a, 0), e0 - s0 - 1);
-        lpi += y[s0 + ac] - l;
-        ent += Hk[k];
-      }
-      if (k == 0 && w != 0.f) {
-        if (amask == 0) flags |= 4u;
-        if (a < 0 || a >= n0 || !((amask >> a) & 1ull)) flags |= 2u;
+#pragma unroll
+    for (int q = 0; q < PPO_MAX_HEADS; ++q) {
+      const bool none = mx[q] == -INFINITY;
+      lse[q] = none ? 0.f : mx[q] + logf(se[q]);
+      Hk[q] = none ? 0.f : lse[q] - sey[q] / se[q];
+      if (q < nh) {
+        const int a = __shfl_sync(0xffffffffu, a_l, q);
+        const bool on = __shfl_sync(0xffffffffu, on_l, q) != 0u;
+        const int sz = p.off[q + 1] - p.off[q];
+        const int ja = p.off[q] + min(max(a, 0), sz - 1);
+        // y[ja] lives in lane ja % 32, register ja / 32
+        float yv = 0.f;
+#pragma unroll
+        for (int i = 0; i < kLossNE; ++i) yv = (i == ja / 32) ? y[i] : yv;
+        yv = __shfl_sync(0xffffffffu, yv, ja & 31);
+        if (on) {
+          lpi += yv - lse[q];
+          ent += Hk[q];
+        }
+        if (q == 0 && w != 0.f) {
+          if (amask == 0) flags |= 4u;
+          if (a < 0 || a >= n0 || !((amask >> a) & 1ull)) flags |= 2u;
+        }
       }
     }
-    const float lo = __shfl_sync(0xffffffffu, cur.lo, 0);
-    const float At = __shfl_sync(0xffffffffu, cur.At, 0);
-    const float Rt = __shfl_sync(0xffffffffu, cur.Rt, 0);
     const float rho = expf(lpi - lo);
     const float s1 = rho * At;
     const float s2 = fminf(fmaxf(rho, 1.f - p.clip_eps), 1.f + p.clip_eps) * At;
     const bool unclipped = s1 <= s2;
     const float pg = -fminf(s1, s2);
-    const float V = y[A - 1];
+    float V = 0.f;
+#pragma unroll
+    for (int i = 0; i < kLossNE; ++i) V = (i == (A - 1) / 32) ? y[i] : V;
+    V = __shfl_sync(0xffffffffu, V, (A - 1) & 31);
     const float vf = (V - Rt) * (V - Rt);
     const float lrow = pg + p.c_v * vf - p.c_e * ent;
     const float gpi = unclipped ? -At * rho * w * p.inv_denom : 0.f;
     const float ce = p.c_e * w * p.inv_denom;
+    // pass 3: gradient (O7).  Per-head constants in registers: the taken action as an index
+    // into the row (p.off[q] + a_q; -1 if the head is not read) and lse, H.
+    int ja_h[PPO_MAX_HEADS];
+#pragma unroll
+    for (int q = 0; q < PPO_MAX_HEADS; ++q) {
+      const int a = __shfl_sync(0xffffffffu, a_l, q);
+      const bool on = __shfl_sync(0xffffffffu, on_l, q) != 0u;
+      ja_h[q] = (q < nh && on) ? p.off[q] + a : -1;
+    }
     TD* dr = dout + row * A;
-#pragma unroll 1
-    for (int k = 0; k < nh; ++k) {
-      const int s0 = p.off[k], e0 = p.off[k + 1];
-      const bool on = __shfl_sync(0xffffffffu, cur.on, k) != 0u;
-      const int a = __shfl_sync(0xffffffffu, cur.a, k);
-      const float lk = lse[k], hk = Hk[k];
-      for (int jj = s0 + lane; jj < e0; jj += 32) {
-        float d = 0.f;
-        if (on && (k != 0 || ((amask >> (jj - s0)) & 1ull))) {
-          const float lp = y[jj] - lk;
-          const float pj = expf(lp);
-          d = gpi * ((jj - s0 == a ? 1.f : 0.f) - pj) + ce * pj * (lp + hk);
+#pragma unroll
+    for (int i = 0; i < kLossNE; ++i) {
+      const int jj = lane + 32 * i;
+      if (jj >= A - 1) continue;
+      const int k = head_of(i);
+      int ja = -1;
+      float l = 0.f, h = 0.f;
+#pragma unroll
+      for (int q = 0; q < PPO_MAX_HEADS; ++q)
+        if (q == k) {
+          l = lse[q];
+          h = Hk[q];
+          ja = ja_h[q];
         }
-        dr[jj] = from_f<TD>(d);
+      float d = 0.f;
+      if (ja >= 0 && allowed(i, k)) {
+        const float lp = y[i] - l;
+        const float pj = expf(lp);
+        d = gpi * ((jj == ja ? 1.f : 0.f) - pj) + ce * pj * (lp + h);
       }
+      dr[jj] = from_f<TD>(d);
     }
     if (lane == 0) {
       dr[A - 1] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
@@ -603,8 +639,6 @@ __global__ void __launch_bounds__(256) loss_kernel(
         acc[6] += w;
       }
     }
-    __syncwarp();
-    cur = nxt;
   }
   if (lane == 0) {
 #pragma unroll
@@ -887,7 +921,7 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
                 const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
                 const float* adv, const float* ret, const uint8_t* valid, void* dout, float* logp,
                 float* stats, cudaStream_t st) {
-  const size_t smem = 8 * (size_t)p.A_pad * sizeof(float);
+  const size_t smem = 0;
   float* partials = stats + PPO_STATS;
   {
   ProfScope _prof("loss", st);
