@@ -437,9 +437,6 @@ __global__ void __launch_bounds__(256, 3) gae_long_kernel(
 }
 
 // ============================================================================ PPO loss
-// One warp per row (row = t*B + b); the row is staged in shared memory; per head a masked
-// log-sum-exp, the entropy, then the analytic gradient (oracle O6/O7).  Statistics go to
-// fixed per-block partial slots and a second kernel reduces them in a fixed order.
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -451,13 +448,9 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-// One warp per row (row = t*B + b).  Lane l holds elements j = l + 32 i (i < 24) of the row in
-// registers; the head of each element is precomputed per lane (fixed layout).  All per-head
-// reductions (max, sum e, sum e*y) run interleaved across the heads, so a row costs three
-// register passes and ~3 x 5 shuffle levels instead of 21 dependent reductions.  Stats go
-// to fixed per-block partial slots, reduced in a fixed order by loss_finalize_kernel.
-constexpr int kLossNE = 24;  // elements per lane (A <= 768)
-
+// One warp per row (row = t*B + b); the row is staged in shared memory; per head a masked
+// log-sum-exp, the entropy, then the analytic gradient (oracle O6/O7).  Statistics go to
+// fixed per-block partial slots and a second kernel reduces them in a fixed order.
 template <class TD>
 __global__ void __launch_bounds__(256) loss_kernel(
     const float* __restrict__ out, const int32_t* __restrict__ act,
@@ -465,119 +458,64 @@ __global__ void __launch_bounds__(256) loss_kernel(
     const float* __restrict__ logp_old, const float* __restrict__ adv,
     const float* __restrict__ ret, const uint8_t* __restrict__ valid, LossParams p,
     TD* __restrict__ dout, float* __restrict__ logp, float* __restrict__ partials) {
+  extern __shared__ float smem_y[];
   __shared__ float red[8][PPO_STATS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* y = smem_y + warp * p.A_pad;
   const int A = p.A, nh = p.nh, n0 = p.off[1];
-  // head index of each of this lane's elements (4 bits each; 15 = value / past the end)
-  uint32_t hk_lo = 0, hk_hi = 0, hk_mid = 0;
-#pragma unroll
-  for (int i = 0; i < kLossNE; ++i) {
-    const int jj = lane + 32 * i;
-    int k = 15;
-    if (jj < A - 1) {
-      k = 0;
-#pragma unroll
-      for (int q = 1; q < PPO_MAX_HEADS; ++q) k += (q < nh && jj >= p.off[q]) ? 1 : 0;
-    }
-    if (i < 8) hk_lo |= (uint32_t)k << (4 * i);
-    else if (i < 16) hk_mid |= (uint32_t)k << (4 * (i - 8));
-    else hk_hi |= (uint32_t)k << (4 * (i - 16));
-  }
-  auto head_of = [&](int i) -> int {
-    return i < 8 ? (hk_lo >> (4 * i)) & 15 : i < 16 ? (hk_mid >> (4 * (i - 8))) & 15
-                                                   : (hk_hi >> (4 * (i - 16))) & 15;
-  };
   float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   uint32_t flags = 0;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.N; row += (int64_t)gridDim.x * 8) {
     const float* yr = out + row * A;
-    float y[kLossNE];
-#pragma unroll
-    for (int i = 0; i < kLossNE; ++i) {
-      const int jj = lane + 32 * i;
-      y[i] = jj < A ? __ldcs(yr + jj) : 0.f;
+    if ((A & 3) == 0) {
+      const float4* y4 = reinterpret_cast<const float4*>(yr);
+      for (int j = lane; j < A / 4; j += 32) reinterpret_cast<float4*>(y)[j] = __ldcs(y4 + j);
+    } else {
+      for (int j = lane; j < A; j += 32) y[j] = __ldcs(yr + j);
     }
+    const uint8_t* av = avail + row * n0;
+    const uint32_t m_lo = __ballot_sync(0xffffffffu, lane < n0 && av[lane] != 0);
+    const uint32_t m_hi = __ballot_sync(0xffffffffu, lane + 32 < n0 && av[min(lane + 32, n0 - 1)] != 0);
+    const uint64_t amask = (uint64_t)m_lo | ((uint64_t)m_hi << 32);
+    __syncwarp();
+    const float w = valid ? (float)valid[row] : 1.f;
+    // per-row metadata loaded lane-parallel once (lane k: head k), broadcast by shuffles
     const int a_l = lane < nh ? act[row * nh + lane] : 0;
     const uint32_t on_l = lane < nh ? head_on[row * nh + lane] : 0u;
-    const uint8_t* av = avail + row * n0;
-    const uint64_t amask =
-        (uint64_t)__ballot_sync(0xffffffffu, lane < n0 && av[lane] != 0) |
-        ((uint64_t)__ballot_sync(0xffffffffu, lane + 32 < n0 && av[min(lane + 32, n0 - 1)] != 0) << 32);
-    const float w = valid ? (float)valid[row] : 1.f;
     const float lo = logp_old[row], At = adv[row], Rt = ret[row];
-    // allowed(i): element belongs to a head and, for the primary head, is available
-    auto allowed = [&](int i, int k) -> bool {
-      const int jj = lane + 32 * i;
-      return k < nh && (k != 0 || ((amask >> jj) & 1ull));
-    };
-    // pass 1: per-head max
-    float mx[PPO_MAX_HEADS];
-#pragma unroll
-    for (int k = 0; k < PPO_MAX_HEADS; ++k) mx[k] = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < kLossNE; ++i) {
-      const int k = head_of(i);
-#pragma unroll
-      for (int q = 0; q < PPO_MAX_HEADS; ++q)
-        if (q == k && allowed(i, k)) mx[q] = fmaxf(mx[q], y[i]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int q = 0; q < PPO_MAX_HEADS; ++q) mx[q] = fmaxf(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], o));
-    // pass 2: sum e and sum e*y per head (one exp per element)
-    float se[PPO_MAX_HEADS], sey[PPO_MAX_HEADS];
-#pragma unroll
-    for (int q = 0; q < PPO_MAX_HEADS; ++q) se[q] = sey[q] = 0.f;
-#pragma unroll
-    for (int i = 0; i < kLossNE; ++i) {
-      const int k = head_of(i);
-      if (allowed(i, k)) {
-        float m = 0.f;
-#pragma unroll
-        for (int q = 0; q < PPO_MAX_HEADS; ++q) m = q == k ? mx[q] : m;
-        const float e = expf(y[i] - m);
-#pragma unroll
-        for (int q = 0; q < PPO_MAX_HEADS; ++q)
-          if (q == k) {
-            se[q] += e;
-            sey[q] = fmaf(e, y[i], sey[q]);
-          }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int q = 0; q < PPO_MAX_HEADS; ++q) {
-        se[q] += __shfl_xor_sync(0xffffffffu, se[q], o);
-        sey[q] += __shfl_xor_sync(0xffffffffu, sey[q], o);
-      }
-    // per head: lse, entropy H = lse - sum p y; log pi(a) and entropy over the heads read
     float lse[PPO_MAX_HEADS], Hk[PPO_MAX_HEADS];
     float lpi = 0.f, ent = 0.f;
-#pragma unroll
-    for (int q = 0; q < PPO_MAX_HEADS; ++q) {
-      const bool none = mx[q] == -INFINITY;
-      lse[q] = none ? 0.f : mx[q] + logf(se[q]);
-      Hk[q] = none ? 0.f : lse[q] - sey[q] / se[q];
-      if (q < nh) {
-        const int a = __shfl_sync(0xffffffffu, a_l, q);
-        const bool on = __shfl_sync(0xffffffffu, on_l, q) != 0u;
-        const int sz = p.off[q + 1] - p.off[q];
-        const int ja = p.off[q] + min(max(a, 0), sz - 1);
-        // y[ja] lives in lane ja % 32, register ja / 32
-        float yv = 0.f;
-#pragma unroll
-        for (int i = 0; i < kLossNE; ++i) yv = (i == ja / 32) ? y[i] : yv;
-        yv = __shfl_sync(0xffffffffu, yv, ja & 31);
-        if (on) {
-          lpi += yv - lse[q];
-          ent += Hk[q];
-        }
-        if (q == 0 && w != 0.f) {
-          if (amask == 0) flags |= 4u;
-          if (a < 0 || a >= n0 || !((amask >> a) & 1ull)) flags |= 2u;
-        }
+    for (int k = 0; k < nh; ++k) {
+      const int s0 = p.off[k], e0 = p.off[k + 1];
+      float mx = -INFINITY;
+      for (int j = s0 + lane; j < e0; j += 32)
+        if (k != 0 || ((amask >> (j - s0)) & 1ull)) mx = fmaxf(mx, y[j]);
+      mx = warp_max(mx);
+      // one exp per element: sum e and sum e*y give lse and the entropy
+      // H = -sum p log p = lse - sum p y  (p = e / se, log p = y - lse)
+      float se = 0.f, sey = 0.f;
+      if (mx != -INFINITY)
+        for (int j = s0 + lane; j < e0; j += 32)
+          if (k != 0 || ((amask >> (j - s0)) & 1ull)) {
+            const float e = expf(y[j] - mx);
+            se += e;
+            sey = fmaf(e, y[j], sey);
+          }
+      se = warp_sum(se);
+      sey = warp_sum(sey);
+      const float l = mx == -INFINITY ? 0.f : mx + logf(se);
+      const float pl = mx == -INFINITY ? 0.f : sey / se - l;  // sum p log p
+      lse[k] = l;
+      Hk[k] = -pl;
+      const int a = __shfl_sync(0xffffffffu, a_l, k);
+      if (__shfl_sync(0xffffffffu, on_l, k)) {
+        const int ac = min(max(a, 0), e0 - s0 - 1);
+        lpi += y[s0 + ac] - l;
+        ent += Hk[k];
+      }
+      if (k == 0 && w != 0.f) {
+        if (amask == 0) flags |= 4u;
+        if (a < 0 || a >= n0 || !((amask >> a) & 1ull)) flags |= 2u;
       }
     }
     const float rho = expf(lpi - lo);
@@ -585,45 +523,25 @@ __global__ void __launch_bounds__(256) loss_kernel(
     const float s2 = fminf(fmaxf(rho, 1.f - p.clip_eps), 1.f + p.clip_eps) * At;
     const bool unclipped = s1 <= s2;
     const float pg = -fminf(s1, s2);
-    float V = 0.f;
-#pragma unroll
-    for (int i = 0; i < kLossNE; ++i) V = (i == (A - 1) / 32) ? y[i] : V;
-    V = __shfl_sync(0xffffffffu, V, (A - 1) & 31);
+    const float V = y[A - 1];
     const float vf = (V - Rt) * (V - Rt);
     const float lrow = pg + p.c_v * vf - p.c_e * ent;
     const float gpi = unclipped ? -At * rho * w * p.inv_denom : 0.f;
     const float ce = p.c_e * w * p.inv_denom;
-    // pass 3: gradient (O7).  Per-head constants in registers: the taken action as an index
-    // into the row (p.off[q] + a_q; -1 if the head is not read) and lse, H.
-    int ja_h[PPO_MAX_HEADS];
-#pragma unroll
-    for (int q = 0; q < PPO_MAX_HEADS; ++q) {
-      const int a = __shfl_sync(0xffffffffu, a_l, q);
-      const bool on = __shfl_sync(0xffffffffu, on_l, q) != 0u;
-      ja_h[q] = (q < nh && on) ? p.off[q] + a : -1;
-    }
     TD* dr = dout + row * A;
-#pragma unroll
-    for (int i = 0; i < kLossNE; ++i) {
-      const int jj = lane + 32 * i;
-      if (jj >= A - 1) continue;
-      const int k = head_of(i);
-      int ja = -1;
-      float l = 0.f, h = 0.f;
-#pragma unroll
-      for (int q = 0; q < PPO_MAX_HEADS; ++q)
-        if (q == k) {
-          l = lse[q];
-          h = Hk[q];
-          ja = ja_h[q];
+    for (int k = 0; k < nh; ++k) {
+      const int s0 = p.off[k], e0 = p.off[k + 1];
+      const bool on = __shfl_sync(0xffffffffu, on_l, k) != 0u;
+      const int a = __shfl_sync(0xffffffffu, a_l, k);
+      for (int j = s0 + lane; j < e0; j += 32) {
+        float d = 0.f;
+        if (on && (k != 0 || ((amask >> (j - s0)) & 1ull))) {
+          const float lp = y[j] - lse[k];
+          const float pj = expf(lp);
+          d = gpi * ((j - s0 == a ? 1.f : 0.f) - pj) + ce * pj * (lp + Hk[k]);
         }
-      float d = 0.f;
-      if (ja >= 0 && allowed(i, k)) {
-        const float lp = y[i] - l;
-        const float pj = expf(lp);
-        d = gpi * ((jj == ja ? 1.f : 0.f) - pj) + ce * pj * (lp + h);
+        dr[j] = from_f<TD>(d);
       }
-      dr[jj] = from_f<TD>(d);
     }
     if (lane == 0) {
       dr[A - 1] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
@@ -639,6 +557,7 @@ __global__ void __launch_bounds__(256) loss_kernel(
         acc[6] += w;
       }
     }
+    __syncwarp();
   }
   if (lane == 0) {
 #pragma unroll
@@ -921,7 +840,7 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
                 const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
                 const float* adv, const float* ret, const uint8_t* valid, void* dout, float* logp,
                 float* stats, cudaStream_t st) {
-  const size_t smem = 0;
+  const size_t smem = 8 * (size_t)p.A_pad * sizeof(float);
   float* partials = stats + PPO_STATS;
   {
   ProfScope _prof("loss", st);
