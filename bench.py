@@ -366,13 +366,26 @@ def main():
                 ent.update(bound="hbm", achieved=ach, unit="GB/s", peak=pk["hbm_gbs"],
                            frac=ach / pk["hbm_gbs"])
         kernels[tag] = ent
+    # DRAM traffic per launch from the committed ncu --set full capture of this config
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            traffic = json.load(f)["kernels"]
+    except (OSError, KeyError, ValueError):
+        pass
+    for tag, ent in kernels.items():
+        if tag in traffic:
+            ent["traffic_per_launch"] = traffic[tag]["dram_bytes_per_launch"]
     dom = max((k for k in kernels if "achieved" in kernels[k]),
               key=lambda k: kernels[k]["ms_per_step"])
     d = kernels[dom]
     n_launch = sum(n for n, _ in prof.values())
     step_flop = sum(w for k, (kind, w) in alg.items() if kind == "flop")
     roofline = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
-                "unit": d["unit"], "frac": d["frac"], "traffic": None, "kernel": dom,
+                "unit": d["unit"], "frac": d["frac"],
+                "traffic": traffic.get(dom, {}).get("dram_bytes_per_launch") if B == 38400 else None,
+                "traffic_source": "profiles/r01_traffic.json (ncu --set full, B=38400)",
+                "kernel": dom, "launches_per_step": d["launches_per_step"],
                 "peak_source": pk["source"] + (" sustained" if d["bound"] == "tensor" else ""),
                 "step_tflops": step_flop / (ms_step / 1e3) / 1e12,
                 "step_frac_of_sustained_bf16": step_flop / (ms_step / 1e3) / 1e12 / pk["bf16_tflops_sustained"]}
