@@ -133,7 +133,8 @@ int lstm_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes /* host */);
  *    rollout states.  out: [T][B][A] fp32 head outputs (655 logits + value).
  * Computes z_t = [x_t | h_{t-1} | 1] W_xh_aug^T with the cell (i,f,o sigmoid, g tanh,
  * c_t = f c_{t-1} + i g, h_t = o tanh c_t) fused into the GEMM epilogue, then
- * y = [h_t | 1] W_o_aug^T.  1 <= B; ws_bytes >= lstm_ws_bytes(). */
+ * y = [h_t | 1] W_o_aug^T.  1 <= B; ws_bytes >= lstm_ws_bytes().
+ * x == NULL (and h0, c0 ignored): the inputs were already placed in ws by ppo_gather. */
 int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const float* h0,
                   const float* c0, int64_t B, void* ws, size_t ws_bytes, float* out,
                   ppo_stream_t s);
@@ -181,6 +182,36 @@ int ppo_comm_destroy(ppo_comm* comm);
 int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, size_t n,
               int64_t t, double lr, double b1, double b2, double eps, double clip_sigma,
               ppo_stream_t s);
+
+/* ---- NEXT-1: experience buffer and minibatch gather ----------
+ * The optimizer's experience buffer holds `capacity` sequences (one hero's 16-step sample,
+ * P:924) in sequence-major slots, all arrays device memory owned by the caller:
+ *   x [cap][T][D] (bf16 bits for PPO_PREC_BF16, fp32 otherwise), h0, c0 [cap][H] fp32,
+ *   act [cap][T][n_heads] int32, head_on [cap][T][n_heads] u8, avail [cap][T][head_sizes[0]]
+ *   u8, logp_old, adv, ret [cap][T] fp32, valid [cap][T] u8 (NULL = all valid).
+ * Rollouts push 256-step segments as 16 consecutive slots; their advantages are
+ * computed at ingest with ppo_gae(seq_T = 0) writing adv/ret + slot*T (the segment's 256
+ * steps are contiguous there).  Minibatches are sampled uniformly WITH replacement
+ * (DESIGN Q19) by a counter-based generator the oracle re-implements:
+ *   idx[i] = splitmix64(seed + (step << 32) + i) mod capacity. */
+typedef struct {
+  const void* x;
+  const float *h0, *c0;
+  const int32_t* act;
+  const uint8_t *head_on, *avail;
+  const float *logp_old, *adv, *ret;
+  const uint8_t* valid;
+  int64_t capacity;
+} ppo_buffer;
+int ppo_sample_indices(int64_t capacity, int64_t B, uint64_t seed, uint64_t step, int32_t* idx,
+                       ppo_stream_t s);
+/* Gather B sequences idx[0..B) of the buffer: x, h0, c0 go straight into the workspace (then
+ * call lstm_bptt_fwd with x = NULL); the per-timestep loss inputs are written time-major
+ * [T][B][.] into act, head_on, avail, logp_old, adv, ret and valid (nullable). */
+int ppo_gather(const ppo_dims* dims, const ppo_buffer* buf /* host struct */, const int32_t* idx,
+               int64_t B, void* ws, size_t ws_bytes, int32_t* act, uint8_t* head_on,
+               uint8_t* avail, float* logp_old, float* adv, float* ret, uint8_t* valid,
+               ppo_stream_t s);
 
 /* ---- tracing: CUDA events around every kernel launch ------------------------
  * ppo_prof_start() enables recording (clears previous records); every library launch then

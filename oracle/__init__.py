@@ -19,6 +19,7 @@ Parity status ("Oracle pins"):
   heads + loss   pinned (clip/entropy closed forms, masking invariants, finite differences)
   adam + clip    pinned (textbook Adam via torch.optim.Adam, hand-evaluated steps, clip window)
   dp average     pinned (shard identity)
+  buffer         sampler pinned to splitmix64's published test vector; gather = indexing
   step           composition of the above, pinned end-to-end by finite differences
 """
 from .gae import gamma_from_horizon, gae, segments_to_sequences  # noqa: F401
@@ -26,3 +27,4 @@ from .lstm import lstm_forward, lstm_backward  # noqa: F401
 from .loss import heads_forward, heads_backward, ppo_loss, STAT_NAMES  # noqa: F401
 from .adam import adam_clip  # noqa: F401
 from .step import ppo_step, dp_average  # noqa: F401
+from . import buffer  # noqa: F401

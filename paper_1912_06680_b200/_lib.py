@@ -50,6 +50,13 @@ class ppo_prof_entry(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", c_int32), ("total_ms", c_double)]
 
 
+class ppo_buffer(ctypes.Structure):
+    _fields_ = [("x", c_void_p), ("h0", c_void_p), ("c0", c_void_p), ("act", c_void_p),
+                ("head_on", c_void_p), ("avail", c_void_p), ("logp_old", c_void_p),
+                ("adv", c_void_p), ("ret", c_void_p), ("valid", c_void_p),
+                ("capacity", c_int64)]
+
+
 class PPOError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"libppo5 error {code}: {msg}")
@@ -86,6 +93,9 @@ _lib_fns = dict(
     ppo_comm_destroy=([c_void_p], c_int),
     adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_double,
                 c_double, c_double, c_double, c_double, c_void_p], c_int),
+    ppo_sample_indices=([c_int64, c_int64, ctypes.c_uint64, ctypes.c_uint64, c_void_p, c_void_p], c_int),
+    ppo_gather=([_D, POINTER(ppo_buffer), c_void_p, c_int64, c_void_p, c_size_t] + [c_void_p] * 8,
+                c_int),
     ppo_prof_start=([], c_int),
     ppo_prof_stop=([POINTER(ppo_prof_entry), c_int32, POINTER(c_int32)], c_int),
     ppo_test_tc_gemm=([c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p], c_int),
@@ -173,6 +183,7 @@ def ppo_gae(rew, val, done, gamma, lam, adv, ret, seq_T=0, scratch=None, stream=
 
 
 def lstm_bptt_fwd(dims, w, x, h0, c0, B, ws, out, stream=None):
+    """x = None: inputs already gathered into ws by ppo_gather"""
     _check(_lib.lstm_bptt_fwd(ctypes.byref(dims), _p(w), _p(x), _p(h0), _p(c0), B, _p(ws),
                               ws.numel() * ws.element_size(), _p(out), _s(stream)))
 
@@ -192,6 +203,26 @@ def lstm_bptt_bwd(dims, w, ws, dout, B, grad, stream=None):
 def adam_step(p, p_bf16, g, m, v, t, lr, b1, b2, eps, clip_sigma, stream=None):
     _check(_lib.adam_step(_p(p), _p(p_bf16), _p(g), _p(m), _p(v), p.numel(), t, lr, b1, b2, eps,
                           clip_sigma, _s(stream)))
+
+
+def make_buffer(t: dict, capacity: int) -> ppo_buffer:
+    """ppo_buffer view of a dict of device tensors (keys as in the struct)"""
+    b = ppo_buffer()
+    for k in ("x", "h0", "c0", "act", "head_on", "avail", "logp_old", "adv", "ret", "valid"):
+        setattr(b, k, None if t.get(k) is None else t[k].data_ptr())
+    b.capacity = capacity
+    return b
+
+
+def ppo_sample_indices(capacity, B, seed, step, idx, stream=None):
+    _check(_lib.ppo_sample_indices(capacity, B, seed, step, _p(idx), _s(stream)))
+
+
+def ppo_gather(dims, buf: ppo_buffer, idx, B, ws, act, head_on, avail, logp_old, adv, ret, valid,
+               stream=None):
+    _check(_lib.ppo_gather(ctypes.byref(dims), ctypes.byref(buf), _p(idx), B, _p(ws),
+                           ws.numel() * ws.element_size(), _p(act), _p(head_on), _p(avail),
+                           _p(logp_old), _p(adv), _p(ret), _p(valid), _s(stream)))
 
 
 def comm_unique_id() -> bytes:

@@ -246,16 +246,19 @@ int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const floa
   if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
   if (s.bf16 && B * s.T > (int64_t)INT32_MAX / 2) return fail(PPO_E_SHAPE, "T*B too large");
   NEED(w);
-  NEED(x);
-  NEED(h0);
-  NEED(c0);
   NEED(out);
+  if (x) {
+    NEED(h0);
+    NEED(c0);
+    if (!aligned(x, 16)) return fail(PPO_E_ALIGN, "x is not 16-byte aligned");
+  }
   if (!ws || !aligned(ws, 1024)) return fail(PPO_E_ALIGN, "ws must be 1024-byte aligned");
   WsLayout L = ws_layout(s, B);
   if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small");
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   float* C = reinterpret_cast<float*>(wsb + L.c);
-  if ((rc = launch_pack_x(s, B, x, h0, c0, wsb + L.xh, C, st))) return rc;
+  // x == NULL: inputs already gathered into the workspace (ppo_gather)
+  if (x && (rc = launch_pack_x(s, B, x, h0, c0, wsb + L.xh, C, st))) return rc;
   if (s.bf16) {
     if ((rc = check_tc_device())) return rc;
     return tc_forward(s, B, w, ws, out, st);

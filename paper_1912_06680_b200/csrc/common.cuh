@@ -9,6 +9,8 @@
 
 #include "../../include/ppo5.h"
 
+#include <algorithm>
+
 namespace ppo {
 
 // ---- error plumbing (ppo_last_error is thread-local) -----------------------------------
