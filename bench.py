@@ -44,8 +44,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1, help="oracle sample: sequences per step")
-    ap.add_argument("--config", choices=["full", "gae"], default="full",
-                    help="full: the PPO step (default); gae: GAE-only HBM sweep (configs[3])")
+    ap.add_argument("--config", choices=["full", "gae", "iteration"], default="full",
+                    help="full: the PPO step (default); gae: GAE-only HBM sweep (configs[3]); "
+                         "iteration: NEXT-1, steps drawn from a device experience buffer")
     return ap.parse_args()
 
 
@@ -271,8 +272,77 @@ def run_gae_sweep(args):
         "sweep": rows}), flush=True)
 
 
+def run_iteration(args):
+    """NEXT-1: gradient steps sampled from a device-resident experience buffer (4x the
+    minibatch), GAE at ingest, gather straight into the workspace, version publish every 32."""
+    import torch
+    import synth
+    from paper_1912_06680_b200 import PPOOptimizer, _lib as L
+    from paper_1912_06680_b200.trainer import ExperienceBuffer, PPOTrainer
+    dev = torch.device("cuda", 0)
+    H, D, T, B = args.H, args.D, 16, args.B
+    cap = 4 * B
+    cfg = synth.Config(H=H, D=D, B=B, T=T)
+    opt = PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16", device=dev)
+    prm = synth.torch_params(cfg, 0, dev)
+    opt.load_canonical(prm["Wx"], prm["Wh"], prm["b"], prm["Wo"], prm["bo"])
+    del prm
+    buf = ExperienceBuffer(cap, D, H, T, cfg.head_sizes, bf16=True, device=dev)
+    gamma = 1.0 - (4.0 / 30.0) / 180.0
+    chunk = B  # push in chunks of B sequences (B/16 segments)
+    for c in range(cap // chunk):
+        sq = synth.torch_sequences(synth.Config(H=H, D=D, B=chunk, T=T), 100 + c, dev)
+        ro = synth.torch_rollouts(chunk // 16, 256, 100 + c, dev)
+        seg = dict(x=sq["x"].transpose(0, 1).contiguous(), h0=sq["h0"], c0=sq["c0"],
+                   act=sq["act"].transpose(0, 1).contiguous(),
+                   head_on=sq["head_on"].transpose(0, 1).contiguous(),
+                   avail=sq["avail"].transpose(0, 1).contiguous(),
+                   logp_old=(sq["logp_noise"] - 10.0).transpose(0, 1).contiguous(),
+                   rew=ro["rew"], val=ro["val"], done=ro["done"])
+        buf.push_segments(seg, gamma, 0.95)
+        del sq, ro, seg
+    torch.cuda.empty_cache()
+    tr = PPOTrainer(opt, buf, seed=1)
+    for _ in range(args.warmup):
+        tr.step()
+    torch.cuda.synchronize()
+    L.prof_start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    n = max(args.steps, 1)
+    for i in range(n):
+        tr.step()
+        if tr.global_step % 32 == 0:
+            tr.published.copy_(opt.weights, non_blocking=True)
+            tr.version += 1
+    e1.record()
+    torch.cuda.synchronize()
+    prof = L.prof_stop()
+    ms = e0.elapsed_time(e1) / n
+    pk = peaks()
+    gx = prof.get("gather_x", (0, 0.0))
+    gr = prof.get("gather_rows", (0, 0.0))
+    # gather: read x (T D 2 B) + h0/c0 (8 H) per sequence, write XH x-part + pads + h/c slots
+    gbytes = B * (2.0 * T * D * 2 + 8 * H + 4 * H + 2 * H + (T + 1) * 128)
+    g_ms = gx[1] / n
+    print(json.dumps({
+        "metric": "PPO train samples/s from the experience buffer (NEXT-1)",
+        "value": B / 5 / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": n, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"B={B} sequences/step sampled with replacement from a "
+                               f"{cap}-sequence device buffer (GAE at ingest)"},
+        "gather": {"ms_per_step": g_ms, "rows_ms_per_step": gr[1] / n,
+                   "achieved_GB_s": gbytes / (g_ms / 1e3) / 1e9 if g_ms else None,
+                   "peak": pk["hbm_gbs"]},
+        "kernels": {k: {"launches": c, "ms_per_step": t / n} for k, (c, t) in prof.items()},
+        "sample_reuse": tr.sample_reuse}), flush=True)
+
+
 def main():
     args = parse()
+    if args.config == "iteration":
+        run_iteration(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
