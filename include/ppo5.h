@@ -213,6 +213,30 @@ int ppo_gather(const ppo_dims* dims, const ppo_buffer* buf /* host struct */, co
                uint8_t* avail, float* logp_old, float* adv, float* ret, uint8_t* valid,
                ppo_stream_t s);
 
+/* ---- NEXT-2: reward pipeline fused into GAE (App. Reward Weights P:1058-1079) -----
+ * Per game g and hero i (0-4 one team, 5-9 the other; stream s = 10 g + i):
+ *   rho_i = shaped_i * decay_base^(t_game / decay_seconds) + win_i,   t_game = (step0[g] + l)
+ *           * step_seconds   (0.6^(T / 10 min); win/loss exempt)
+ *   r_i   = (1 - tau) rho_i + tau mean_team(rho) - [zero_sum] mean_enemy(rho)
+ *   r_i  /= sigma, the running std of all final rewards of PREVIOUS calls (1 before any data);
+ *           this call's r then updates stats = {count, mean, M2} (device, fp64)
+ *   then GAE exactly as ppo_gae on the normalised rewards (streams of length L, seq_T layout).
+ * shaped, win [G][10][L]; step0 [G] int32; val [10G][L+1]; done [G][L] (per game); adv, ret
+ * and rew_out (nullable: normalised r) laid out like ppo_gae's outputs for R = 10 G.
+ * scratch: ppo_reward_gae_scratch_bytes() of 8-byte aligned device memory.  DESIGN Q20, Q21. */
+typedef struct {
+  float tau;            /* team spirit, 0.3 -> 0.8 in Rerun */
+  float decay_base;     /* 0.6 */
+  float decay_seconds;  /* 600 (10 minutes of game time) */
+  float step_seconds;   /* 4/30 (frameskip 4 at 30 fps) */
+  int32_t zero_sum;     /* 1: subtract the enemy team's mean reward */
+} ppo_reward_cfg;
+int ppo_reward_gae_scratch_bytes(size_t* bytes /* host */);
+int ppo_reward_gae(const float* shaped, const float* win, const int32_t* step0, int64_t G,
+                   int64_t L, const float* val, const uint8_t* done, const ppo_reward_cfg* cfg,
+                   double* stats, float gamma, float lam, int32_t seq_T, float* rew_out,
+                   float* adv, float* ret, void* scratch, size_t scratch_bytes, ppo_stream_t s);
+
 /* ---- tracing: CUDA events around every kernel launch ------------------------
  * ppo_prof_start() enables recording (clears previous records); every library launch then
  * records a start/end event pair on its stream.  ppo_prof_stop() synchronises those events,

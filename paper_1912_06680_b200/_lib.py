@@ -57,6 +57,11 @@ class ppo_buffer(ctypes.Structure):
                 ("capacity", c_int64)]
 
 
+class ppo_reward_cfg(ctypes.Structure):
+    _fields_ = [("tau", c_float), ("decay_base", c_float), ("decay_seconds", c_float),
+                ("step_seconds", c_float), ("zero_sum", c_int32)]
+
+
 class PPOError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"libppo5 error {code}: {msg}")
@@ -96,6 +101,10 @@ _lib_fns = dict(
     ppo_sample_indices=([c_int64, c_int64, ctypes.c_uint64, ctypes.c_uint64, c_void_p, c_void_p], c_int),
     ppo_gather=([_D, POINTER(ppo_buffer), c_void_p, c_int64, c_void_p, c_size_t] + [c_void_p] * 8,
                 c_int),
+    ppo_reward_gae_scratch_bytes=([POINTER(c_size_t)], c_int),
+    ppo_reward_gae=([c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p,
+                     POINTER(ppo_reward_cfg), c_void_p, c_float, c_float, c_int32, c_void_p,
+                     c_void_p, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
     ppo_prof_start=([], c_int),
     ppo_prof_stop=([POINTER(ppo_prof_entry), c_int32, POINTER(c_int32)], c_int),
     ppo_test_tc_gemm=([c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p], c_int),
@@ -223,6 +232,21 @@ def ppo_gather(dims, buf: ppo_buffer, idx, B, ws, act, head_on, avail, logp_old,
     _check(_lib.ppo_gather(ctypes.byref(dims), ctypes.byref(buf), _p(idx), B, _p(ws),
                            ws.numel() * ws.element_size(), _p(act), _p(head_on), _p(avail),
                            _p(logp_old), _p(adv), _p(ret), _p(valid), _s(stream)))
+
+
+def reward_gae_scratch_bytes() -> int:
+    n = c_size_t()
+    _check(_lib.ppo_reward_gae_scratch_bytes(ctypes.byref(n)))
+    return n.value
+
+
+def ppo_reward_gae(shaped, win, step0, val, done, cfg, stats, gamma, lam, adv, ret, scratch,
+                   seq_T=0, rew_out=None, stream=None):
+    G, _, Lr = shaped.shape
+    _check(_lib.ppo_reward_gae(_p(shaped), _p(win), _p(step0), G, Lr, _p(val), _p(done),
+                               ctypes.byref(cfg), _p(stats), gamma, lam, seq_T, _p(rew_out),
+                               _p(adv), _p(ret), _p(scratch),
+                               scratch.numel() * scratch.element_size(), _s(stream)))
 
 
 def comm_unique_id() -> bytes:

@@ -154,3 +154,210 @@ int ppo_gather(const ppo_dims* dims, const ppo_buffer* buf, const int32_t* idx, 
 }
 
 }  // extern "C"
+
+// ============================================================================ NEXT-2
+// Reward pipeline fused into the GAE load stage (App. Reward Weights P:1058-1079):
+// game-time weighting of the shaped rewards (0.6^(T/10 min); win/loss exempt), team spirit
+// r_i = (1-tau) rho_i + tau mean_team(rho), zero-sum (minus the enemy team's mean), division
+// by the running reward std of the previous calls, then GAE.  One warp per game: a lane owns
+// 8 consecutive steps of all 10 heroes (2 teams x 5), the 10 GAE recurrences are scanned
+// across lanes together.  Per-block partial moments of the (unnormalised) final rewards are
+// merged into the running statistics by reward_stats_kernel afterwards (fixed order).
+namespace ppo {
+namespace {
+
+constexpr int kRewardBlocks = 148 * 4;
+
+__global__ void __launch_bounds__(128) reward_gae_kernel(
+    const float* __restrict__ shaped, const float* __restrict__ win,
+    const int32_t* __restrict__ step0, int64_t G, int64_t L, const float* __restrict__ val,
+    const uint8_t* __restrict__ done, ppo_reward_cfg cfg, const double* __restrict__ stats,
+    float gamma, float lam, int seq_T, float* __restrict__ rew_out, float* __restrict__ adv,
+    float* __restrict__ ret, double* __restrict__ partials) {
+  constexpr int NH = 10;
+  __shared__ double red[4][3];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const double cnt = stats[0];
+  const float inv_sigma = cnt > 0 ? (float)(1.0 / sqrt(fmax(stats[2] / cnt, 1e-16))) : 1.f;
+  const float gl = gamma * lam;
+  const float tau = cfg.tau;
+  // 0.6^(T/10 min) = exp2(log2(0.6) * step * T_step / 600)
+  const float dk = log2f(cfg.decay_base) * cfg.step_seconds / cfg.decay_seconds;
+  const int64_t S = G * NH;
+  const int64_t spr = seq_T > 0 ? L / seq_T : 0, nseq = S * spr;
+  double ps = 0.0, pss = 0.0, pn = 0.0;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < G; g += nwarps) {
+    float carry[NH];
+#pragma unroll
+    for (int i = 0; i < NH; ++i) carry[i] = 0.f;
+    const int64_t s0 = g * NH;
+    for (int64_t w_end = L; w_end > 0; w_end -= 256) {
+      const int64_t w_start = w_end > 256 ? w_end - 256 : 0;
+      const int64_t t0 = w_start + 8 * lane;
+      const int n = (int)max((int64_t)0, min((int64_t)8, w_end - t0));
+      // per step: decay, team means of the decayed raw rewards, GAE coefficient
+      float cf[8], dec[8], mA[8], mB[8], nds[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool ok = e < n;
+        const int64_t t = t0 + e;
+        nds[e] = ok && !done[g * L + t] ? 1.f : 0.f;
+        cf[e] = ok ? gl * nds[e] : 1.f;
+        dec[e] = ok ? exp2f(dk * (float)(step0[g] + t)) : 0.f;
+        float a = 0.f, b = 0.f;
+        if (ok) {
+#pragma unroll
+          for (int i = 0; i < NH; ++i) {
+            const float rho = shaped[(s0 + i) * L + t] * dec[e] + win[(s0 + i) * L + t];
+            if (i < 5) a += rho;
+            else b += rho;
+          }
+        }
+        mA[e] = 0.2f * a;
+        mB[e] = 0.2f * b;
+      }
+#pragma unroll 1
+      for (int i = 0; i < NH; ++i) {
+        const float* vv = val + (s0 + i) * (L + 1);
+        float delta[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const bool ok = e < n;
+          const int64_t t = t0 + e;
+          float dl = 0.f;
+          if (ok) {
+            const float rho = shaped[(s0 + i) * L + t] * dec[e] + win[(s0 + i) * L + t];
+            const float mt = i < 5 ? mA[e] : mB[e], me = i < 5 ? mB[e] : mA[e];
+            float r = (1.f - tau) * rho + tau * mt;
+            if (cfg.zero_sum) r -= me;
+            ps += r;
+            pss += (double)r * r;
+            pn += 1.0;
+            r *= inv_sigma;
+            if (rew_out) rew_out[(s0 + i) * L + t] = r;
+            dl = r + gamma * nds[e] * vv[t + 1] - vv[t];
+          }
+          delta[e] = dl;
+        }
+        float P = 0.f, Q = 1.f;
+#pragma unroll
+        for (int e = 7; e >= 0; --e) {
+          P = delta[e] + cf[e] * P;
+          Q = cf[e] * Q;
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float P2 = __shfl_down_sync(0xffffffffu, P, off);
+          const float Q2 = __shfl_down_sync(0xffffffffu, Q, off);
+          if (lane + off < 32) {
+            P = P + Q * P2;
+            Q = Q * Q2;
+          }
+        }
+        const float a_first = P + Q * carry[i];
+        float a = __shfl_down_sync(0xffffffffu, a_first, 1);
+        if (lane == 31) a = carry[i];
+#pragma unroll
+        for (int e = 7; e >= 0; --e) {
+          if (e < n) {
+            const int64_t t = t0 + e;
+            a = delta[e] + cf[e] * a;
+            int64_t o;
+            if (seq_T > 0) {
+              const int64_t k = t / seq_T, tt = t - k * seq_T;
+              o = tt * nseq + (s0 + i) * spr + k;
+            } else {
+              o = (s0 + i) * L + t;
+            }
+            adv[o] = a;
+            ret[o] = a + vv[t];
+          }
+        }
+        carry[i] = __shfl_sync(0xffffffffu, a_first, 0);
+      }
+    }
+  }
+  // deterministic partial moments: warp tree, then the block's 4 warps in order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    pss += __shfl_xor_sync(0xffffffffu, pss, o);
+    pn += __shfl_xor_sync(0xffffffffu, pn, o);
+  }
+  if (lane == 0) {
+    red[wib][0] = pn;
+    red[wib][1] = ps;
+    red[wib][2] = pss;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int k = 0; k < 4; ++k) v += red[k][threadIdx.x];
+    partials[blockIdx.x * 3 + threadIdx.x] = v;
+  }
+}
+
+// Merge the batch moments into the running (count, mean, M2): Chan et al. pairwise update.
+__global__ void reward_stats_kernel(const double* __restrict__ partials, int nblocks,
+                                    double* __restrict__ stats) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double nb = 0.0, sb = 0.0, ssb = 0.0;
+  for (int b = 0; b < nblocks; ++b) {
+    nb += partials[3 * b];
+    sb += partials[3 * b + 1];
+    ssb += partials[3 * b + 2];
+  }
+  if (nb <= 0.0) return;
+  const double mb = sb / nb;
+  const double m2b = fmax(ssb - nb * mb * mb, 0.0);
+  const double n0 = stats[0], mean0 = stats[1], m20 = stats[2];
+  const double n = n0 + nb;
+  const double d = mb - mean0;
+  stats[0] = n;
+  stats[1] = mean0 + d * nb / n;
+  stats[2] = m20 + m2b + d * d * n0 * nb / n;
+}
+
+}  // namespace
+}  // namespace ppo
+
+extern "C" {
+
+int ppo_reward_gae_scratch_bytes(size_t* bytes) {
+  if (!bytes) return fail(PPO_E_ARG, "bytes is NULL");
+  *bytes = sizeof(double) * 3 * kRewardBlocks;
+  return PPO_OK;
+}
+
+int ppo_reward_gae(const float* shaped, const float* win, const int32_t* step0, int64_t G,
+                   int64_t L, const float* val, const uint8_t* done, const ppo_reward_cfg* cfg,
+                   double* stats, float gamma, float lam, int32_t seq_T, float* rew_out,
+                   float* adv, float* ret, void* scratch, size_t scratch_bytes,
+                   ppo_stream_t st_) {
+  cudaStream_t st = (cudaStream_t)st_;
+  if (G < 0 || L < 0) return fail(PPO_E_SHAPE, "G and L must be >= 0");
+  if (G == 0 || L == 0) return PPO_OK;
+  if (!shaped || !win || !step0 || !val || !done || !cfg || !stats || !adv || !ret)
+    return fail(PPO_E_ARG, "NULL pointer");
+  if (seq_T < 0 || (seq_T > 0 && L % seq_T)) return fail(PPO_E_SHAPE, "L must be a multiple of seq_T");
+  if (!scratch || scratch_bytes < sizeof(double) * 3 * kRewardBlocks || !aligned(scratch, 8))
+    return fail(PPO_E_ARG, "scratch too small (ppo_reward_gae_scratch_bytes)");
+  if (!(cfg->tau >= 0.f && cfg->tau <= 1.f) || !(cfg->decay_base > 0.f) ||
+      !(cfg->decay_seconds > 0.f) || !(cfg->step_seconds > 0.f))
+    return fail(PPO_E_ARG, "bad reward config");
+  double* partials = static_cast<double*>(scratch);
+  {
+    ProfScope _prof("reward_gae", st);
+    reward_gae_kernel<<<kRewardBlocks, 128, 0, st>>>(shaped, win, step0, G, L, val, done, *cfg,
+                                                     stats, gamma, lam, seq_T, rew_out, adv, ret,
+                                                     partials);
+    PPO_LAUNCH_CHECK("reward_gae_kernel");
+  }
+  ProfScope _prof("reward_stats", st);
+  reward_stats_kernel<<<1, 32, 0, st>>>(partials, kRewardBlocks, stats);
+  PPO_LAUNCH_CHECK("reward_stats_kernel");
+  return PPO_OK;
+}
+
+}  // extern "C"
