@@ -261,7 +261,43 @@ def run_gae_sweep(args):
                          "frac": gbs / pk["hbm_gbs"], "timesteps_per_s": n / (ms / 1e3)})
             del ro, adv, ret, scratch
             torch.cuda.empty_cache()
-    top = max((r for r in rows if r["timesteps"] >= 10 ** 9), key=lambda r: r["GB_s"])
+    # NEXT-2: reward pipeline fused into GAE, 10 heroes per game, L = 256 segments
+    rrows = []
+    for steps in (10 ** 8, 10 ** 9):
+        Lr = 256
+        G = steps // (10 * Lr)
+        n = G * 10 * Lr
+        g = torch.Generator(device=dev).manual_seed(3)
+        shaped = torch.randn((G, 10, Lr), generator=g, device=dev)
+        win = torch.zeros((G, 10, Lr), device=dev)
+        step0 = torch.randint(0, 20000, (G,), generator=g, device=dev, dtype=torch.int32)
+        val = torch.randn((G * 10, Lr + 1), generator=g, device=dev)
+        done = (torch.rand((G, Lr), generator=g, device=dev) < 1e-4).to(torch.uint8)
+        adv = torch.empty((G * 10, Lr), device=dev)
+        ret = torch.empty((G * 10, Lr), device=dev)
+        stats = torch.zeros(3, dtype=torch.float64, device=dev)
+        scratch = torch.empty(L.reward_gae_scratch_bytes(), dtype=torch.uint8, device=dev)
+        cfg = L.ppo_reward_cfg(0.3, 0.6, 600.0, 4.0 / 30.0, 1)
+        call = lambda: L.ppo_reward_gae(shaped, win, step0, val, done, cfg, stats, gamma, 0.95,
+                                        adv, ret, scratch)
+        for _ in range(args.warmup):
+            call()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            call()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        # algorithmic: shaped, win, V in; A, R out (4 B each) + done (1 B per game-step)
+        gbs = (20.0 * n + 1.0 * n / 10) / (ms / 1e3) / 1e9
+        rrows.append({"kernel": "reward_gae", "L": Lr, "games": G, "hero_steps": n, "ms": ms,
+                      "GB_s": gbs, "frac": gbs / pk["hbm_gbs"]})
+        del shaped, win, step0, val, done, adv, ret
+        torch.cuda.empty_cache()
+    rows += rrows
+    top = max((r for r in rows if r.get("timesteps", 0) >= 10 ** 9), key=lambda r: r["GB_s"])
     print(json.dumps({
         "metric": "GAE timesteps/s (configs[3] sweep)", "value": top["timesteps_per_s"],
         "unit": "timesteps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
