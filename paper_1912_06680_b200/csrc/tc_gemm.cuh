@@ -492,25 +492,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 // overlaps the mainloop of tile i+1), 32 KB stages x 6.  MB = 2: 512x256 tiles (two MMAs per
 // K step, one per 128-row block), one accumulator filling all 512 TMEM columns, 48 KB stages
 // x 4 -- 27% less operand traffic per FLOP, for the long-K weight-gradient GEMM.
-template <bool A_MN, bool B_MN, int STAGES, int MB = 1>
+template <bool A_MN, bool B_MN, int STAGES, int MB = 1, int BN = 256>
 struct Smem2 {
-  static constexpr int A_BYTES = MB * BM * BK * 2;  // this CTA's 128 MB rows of A
-  static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's 128 rows (N-half) of B
+  static constexpr int A_BYTES = MB * BM * BK * 2;       // this CTA's 128 MB rows of A
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;      // this CTA's N-half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4 + 2 * kSchedDepth) * 8 + 32 + 1024;
 };
 
-template <bool A_MN, bool B_MN, int STAGES, int MB, class Epi>
+template <bool A_MN, bool B_MN, int STAGES, int MB, int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                     const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
                     const TileShape sh, const Epi epi) {
-  constexpr int BN = 256;
   constexpr int TM = 2 * BM * MB;           // rows per cluster tile
   constexpr int NACC = MB == 1 ? 2 : 1;     // TMEM accumulator buffers (256 columns per block)
   static_assert(MB == 1 || MB == 2, "MB");
-  using L = Smem2<A_MN, B_MN, STAGES, MB>;
+  static_assert(BN % 32 == 0 && BN <= 256, "pair UMMA N: multiple of 16 per CTA half");
+  static_assert(!B_MN || (BN / 2) % 64 == 0, "MN-major B needs 64-wide panels per CTA half");
+  using L = Smem2<A_MN, B_MN, STAGES, MB, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -533,6 +534,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int num_n = (sh.N + BN - 1) / BN;
   const int ntiles = num_m * num_n;
   const int nkb = sh.nkb0 + sh.nkb1;
+  const int nsplit = sh.ksplit > 1 ? sh.ksplit : 1;
+  const int nunits = ntiles * nsplit;  // split-K: unit = split * ntiles + tile
 
   if (threadIdx.x == 0) {
     prefetch_map(&ta0);
@@ -584,7 +587,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int tile;
         if (leader) {
           mbar_wait(&sempty[sslot], sphase ^ 1);
-          tile = sched_fetch(sh.sched, ntiles, nclusters);
+          tile = sched_fetch(sh.sched, nunits, nclusters);
           ring[sslot] = tile;
           st_shared_cluster(ring_f0 + 4 * sslot, tile);
           mbar_arrive(&sfull[sslot]);
@@ -598,12 +601,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           sslot = 0;
           sphase ^= 1;
         }
-        if (tile >= ntiles) break;
+        if (tile >= nunits) break;
+        const int split = tile / ntiles;
+        tile -= split * ntiles;
+        const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
         int mb, nb;
         tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
         const int m_row = mb * TM + rank * BM * MB;  // this CTA's A rows
-        const int n_row = nb * BN + rank * 128;    // this CTA's B rows (N-half)
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int n_row = nb * BN + rank * (BN / 2);  // this CTA's B rows (N-half)
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fbar = mapa_shared(smem_u32(&full[stage]), 0);
           if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
@@ -626,7 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_3d_pair(tb, fbar, b_dst, kk, n_row, zb);
           } else {
 #pragma unroll
-            for (int p = 0; p < 2; ++p)
+            for (int p = 0; p < BN / 128; ++p)
               tma_load_3d_pair(tb, fbar, b_dst + p * (BK * 128), n_row + p * 64, kk, zb);
           }
           if (++stage == STAGES) {
@@ -660,11 +666,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           sslot = 0;
           sphase ^= 1;
         }
-        if (tile >= ntiles) break;
+        if (tile >= nunits) break;
+        const int split = tile / ntiles;
+        const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (L::A_BYTES >> 4));
@@ -675,7 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int b = 0; b < MB; ++b)
                 umma_bf16_pair(d_tmem + b * 256, ad + b * a_blk + k * a_k, bd + k * b_k, idesc,
-                               (kb | k) != 0 ? 1u : 0u);
+                               ((kb - kb_lo) | k) != 0 ? 1u : 0u);
             umma_commit_pair(&empty[stage]);
           }
           __syncwarp();
@@ -712,16 +720,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         sslot = 0;
         sphase ^= 1;
       }
-      if (tile >= ntiles) break;
+      if (tile >= nunits) break;
+      const int split = tile / ntiles;
       int mb, nb;
-      tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
+      tile_coords(tile - split * ntiles, num_m, num_n, sh.group, sh.group_n, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr =
           tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
 #pragma unroll 1
       for (int b = 0; b < MB; ++b)
-        epi.template apply<BN>(mb * TM + rank * BM * MB + b * BM, nb * BN, row, taddr + b * 256, 0);
+        epi.template apply<BN>(mb * TM + rank * BM * MB + b * BM, nb * BN, row, taddr + b * 256,
+                               split);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);

@@ -96,12 +96,12 @@ int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const 
 }
 
 // CTA-pair launch: 256x256 tiles, grid = 2 x clusters (one CTA per SM, persistent).
-template <bool A_MN, bool B_MN, class Epi, int MB = 1>
+template <bool A_MN, bool B_MN, class Epi, int MB = 1, int BN = 256>
 int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
             const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
   constexpr int STAGES = MB == 1 ? 6 : 4;
-  using L = tc::Smem2<A_MN, B_MN, STAGES, MB>;
-  auto kern = tc::tc_gemm2_kernel<A_MN, B_MN, STAGES, MB, Epi>;
+  using L = tc::Smem2<A_MN, B_MN, STAGES, MB, BN>;
+  auto kern = tc::tc_gemm2_kernel<A_MN, B_MN, STAGES, MB, BN, Epi>;
   static bool configured = false;
   if (!configured) {
     PPO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
@@ -109,7 +109,8 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
   }
   if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
   if (!sh.sched) return fail(PPO_E_CUDA, "tile scheduler counter unavailable");
-  const int64_t ntiles = (int64_t)((sh.M + 256 * MB - 1) / (256 * MB)) * ((sh.N + 255) / 256);
+  const int64_t ntiles = (int64_t)((sh.M + 256 * MB - 1) / (256 * MB)) * ((sh.N + BN - 1) / BN) *
+                         std::max(sh.ksplit, 1);
   // PPO_GRID_ALL_TILES=1: one cluster per tile (hardware-ordered dispatch; experiment knob)
   const bool all_tiles = getenv("PPO_GRID_ALL_TILES") && atoi(getenv("PPO_GRID_ALL_TILES"));
   const int clusters = (int)std::min<int64_t>(ntiles, all_tiles ? (int64_t)1 << 30 : num_sms() / 2);
@@ -204,13 +205,18 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
     if (rc) return rc;
   }
   // heads: y = [h_t | 1] W_o_aug^T over all T*B rows (XH slots 1..T, columns D..D+Ko).
+  // heads: CTA pair, 256 x 224 tiles (3 N-tiles cover A = 656); the 3 N-tiles of a row
+  // block run back to back so the head outputs' A rows are read once.
   CUtensorMap hA, hB;
+  const bool pair_h = use_pair("HEADS", true);
   if ((rc = map_kmajor(&hA, P.xh + B * s.Kx + s.D, s.Ko, s.T * B, s.Kx, 1, 0, tc::BM))) return rc;
-  if ((rc = map_kmajor(&hB, wo, s.Ko, s.A, s.Ko, 1, 0, 224))) return rc;
-  tc::TileShape sh{(int)(s.T * B), (int)s.A, cdiv(s.Ko, tc::BK), 0, 0, 0, 0, 0, 16, 0};
-  raster(sh, "HEADS", 16, 0);
+  if ((rc = map_kmajor(&hB, wo, s.Ko, s.A, s.Ko, 1, 0, pair_h ? 112 : 224))) return rc;
+  tc::TileShape sh{(int)(s.T * B), (int)s.A, cdiv(s.Ko, tc::BK), 0, 0, 0, 0, 0, 3, 1};
+  raster(sh, "HEADS", 3, 1);
   sh.sched = sched_counter(kSchedHeads);
   tc::EpiStoreF32 epi{out, s.A, (int)(s.T * B), (int)s.A};
+  if (pair_h)
+    return launch2<false, false, tc::EpiStoreF32, 1, 224>("heads_fwd", hA, hA, hB, hB, sh, epi, st);
   return launch<224, false, false>("heads_fwd", hA, hA, hB, hB, sh, epi, st);
 }
 
@@ -282,8 +288,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     // dW_o has only ceil(A/128) x ceil(Ko/256) = 102 tiles at full size (< 148 SMs) and
     // K = T*B: split K so the grid fills the SMs; partials are reduced in a fixed order.
     tc::TileShape sh{(int)s.A, (int)s.Ko, cdiv(rows, tc::BK), 0, 0, 0, 0, 0, 16, 0};
-    const int tiles = cdiv(s.A, tc::BM) * cdiv(s.Ko, 256);
-    sh.ksplit = pick_split(tiles, num_sms(), cdiv(rows, tc::BK));
+    const bool pair_o = use_pair("WGRAD_O", true);
+    const int tiles = pair_o ? cdiv(s.A, 256) * cdiv(s.Ko, 256) : cdiv(s.A, tc::BM) * cdiv(s.Ko, 256);
+    sh.ksplit = pick_split(tiles, pair_o ? num_sms() / 2 : num_sms(), cdiv(rows, tc::BK));
     sh.sched = sched_counter(kSchedWgradO);
     float* dwo = grad + s.G4 * s.Kx;
     const int64_t n_o = s.A * s.Ko;
@@ -291,7 +298,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
                                                               ws_layout(s, B).splitk)
                                 : dwo;
     tc::EpiStoreF32 epi{part, s.Ko, (int)s.A, (int)s.Ko, n_o};
-    if ((rc = launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st))) return rc;
+    rc = pair_o ? launch2<true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st)
+                : launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st);
+    if (rc) return rc;
     if (sh.ksplit > 1 && (rc = launch_splitk_reduce(part, sh.ksplit, (size_t)n_o, dwo, st)))
       return rc;
   }
@@ -317,7 +326,14 @@ int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N
   raster(sh, "TEST", 16, 0);
   sh.sched = sched_counter(kSchedTest);
   tc::EpiStoreF32 epi{C, N, M, N};
-  const bool wide = mode & 16;
+  const bool wide = mode & 16, n224p = mode & 32;
+  if (pair && n224p) {
+    if (a_mn || b_mn) return fail(PPO_E_ARG, "pair N=224 test only for K-major operands");
+    CUtensorMap mb2;
+    if ((rc = map_kmajor(&mb2, Bm, K, N, K, 1, 0, 112))) return rc;
+    return launch2<false, false, tc::EpiStoreF32, 1, 224>("test_gemm2n224", ma, ma, mb2, mb2, sh,
+                                                           epi, st);
+  }
   if (pair && wide) {
     if (a_mn && b_mn)
       return launch2<true, true, tc::EpiStoreF32, 2>("test_gemm2w", ma, ma, mb, mb, sh, epi, st);

@@ -32,6 +32,8 @@ def L():
     (11, 384, 768, 448), (11, 136, 320, 72), (11, 2048, 1024, 4096),
     # CTA pair with 512-row tiles (two MMAs per K step), MN-major operands (weight gradient)
     (27, 512, 256, 64), (27, 600, 520, 200), (27, 2048, 1024, 4096),
+    # CTA pair with N=224 tiles (heads), K-major
+    (40, 300, 656, 4160), (40, 1000, 448, 192),
 ])
 def test_tc_gemm_vs_torch(L, mode, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
