@@ -224,6 +224,8 @@ def algorithmic(H, D, T, B, A, nparam):
         "loss": ("byte", rows * (4.0 * A + 2.0 * A + 4 * 7 + 7 + 30 + 4 * 4 + 1)),
         "adam": ("byte", 30.0 * nparam),
         "pack_x": ("byte", rows * D * 2.0 + (T + 1) * B * (D + H + 64) * 2.0 + 8.0 * B * H),
+        # h0, c0 in (fp32); h0 bf16 + c0 fp32 out; the [1 | 0...] pad of T+1 slots
+        "pack_state": ("byte", 8.0 * B * H + 6.0 * B * H + (T + 1) * B * 64 * 2.0),
     }
 
 
@@ -407,7 +409,7 @@ def main():
     H, D, T, B = args.H, args.D, 16, args.B
     cfg = synth.Config(H=H, D=D, B=B, T=T)
     opt = PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16", device=device, comm=comm,
-                       n_buckets=8)
+                       n_buckets=8, n_ws=1 if args.no_e2e else 2)
     prm = synth.torch_params(cfg, 0, device)          # same init on every rank
     opt.load_canonical(prm["Wx"], prm["Wh"], prm["b"], prm["Wo"], prm["bo"])
     del prm
@@ -419,6 +421,10 @@ def main():
                  done=ro["done"])
     # behaviour log-probs = current policy + N(0, 0.1^2) (forward-pass GPUs)
     batch["logp_old"] = opt.current_logp(batch) + seq["logp_noise"]
+    # the resident batch's x lives in the workspace's x rows (zero-copy, ppo_copy_x): the step
+    # packs only h0/c0 into the recurrent slots
+    opt.put_x(batch["x"])
+    x_dev = batch.pop("x")
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -503,9 +509,14 @@ def main():
         # from pinned host memory (H2D) and its stats read back (D2H) inside the timed region.
         # Inputs are double-buffered on the device: the H2D of step k+1 runs on a copy stream
         # while step k computes (the first step's copy is not overlapped).
-        keys = ("x", "h0", "c0", "act", "head_on", "avail", "logp_old", "rew", "val", "done")
+        # x goes straight from pinned host memory into the x rows of one of two workspaces
+        # (ppo_copy_x); the other inputs into double-buffered device tensors.
+        keys = ("h0", "c0", "act", "head_on", "avail", "logp_old", "rew", "val", "done")
         host = {k: batch[k].cpu().pin_memory() for k in keys}
-        h2d = sum(v.numel() * v.element_size() for v in host.values())
+        host_x = x_dev.cpu().pin_memory()
+        del x_dev
+        h2d = sum(v.numel() * v.element_size() for v in host.values()) + \
+            host_x.numel() * host_x.element_size()
         bufs = [{k: batch[k] for k in keys}, {k: torch.empty_like(batch[k]) for k in keys}]
         st_host = torch.empty(8, dtype=torch.float32).pin_memory()
         d2h = st_host.numel() * 4
@@ -518,6 +529,7 @@ def main():
             with torch.cuda.stream(copy_stream):
                 for k in keys:
                     bufs[slot][k].copy_(host[k], non_blocking=True)
+                opt.put_x(host_x, ws=slot, stream=copy_stream)
             h2d_done[slot].record(copy_stream)
 
         def run(nsteps):
@@ -527,6 +539,7 @@ def main():
                 stream.wait_event(h2d_done[cur])
                 if i + 1 < nsteps:
                     upload(1 - cur)
+                opt.select_ws(cur)
                 opt.step(bufs[cur])
                 used[cur].record(stream)
                 st_host.copy_(opt.stats[:8], non_blocking=True)
@@ -544,7 +557,8 @@ def main():
         e2e = {"value": B * world / (ems / args.steps / 1e3) / SEQ_PER_SAMPLE, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / args.steps,
-               "overlap": "H2D of step k+1 on a copy stream during step k (double-buffered inputs)"}
+               "overlap": "H2D of step k+1 on a copy stream during step k (double-buffered "
+                          "inputs; x straight into the workspace of step k+1)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

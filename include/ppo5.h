@@ -134,10 +134,22 @@ int lstm_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes /* host */);
  * Computes z_t = [x_t | h_{t-1} | 1] W_xh_aug^T with the cell (i,f,o sigmoid, g tanh,
  * c_t = f c_{t-1} + i g, h_t = o tanh c_t) fused into the GEMM epilogue, then
  * y = [h_t | 1] W_o_aug^T.  1 <= B; ws_bytes >= lstm_ws_bytes().
- * x == NULL (and h0, c0 ignored): the inputs were already placed in ws by ppo_gather. */
+ * x == NULL: x is already in the workspace -- written by the caller through lstm_ws_x /
+ * ppo_copy_x (then h0, c0 are packed as usual) or, with h0 == c0 == NULL too, placed together
+ * with h0/c0 by ppo_gather. */
 int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const float* h0,
                   const float* c0, int64_t B, void* ws, size_t ws_bytes, float* out,
                   ppo_stream_t s);
+
+/* Zero-copy inputs: where x lives inside ws.  Row (t, b) of x starts at *x + (t*B + b) * *ld
+ * elements (bf16 for PPO_PREC_BF16, fp32 otherwise); *ld = D + H + 64 >= D.  Rows only carry x
+ * in their first D elements; everything else in ws belongs to the library. */
+int lstm_ws_x(const ppo_dims* dims, int64_t B, void* ws, void** x /* host out */,
+              int64_t* ld /* host out */);
+/* Copy x [T*B][D] with row stride src_ld elements (host -- pinned for async -- or device
+ * memory) into the workspace rows: one cudaMemcpy2DAsync on the stream. */
+int ppo_copy_x(const ppo_dims* dims, int64_t B, const void* src, int64_t src_ld, void* ws,
+               size_t ws_bytes, ppo_stream_t s);
 
 /* ---- a5: PPO loss and its gradient (O6, O7) --
  * out [T·B][A] fp32 (row = t*B + b); act [T·B][n_heads] int32; head_on [T·B][n_heads] u8

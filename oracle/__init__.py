@@ -21,6 +21,8 @@ Parity status ("Oracle pins"):
   dp average     pinned (shard identity)
   buffer         sampler pinned to splitmix64's published test vector; gather = indexing
   step           composition of the above, pinned end-to-end by finite differences
+  infer (NEXT-3) state carry = 2-step LSTM; Gumbel-max frequencies = softmax (chi-square);
+                 masks, target-type table, logp = the loss oracle's log pi
 """
 from .gae import gamma_from_horizon, gae, segments_to_sequences  # noqa: F401
 from .lstm import lstm_forward, lstm_backward  # noqa: F401
@@ -28,3 +30,4 @@ from .loss import heads_forward, heads_backward, ppo_loss, STAT_NAMES  # noqa: F
 from .adam import adam_clip  # noqa: F401
 from .step import ppo_step, dp_average  # noqa: F401
 from . import buffer  # noqa: F401
+from . import infer  # noqa: F401

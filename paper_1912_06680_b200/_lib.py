@@ -89,6 +89,8 @@ _lib_fns = dict(
     lstm_ws_bytes=([_D, c_int64, POINTER(c_size_t)], c_int),
     lstm_bptt_fwd=([_D, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_size_t,
                     c_void_p, c_void_p], c_int),
+    lstm_ws_x=([_D, c_int64, c_void_p, POINTER(c_void_p), POINTER(c_int64)], c_int),
+    ppo_copy_x=([_D, c_int64, c_void_p, c_int64, c_void_p, c_size_t, c_void_p], c_int),
     ppo_loss_grad=([_D] + [c_void_p] * 8 + [c_int64, POINTER(ppo_loss_cfg), c_void_p, c_void_p,
                                              c_void_p, c_void_p], c_int),
     lstm_bptt_bwd=([_D, c_void_p, c_void_p, c_size_t, c_void_p, c_int64, c_void_p, c_void_p], c_int),
@@ -195,6 +197,19 @@ def lstm_bptt_fwd(dims, w, x, h0, c0, B, ws, out, stream=None):
     """x = None: inputs already gathered into ws by ppo_gather"""
     _check(_lib.lstm_bptt_fwd(ctypes.byref(dims), _p(w), _p(x), _p(h0), _p(c0), B, _p(ws),
                               ws.numel() * ws.element_size(), _p(out), _s(stream)))
+
+
+def lstm_ws_x(dims, B, ws):
+    """-> (device address, row stride in elements) of x inside the workspace"""
+    p, ld = c_void_p(), c_int64()
+    _check(_lib.lstm_ws_x(ctypes.byref(dims), B, _p(ws), ctypes.byref(p), ctypes.byref(ld)))
+    return p.value, ld.value
+
+
+def ppo_copy_x(dims, B, src, ws, stream=None):
+    """src: contiguous [T][B][D] tensor (pinned host or device)"""
+    _check(_lib.ppo_copy_x(ctypes.byref(dims), B, _p(src), src.shape[-1], _p(ws),
+                           ws.numel() * ws.element_size(), _s(stream)))
 
 
 def ppo_loss_grad(dims, out, act, head_on, avail, logp_old, adv, ret, valid, B, cfg, dout, logp,

@@ -257,8 +257,15 @@ int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const floa
   if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small");
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   float* C = reinterpret_cast<float*>(wsb + L.c);
-  // x == NULL: inputs already gathered into the workspace (ppo_gather)
-  if (x && (rc = launch_pack_x(s, B, x, h0, c0, wsb + L.xh, C, st))) return rc;
+  // x == NULL: x already in the workspace (lstm_ws_x / ppo_copy_x: pack h0, c0 and the pad
+  // columns; or ppo_gather, which also placed h0/c0: nothing to do)
+  if (x) {
+    if ((rc = launch_pack_x(s, B, x, h0, c0, wsb + L.xh, C, st))) return rc;
+  } else if (h0 || c0) {
+    if (!h0 || !c0 || !aligned(h0, 16) || !aligned(c0, 16))
+      return fail(PPO_E_ARG, "h0 and c0 must both be given (16-byte aligned)");
+    if ((rc = launch_pack_state(s, B, h0, c0, wsb + L.xh, C, st))) return rc;
+  }
   if (s.bf16) {
     if ((rc = check_tc_device())) return rc;
     return tc_forward(s, B, w, ws, out, st);
@@ -280,6 +287,35 @@ int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const floa
   SimtOp a{{XH + B * s.Kx + s.D, nullptr}, {s.Kx, 0}, {s.T * B, 0}, {s.Ko, 0}, s.Ko, false};
   SimtOp b{{Wo, nullptr}, {s.Ko, 0}, {s.A, 0}, {s.Ko, 0}, s.Ko, false};
   return launch_simt_gemm(a, b, s.T * B, s.A, s.Ko, out, s.A, st);
+}
+
+int lstm_ws_x(const ppo_dims* dims, int64_t B, void* ws, void** x, int64_t* ld) {
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
+  if (!ws || !x || !ld) return fail(PPO_E_ARG, "NULL pointer");
+  *x = static_cast<uint8_t*>(ws) + ws_layout(s, B).xh;
+  *ld = s.Kx;
+  return PPO_OK;
+}
+
+int ppo_copy_x(const ppo_dims* dims, int64_t B, const void* src, int64_t src_ld, void* ws,
+               size_t ws_bytes, ppo_stream_t st) {
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
+  if (!src || !ws) return fail(PPO_E_ARG, "NULL pointer");
+  if (src_ld < s.D) return fail(PPO_E_ARG, "src_ld < D");
+  WsLayout L = ws_layout(s, B);
+  if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small");
+  const size_t esz = s.bf16 ? 2 : 4;
+  ProfScope _prof("copy_x", (cudaStream_t)st);
+  PPO_CUDA_CHECK(cudaMemcpy2DAsync(static_cast<uint8_t*>(ws) + L.xh, s.Kx * esz, src,
+                                   src_ld * esz, s.D * esz, s.T * B, cudaMemcpyDefault,
+                                   (cudaStream_t)st));
+  return PPO_OK;
 }
 
 int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,

@@ -109,6 +109,38 @@ __global__ void __launch_bounds__(256) pack_x_kernel(Shape s, int64_t B, const T
   }
 }
 
+// h0 -> XH[0][b][D:D+H], c0 -> C[0], pad columns [1 | 0...] of all T+1 slots (x is already
+// in the workspace).  One warp per XH row.
+template <class TA>
+__global__ void __launch_bounds__(256) pack_state_kernel(Shape s, int64_t B,
+                                                         const float* __restrict__ h0,
+                                                         const float* __restrict__ c0,
+                                                         TA* __restrict__ xh, float* __restrict__ c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (s.T + 1) * B;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows;
+       row += nwarps) {
+    TA* dst = xh + row * s.Kx;
+    if (row < B) {
+      const int64_t b = row;
+      const float4* hs = reinterpret_cast<const float4*>(h0 + b * s.H);
+      const float4* cs = reinterpret_cast<const float4*>(c0 + b * s.H);
+      float4* cd = reinterpret_cast<float4*>(c + b * s.H);
+      for (int i = lane; i < s.H / 4; i += 32) {
+        const float4 h = hs[i];
+        TA* o = dst + s.D + 4 * i;
+        o[0] = from_f<TA>(h.x);
+        o[1] = from_f<TA>(h.y);
+        o[2] = from_f<TA>(h.z);
+        o[3] = from_f<TA>(h.w);
+        cd[i] = cs[i];
+      }
+    }
+    for (int i = lane; i < 64; i += 32) dst[s.D + s.H + i] = from_f<TA>(i == 0 ? 1.f : 0.f);
+  }
+}
+
 // ============================================================================ GAE
 
 // NV consecutive floats from an arbitrarily aligned p, using aligned 16-byte loads (streaming,
@@ -814,6 +846,17 @@ size_t gae_scratch_bytes(int64_t R, int64_t L) {
   if (gae_use_short(R, L)) return 0;
   const int64_t nck = (L + kGaeChunk - 1) / kGaeChunk;
   return 256 + (size_t)(R * nck) * sizeof(GaeStatus);
+}
+int launch_pack_state(const Shape& s, int64_t B, const float* h0, const float* c0, void* xh,
+                      float* c, cudaStream_t st) {
+  ProfScope _prof("pack_state", st);
+  const int64_t n = (s.T + 1) * B * 32;
+  if (s.bf16)
+    pack_state_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(s, B, h0, c0, (__nv_bfloat16*)xh, c);
+  else
+    pack_state_kernel<float><<<grid_for(n), 256, 0, st>>>(s, B, h0, c0, (float*)xh, c);
+  PPO_LAUNCH_CHECK("pack_state_kernel");
+  return PPO_OK;
 }
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
                float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,

@@ -32,6 +32,9 @@ int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, con
 constexpr int64_t kGaeShortL = 8192;  // up to this length: one warp per stream
 constexpr int64_t kGaeChunk = 4096;   // longer: chunk-parallel look-back kernel
 size_t gae_scratch_bytes(int64_t R, int64_t L);
+// h0 -> XH[0] h-part, c0 -> C[0], pad columns of every slot (x already in the workspace)
+int launch_pack_state(const Shape& s, int64_t B, const float* h0, const float* c0, void* xh,
+                      float* c, cudaStream_t st);
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
                float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,
                cudaStream_t st);

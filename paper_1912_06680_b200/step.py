@@ -31,7 +31,7 @@ class PPOOptimizer:
 
     def __init__(self, D: int, H: int, B: int, T: int = 16, head_sizes=HEAD_SIZES,
                  precision: str = "bf16", device="cuda", hyper: dict | None = None,
-                 comm=None, n_buckets: int = 1):
+                 comm=None, n_buckets: int = 1, n_ws: int = 1):
         self.D, self.H, self.B, self.T = D, H, B, T
         self.head_sizes = tuple(head_sizes)
         self.A = sum(self.head_sizes) + 1
@@ -49,7 +49,10 @@ class PPOOptimizer:
         self.v = torch.zeros(n, **f32)
         self.grad = torch.zeros(n, **f32)
         self.shadow = torch.zeros(n, dtype=torch.bfloat16, device=dev) if self.bf16 else None
-        self.ws = _aligned_empty(L.ws_bytes(self.dims, B), dev)
+        # activation workspaces; n_ws = 2 lets the next step's x be uploaded into one while
+        # the current step runs in the other
+        self.ws_list = [_aligned_empty(L.ws_bytes(self.dims, B), dev) for _ in range(n_ws)]
+        self.ws = self.ws_list[0]
         act_dtype = torch.bfloat16 if self.bf16 else torch.float32
         rows = T * B
         self.out = torch.empty(rows, self.A, **f32)
@@ -87,6 +90,16 @@ class PPOOptimizer:
                             stream)
         return out
 
+    # ---------------------------------------------------------------- zero-copy inputs
+    def select_ws(self, i: int):
+        """make workspace i the one the next forward/backward use"""
+        self.ws = self.ws_list[i]
+
+    def put_x(self, x: torch.Tensor, ws: int | None = None, stream=None):
+        """copy x [T][B][D] (pinned host or device) straight into a workspace's x rows; the
+        step then runs with batch["x"] = None (ppo_copy_x)"""
+        L.ppo_copy_x(self.dims, self.B, x, self.ws if ws is None else self.ws_list[ws], stream)
+
     # ---------------------------------------------------------------- the step
     def gae(self, batch, stream=None):
         """a1: advantages/returns written time-major [T][B] for the minibatch"""
@@ -95,8 +108,8 @@ class PPOOptimizer:
                   self.ret, seq_T=self.T, stream=stream)
 
     def forward(self, batch, stream=None):
-        """a2-a4"""
-        L.lstm_bptt_fwd(self.dims, self.weights, batch["x"], batch["h0"], batch["c0"], self.B,
+        """a2-a4; batch["x"] None = x already in the workspace (put_x / ppo_gather)"""
+        L.lstm_bptt_fwd(self.dims, self.weights, batch.get("x"), batch["h0"], batch["c0"], self.B,
                         self.ws, self.out, stream)
 
     def loss(self, batch, logp_old=None, stream=None):

@@ -153,3 +153,29 @@ def test_dp_equivalence_shards(precision):
     torch.cuda.synchronize()
     e = (torch.linalg.vector_norm(acc - ref.grad) / torch.linalg.vector_norm(ref.grad)).item()
     assert e < 1e-5, e
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_zero_copy_x_matches_packed(precision):
+    """x placed in the workspace by ppo_copy_x (from pinned host and from device memory) gives
+    the same forward outputs, bit for bit, as the packed path; ragged B, two workspaces."""
+    from paper_1912_06680_b200 import PPOOptimizer, _lib as L
+    cfg = synth.Config(H=256, D=192, B=176, T=16)
+    case = make_case(cfg, 5, pad_frac=0.2)
+    opt = PPOOptimizer(cfg.D, cfg.H, cfg.B, cfg.T, cfg.head_sizes, precision=precision, n_ws=2)
+    load_params(opt, case["params"])
+    batch = device_batch(case, precision == "bf16")
+    opt.forward(batch)
+    ref = opt.out.clone()
+    xh = batch["x"].cpu().pin_memory()
+    for ws, src in ((1, xh), (0, batch["x"])):
+        opt.out.zero_()
+        opt.put_x(src, ws=ws)
+        opt.select_ws(ws)
+        opt.forward(dict(batch, x=None))
+        torch.cuda.synchronize()
+        assert torch.equal(opt.out, ref), ws
+    p, ld = L.lstm_ws_x(opt.dims, cfg.B, opt.ws_list[1])
+    assert p == opt.ws_list[1].data_ptr() and ld == cfg.D + cfg.H + 64
+    with pytest.raises(RuntimeError):
+        opt.forward(dict(batch, x=None, c0=None))
