@@ -44,7 +44,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1, help="oracle sample: sequences per step")
-    ap.add_argument("--config", choices=["full", "gae", "iteration"], default="full",
+    ap.add_argument("--infer-B", type=str, default="60,1,240,960",
+                    help="--config infer: comma-separated batch sizes (first = headline)")
+    ap.add_argument("--config", choices=["full", "gae", "iteration", "infer"], default="full",
                     help="full: the PPO step (default); gae: GAE-only HBM sweep (configs[3]); "
                          "iteration: NEXT-1, steps drawn from a device experience buffer")
     return ap.parse_args()
@@ -376,8 +378,119 @@ def run_iteration(args):
         "sample_reuse": tr.sample_reuse}), flush=True)
 
 
+def run_infer(args):
+    """NEXT-3: forward-pass inference steps at the rollout batch (~60): one LSTM step +
+    heads + masked sampling per call, state carried.  HBM-bound on the weights: algorithmic
+    bytes per step = W_xh_aug + W_o_aug (bf16) + x + h/c read and written + outputs."""
+    import torch
+    import synth
+    from paper_1912_06680_b200 import _lib as L
+    from paper_1912_06680_b200.infer import PolicyServer
+    dev = torch.device("cuda", 0)
+    H, D = args.H, args.D
+    pk = peaks()
+    cfg0 = synth.Config(H=H, D=D, B=1, T=1)
+    prm = synth.torch_params(cfg0, 0, dev)
+    rows = []
+    for B in [int(v) for v in args.infer_B.split(",")]:
+        cfg = synth.Config(H=H, D=D, B=B, T=1)
+        table = torch.from_numpy(synth.heads_on_table(cfg.head_sizes))
+        srv = PolicyServer(D, H, B, cfg.head_sizes, device=dev, head_table=table, seed=3)
+        theta = torch.empty(srv.layout.n_total, device=dev)
+        L.ppo_pack_params(srv.dims, prm["Wx"], prm["Wh"], prm["b"], prm["Wo"], prm["bo"], theta)
+        shadow = torch.empty(srv.layout.n_total, dtype=torch.bfloat16, device=dev)
+        L.ppo_cast_bf16(theta, shadow)
+        srv.load(shadow)
+        del theta
+        sq = synth.torch_sequences(synth.Config(H=H, D=D, B=B, T=16), 5, dev)
+        xs = sq["x"]                      # [16][B][D] bf16: 16 distinct steps of input
+        avail = sq["avail"]
+        srv.reset(sq["h0"], sq["c0"])
+        nsteps = max(args.steps, 16) * 8
+        for i in range(args.warmup * 8):
+            srv.step(xs[i % 16], avail[i % 16])
+        torch.cuda.synchronize()
+        L.prof_start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(nsteps):
+            srv.step(xs[i % 16], avail[i % 16], want_out=False)
+        e1.record()
+        torch.cuda.synchronize()
+        prof = L.prof_stop()
+        us = e0.elapsed_time(e1) / nsteps * 1e3
+        # CUDA graph of 16 consecutive steps (distinct inputs and counters), replayed
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            srv.step(xs[0], avail[0], want_out=False)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                for i in range(16):
+                    srv.step(xs[i], avail[i], want_out=False)
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        reps = max(1, nsteps // 16)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us_graph = e0.elapsed_time(e1) / (reps * 16) * 1e3
+        # cuBLAS reference for the dominant GEMM (library baseline, same operands)
+        lay = srv.layout
+        Kx, G4 = D + H + 64, 4 * H
+        wx = shadow[:G4 * Kx].view(G4, Kx)
+        xh = torch.randn(B, Kx, device=dev).bfloat16()
+        for _ in range(3):
+            torch.matmul(xh, wx.t())
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(nsteps):
+            torch.matmul(xh, wx.t())
+        e1.record()
+        torch.cuda.synchronize()
+        us_cublas = e0.elapsed_time(e1) / nsteps * 1e3
+        A, Ko = cfg.A, H + 64
+        w_bytes = 2.0 * (G4 * Kx + A * Ko)
+        io_bytes = B * (2.0 * D + 16.0 * H + 4 * 7 + 7 + 8 + A)
+        step_bytes = w_bytes + io_bytes
+        gates = prof.get("infer_gates", (1, 0.0))
+        g_us = gates[1] / gates[0] * 1e3
+        kern = {k: {"launches_per_step": c // nsteps, "us_per_step": t / nsteps * 1e3}
+                for k, (c, t) in prof.items()}
+        rows.append({
+            "B": B, "us_per_step": us, "us_per_step_graph": us_graph,
+            "steps_per_s": 1e6 / us_graph, "hero_actions_per_s": B * 1e6 / us_graph,
+            "achieved_GB_s": step_bytes / (us_graph * 1e-6) / 1e9,
+            "frac": step_bytes / (us_graph * 1e-6) / 1e9 / pk["hbm_gbs"],
+            "gates_gemm": {"us": g_us, "GB_s": 2.0 * G4 * Kx / (g_us * 1e-6) / 1e9,
+                           "frac": 2.0 * G4 * Kx / (g_us * 1e-6) / 1e9 / pk["hbm_gbs"],
+                           "cublas_us": us_cublas},
+            "kernels": kern})
+        del srv, sq, xs, avail, g, shadow, wx, xh
+        torch.cuda.empty_cache()
+    head = rows[0]
+    print(json.dumps({
+        "metric": "inference step latency (NEXT-3: LSTM step + heads + masked sampling)",
+        "value": head["us_per_step_graph"], "unit": "us/step", "higher_is_better": False,
+        "n_gpus": 1, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"forward-pass batch B={head['B']} (P:1263), H={H}, D={D}",
+                   "l2": f"weights {2.0 * (4 * H * (D + H + 64)) / 1e6:.0f} MB > L2: streamed "
+                         "from HBM every step"},
+        "roofline": {"bound": "hbm", "achieved": head["achieved_GB_s"], "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": head["frac"], "kernel": "whole step (graph)"},
+        "sweep": rows}), flush=True)
+
+
 def main():
     args = parse()
+    if args.config == "infer":
+        run_infer(args)
+        return
     if args.config == "iteration":
         run_iteration(args)
         return

@@ -249,6 +249,40 @@ int ppo_reward_gae(const float* shaped, const float* win, const int32_t* step0, 
                    double* stats, float gamma, float lam, int32_t seq_T, float* rew_out,
                    float* adv, float* ret, void* scratch, size_t scratch_bytes, ppo_stream_t s);
 
+/* ---- NEXT-3: forward-pass inference step ---------------------------------------
+ * "a separate pool of GPU machines which run forward passes in larger batches of
+ * approximately 60": one policy step for B heroes.
+ *   z = W_xh_aug [x | h | 1]; LSTM cell -> h', c' (written back in place)
+ *   y = W_o_aug [h' | 1]  (logits of the n_heads heads | value)
+ *   act[b][k] = argmax over allowed j of (y_kj + g_kj), g = -log(-log u) Gumbel noise, ties
+ *     to the smallest j (DESIGN reading Q22); allowed = avail[b] for the primary head (action
+ *     filters), every entry for the parameter heads;
+ *     u(b, j) = ((splitmix64(seed + (step << 32) + 1024 b + j) >> 41) + 1/2) / 2^23 over the
+ *     concatenated head logits j (the oracle implements the same counter generator);
+ *   head_on[b] = head_table[act[b][0]] (Table target types);
+ *   logp[b] = sum_k head_on[b][k] log softmax_allowed(y_k)[act[b][k]] (behaviour log-prob);
+ *   value[b] = y[b][A-1].
+ * A row with no available primary (reading Q23) gets act[b][0] = -1, head_on 0, logp 0.
+ * Layouts: w = weights tiled by ppo_infer_pack_weights; x [B][D] bf16 bits; h, c [B][H] fp32,
+ * updated in place; avail [B][head_sizes[0]] uint8; head_table [head_sizes[0]][n_heads]
+ * uint8; act [B][n_heads] int32; head_on [B][n_heads] uint8 (may be NULL); logp [B] fp32;
+ * value [B] (may be NULL); out [B][A] fp32 head outputs (may be NULL).  All device
+ * pointers; w, x, h, c 16-byte aligned; ws 1024-byte aligned, >= ppo_infer_ws_bytes.
+ * bf16 precision only (PPO_E_ARG otherwise); PPO_E_UNSUPPORTED off sm_100.
+ * Asynchronous on the stream. */
+int ppo_infer_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes /* host out */);
+/* The served weights, re-laid out once per published version for streaming: every
+ * [128 rows][64 k] block of W_xh_aug and W_o_aug becomes one contiguous 16 KB tile (rows past
+ * the matrix zero), gates then heads.  w: the bf16 shadow in ppo_param_layout (device);
+ * wt: device, 16-byte aligned, >= ppo_infer_weights_bytes. */
+int ppo_infer_weights_bytes(const ppo_dims* dims, size_t* bytes /* host out */);
+int ppo_infer_pack_weights(const ppo_dims* dims, const void* w, void* wt, size_t wt_bytes,
+                           ppo_stream_t s);
+int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
+                   const uint8_t* avail, const uint8_t* head_table, uint64_t seed,
+                   uint64_t step, int64_t B, void* ws, size_t ws_bytes, int32_t* act,
+                   uint8_t* head_on, float* logp, float* value, float* out, ppo_stream_t s);
+
 /* ---- tracing: CUDA events around every kernel launch ------------------------
  * ppo_prof_start() enables recording (clears previous records); every library launch then
  * records a start/end event pair on its stream.  ppo_prof_stop() synchronises those events,

@@ -11,9 +11,12 @@ optimizer's PPO ratio divides by).
 
 Reading Q22: sampling is exact sampling from the softmax at temperature 1 by
 the Gumbel-max rule  a = argmax_k (l_k + g_k),  g_k = -log(-log u_k),  ties -> smallest k,
-with u drawn by the counter-based generator both sides implement:
-    u(b, k) = ((splitmix64(seed + (step << 32) + 1024 b + k) >> 40) + 1/2) / 2^24
-for row b and logit k (0..654, the concatenated head logits).
+Reading Q23: a row with no available primary action gets act = -1 for the primary, no read
+heads and logp = 0 (parameter heads are still drawn).
+With u drawn by the counter-based generator both sides implement:
+    u(b, k) = ((splitmix64(seed + (step << 32) + 1024 b + k) >> 41) + 1/2) / 2^23
+for row b and logit k (0..654, the concatenated head logits) -- 23 bits, so that every u is
+exactly representable in binary32 as well (u <= 1 - 2^-24).
 """
 import numpy as np
 
@@ -29,7 +32,7 @@ def uniforms(seed: int, step: int, B: int, n_logits: int) -> np.ndarray:
     for b in range(B):
         for k in range(n_logits):
             z = splitmix64((base + 1024 * b + k) & M64)
-            u[b, k] = ((z >> 40) + 0.5) / float(1 << 24)
+            u[b, k] = ((z >> 41) + 0.5) / float(1 << 23)
     return u
 
 
@@ -57,12 +60,16 @@ def sample(y, u, avail, head_table, head_sizes):
         s = np.where(allowed, lk + g[:, off[k]:off[k + 1]], -np.inf)
         score[:, off[k]:off[k + 1]] = s
         act[:, k] = np.argmax(s, axis=1)          # first maximum on ties
-        lps.append(_masked_log_softmax(lk, allowed))
-    head_on = table[act[:, 0]]                    # Table target types
+        with np.errstate(divide="ignore", invalid="ignore"):   # rows with nothing allowed
+            lps.append(_masked_log_softmax(lk, allowed))
+    none = ~avail.any(axis=1)                     # reading Q23: no available primary
+    act[none, 0] = -1
+    head_on = np.where(none[:, None], False, table[np.maximum(act[:, 0], 0)])
     logp = np.zeros(B)
     for k in range(len(head_sizes)):
-        sel = lps[k][np.arange(B), act[:, k]]
-        logp += np.where(head_on[:, k], sel, 0.0)  # ignored heads do not count
+        on = head_on[:, k]
+        sel = lps[k][np.arange(B), np.maximum(act[:, k], 0)]
+        logp += np.where(on, sel, 0.0)            # ignored heads do not count
     return act, head_on.astype(np.uint8), logp, score
 
 

@@ -107,6 +107,12 @@ _lib_fns = dict(
     ppo_reward_gae=([c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p,
                      POINTER(ppo_reward_cfg), c_void_p, c_float, c_float, c_int32, c_void_p,
                      c_void_p, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
+    ppo_infer_ws_bytes=([_D, c_int64, POINTER(c_size_t)], c_int),
+    ppo_infer_weights_bytes=([_D, POINTER(c_size_t)], c_int),
+    ppo_infer_pack_weights=([_D, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
+    ppo_infer_step=([_D, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                     ctypes.c_uint64, ctypes.c_uint64, c_int64, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
+                     c_void_p, c_void_p, c_void_p], c_int),
     ppo_prof_start=([], c_int),
     ppo_prof_stop=([POINTER(ppo_prof_entry), c_int32, POINTER(c_int32)], c_int),
     ppo_test_tc_gemm=([c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p], c_int),
@@ -262,6 +268,31 @@ def ppo_reward_gae(shaped, win, step0, val, done, cfg, stats, gamma, lam, adv, r
                                ctypes.byref(cfg), _p(stats), gamma, lam, seq_T, _p(rew_out),
                                _p(adv), _p(ret), _p(scratch),
                                scratch.numel() * scratch.element_size(), _s(stream)))
+
+
+def infer_ws_bytes(dims, B) -> int:
+    n = c_size_t()
+    _check(_lib.ppo_infer_ws_bytes(ctypes.byref(dims), B, ctypes.byref(n)))
+    return n.value
+
+
+def infer_weights_bytes(dims) -> int:
+    n = c_size_t()
+    _check(_lib.ppo_infer_weights_bytes(ctypes.byref(dims), ctypes.byref(n)))
+    return n.value
+
+
+def ppo_infer_pack_weights(dims, w, wt, stream=None):
+    _check(_lib.ppo_infer_pack_weights(ctypes.byref(dims), _p(w), _p(wt),
+                                       wt.numel() * wt.element_size(), _s(stream)))
+
+
+def ppo_infer_step(dims, w, x, h, c, avail, head_table, seed, step, B, ws, act, head_on, logp,
+                   value=None, out=None, stream=None):
+    _check(_lib.ppo_infer_step(ctypes.byref(dims), _p(w), _p(x), _p(h), _p(c), _p(avail),
+                               _p(head_table), seed, step, B, _p(ws),
+                               ws.numel() * ws.element_size(), _p(act), _p(head_on), _p(logp),
+                               _p(value), _p(out), _s(stream)))
 
 
 def comm_unique_id() -> bytes:

@@ -151,7 +151,7 @@ static int need(const void* p, const char* name) {
     if (_r) return _r;                   \
   } while (0)
 
-static int check_tc_device() {
+int check_tc_device() {
   int dev = 0, major = 0;
   PPO_CUDA_CHECK(cudaGetDevice(&dev));
   PPO_CUDA_CHECK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/ppo5.h"
 
@@ -51,6 +52,29 @@ struct Shape {
   bool bf16;
 };
 int check_dims(const ppo_dims* d, Shape* s);
+int check_tc_device();  // PPO_E_UNSUPPORTED unless an sm_100 device is current
+
+// Launch with programmatic stream serialisation (PDL): the kernel may start while the previous
+// kernel on the stream drains; it must execute griddepcontrol.wait before reading its inputs.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Workspace regions (byte offsets from ws base); esz = activation element size.
 constexpr int kMaxSplitK = 16;

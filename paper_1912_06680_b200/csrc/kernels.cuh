@@ -62,6 +62,15 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
 int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
                 cudaStream_t st);
 // Standalone test GEMM (exported for tests): C = A B^T variants on bf16 inputs.
+// NEXT-3: split-K skinny GEMMs of the inference step (weights x batch); *split = partials
+int tc_infer_gates(const Shape& s, int64_t B, const void* w, const void* xh, float* part,
+                   int* split, cudaStream_t st);
+int tc_infer_heads(const Shape& s, int64_t B, const void* w, const void* ho, float* part,
+                   int* split, cudaStream_t st);
+int tc_infer_max_split();
+// pre-tiled inference weights: [128][64] bf16 tiles, gates then heads (elements)
+size_t tc_infer_tiled_offset_heads(const Shape& s);
+size_t tc_infer_tiled_elems(const Shape& s);
 int tc_test_gemm(int mode, const void* A, const void* B, float* C, int M, int N, int K,
                  cudaStream_t st);
 

@@ -35,6 +35,11 @@ struct TileShape {
   int kb_off;        // k-block offset added to source-0 K coordinates (K-chunked launches)
   unsigned int* sched;  // dynamic tile scheduler: {next unit, exited fetchers}, zero at launch;
                         // the last fetcher resets both (one launch per counter at a time)
+  int a_evict_first;    // single-CTA kernel, K-major A: L2 evict_first hint on A's TMA loads
+                        // (an operand streamed once, e.g. the weights of the inference GEMMs)
+  int a_tiled_nkb;      // > 0: A is pre-tiled (16 KB [128 rows][64 k] tiles, tile index
+                        // m_tile * a_tiled_nkb + k_block, map dims {64, 128, tiles}) so every
+                        // TMA box is one contiguous DRAM stream
 };
 constexpr int kSchedDepth = 4;  // tile-index ring between the fetcher and the consumers
 
@@ -88,6 +93,20 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_3d_hint(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                                 int c0, int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
@@ -331,6 +350,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Programmatic dependent launch (no-ops without the launch attribute): the set-up above
+  // overlaps the previous kernel's tail; operands are read only after it has completed.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tbase = *tslot;
 
   if (warp == 0) {
@@ -368,7 +391,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* a_dst = sA + stage * L::A_BYTES;
           uint8_t* b_dst = sB + stage * L::B_BYTES;
           if (!A_MN) {
-            tma_load_3d(ta, &full[stage], a_dst, kk, mb * BM, za);
+            const int a0 = sh.a_tiled_nkb ? 0 : kk;
+            const int a1 = sh.a_tiled_nkb ? 0 : mb * BM;
+            const int a2 = sh.a_tiled_nkb ? mb * sh.a_tiled_nkb + kk / BK : za;
+            if (sh.a_evict_first)
+              tma_load_3d_hint(ta, &full[stage], a_dst, a0, a1, a2, policy_evict_first());
+            else
+              tma_load_3d(ta, &full[stage], a_dst, a0, a1, a2);
           } else {
 #pragma unroll
             for (int p = 0; p < BM / 64; ++p)
@@ -792,6 +821,32 @@ struct EpiStoreF32 {
         for (int i = 0; i < 16; ++i)
           if (n0 + i < N) dst[i] = accumulate ? dst[i] + v[i] : v[i];
       }
+    }
+  }
+};
+
+// Transposed fp32 store: out[split][n][m] (ldc = row stride of the [N][M] output).  Lane =
+// row m, so each store instruction writes 32 consecutive m of one column n (coalesced).
+// Used by the skinny inference GEMMs (weights = M, batch = N) so consumers read per batch row.
+struct EpiStoreF32T {
+  float* out;
+  int64_t ldc;
+  int M, N;
+  int64_t split_stride;
+  template <int BN>
+  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
+                                        int split) const {
+    const int m = m_base + row;
+    float* base = out + split * split_stride + m;
+#pragma unroll 1
+    for (int c = 0; c < BN / 16; ++c) {
+      float v[16];
+      tmem_ld16(taddr + c * 16, v);
+      const int n0 = n_base + c * 16;
+      if (m >= M || n0 >= N) continue;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (n0 + i < N) base[static_cast<int64_t>(n0 + i) * ldc] = v[i];
     }
   }
 };

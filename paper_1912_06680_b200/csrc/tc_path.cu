@@ -12,7 +12,10 @@ namespace {
 
 // Dynamic tile-scheduler counters (zero-initialised; each kernel resets its pair on exit).
 // One slot per GEMM call site, so stream-ordered launches never share a live counter.
-enum SchedSlot { kSchedFwd = 0, kSchedHeads, kSchedBwd, kSchedWgrad, kSchedWgradO, kSchedTest, kSchedSlots };
+enum SchedSlot {
+  kSchedFwd = 0, kSchedHeads, kSchedBwd, kSchedWgrad, kSchedWgradO, kSchedTest,
+  kSchedInferGates, kSchedInferHeads, kSchedSlots
+};
 __device__ unsigned int g_sched_ctr[2 * kSchedSlots];
 
 unsigned int* sched_counter(int slot) {
@@ -71,10 +74,10 @@ int map_mnmajor(CUtensorMap* m, const void* base, uint64_t MN, uint64_t K, uint6
   return make_map(m, base, MN, K, 1, ld_elems * 2, 0, 64, tc::BK);
 }
 
-template <int BN, bool A_MN, bool B_MN, class Epi>
+template <int BN, bool A_MN, bool B_MN, class Epi, int STAGES = 4>
 int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
-           const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
-  constexpr int STAGES = 4;
+           const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st,
+           bool pdl = false) {
   using L = tc::Smem<BN, A_MN, B_MN, STAGES>;
   auto kern = tc::tc_gemm_kernel<BN, A_MN, B_MN, STAGES, Epi>;
   static bool configured = false;
@@ -90,7 +93,12 @@ int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const 
                                           all_tiles ? (int64_t)1 << 30 : num_sms());
   if (grid <= 0) return PPO_OK;
   ProfScope _prof(tag, st);
-  kern<<<grid, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, sh, epi);
+  if (pdl) {
+    PPO_CUDA_CHECK(launch_pdl(kern, dim3(grid), dim3(tc::kThreads), L::TOTAL, st, a0, a1, b0,
+                              b1, sh, epi));
+  } else {
+    kern<<<grid, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, sh, epi);
+  }
   PPO_LAUNCH_CHECK("tc_gemm_kernel");
   return PPO_OK;
 }
@@ -306,6 +314,86 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   }
   return PPO_OK;
 }
+
+// ---------------------------------------------------------------- NEXT-3 inference GEMMs
+// Skinny GEMMs of one policy step at batch B ~ 60: the weights are the M side
+// (128-row tiles streamed once by TMA, 8-stage ring), the batch the N side (one 64-wide
+// tile), K split so the units fill whole waves of the SMs.  Deterministic fp32 partials
+// out[split][b][m] (transposed store); the consumer kernel sums them in split order.
+namespace {
+int infer_split(int tiles, int nkb, int min_kb) {
+  const char* e = getenv("PPO_INFER_SPLIT");
+  if (e && atoi(e) > 0) return std::min(std::min(atoi(e), kMaxSplitK), nkb);
+  const int sms = num_sms();
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= kMaxSplitK && nkb / sp >= min_kb; ++sp) {
+    const int units = tiles * sp;
+    const double eff = (double)units / ((double)((units + sms - 1) / sms) * sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+// N tile by batch size: 64 at the paper's ~60, wider tiles once the batch fills them (the
+// MMA needs N >= 128 to stop being shared-memory bound).
+// W is pre-tiled (tc_infer_tile_weights): [ceil(M/128) * nkb] tiles of [128][64] bf16.
+template <int BN>
+int infer_gemm_bn(const char* tag, int slot, const void* W, int64_t M, int64_t K,
+                  const void* act, int64_t B, int64_t ld_act, float* part, int* split_out,
+                  cudaStream_t st) {
+  CUtensorMap ma, mb;
+  int rc;
+  const int nkb = cdiv(K, tc::BK);
+  const int64_t wtiles = (int64_t)cdiv(M, tc::BM) * nkb;
+  if ((rc = make_map(&ma, W, tc::BK, tc::BM, wtiles, tc::BK * 2, tc::BK * tc::BM * 2, tc::BK,
+                     tc::BM)))
+    return rc;
+  if ((rc = map_kmajor(&mb, act, K, B, ld_act, 1, 0, BN))) return rc;
+  const int tiles = cdiv(M, tc::BM) * cdiv(B, BN);
+  const int sp = infer_split(tiles, nkb, 4);
+  tc::TileShape sh{(int)M, (int)B, nkb, 0, 0, 0, 0, 0, 1, 0};
+  sh.ksplit = sp;
+  sh.sched = sched_counter(slot);
+  const char* e = getenv("PPO_INFER_EVICT_FIRST");
+  sh.a_evict_first = e ? atoi(e) : 1;
+  sh.a_tiled_nkb = nkb;
+  tc::EpiStoreF32T epi{part, M, (int)M, (int)B, M * B};
+  *split_out = sp;
+  constexpr int STAGES = BN == 64 ? 8 : BN == 128 ? 6 : 4;
+  return launch<BN, false, false, tc::EpiStoreF32T, STAGES>(tag, ma, ma, mb, mb, sh, epi, st,
+                                                             true);
+}
+int infer_gemm(const char* tag, int slot, const void* W, int64_t M, int64_t K, const void* act,
+               int64_t B, int64_t ld_act, float* part, int* split_out, cudaStream_t st) {
+  if (B <= 64)
+    return infer_gemm_bn<64>(tag, slot, W, M, K, act, B, ld_act, part, split_out, st);
+  if (B <= 128)
+    return infer_gemm_bn<128>(tag, slot, W, M, K, act, B, ld_act, part, split_out, st);
+  return infer_gemm_bn<256>(tag, slot, W, M, K, act, B, ld_act, part, split_out, st);
+}
+
+}  // namespace
+
+size_t tc_infer_tiled_offset_heads(const Shape& s) {
+  return (size_t)cdiv(s.G4, tc::BM) * cdiv(s.Kx, tc::BK) * tc::BM * tc::BK;  // elements
+}
+size_t tc_infer_tiled_elems(const Shape& s) {
+  return tc_infer_tiled_offset_heads(s) + (size_t)cdiv(s.A, tc::BM) * cdiv(s.Ko, tc::BK) * tc::BM * tc::BK;
+}
+int tc_infer_gates(const Shape& s, int64_t B, const void* wt, const void* xh, float* part,
+                   int* split, cudaStream_t st) {
+  return infer_gemm("infer_gates", kSchedInferGates, wt, s.G4, s.Kx, xh, B, s.Kx, part, split, st);
+}
+int tc_infer_heads(const Shape& s, int64_t B, const void* wt, const void* ho, float* part,
+                   int* split, cudaStream_t st) {
+  const __nv_bfloat16* wo = static_cast<const __nv_bfloat16*>(wt) + tc_infer_tiled_offset_heads(s);
+  return infer_gemm("infer_heads", kSchedInferHeads, wo, s.A, s.Ko, ho, B, s.Ko, part, split, st);
+}
+int tc_infer_max_split() { return kMaxSplitK; }
 
 // ---------------------------------------------------------------- standalone test GEMM
 // mode bit0: B is MN-major ([K][N]) else K-major ([N][K]); bit1: A is MN-major ([K][M]).

@@ -1,0 +1,116 @@
+"""NEXT-3 on the GPU: ppo_infer_step (LSTM step + heads + masked Gumbel-max sampling) against
+the oracle (oracle/infer.py), carrying the recurrent state over several steps.
+
+Tolerances (bf16 tensor-core path): state h, c and head outputs
+normwise 2e-2.  Sampled actions are integers decided by floating point: where the oracle's
+best Gumbel score leads the runner-up by more than DELTA the draw must be identical; inside
+that window the GPU's draw must be a valid near-maximum of the oracle's scores.  logp is
+compared on rows whose draws all agree.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle.infer as oi
+import synth
+from gpu_util import dev, normwise
+
+pytestmark = pytest.mark.gpu
+KEYS = ("Wx", "Wh", "b", "Wo", "bo")
+DELTA = 0.05
+
+
+def _server(cfg, B, prm, table, seed):
+    from paper_1912_06680_b200 import _lib as L
+    from paper_1912_06680_b200.infer import PolicyServer
+    srv = PolicyServer(cfg.D, cfg.H, B, cfg.head_sizes, head_table=dev(table), seed=seed)
+    theta = torch.empty(srv.layout.n_total, device="cuda")
+    L.ppo_pack_params(srv.dims, *(dev(prm[k]) for k in KEYS), theta)
+    shadow = torch.empty(srv.layout.n_total, dtype=torch.bfloat16, device="cuda")
+    L.ppo_cast_bf16(theta, shadow)
+    srv.load(shadow)
+    return srv
+
+
+def _check_actions(act, ref, avail, table, head_sizes):
+    off = np.concatenate([[0], np.cumsum(head_sizes)])
+    B, nh = act.shape
+    mism = 0
+    for b in range(B):
+        if ref["act"][b, 0] < 0:
+            assert act[b, 0] == -1
+        for k in range(nh):
+            a, r = act[b, k], ref["act"][b, k]
+            if k == 0 and r < 0:
+                continue
+            sc = ref["score"][b, off[k]:off[k + 1]]
+            top2 = np.sort(sc)[-2:] if sc.size > 1 else np.array([-np.inf, sc[0]])
+            if a != r:
+                mism += 1
+                assert top2[1] - top2[0] <= DELTA, (b, k, a, r, top2)
+                assert 0 <= a < head_sizes[k] and sc[a] >= top2[1] - DELTA, (b, k, a, sc[a], top2)
+            if k == 0:
+                assert avail[b, a] == 1
+    assert mism <= max(1, 0.02 * B * nh), mism
+    return mism
+
+
+@pytest.mark.parametrize("H,D,B", [(256, 192, 60), (256, 192, 1), (128, 256, 130),
+                                   (4096, 4032, 60)])
+def test_infer_steps_vs_oracle(H, D, B):
+    cfg = synth.Config(H=H, D=D, B=B, T=3)
+    prm = synth.make_params(cfg, 7, bo_scale=0.3)
+    prm["Wo"] = prm["Wo"] * 50.0                   # logits O(1): real preferences to sample
+    prm = {k: synth.round_bf16(v) for k, v in prm.items()}   # the weights the kernel reads
+    s = synth.make_sequences(cfg, 8)
+    avail = s["avail"].copy()
+    if B > 3:
+        avail[:, 3] = 0                             # a row with nothing available (Q23)
+    table = synth.heads_on_table(cfg.head_sizes)
+    seed = 12345
+    srv = _server(cfg, B, prm, table, seed)
+    srv.reset(dev(s["h0"]), dev(s["c0"]))
+    h, c = s["h0"].astype(np.float64), s["c0"].astype(np.float64)
+    p64 = {k: v.astype(np.float64) for k, v in prm.items()}
+    for t in range(cfg.T):
+        act, head_on, logp, value = srv.step(dev(s["x"][t]).bfloat16(), dev(avail[t]))
+        torch.cuda.synchronize()
+        ref = oi.infer_step(p64, s["x"][t], h, c, avail[t], table, seed, t, cfg.head_sizes)
+        h, c = ref["h"], ref["c"]
+        assert normwise(srv.h.cpu().numpy(), h) < 2e-2, t
+        assert normwise(srv.c.cpu().numpy(), c) < 2e-2, t
+        assert normwise(srv.out.cpu().numpy(), ref["y"]) < 2e-2, t
+        # the value is the last head output (its parity is part of out's)
+        assert torch.equal(value, srv.out[:, -1])
+        a = act.cpu().numpy()
+        _check_actions(a, ref, avail[t], table, cfg.head_sizes)
+        # head_on is the table row of the GPU's own primary draw (-1: none)
+        ho = head_on.cpu().numpy()
+        for b in range(B):
+            exp = table[a[b, 0]] if a[b, 0] >= 0 else np.zeros_like(table[0])
+            assert np.array_equal(ho[b], exp), b
+        same = np.all(a == ref["act"], axis=1)
+        assert same.mean() > 0.8
+        lp = logp.cpu().numpy()
+        err = np.abs(lp[same] - ref["logp"][same])
+        assert np.all(err <= 2e-2 * (1.0 + np.abs(ref["logp"][same]))), err.max()
+        if B > 3:
+            assert a[3, 0] == -1 and lp[3] == 0.0 and not ho[3].any()
+    # the state was actually carried (not reset) across the steps
+    assert not np.allclose(h, s["h0"])
+
+
+def test_infer_deterministic_and_counter():
+    cfg = synth.Config(H=128, D=128, B=40, T=1)
+    prm = {k: synth.round_bf16(v) for k, v in synth.make_params(cfg, 1, bo_scale=0.3).items()}
+    s = synth.make_sequences(cfg, 2)
+    table = synth.heads_on_table(cfg.head_sizes)
+    outs = []
+    for _ in range(2):
+        srv = _server(cfg, cfg.B, prm, table, seed=5)
+        srv.reset(dev(s["h0"]), dev(s["c0"]))
+        a, _, lp, _ = srv.step(dev(s["x"][0]).bfloat16(), dev(s["avail"][0]))
+        outs.append((a.clone(), lp.clone(), srv.h.clone()))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert torch.equal(outs[0][2], outs[1][2])

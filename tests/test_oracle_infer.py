@@ -4,7 +4,7 @@ What pins it to something other than itself:
   * the carried state: two inference steps == the (pinned) LSTM oracle over a 2-step sequence;
   * Gumbel-max: empirical action frequencies over many counter draws == softmax probabilities
     (chi-square), which a sign or direction error in g = -log(-log u) fails;
-  * the generator: u strictly inside (0, 1), 24-bit grid, moments of U(0, 1);
+  * the generator: u strictly inside (0, 1), 23-bit grid exact in binary32, moments of U(0, 1);
   * masks: an unavailable primary is never drawn, a lone available one always (log p = 0);
   * bookkeeping: head_on = table[primary]; logp == the (pinned) loss oracle's log pi of the
     sampled actions; inactive heads add nothing.
@@ -47,9 +47,10 @@ def test_state_carry_equals_two_step_lstm():
 def test_uniform_generator():
     u = oi.uniforms(123, 5, 40, 655)
     assert u.min() > 0.0 and u.max() < 1.0
-    # 24-bit grid: (j + 1/2) / 2^24
-    j = u * (1 << 24) - 0.5
+    # 23-bit grid: (j + 1/2) / 2^23, every value exact in binary32
+    j = u * (1 << 23) - 0.5
     assert np.array_equal(j, np.round(j))
+    assert np.array_equal(u.astype(np.float32).astype(np.float64), u)
     assert abs(u.mean() - 0.5) < 0.01 and abs(u.var() - 1.0 / 12) < 0.005
     # distinct rows / steps give distinct draws; same counter gives the same draw
     assert not np.array_equal(u[0], u[1])
@@ -99,6 +100,19 @@ def test_primary_mask_and_lone_action():
         sk = score[:, off[k]:off[k + 1]]
         assert np.array_equal(act[:, k], sk.argmax(1))
     assert np.array_equal(np.isinf(score[:, :hs[0]]), avail == 0)
+
+
+def test_no_available_primary():
+    hs = CFG.head_sizes
+    rng = np.random.default_rng(1)
+    y = rng.standard_normal((3, sum(hs) + 1))
+    avail = np.ones((3, hs[0]), np.uint8)
+    avail[1] = 0
+    act, head_on, logp, _ = oi.sample(y, oi.uniforms(0, 0, 3, sum(hs)), avail,
+                                      synth.heads_on_table(hs), hs)
+    assert act[1, 0] == -1 and not head_on[1].any() and logp[1] == 0.0
+    assert act[0, 0] >= 0 and head_on[0, 0] == 1 and logp[0] < 0
+    assert np.all(act[1, 1:] >= 0)
 
 
 def test_logp_equals_loss_oracle_log_pi():
