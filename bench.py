@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1, help="oracle sample: sequences per step")
+    ap.add_argument("--dx", action="store_true",
+                    help="NEXT-4: also produce dL/dx for the observation network each step")
     ap.add_argument("--infer-B", type=str, default="60,1,240,960",
                     help="--config infer: comma-separated batch sizes (first = headline)")
     ap.add_argument("--config", choices=["full", "gae", "iteration", "infer"], default="full",
@@ -201,12 +203,15 @@ def workload_config(args, n):
     return {
         "workload": (f"full OpenAI-Five LSTM-{args.H} PPO step: D={args.D}, T=16, "
                      f"B={args.B} sequences/GPU ({args.B // SEQ_PER_SAMPLE} paper samples), "
-                     f"A=656 (7 factorised heads + value), GAE over 256-step segments"),
+                     f"A=656 (7 factorised heads + value), GAE over 256-step segments"
+                     + (", + dL/dx for the observation network" if getattr(args, "dx", False)
+                        else "")),
         "H": args.H, "D": args.D, "T": 16, "B_per_gpu": args.B,
         "global_batch_samples": args.B * n // SEQ_PER_SAMPLE,
         "global_batch_timesteps": args.B * n * 16,
         "parallelism": f"dp{n}",
         "l2": "inputs larger than L2 (x alone is T*B*D*2 bytes per step)",
+        "dx": bool(getattr(args, "dx", False)),
     }
 
 
@@ -228,6 +233,7 @@ def algorithmic(H, D, T, B, A, nparam):
         "pack_x": ("byte", rows * D * 2.0 + (T + 1) * B * (D + H + 64) * 2.0 + 8.0 * B * H),
         # h0, c0 in (fp32); h0 bf16 + c0 fp32 out; the [1 | 0...] pad of T+1 slots
         "pack_state": ("byte", 8.0 * B * H + 6.0 * B * H + (T + 1) * B * 64 * 2.0),
+        "input_grad": ("flop", 2.0 * rows * G4 * D),
     }
 
 
@@ -546,8 +552,9 @@ def main():
         if world > 1:
             dist.barrier()
 
+    dx = torch.empty(T, B, D, device=device) if args.dx else None
     for _ in range(args.warmup):
-        opt.step(batch)
+        opt.step(batch, dx=dx)
     torch.cuda.synchronize()
     stats = opt.stats[:8].cpu().tolist()
 
@@ -561,7 +568,7 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        opt.step(batch)
+        opt.step(batch, dx=dx)
     e1.record(stream)
     torch.cuda.synchronize()
     prof = L.prof_stop()
@@ -653,7 +660,7 @@ def main():
                 if i + 1 < nsteps:
                     upload(1 - cur)
                 opt.select_ws(cur)
-                opt.step(bufs[cur])
+                opt.step(bufs[cur], dx=dx)
                 used[cur].record(stream)
                 st_host.copy_(opt.stats[:8], non_blocking=True)
 

@@ -171,6 +171,13 @@ int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,
 int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
                   const void* dout, int64_t B, float* grad, ppo_stream_t s);
 
+/* NEXT-4: dL/dx for the upstream observation-processing network (the processed
+ * observation vector is the LSTM input).  dx[t][b][:] = dz_t[b] W_x for all t, from the dz
+ * that lstm_bptt_bwd left in ws (call it after lstm_bptt_bwd, same w, ws, B).
+ * dx: [T][B][D] fp32, device, 16-byte aligned, overwritten.  Asynchronous. */
+int lstm_input_grad(const ppo_dims* dims, const void* w, const void* ws, size_t ws_bytes,
+                    int64_t B, float* dx, ppo_stream_t s);
+
 /* ---- a9: data-parallel gradient average (P:1251 NCCL allreduce; O9) --------------------- */
 typedef struct ppo_comm ppo_comm;
 #define PPO_COMM_ID_BYTES 128

@@ -25,7 +25,7 @@ Parity status ("Oracle pins"):
                  masks, target-type table, logp = the loss oracle's log pi
 """
 from .gae import gamma_from_horizon, gae, segments_to_sequences  # noqa: F401
-from .lstm import lstm_forward, lstm_backward  # noqa: F401
+from .lstm import lstm_forward, lstm_backward, lstm_input_grad  # noqa: F401
 from .loss import heads_forward, heads_backward, ppo_loss, STAT_NAMES  # noqa: F401
 from .adam import adam_clip  # noqa: F401
 from .step import ppo_step, dp_average  # noqa: F401

@@ -90,3 +90,10 @@ def lstm_backward(cache, dh_out):
         dWh += dz.T @ h_prev
         db += dz.sum(axis=0)
     return dWx, dWh, db, dzs
+
+
+def lstm_input_grad(Wx, dz):
+    """NEXT-4, the dX output for upstream observation processing (P:1204-1212 [§3.1]: the
+    LSTM input is the output of the observation-processing network, which is trained
+    through it): dL/dx_t = dz_t W_x for every t.  dz [T][B][4H] from lstm_backward."""
+    return np.asarray(dz, np.float64) @ np.asarray(Wx, np.float64)

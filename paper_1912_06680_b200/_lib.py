@@ -107,6 +107,7 @@ _lib_fns = dict(
     ppo_reward_gae=([c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p,
                      POINTER(ppo_reward_cfg), c_void_p, c_float, c_float, c_int32, c_void_p,
                      c_void_p, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
+    lstm_input_grad=([_D, c_void_p, c_void_p, c_size_t, c_int64, c_void_p, c_void_p], c_int),
     ppo_infer_ws_bytes=([_D, c_int64, POINTER(c_size_t)], c_int),
     ppo_infer_weights_bytes=([_D, POINTER(c_size_t)], c_int),
     ppo_infer_pack_weights=([_D, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
@@ -268,6 +269,11 @@ def ppo_reward_gae(shaped, win, step0, val, done, cfg, stats, gamma, lam, adv, r
                                ctypes.byref(cfg), _p(stats), gamma, lam, seq_T, _p(rew_out),
                                _p(adv), _p(ret), _p(scratch),
                                scratch.numel() * scratch.element_size(), _s(stream)))
+
+
+def lstm_input_grad(dims, w, ws, B, dx, stream=None):
+    _check(_lib.lstm_input_grad(ctypes.byref(dims), _p(w), _p(ws), ws.numel() * ws.element_size(),
+                                B, _p(dx), _s(stream)))
 
 
 def infer_ws_bytes(dims, B) -> int:

@@ -407,6 +407,31 @@ int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes
   return PPO_OK;
 }
 
+int lstm_input_grad(const ppo_dims* dims, const void* w, const void* ws, size_t ws_bytes,
+                    int64_t B, float* dx, ppo_stream_t st_) {
+  cudaStream_t st = (cudaStream_t)st_;
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
+  NEED(w);
+  NEED(dx);
+  if (!ws || !aligned(ws, 1024)) return fail(PPO_E_ALIGN, "ws must be 1024-byte aligned");
+  WsLayout L = ws_layout(s, B);
+  if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small");
+  void* wsm = const_cast<void*>(ws);
+  if (s.bf16) {
+    if ((rc = check_tc_device())) return rc;
+    return tc_input_grad(s, B, w, wsm, dx, st);
+  }
+  const float* G = reinterpret_cast<const float*>(static_cast<const uint8_t*>(ws) + L.g);
+  const int64_t rows = s.T * B;
+  SimtOp a{{G, nullptr}, {s.G4, 0}, {rows, 0}, {s.G4, 0}, s.G4, false};
+  SimtOp b{{static_cast<const float*>(w), nullptr}, {s.Kx, 0}, {s.D, 0}, {s.G4, 0}, s.G4, true};
+  ProfScope _prof("input_grad", st);
+  return launch_simt_gemm(a, b, rows, s.D, s.G4, dx, s.D, st);
+}
+
 int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, size_t n,
               int64_t t, double lr, double b1, double b2, double eps, double clip_sigma,
               ppo_stream_t st) {

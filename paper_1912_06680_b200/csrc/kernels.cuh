@@ -62,6 +62,8 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
 int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
                 cudaStream_t st);
 // Standalone test GEMM (exported for tests): C = A B^T variants on bf16 inputs.
+// NEXT-4: dX = dz W_x over all T*B rows (bf16 path)
+int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx, cudaStream_t st);
 // NEXT-3: split-K skinny GEMMs of the inference step (weights x batch); *split = partials
 int tc_infer_gates(const Shape& s, int64_t B, const void* w, const void* xh, float* part,
                    int* split, cudaStream_t st);

@@ -14,7 +14,7 @@ namespace {
 // One slot per GEMM call site, so stream-ordered launches never share a live counter.
 enum SchedSlot {
   kSchedFwd = 0, kSchedHeads, kSchedBwd, kSchedWgrad, kSchedWgradO, kSchedTest,
-  kSchedInferGates, kSchedInferHeads, kSchedSlots
+  kSchedInferGates, kSchedInferHeads, kSchedDx, kSchedSlots
 };
 __device__ unsigned int g_sched_ctr[2 * kSchedSlots];
 
@@ -313,6 +313,24 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
       return rc;
   }
   return PPO_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-4: dL/dx
+// dX[t][b] = dz_t[b] W_x for all t at once: A = dz (G, [T*B][4H] K-major), B = W_x (the
+// first D columns of W_xh_aug, MN-major [4H][D] with ld Kx); CTA-pair 256x256 tiles.
+int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx, cudaStream_t st) {
+  WsPtrs P = ws_ptrs(s, B, ws);
+  const __nv_bfloat16* wxh = static_cast<const __nv_bfloat16*>(w);
+  const int64_t rows = s.T * B;
+  CUtensorMap ma, mb;
+  int rc;
+  if ((rc = map_kmajor(&ma, P.g, s.G4, rows, s.G4, 1, 0, tc::BM))) return rc;
+  if ((rc = map_mnmajor(&mb, wxh, s.D, s.G4, s.Kx))) return rc;
+  tc::TileShape sh{(int)rows, (int)s.D, cdiv(s.G4, tc::BK), 0, 0, 0, 0, 0, 8, 0};
+  raster(sh, "DX", 8, 0);
+  sh.sched = sched_counter(kSchedDx);
+  tc::EpiStoreF32 epi{dx, s.D, (int)rows, (int)s.D};
+  return launch2<false, true>("input_grad", ma, ma, mb, mb, sh, epi, st);
 }
 
 // ---------------------------------------------------------------- NEXT-3 inference GEMMs

@@ -123,6 +123,10 @@ class PPOOptimizer:
         """a6-a8"""
         L.lstm_bptt_bwd(self.dims, self.weights, self.ws, self.dout, self.B, self.grad, stream)
 
+    def input_grad(self, dx: torch.Tensor, stream=None):
+        """NEXT-4: dL/dx [T][B][D] fp32 for the observation-processing network (after backward)"""
+        L.lstm_input_grad(self.dims, self.weights, self.ws, self.B, dx, stream)
+
     def allreduce(self, stream=None):
         """a9"""
         if self.comm is not None:
@@ -135,12 +139,15 @@ class PPOOptimizer:
         L.adam_step(self.theta, self.shadow, self.grad, self.m, self.v, self.t, h["lr"],
                     h["beta1"], h["beta2"], h["adam_eps"], h["clip_sigma"], stream)
 
-    def step(self, batch, stream=None):
-        """One full optimizer step a1-a10 on this rank; returns the device stats tensor."""
+    def step(self, batch, stream=None, dx=None):
+        """One full optimizer step a1-a10 on this rank; returns the device stats tensor.
+        dx: optional [T][B][D] fp32 output for dL/dx (NEXT-4)."""
         self.gae(batch, stream)
         self.forward(batch, stream)
         self.loss(batch, stream=stream)
         self.backward(stream)
+        if dx is not None:
+            self.input_grad(dx, stream)
         self.allreduce(stream)
         self.apply(stream)
         return self.stats[:L.PPO_STATS]

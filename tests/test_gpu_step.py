@@ -179,3 +179,41 @@ def test_zero_copy_x_matches_packed(precision):
     assert p == opt.ws_list[1].data_ptr() and ld == cfg.D + cfg.H + 64
     with pytest.raises(RuntimeError):
         opt.forward(dict(batch, x=None, c0=None))
+
+
+def test_lstm2048_full_width_bf16():
+    """NEXT-4: the LSTM-2048 variant (the hidden size before the 4096 surgery)
+    with the paper's D = 4032 (DESIGN Q1)."""
+    cfg = synth.Config(H=2048, D=4032, B=48)
+    case = make_case(cfg, 9, pad_frac=0.1, wo_scale=5.0)
+    _check_step(case, cfg, "bf16", 2e-2, 2e-2)
+
+
+def test_lstm2048_fp32():
+    cfg = synth.Config(H=2048, D=4032, B=16)
+    case = make_case(cfg, 10, pad_frac=0.1, wo_scale=5.0)
+    _check_step(case, cfg, "fp32", 1e-4, 1e-4)
+
+
+@pytest.mark.parametrize("precision,H,D,B,tol", [("fp32", 256, 192, 176, 1e-4),
+                                                 ("bf16", 256, 192, 176, 2e-2),
+                                                 ("bf16", 4096, 4032, 48, 2e-2)])
+def test_input_grad(precision, H, D, B, tol):
+    """NEXT-4: dL/dx for the observation-processing network (lstm_input_grad) against the
+    oracle's dz W_x (oracle.lstm_input_grad, pinned to autograd)."""
+    from paper_1912_06680_b200 import PPOOptimizer
+    cfg = synth.Config(H=H, D=D, B=B)
+    case = make_case(cfg, 6, pad_frac=0.1, wo_scale=10.0)
+    opt = PPOOptimizer(cfg.D, cfg.H, cfg.B, cfg.T, cfg.head_sizes, precision=precision)
+    load_params(opt, case["params"])
+    batch = device_batch(case, precision == "bf16")
+    opt.gae(batch)
+    opt.forward(batch)
+    opt.loss(batch)
+    opt.backward()
+    dx = torch.full((cfg.T, cfg.B, cfg.D), float("nan"), device="cuda")
+    opt.input_grad(dx)
+    torch.cuda.synchronize()
+    ref = oracle.lstm_input_grad(case["params"]["Wx"], case["inter"]["dz"])
+    e = normwise(dx.cpu().numpy(), ref)
+    assert e < tol, e

@@ -42,13 +42,16 @@ def test_matches_torch_lstm_forward_and_grads(seed):
         lstm.weight_hh_l0.copy_(torch.from_numpy(Wh))
         lstm.bias_ih_l0.copy_(torch.from_numpy(b))
         lstm.bias_hh_l0.zero_()
-    hs, (hT, cT) = lstm(torch.from_numpy(x), (torch.from_numpy(h0)[None], torch.from_numpy(c0)[None]))
+    xt = torch.from_numpy(x).requires_grad_(True)
+    hs, (hT, cT) = lstm(xt, (torch.from_numpy(h0)[None], torch.from_numpy(c0)[None]))
     (hs * torch.from_numpy(G)).sum().backward()
 
     out = oracle.lstm_forward(Wx, Wh, b, x, h0, c0)
     np.testing.assert_allclose(out["h"], hs.detach().numpy(), rtol=0, atol=1e-13)
     np.testing.assert_allclose(out["c"][-1], cT[0].detach().numpy(), rtol=0, atol=1e-13)
-    dWx, dWh, db, _ = oracle.lstm_backward(out, G)
+    dWx, dWh, db, dz = oracle.lstm_backward(out, G)
+    # NEXT-4: the input gradient dL/dx_t = dz_t W_x equals autograd's x.grad
+    np.testing.assert_allclose(oracle.lstm_input_grad(Wx, dz), xt.grad.numpy(), rtol=0, atol=1e-12)
     np.testing.assert_allclose(dWx, lstm.weight_ih_l0.grad.numpy(), rtol=0, atol=1e-12)
     np.testing.assert_allclose(dWh, lstm.weight_hh_l0.grad.numpy(), rtol=0, atol=1e-12)
     np.testing.assert_allclose(db, lstm.bias_ih_l0.grad.numpy(), rtol=0, atol=1e-12)
