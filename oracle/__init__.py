@@ -21,6 +21,10 @@ Parity status ("Oracle pins"):
   dp average     pinned (shard identity)
   buffer         sampler pinned to splitmix64's published test vector; gather = indexing
   step           composition of the above, pinned end-to-end by finite differences
+  aux (NEXT-4)   labels = the paper's piecewise equation + closed-form 2-min discount; losses:
+                 ln 2 / ln n closed forms, finite differences; routing: FD of the composed
+                 step (trunk sees L_ppo + w c_win L_win, aux rows the whole loss)
+  lstm_input_grad (NEXT-4) = torch autograd's x.grad
   infer (NEXT-3) state carry = 2-step LSTM; Gumbel-max frequencies = softmax (chi-square);
                  masks, target-type table, logp = the loss oracle's log pi
 """
@@ -31,3 +35,4 @@ from .adam import adam_clip  # noqa: F401
 from .step import ppo_step, dp_average  # noqa: F401
 from . import buffer  # noqa: F401
 from . import infer  # noqa: F401
+from . import aux  # noqa: F401

@@ -69,10 +69,12 @@ class Config:
     B: int
     T: int = 16
     head_sizes: tuple = field(default=HEAD_SIZES)
+    #: NEXT-4 aux heads (n_win, n_rank, n_bld) appended after the value (DESIGN Q24)
+    aux: tuple = field(default=(0, 0, 0))
 
     @property
     def A(self) -> int:
-        return sum(self.head_sizes) + 1
+        return sum(self.head_sizes) + 1 + sum(self.aux)
 
     @property
     def rows(self) -> int:
@@ -190,6 +192,30 @@ def make_rollouts(R: int, L: int, seed: int, p_done: float = 1.0 / 20000) -> dic
     V = rng.standard_normal((R, L + 1)).astype(np.float32)
     d = (rng.uniform(0, 1, (R, L)) < p_done).astype(np.uint8)
     return dict(r=r, V=V, done=d)
+
+
+#: NEXT-4 defaults: win probability, net-worth rank among the 5 heroes, the enemy team's 18
+#: buildings (11 towers, 6 barracks, the ancient) (DESIGN Q24).
+AUX_SIZES = (1, 5, 18)
+
+
+def make_aux(R: int, L: int, aux: tuple, seed: int, p_last: float = 0.1,
+             p_event: float = 1.0 / 2000) -> dict:
+    """Per 256-step segment: whether it is the game's last (p_last), the outcome (win 0/1)
+    and final net-worth rank (0-based), building events [R][L][n_bld] (Bernoulli p_event per
+    step), and the model's bootstrap predictions after the last step: win ~ U(0,1), rank a
+    normalised U(0,1) vector, buildings ~ U(0, 0.3)."""
+    n_win, n_rank, n_bld = aux
+    rng = _rng(seed)
+    boot = [rng.uniform(0, 1, size=(R, n_win))]
+    rk = rng.uniform(0, 1, size=(R, n_rank))
+    boot.append(rk / np.maximum(rk.sum(axis=1, keepdims=True), 1e-12) if n_rank else rk)
+    boot.append(rng.uniform(0, 0.3, size=(R, n_bld)))
+    return dict(last=(rng.random(R) < p_last).astype(np.uint8),
+                outcome=(rng.random(R) < 0.5).astype(np.float32),
+                rank=rng.integers(0, max(n_rank, 1), size=R).astype(np.int32),
+                events=(rng.random((R, L, n_bld)) < p_event).astype(np.uint8),
+                boot=np.concatenate(boot, axis=1).astype(np.float32))
 
 
 def make_logits(rows: int, A: int, seed: int, scale: float = 1.0) -> np.ndarray:
