@@ -556,7 +556,7 @@ def main():
     for _ in range(args.warmup):
         opt.step(batch, dx=dx)
     torch.cuda.synchronize()
-    stats = opt.stats[:8].cpu().tolist()
+    stats = opt.stats[:L.PPO_STATS].cpu().tolist()
 
     clocks = Clocks(local)
     barrier()

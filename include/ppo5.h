@@ -56,6 +56,13 @@ typedef struct {
   int32_t n_heads;
   int32_t head_sizes[PPO_MAX_HEADS];
   int32_t precision;
+  /* NEXT-4 auxiliary heads (DESIGN Q24-Q27), appended after the value output:
+   * n_aux_win in {0,1} logistic win probability, n_aux_rank in [0,32] softmax net-worth
+   * rank, n_aux_bld in [0,64] logistic enemy-building predictions.  aux_win_trunk >= 0 is
+   * the weight of the win head's gradient into the LSTM ("a very small weight");
+   * the rank and building heads are stop_gradient.  All zero = no aux heads. */
+  int32_t n_aux_win, n_aux_rank, n_aux_bld;
+  float aux_win_trunk;
 } ppo_dims;
 
 /* Flat parameter vector theta (fp32 master; grads, Adam m and v share the layout).
@@ -76,6 +83,7 @@ typedef struct {
   float c_v;      /* value loss weight, 1.0 */
   float c_e;      /* entropy coefficient, 0.01 */
   float denom;    /* loss denominator; <= 0 means T*B (DESIGN Q9) */
+  float c_win, c_rank, c_bld; /* NEXT-4 aux loss weights (DESIGN Q25); unused without aux */
 } ppo_loss_cfg;
 
 /* stats[] layout written by ppo_loss_grad (all Σ_rows w·x / denom unless noted) */
@@ -85,10 +93,11 @@ enum {
   PPO_STAT_CLIPFRAC = 5,  /* rows on the clipped (zero-gradient) side */
   PPO_STAT_NVALID = 6,    /* Σ w */
   PPO_STAT_FLAGS = 7,     /* bit0 non-finite, bit1 taken primary unavailable, bit2 empty avail */
-  PPO_STATS = 8
+  PPO_STAT_AUX = 8,       /* NEXT-4: the aux part of LOSS, sum of c_k * aux loss k */
+  PPO_STATS = 9
 };
 #define PPO_LOSS_BLOCKS 1184                       /* 148 SMs x 8 */
-#define PPO_STATS_BUF (PPO_STATS * (1 + PPO_LOSS_BLOCKS)) /* floats; [0,8) = result */
+#define PPO_STATS_BUF (PPO_STATS * (1 + PPO_LOSS_BLOCKS)) /* floats; [0,PPO_STATS) = result */
 
 /* ---- library / errors ---------------------------------------------------------------- */
 const char* ppo_last_error(void);                  /* thread-local message of the last error */
@@ -156,18 +165,38 @@ int ppo_copy_x(const ppo_dims* dims, int64_t B, const void* src, int64_t src_ld,
  * (heads read by the taken primary action, Table target types P:350-368); avail
  * [T·B][head_sizes[0]] u8 (action filter); logp_old, adv, ret [T·B] fp32;
  * valid [T·B] u8 or NULL (= all rows valid).
+ * aux_label [T·B][n_aux] fp32 (n_aux = n_aux_win + n_aux_rank + n_aux_bld; NULL when 0):
+ * the NEXT-4 targets from ppo_aux_labels; the aux losses (DESIGN Q25) join the loss.
+ * Output columns: [policy logits | value | aux]; the value is column head_off[n_heads].
  * dout [T·B][A]: dL/dout, in the path's activation type (bf16 bits / fp32), consumed by
- * lstm_bptt_bwd.  logp [T·B] fp32 or NULL: current log pi(a).  stats [PPO_STATS_BUF]. */
+ * lstm_bptt_bwd; the win column holds aux_win_trunk x its gradient when aux_win_trunk > 0
+ * (lstm_bptt_bwd undoes the factor for the win head's own weights, DESIGN Q26).
+ * logp [T·B] fp32 or NULL: current log pi(a).  stats [PPO_STATS_BUF]. */
 int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,
                   const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
-                  const float* adv, const float* ret, const uint8_t* valid, int64_t B,
-                  const ppo_loss_cfg* cfg, void* dout, float* logp, float* stats,
-                  ppo_stream_t s);
+                  const float* adv, const float* ret, const uint8_t* valid,
+                  const float* aux_label, int64_t B, const ppo_loss_cfg* cfg, void* dout,
+                  float* logp, float* stats, ppo_stream_t s);
+
+/* NEXT-4: aux-head targets per 256-step segment (Eq.; DESIGN Q27), computed at
+ * ingest like GAE.  R segments of L steps; last [R] u8 (the game's last segment), outcome
+ * [R] fp32 (1 = win), rank [R] int32 (0-based final net-worth rank), events [R][L][n_aux_bld]
+ * u8 (the hero helped destroy building j at that step), boot [R][n_aux] fp32 (the model's
+ * predictions after the segment's last step: win probability, rank distribution, building
+ * values), gamma2 = 1 - T_step / 120 s.  labels: seq_T == 0 -> [R][L][n_aux];
+ * seq_T > 0 (L % seq_T == 0) -> minibatch layout [seq_T][R*L/seq_T][n_aux] (sequence
+ * r*(L/seq_T) + l/seq_T, step l % seq_T), as ppo_gae.  Device pointers; asynchronous. */
+int ppo_aux_labels(const ppo_dims* dims, int64_t R, int64_t L, const uint8_t* last,
+                   const float* outcome, const int32_t* rank, const uint8_t* events,
+                   const float* boot, float gamma2, int32_t seq_T, float* labels,
+                   ppo_stream_t s);
 
 /* ---- a6-a8: backward (TBPTT, no gradient into h0/c0; O8) ------------------------
  * ws: the workspace filled by lstm_bptt_fwd for the same (w, B) (it is modified: saved gates
  * are overwritten by dz).  dout: from ppo_loss_grad.  grad: [n_total] fp32, OVERWRITTEN with
- * dL/dtheta in the theta layout (bias gradients fall out of the augmented columns). */
+ * dL/dtheta in the theta layout (bias gradients fall out of the augmented columns).
+ * Aux heads (NEXT-4): the LSTM receives the policy, value and (scaled) win columns of dout
+ * only; every output row of W_o_aug gets its head's full gradient (DESIGN Q26). */
 int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
                   const void* dout, int64_t B, float* grad, ppo_stream_t s);
 

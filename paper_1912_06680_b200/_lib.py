@@ -25,16 +25,18 @@ PPO_OK, PPO_E_ARG, PPO_E_SHAPE, PPO_E_ALIGN, PPO_E_CUDA, PPO_E_NCCL, PPO_E_UNSUP
     0, -1, -2, -3, -4, -5, -6)
 PPO_PREC_BF16, PPO_PREC_FP32 = 0, 1
 PPO_MAX_HEADS = 8
-PPO_STATS = 8
+PPO_STATS = 9
 PPO_LOSS_BLOCKS = 1184
 PPO_STATS_BUF = PPO_STATS * (1 + PPO_LOSS_BLOCKS)
 PPO_COMM_ID_BYTES = 128
-STAT_NAMES = ("loss", "pg", "vf", "ent", "approx_kl", "clipfrac", "n_valid", "flags")
+STAT_NAMES = ("loss", "pg", "vf", "ent", "approx_kl", "clipfrac", "n_valid", "flags", "aux")
 
 
 class ppo_dims(ctypes.Structure):
     _fields_ = [("D", c_int32), ("H", c_int32), ("T", c_int32), ("n_heads", c_int32),
-                ("head_sizes", c_int32 * PPO_MAX_HEADS), ("precision", c_int32)]
+                ("head_sizes", c_int32 * PPO_MAX_HEADS), ("precision", c_int32),
+                ("n_aux_win", c_int32), ("n_aux_rank", c_int32), ("n_aux_bld", c_int32),
+                ("aux_win_trunk", c_float)]
 
 
 class ppo_param_layout(ctypes.Structure):
@@ -43,7 +45,8 @@ class ppo_param_layout(ctypes.Structure):
 
 
 class ppo_loss_cfg(ctypes.Structure):
-    _fields_ = [("clip_eps", c_float), ("c_v", c_float), ("c_e", c_float), ("denom", c_float)]
+    _fields_ = [("clip_eps", c_float), ("c_v", c_float), ("c_e", c_float), ("denom", c_float),
+                ("c_win", c_float), ("c_rank", c_float), ("c_bld", c_float)]
 
 
 class ppo_prof_entry(ctypes.Structure):
@@ -91,8 +94,10 @@ _lib_fns = dict(
                     c_void_p, c_void_p], c_int),
     lstm_ws_x=([_D, c_int64, c_void_p, POINTER(c_void_p), POINTER(c_int64)], c_int),
     ppo_copy_x=([_D, c_int64, c_void_p, c_int64, c_void_p, c_size_t, c_void_p], c_int),
-    ppo_loss_grad=([_D] + [c_void_p] * 8 + [c_int64, POINTER(ppo_loss_cfg), c_void_p, c_void_p,
+    ppo_loss_grad=([_D] + [c_void_p] * 9 + [c_int64, POINTER(ppo_loss_cfg), c_void_p, c_void_p,
                                              c_void_p, c_void_p], c_int),
+    ppo_aux_labels=([_D, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                     c_float, c_int32, c_void_p, c_void_p], c_int),
     lstm_bptt_bwd=([_D, c_void_p, c_void_p, c_size_t, c_void_p, c_int64, c_void_p, c_void_p], c_int),
     ppo_comm_unique_id=([POINTER(c_uint8)], c_int),
     ppo_comm_init=([POINTER(c_uint8), c_int, c_int, POINTER(c_void_p)], c_int),
@@ -149,13 +154,16 @@ def _s(stream):
     return c_void_p(stream.cuda_stream)
 
 
-def make_dims(D, H, T, head_sizes, precision=PPO_PREC_BF16) -> ppo_dims:
+def make_dims(D, H, T, head_sizes, precision=PPO_PREC_BF16, aux=(0, 0, 0),
+              win_trunk=0.0) -> ppo_dims:
     d = ppo_dims()
     d.D, d.H, d.T = D, H, T
     d.n_heads = len(head_sizes)
     for i, h in enumerate(head_sizes):
         d.head_sizes[i] = h
     d.precision = precision
+    d.n_aux_win, d.n_aux_rank, d.n_aux_bld = aux
+    d.aux_win_trunk = win_trunk
     return d
 
 
@@ -220,10 +228,18 @@ def ppo_copy_x(dims, B, src, ws, stream=None):
 
 
 def ppo_loss_grad(dims, out, act, head_on, avail, logp_old, adv, ret, valid, B, cfg, dout, logp,
-                  stats, stream=None):
+                  stats, stream=None, aux_label=None):
     _check(_lib.ppo_loss_grad(ctypes.byref(dims), _p(out), _p(act), _p(head_on), _p(avail),
-                              _p(logp_old), _p(adv), _p(ret), _p(valid), B, ctypes.byref(cfg),
-                              _p(dout), _p(logp), _p(stats), _s(stream)))
+                              _p(logp_old), _p(adv), _p(ret), _p(valid), _p(aux_label), B,
+                              ctypes.byref(cfg), _p(dout), _p(logp), _p(stats), _s(stream)))
+
+
+def ppo_aux_labels(dims, last, outcome, rank, events, boot, gamma2, labels, seq_T=0,
+                   stream=None):
+    """NEXT-4 targets per segment: events [R][L][n_bld] (L from its shape)"""
+    R, Lseg = events.shape[0], events.shape[1]
+    _check(_lib.ppo_aux_labels(ctypes.byref(dims), R, Lseg, _p(last), _p(outcome), _p(rank),
+                               _p(events), _p(boot), gamma2, seq_T, _p(labels), _s(stream)))
 
 
 def lstm_bptt_bwd(dims, w, ws, dout, B, grad, stream=None):

@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libppo5.so")
-SOURCES = ["api.cu", "kernels.cu", "tc_path.cu", "comm.cu", "buffer.cu", "infer.cu"]
+SOURCES = ["api.cu", "kernels.cu", "tc_path.cu", "comm.cu", "buffer.cu", "infer.cu", "aux.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -99,7 +99,20 @@ int check_dims(const ppo_dims* d, Shape* s) {
     s->head_off[k + 1] = s->head_off[k] + d->head_sizes[k];
   }
   if (d->head_sizes[0] > 64) return fail(PPO_E_SHAPE, "primary head must have <= 64 actions");
-  s->A = s->head_off[d->n_heads] + 1;
+  if (d->n_aux_win < 0 || d->n_aux_win > 1 || d->n_aux_rank < 0 || d->n_aux_rank > 32 ||
+      d->n_aux_bld < 0 || d->n_aux_bld > 64)
+    return fail(PPO_E_SHAPE, "aux heads: n_aux_win in {0,1}, n_aux_rank <= 32, n_aux_bld <= 64");
+  if (!(d->aux_win_trunk >= 0.f) || !(d->aux_win_trunk < 1e30f))
+    return fail(PPO_E_ARG, "aux_win_trunk must be finite and >= 0");
+  s->vcol = s->head_off[d->n_heads];
+  s->n_win = d->n_aux_win;
+  s->n_rank = d->n_aux_rank;
+  s->n_bld = d->n_aux_bld;
+  s->n_aux = s->n_win + s->n_rank + s->n_bld;
+  s->win_trunk = d->aux_win_trunk;
+  s->win_pass = s->n_win && d->aux_win_trunk > 0.f;
+  s->A = s->vcol + 1 + s->n_aux;
+  s->A_pass = s->vcol + 1 + (s->win_pass ? 1 : 0);
   s->bf16 = d->precision == PPO_PREC_BF16;
   if (s->bf16 && (s->A * 2) % 16)
     return fail(PPO_E_SHAPE, "bf16 path needs A*2 to be a multiple of 16 bytes (TMA stride)");
@@ -320,18 +333,27 @@ int ppo_copy_x(const ppo_dims* dims, int64_t B, const void* src, int64_t src_ld,
 
 int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,
                   const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
-                  const float* adv, const float* ret, const uint8_t* valid, int64_t B,
-                  const ppo_loss_cfg* cfg, void* dout, float* logp, float* stats,
-                  ppo_stream_t st) {
+                  const float* adv, const float* ret, const uint8_t* valid,
+                  const float* aux_label, int64_t B, const ppo_loss_cfg* cfg, void* dout,
+                  float* logp, float* stats, ppo_stream_t st) {
   Shape s;
   int rc = check_dims(dims, &s);
   if (rc) return rc;
   if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
   if (!out || !act || !head_on || !avail || !logp_old || !adv || !ret || !cfg || !dout || !stats)
     return fail(PPO_E_ARG, "NULL pointer");
+  if (s.n_aux && !aux_label) return fail(PPO_E_ARG, "aux heads need aux_label");
   LossParams p{};
   p.N = s.T * B;
   p.A = (int)s.A;
+  p.vcol = s.vcol;
+  p.n_win = s.n_win;
+  p.n_rank = s.n_rank;
+  p.n_aux = s.n_aux;
+  p.c_win = cfg->c_win;
+  p.c_rank = cfg->c_rank;
+  p.c_bld = cfg->c_bld;
+  p.win_scale = s.win_pass ? s.win_trunk : 1.f;
   p.A_pad = (int)((s.A + 31) / 32 * 32);
   p.nh = s.n_heads;
   for (int k = 0; k <= s.n_heads; ++k) p.off[k] = s.head_off[k];
@@ -342,8 +364,8 @@ int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,
   p.inv_denom = (float)(1.0 / denom);
   if ((size_t)p.A_pad * 8 * sizeof(float) > 48 * 1024) return fail(PPO_E_SHAPE, "A too large");
   if (s.A > 6 * 128) return fail(PPO_E_SHAPE, "loss kernel supports A <= 768");
-  return launch_loss(p, s.bf16, out, act, head_on, avail, logp_old, adv, ret, valid, dout, logp,
-                     stats, (cudaStream_t)st);
+  return launch_loss(p, s.bf16, out, act, head_on, avail, logp_old, adv, ret, valid, aux_label,
+                     dout, logp, stats, (cudaStream_t)st);
 }
 
 int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
@@ -379,14 +401,16 @@ int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes
     const float* dYt = dY + t * B * s.A;
     SimtOp a, b;
     int64_t K;
+    // only the first A_pass output columns reach the LSTM (stop_gradient aux heads, Q26)
     if (last) {  // dh_{T-1} = dy_{T-1} W_o only
-      a = SimtOp{{dYt, nullptr}, {s.A, 0}, {B, 0}, {s.A, 0}, s.A, false};
-      b = SimtOp{{Wo, nullptr}, {s.Ko, 0}, {s.H, 0}, {s.A, 0}, s.A, true};
-      K = s.A;
+      a = SimtOp{{dYt, nullptr}, {s.A, 0}, {B, 0}, {s.A_pass, 0}, s.A_pass, false};
+      b = SimtOp{{Wo, nullptr}, {s.Ko, 0}, {s.H, 0}, {s.A_pass, 0}, s.A_pass, true};
+      K = s.A_pass;
     } else {     // dh_t = dz_{t+1} W_h + dy_t W_o
-      a = SimtOp{{G + (t + 1) * B * s.G4, dYt}, {s.G4, s.A}, {B, B}, {s.G4, s.A}, s.G4, false};
-      b = SimtOp{{W + s.D, Wo}, {s.Kx, s.Ko}, {s.H, s.H}, {s.G4, s.A}, s.G4, true};
-      K = s.G4 + s.A;
+      a = SimtOp{{G + (t + 1) * B * s.G4, dYt}, {s.G4, s.A}, {B, B}, {s.G4, s.A_pass}, s.G4,
+                 false};
+      b = SimtOp{{W + s.D, Wo}, {s.Kx, s.Ko}, {s.H, s.H}, {s.G4, s.A_pass}, s.G4, true};
+      K = s.G4 + s.A_pass;
     }
     if ((rc = launch_simt_gemm(a, b, B, s.H, K, raw, s.H, st))) return rc;
     if ((rc = launch_simt_cell_bwd(s, B, raw, G + t * B * s.G4, C + (t + 1) * B * s.H,
@@ -404,6 +428,9 @@ int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes
     SimtOp b{{XH + B * s.Kx + s.D, nullptr}, {s.Kx, 0}, {s.Ko, 0}, {rows, 0}, rows, true};
     if ((rc = launch_simt_gemm(a, b, s.A, s.Ko, rows, grad + s.G4 * s.Kx, s.Ko, st))) return rc;
   }
+  if (s.win_pass)  // dout's win column carries win_trunk x the gradient (Q26)
+    return launch_scale(grad + s.G4 * s.Kx + (int64_t)(s.vcol + 1) * s.Ko, s.Ko,
+                        1.f / s.win_trunk, st);
   return PPO_OK;
 }
 

@@ -46,10 +46,16 @@ struct ProfScope {
 
 // ---- derived shapes ----------------------------------------------------------------------
 struct Shape {
-  int64_t D, H, T, A, G4, Kx, Ko;  // G4 = 4H gate rows
+  int64_t D, H, T, A, G4, Kx, Ko;  // G4 = 4H gate rows; A = all head outputs (incl. aux)
   int n_heads;
   int head_off[PPO_MAX_HEADS + 1];
   bool bf16;
+  // NEXT-4 aux heads: outputs [vcol + 1, A); A_pass = the output columns whose gradient
+  // reaches the LSTM (policy, value, and the win head when win_trunk > 0)
+  int vcol, n_win, n_rank, n_bld, n_aux;
+  int64_t A_pass;
+  float win_trunk;
+  bool win_pass;
 };
 int check_dims(const ppo_dims* d, Shape* s);
 int check_tc_device();  // PPO_E_UNSUPPORTED unless an sm_100 device is current

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256) infer_sample_kernel(
     for (int o = 1; o < 32; o <<= 1) lp += __shfl_xor_sync(0xffffffffu, lp, o);
     if (lane == 0) {
       logp[b] = lp;
-      if (value) value[b] = ys[A - 1];
+      if (value) value[b] = ys[s.vcol];
     }
   }
 }

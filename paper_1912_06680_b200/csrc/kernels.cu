@@ -488,14 +488,16 @@ __global__ void __launch_bounds__(256) loss_kernel(
     const float* __restrict__ out, const int32_t* __restrict__ act,
     const uint8_t* __restrict__ head_on, const uint8_t* __restrict__ avail,
     const float* __restrict__ logp_old, const float* __restrict__ adv,
-    const float* __restrict__ ret, const uint8_t* __restrict__ valid, LossParams p,
-    TD* __restrict__ dout, float* __restrict__ logp, float* __restrict__ partials) {
+    const float* __restrict__ ret, const uint8_t* __restrict__ valid,
+    const float* __restrict__ aux_label, LossParams p, TD* __restrict__ dout,
+    float* __restrict__ logp, float* __restrict__ partials) {
   extern __shared__ float smem_y[];
   __shared__ float red[8][PPO_STATS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* y = smem_y + warp * p.A_pad;
   const int A = p.A, nh = p.nh, n0 = p.off[1];
-  float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  // stat sums by PPO_STAT_* index; [7] (flags) is kept apart
+  float acc[PPO_STATS] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   uint32_t flags = 0;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.N; row += (int64_t)gridDim.x * 8) {
     const float* yr = out + row * A;
@@ -555,7 +557,7 @@ __global__ void __launch_bounds__(256) loss_kernel(
     const float s2 = fminf(fmaxf(rho, 1.f - p.clip_eps), 1.f + p.clip_eps) * At;
     const bool unclipped = s1 <= s2;
     const float pg = -fminf(s1, s2);
-    const float V = y[A - 1];
+    const float V = y[p.vcol];
     const float vf = (V - Rt) * (V - Rt);
     const float lrow = pg + p.c_v * vf - p.c_e * ent;
     const float gpi = unclipped ? -At * rho * w * p.inv_denom : 0.f;
@@ -575,12 +577,44 @@ __global__ void __launch_bounds__(256) loss_kernel(
         dr[j] = from_f<TD>(d);
       }
     }
+    // NEXT-4 aux heads (oracle aux_loss, DESIGN Q25/Q26): logistic win and building
+    // columns lane-parallel, the rank softmax across lanes (n_rank <= 32)
+    float laux = 0.f;
+    if (p.n_aux) {
+      const float* lab = aux_label + row * p.n_aux;
+      const int c0 = p.vcol + 1, r0 = p.n_win, r1 = p.n_win + p.n_rank;
+      const float wd = w * p.inv_denom;
+      for (int j = lane; j < p.n_aux; j += 32) {
+        if (j >= r0 && j < r1) continue;
+        const float z = y[c0 + j], t = lab[j];
+        const float cw = j < r0 ? p.c_win : p.c_bld;
+        laux += cw * (fmaxf(z, 0.f) + log1pf(expf(-fabsf(z))) - t * z);
+        const float d = cw * wd * (1.f / (1.f + expf(-z)) - t);
+        dr[c0 + j] = from_f<TD>(j < r0 ? d * p.win_scale : d);
+      }
+      if (p.n_rank) {
+        const bool in = lane < p.n_rank;
+        const float z = in ? y[c0 + r0 + lane] : -INFINITY;
+        const float t = in ? lab[r0 + lane] : 0.f;
+        const float mx = warp_max(z);
+        const float e = in ? expf(z - mx) : 0.f;
+        const float se = warp_sum(e);
+        const float ty = warp_sum(t);
+        const float lse = mx + logf(se);
+        if (in) {
+          laux += p.c_rank * (-t * (z - lse));
+          dr[c0 + r0 + lane] = from_f<TD>(p.c_rank * wd * (e / se * ty - t));
+        }
+      }
+      laux = warp_sum(laux);
+    }
     if (lane == 0) {
-      dr[A - 1] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
+      dr[p.vcol] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
       if (logp) logp[row] = lpi;
       if (w != 0.f) {
-        if (!isfinite(lrow)) flags |= 1u;
-        acc[0] += w * lrow;
+        if (!isfinite(lrow) || !isfinite(laux)) flags |= 1u;
+        acc[0] += w * (lrow + laux);
+        acc[PPO_STAT_AUX] += w * laux;
         acc[1] += w * pg;
         acc[2] += w * vf;
         acc[3] += w * ent;
@@ -593,8 +627,8 @@ __global__ void __launch_bounds__(256) loss_kernel(
   }
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < 7; ++i) red[warp][i] = acc[i];
-    red[warp][7] = __uint_as_float(flags);
+    for (int i = 0; i < PPO_STATS; ++i) red[warp][i] = acc[i];
+    red[warp][PPO_STAT_FLAGS] = __uint_as_float(flags);
   }
   __syncthreads();
   if (threadIdx.x < PPO_STATS) {
@@ -602,10 +636,10 @@ __global__ void __launch_bounds__(256) loss_kernel(
     float v = 0.f;
     uint32_t f = 0;
     for (int wi = 0; wi < 8; ++wi) {
-      if (i < 7) v += red[wi][i];
-      else f |= __float_as_uint(red[wi][7]);
+      if (i != PPO_STAT_FLAGS) v += red[wi][i];
+      else f |= __float_as_uint(red[wi][i]);
     }
-    partials[blockIdx.x * PPO_STATS + i] = i < 7 ? v : __uint_as_float(f);
+    partials[blockIdx.x * PPO_STATS + i] = i != PPO_STAT_FLAGS ? v : __uint_as_float(f);
   }
 }
 
@@ -617,7 +651,7 @@ __global__ void loss_finalize_kernel(const float* __restrict__ partials, int nbl
     float v = 0.f;
     uint32_t f = 0;
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
-      if (i < 7) v += partials[b * PPO_STATS + i];
+      if (i != PPO_STAT_FLAGS) v += partials[b * PPO_STATS + i];
       else f |= __float_as_uint(partials[b * PPO_STATS + i]);
     }
     sv[threadIdx.x] = v;
@@ -631,9 +665,9 @@ __global__ void loss_finalize_kernel(const float* __restrict__ partials, int nbl
       __syncthreads();
     }
     if (threadIdx.x == 0) {
-      if (i < 6) stats[i] = sv[0] * inv_denom;
-      else if (i == 6) stats[i] = sv[0];
-      else stats[i] = (float)sf[0];
+      if (i == PPO_STAT_NVALID) stats[i] = sv[0];
+      else if (i == PPO_STAT_FLAGS) stats[i] = (float)sf[0];
+      else stats[i] = sv[0] * inv_denom;
     }
     __syncthreads();
   }
@@ -881,23 +915,36 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
 }
 int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t* act,
                 const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
-                const float* adv, const float* ret, const uint8_t* valid, void* dout, float* logp,
-                float* stats, cudaStream_t st) {
+                const float* adv, const float* ret, const uint8_t* valid, const float* aux_label,
+                void* dout, float* logp, float* stats, cudaStream_t st) {
   const size_t smem = 8 * (size_t)p.A_pad * sizeof(float);
   float* partials = stats + PPO_STATS;
   {
   ProfScope _prof("loss", st);
   if (bf16)
     loss_kernel<__nv_bfloat16><<<PPO_LOSS_BLOCKS, 256, smem, st>>>(
-        out, act, head_on, avail, logp_old, adv, ret, valid, p, (__nv_bfloat16*)dout, logp, partials);
+        out, act, head_on, avail, logp_old, adv, ret, valid, aux_label, p, (__nv_bfloat16*)dout,
+        logp, partials);
   else
     loss_kernel<float><<<PPO_LOSS_BLOCKS, 256, smem, st>>>(
-        out, act, head_on, avail, logp_old, adv, ret, valid, p, (float*)dout, logp, partials);
+        out, act, head_on, avail, logp_old, adv, ret, valid, aux_label, p, (float*)dout, logp,
+        partials);
   PPO_LAUNCH_CHECK("loss_kernel");
   }
   ProfScope _prof("loss_finalize", st);
   loss_finalize_kernel<<<1, 256, 0, st>>>(partials, PPO_LOSS_BLOCKS, p.inv_denom, stats);
   PPO_LAUNCH_CHECK("loss_finalize_kernel");
+  return PPO_OK;
+}
+__global__ void scale_kernel(float* __restrict__ x, int64_t n, float f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= f;
+}
+int launch_scale(float* x, int64_t n, float f, cudaStream_t st) {
+  ProfScope _prof("scale", st);
+  scale_kernel<<<grid_for(n), 256, 0, st>>>(x, n, f);
+  PPO_LAUNCH_CHECK("scale_kernel");
   return PPO_OK;
 }
 int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n,

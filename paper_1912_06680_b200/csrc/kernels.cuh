@@ -9,6 +9,8 @@ struct LossParams {
   int A, A_pad, nh;
   int off[PPO_MAX_HEADS + 1];
   float clip_eps, c_v, c_e, inv_denom;
+  int vcol, n_win, n_rank, n_aux;        // value column; NEXT-4 aux heads after it
+  float c_win, c_rank, c_bld, win_scale; // aux loss weights; win column gradient factor
 };
 
 // Operand of the SIMT reference GEMM (see common.cuh Operand); fp32 only.
@@ -35,13 +37,15 @@ size_t gae_scratch_bytes(int64_t R, int64_t L);
 // h0 -> XH[0] h-part, c0 -> C[0], pad columns of every slot (x already in the workspace)
 int launch_pack_state(const Shape& s, int64_t B, const float* h0, const float* c0, void* xh,
                       float* c, cudaStream_t st);
+// x[i] *= f for i < n (the win-head row fix-up of dW_o, DESIGN Q26)
+int launch_scale(float* x, int64_t n, float f, cudaStream_t st);
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
                float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,
                cudaStream_t st);
 int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t* act,
                 const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
-                const float* adv, const float* ret, const uint8_t* valid, void* dout, float* logp,
-                float* stats, cudaStream_t st);
+                const float* adv, const float* ret, const uint8_t* valid, const float* aux_label,
+                void* dout, float* logp, float* stats, cudaStream_t st);
 struct AdamParams {
   float alpha, b1, omb1, b2, omb2, eps, clip;
 };

@@ -245,12 +245,14 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   CUtensorMap a0, a1, b0, b1;
   const bool pair = use_pair("BWD", true);
   if ((rc = map_kmajor(&a0, P.g, s.G4, B, s.G4, s.T, B * s.G4, tc::BM))) return rc;
-  if ((rc = map_kmajor(&a1, dY, s.A, B, s.A, s.T, B * s.A, tc::BM))) return rc;
+  // only the first A_pass output columns reach the LSTM (stop_gradient aux heads, Q26): the
+  // dY / W_o maps end there and TMA zero-fills the rest of the last k-block
+  if ((rc = map_kmajor(&a1, dY, s.A_pass, B, s.A, s.T, B * s.A, tc::BM))) return rc;
   if ((rc = map_mnmajor(&b0, wxh + s.D, s.H, s.G4, s.Kx))) return rc;
-  if ((rc = map_mnmajor(&b1, wo, s.H, s.A, s.Ko))) return rc;
+  if ((rc = map_mnmajor(&b1, wo, s.H, s.A_pass, s.Ko))) return rc;
   for (int t = (int)s.T - 1; t >= 0; --t) {
     const bool last = t == s.T - 1;
-    tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A, tc::BK),
+    tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A_pass, tc::BK),
                      t + 1, t, 0, 0, 8, 1};
     raster(sh, "BWD", 8, 1);
     sh.sched = sched_counter(kSchedBwd);
@@ -310,6 +312,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
                 : launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st);
     if (rc) return rc;
     if (sh.ksplit > 1 && (rc = launch_splitk_reduce(part, sh.ksplit, (size_t)n_o, dwo, st)))
+      return rc;
+    if (s.win_pass &&  // dout's win column carries win_trunk x the gradient (Q26)
+        (rc = launch_scale(dwo + (int64_t)(s.vcol + 1) * s.Ko, s.Ko, 1.f / s.win_trunk, st)))
       return rc;
   }
   return PPO_OK;

@@ -16,7 +16,9 @@ HEAD_SIZES = (30, 4, 189, 189, 81, 81, 81)
 
 #: Baseline hyperparameters, Table hyperparams; DESIGN Q3/Q4.
 DEFAULT_HYPER = dict(T_step=4.0 / 30.0, horizon_s=180.0, lam=0.95, clip_eps=0.2, c_v=1.0,
-                     c_e=0.01, lr=5e-5, beta1=0.9, beta2=0.999, adam_eps=1e-8, clip_sigma=5.0)
+                     c_e=0.01, lr=5e-5, beta1=0.9, beta2=0.999, adam_eps=1e-8, clip_sigma=5.0,
+                     # NEXT-4 aux heads (DESIGN Q25/Q26; the paper gives no values)
+                     c_win=1.0, c_rank=1.0, c_bld=1.0, aux_win_trunk=0.01, aux_horizon_s=120.0)
 
 
 def _aligned_empty(nbytes: int, device, align: int = 1024) -> torch.Tensor:
@@ -31,15 +33,17 @@ class PPOOptimizer:
 
     def __init__(self, D: int, H: int, B: int, T: int = 16, head_sizes=HEAD_SIZES,
                  precision: str = "bf16", device="cuda", hyper: dict | None = None,
-                 comm=None, n_buckets: int = 1, n_ws: int = 1):
+                 comm=None, n_buckets: int = 1, n_ws: int = 1, aux=(0, 0, 0)):
         self.D, self.H, self.B, self.T = D, H, B, T
         self.head_sizes = tuple(head_sizes)
-        self.A = sum(self.head_sizes) + 1
+        self.aux = tuple(aux)           # NEXT-4 (n_win, n_rank, n_bld) heads after the value
+        self.A = sum(self.head_sizes) + 1 + sum(self.aux)
         self.bf16 = precision == "bf16"
         self.device = torch.device(device)
         self.hyper = dict(DEFAULT_HYPER, **(hyper or {}))
         self.dims = L.make_dims(D, H, T, self.head_sizes,
-                                L.PPO_PREC_BF16 if self.bf16 else L.PPO_PREC_FP32)
+                                L.PPO_PREC_BF16 if self.bf16 else L.PPO_PREC_FP32, self.aux,
+                                self.hyper["aux_win_trunk"] if sum(self.aux) else 0.0)
         self.layout = L.param_layout(self.dims)
         n = self.layout.n_total
         dev = self.device
@@ -66,7 +70,8 @@ class PPOOptimizer:
         self.n_buckets = n_buckets
         h = self.hyper
         self.gamma = 1.0 - h["T_step"] / h["horizon_s"]  # Eq. horizon
-        self.loss_cfg = L.ppo_loss_cfg(h["clip_eps"], h["c_v"], h["c_e"], 0.0)
+        self.loss_cfg = L.ppo_loss_cfg(h["clip_eps"], h["c_v"], h["c_e"], 0.0, h["c_win"],
+                                       h["c_rank"], h["c_bld"])
 
     # ---------------------------------------------------------------- parameters
     @property
@@ -117,7 +122,7 @@ class PPOOptimizer:
         L.ppo_loss_grad(self.dims, self.out, batch["act"], batch["head_on"], batch["avail"],
                         batch["logp_old"] if logp_old is None else logp_old, self.adv, self.ret,
                         batch.get("valid"), self.B, self.loss_cfg, self.dout, self.logp,
-                        self.stats, stream)
+                        self.stats, stream, aux_label=batch.get("aux_label"))
 
     def backward(self, stream=None):
         """a6-a8"""

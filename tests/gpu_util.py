@@ -30,7 +30,28 @@ def dev(a, device="cuda", dtype=None):
     return t if dtype is None else t.to(dtype)
 
 
-def make_case(cfg, seed, pad_frac=0.0, bo_scale=0.05, wo_scale=1.0):
+AUX_HYPER = dict(c_win=1.0, c_rank=1.0, c_bld=1.0, aux_win_trunk=0.01)
+
+
+def aux_case(cfg, R, L, seed, hyper):
+    """NEXT-4 inputs of R segments + the oracle's labels in minibatch layout [T][B][n_aux]
+    (gamma2 fp32-rounded on both sides, like gamma in DESIGN Q18)."""
+    from oracle.aux import aux_labels
+    n_win, n_rank, n_bld = cfg.aux
+    ax = synth.make_aux(R, L, cfg.aux, seed, p_last=0.3, p_event=0.02)
+    g2 = float(np.float32(oracle.gamma_from_horizon(120.0, HYPER["T_step"])))
+    lab = aux_labels(ax["last"].astype(bool), ax["outcome"], ax["rank"], ax["events"],
+                     ax["boot"], g2, n_win, n_rank, n_bld)                 # [R][L][n_aux]
+    n_aux = lab.shape[2]
+    per = L // cfg.T
+    # sequence b = r*per + l//T, step t = l % T  (the GAE minibatch mapping, DESIGN O3)
+    mb = lab.reshape(R, per, cfg.T, n_aux).transpose(2, 0, 1, 3).reshape(cfg.T, R * per, n_aux)
+    aux = dict(labels=mb, n_win=n_win, n_rank=n_rank, n_bld=n_bld, c_win=hyper["c_win"],
+               c_rank=hyper["c_rank"], c_bld=hyper["c_bld"], win_trunk=hyper["aux_win_trunk"])
+    return ax, g2, lab, aux
+
+
+def make_case(cfg, seed, pad_frac=0.0, bo_scale=0.05, wo_scale=1.0, aux_hyper=None):
     """Seeded params/sequences/rollouts + oracle reference of one full step."""
     params = synth.make_params(cfg, seed, bo_scale=bo_scale)
     params["Wo"] = (params["Wo"] * wo_scale).astype(np.float32)
@@ -48,17 +69,20 @@ def make_case(cfg, seed, pad_frac=0.0, bo_scale=0.05, wo_scale=1.0):
     p64 = {k: v.astype(np.float64) for k, v in params.items()}
     lp = loss_and_grads(p64, seq, np.zeros((cfg.T, cfg.B)), adv, ret, cfg.head_sizes)[3]["logpi"]
     logp_old = (lp.reshape(cfg.T, cfg.B) + seq["logp_noise"]).astype(np.float32)
+    aux = None
+    if sum(cfg.aux):
+        _, _, _, aux = aux_case(cfg, R, L, seed, aux_hyper or AUX_HYPER)
     Lval, grads, stats, inter = loss_and_grads(p64, seq, logp_old.astype(np.float64), adv, ret,
                                                cfg.head_sizes, HYPER["clip_eps"], HYPER["c_v"],
-                                               HYPER["c_e"])
+                                               HYPER["c_e"], aux=aux)
     return dict(params=params, seq=seq, ro=ro, adv=adv, ret=ret, logp_old=logp_old, loss=Lval,
-                grads=grads, stats=stats, inter=inter, gamma32=gamma32)
+                grads=grads, stats=stats, inter=inter, gamma32=gamma32, aux=aux)
 
 
 def device_batch(case, bf16, device="cuda"):
     s = case["seq"]
     ro = case["ro"]
-    return dict(
+    b = dict(
         x=dev(s["x"], device, torch.bfloat16 if bf16 else torch.float32),
         h0=dev(s["h0"], device), c0=dev(s["c0"], device),
         act=dev(s["act"], device), head_on=dev(s["head_on"], device),
@@ -66,6 +90,9 @@ def device_batch(case, bf16, device="cuda"):
         logp_old=dev(case["logp_old"], device),
         rew=dev(ro["r"], device), val=dev(ro["V"], device), done=dev(ro["done"], device),
     )
+    if case.get("aux") is not None:
+        b["aux_label"] = dev(case["aux"]["labels"].astype(np.float32), device)
+    return b
 
 
 def load_params(opt, params, device="cuda"):
