@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1, help="oracle sample: sequences per step")
+    ap.add_argument("--aux", action="store_true",
+                    help="NEXT-4: with the aux heads (win, rank, 18 buildings) and their targets")
     ap.add_argument("--dx", action="store_true",
                     help="NEXT-4: also produce dL/dx for the observation network each step")
     ap.add_argument("--infer-B", type=str, default="60,1,240,960",
@@ -203,8 +205,11 @@ def workload_config(args, n):
     return {
         "workload": (f"full OpenAI-Five LSTM-{args.H} PPO step: D={args.D}, T=16, "
                      f"B={args.B} sequences/GPU ({args.B // SEQ_PER_SAMPLE} paper samples), "
-                     f"A=656 (7 factorised heads + value), GAE over 256-step segments"
+                     f"A={656 + (sum(__import__('synth').AUX_SIZES) if getattr(args, 'aux', False) else 0)}"
+                     f" (7 factorised heads + value), GAE over 256-step segments"
                      + (", + dL/dx for the observation network" if getattr(args, "dx", False)
+                        else "")
+                     + (", + aux heads (win, rank, 18 buildings)" if getattr(args, "aux", False)
                         else "")),
         "H": args.H, "D": args.D, "T": 16, "B_per_gpu": args.B,
         "global_batch_samples": args.B * n // SEQ_PER_SAMPLE,
@@ -212,6 +217,7 @@ def workload_config(args, n):
         "parallelism": f"dp{n}",
         "l2": "inputs larger than L2 (x alone is T*B*D*2 bytes per step)",
         "dx": bool(getattr(args, "dx", False)),
+        "aux_heads": list(__import__("synth").AUX_SIZES) if getattr(args, "aux", False) else None,
     }
 
 
@@ -526,9 +532,10 @@ def main():
     comm = pdist.make_comm(device)
 
     H, D, T, B = args.H, args.D, 16, args.B
-    cfg = synth.Config(H=H, D=D, B=B, T=T)
+    aux = synth.AUX_SIZES if args.aux else (0, 0, 0)
+    cfg = synth.Config(H=H, D=D, B=B, T=T, aux=aux)
     opt = PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16", device=device, comm=comm,
-                       n_buckets=8, n_ws=1 if args.no_e2e else 2)
+                       n_buckets=8, n_ws=1 if args.no_e2e else 2, aux=aux)
     prm = synth.torch_params(cfg, 0, device)          # same init on every rank
     opt.load_canonical(prm["Wx"], prm["Wh"], prm["b"], prm["Wo"], prm["bo"])
     del prm
@@ -538,6 +545,8 @@ def main():
     batch = dict(x=seq["x"], h0=seq["h0"], c0=seq["c0"], act=seq["act"],
                  head_on=seq["head_on"], avail=seq["avail"], rew=ro["rew"], val=ro["val"],
                  done=ro["done"])
+    if args.aux:
+        batch.update(synth.torch_aux(R, 256, aux, 1000 + rank, device))
     # behaviour log-probs = current policy + N(0, 0.1^2) (forward-pass GPUs)
     batch["logp_old"] = opt.current_logp(batch) + seq["logp_noise"]
     # the resident batch's x lives in the workspace's x rows (zero-copy, ppo_copy_x): the step
@@ -631,7 +640,8 @@ def main():
         # while step k computes (the first step's copy is not overlapped).
         # x goes straight from pinned host memory into the x rows of one of two workspaces
         # (ppo_copy_x); the other inputs into double-buffered device tensors.
-        keys = ("h0", "c0", "act", "head_on", "avail", "logp_old", "rew", "val", "done")
+        keys = ("h0", "c0", "act", "head_on", "avail", "logp_old", "rew", "val", "done") + \
+            (("last", "outcome", "rank", "events", "boot") if args.aux else ())
         host = {k: batch[k].cpu().pin_memory() for k in keys}
         host_x = x_dev.cpu().pin_memory()
         del x_dev

@@ -112,6 +112,17 @@ class PPOOptimizer:
         L.ppo_gae(batch["rew"], batch["val"], batch["done"], self.gamma, h["lam"], self.adv,
                   self.ret, seq_T=self.T, stream=stream)
 
+    def aux_labels(self, batch, stream=None):
+        """NEXT-4: aux-head targets of the minibatch from its segments' aux inputs (last,
+        outcome, rank, events, boot; DESIGN Q27), into batch["aux_label"] [T][B][n_aux]"""
+        if "aux_label" not in batch or batch["aux_label"] is None:
+            batch["aux_label"] = torch.empty(self.T, self.B, sum(self.aux), device=self.device)
+        h = self.hyper
+        g2 = 1.0 - h["T_step"] / h["aux_horizon_s"]     # 2-minute horizon (P:1771, P:1527)
+        L.ppo_aux_labels(self.dims, batch["last"], batch["outcome"], batch["rank"],
+                         batch["events"], batch["boot"], g2, batch["aux_label"], seq_T=self.T,
+                         stream=stream)
+
     def forward(self, batch, stream=None):
         """a2-a4; batch["x"] None = x already in the workspace (put_x / ppo_gather)"""
         L.lstm_bptt_fwd(self.dims, self.weights, batch.get("x"), batch["h0"], batch["c0"], self.B,
@@ -148,6 +159,8 @@ class PPOOptimizer:
         """One full optimizer step a1-a10 on this rank; returns the device stats tensor.
         dx: optional [T][B][D] fp32 output for dL/dx (NEXT-4)."""
         self.gae(batch, stream)
+        if sum(self.aux) and "events" in batch:
+            self.aux_labels(batch, stream)
         self.forward(batch, stream)
         self.loss(batch, stream=stream)
         self.backward(stream)
@@ -161,6 +174,8 @@ class PPOOptimizer:
         """log pi_theta(a) for the batch (forward + loss pass); used to synthesise behaviour
         log-probs like the forward-pass GPUs'."""
         self.gae(batch, stream)
+        if sum(self.aux) and "events" in batch:
+            self.aux_labels(batch, stream)
         self.forward(batch, stream)
         self.loss(batch, logp_old=torch.zeros_like(self.logp), stream=stream)
         return self.logp.view(self.T, self.B).clone()

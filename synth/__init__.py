@@ -263,6 +263,26 @@ def torch_rollouts(R: int, L: int, seed: int, device, p_done: float = 1.0 / 2000
                 done=(torch.rand((R, L), generator=g, device=device) < p_done).to(torch.uint8))
 
 
+def torch_aux(R: int, L: int, aux: tuple, seed: int, device, p_last: float = 0.1,
+              p_event: float = 1.0 / 2000) -> dict:
+    """Device twin of make_aux (same recipe, torch Philox draws)."""
+    import torch
+    n_win, n_rank, n_bld = aux
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 11)
+    rk = torch.rand((R, n_rank), generator=g, device=device)
+    rk = rk / rk.sum(dim=1, keepdim=True).clamp_min(1e-12)
+    boot = torch.cat([torch.rand((R, n_win), generator=g, device=device), rk,
+                      0.3 * torch.rand((R, n_bld), generator=g, device=device)], dim=1)
+    return dict(last=(torch.rand(R, generator=g, device=device) < p_last).to(torch.uint8),
+                outcome=(torch.rand(R, generator=g, device=device) < 0.5).float(),
+                rank=torch.randint(0, max(n_rank, 1), (R,), generator=g, device=device,
+                                   dtype=torch.int32),
+                events=(torch.rand((R, L, n_bld), generator=g, device=device) < p_event)
+                .to(torch.uint8),
+                boot=boot.contiguous())
+
+
 def torch_params(cfg: Config, seed: int, device, bo_scale: float = 0.0) -> dict:
     import torch
     g = torch.Generator(device=device)
