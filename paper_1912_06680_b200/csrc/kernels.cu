@@ -643,6 +643,274 @@ __global__ void __launch_bounds__(256) loss_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// The paper's action layout (DESIGN Q17: heads of 30, 4, 189, 189, 81, 81, 81 logits, then the
+// value) with compile-time offsets: a warp per row; each lane keeps its 23 logit slots in
+// registers for the whole row (one coalesced global read), the 7 per-head reductions run
+// interleaved, exp/log are the SFU approximations (ex2/lg2.approx, rel. error ~2^-22), and
+// the gradient recomputes p from the registers.  Same arithmetic as loss_kernel (oracle
+// O6/O7) with a fraction of its instructions (no per-element index math or branches).
+namespace fastloss {
+constexpr int NH = 7, NS = 23;
+// (closed forms, not recursion: they must fold to constants in the unrolled loops)
+__host__ __device__ __forceinline__ constexpr int sz(int k) {   // logits of head k
+  return k == 0 ? 30 : k == 1 ? 4 : k <= 3 ? 189 : 81;
+}
+__host__ __device__ __forceinline__ constexpr int off(int k) {  // first logit of head k
+  return k == 0 ? 0 : k == 1 ? 30 : k == 2 ? 34 : k == 3 ? 223 : k == 4 ? 412 : k == 5 ? 493
+       : k == 6 ? 574 : 655;
+}
+__host__ __device__ __forceinline__ constexpr int ni(int k) {   // slots per lane
+  return (sz(k) + 31) / 32;
+}
+__host__ __device__ __forceinline__ constexpr int sb(int k) {   // first slot of head k
+  return k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 8 : k == 4 ? 14 : k == 5 ? 17
+       : k == 6 ? 20 : 23;
+}
+__host__ __device__ __forceinline__ constexpr int hd(int s) {   // head of slot s
+  return s < 1 ? 0 : s < 2 ? 1 : s < 8 ? 2 : s < 14 ? 3 : s < 17 ? 4 : s < 20 ? 5 : 6;
+}
+__host__ __device__ __forceinline__ constexpr int ix(int s) { return s - sb(hd(s)); }
+// slot s of lane l holds logit off(hd(s)) + l + 32 ix(s); it exists iff l < lim(s)
+__host__ __device__ __forceinline__ constexpr int lim(int s) { return sz(hd(s)) - 32 * ix(s); }
+static_assert(off(1) == sz(0) && off(2) == off(1) + sz(1) && off(3) == off(2) + sz(2) &&
+              off(4) == off(3) + sz(3) && off(5) == off(4) + sz(4) &&
+              off(6) == off(5) + sz(5) && off(7) == off(6) + sz(6), "offsets");
+static_assert(sb(1) == ni(0) && sb(2) == sb(1) + ni(1) && sb(3) == sb(2) + ni(2) &&
+              sb(4) == sb(3) + ni(3) && sb(5) == sb(4) + ni(4) && sb(6) == sb(5) + ni(5) &&
+              sb(7) == sb(6) + ni(6), "slot bases");
+static_assert(sb(NH) == NS && off(NH) == 655, "paper head layout");
+constexpr float NEG = -1e30f;   // masked logit (finite: 0 * NEG = 0 in the sums)
+constexpr float L2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
+__device__ __forceinline__ float ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float warp_max_redux(float x) {   // sm_100a: one CREDUX
+  float r;
+  asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
+  return r;
+}
+// Sum 16 per-lane values over the warp by recursive halving (reduce-scatter): 31 shuffles
+// instead of 80.  Returns, in every lane, the total of value index q(lane) =
+// 8*b4 + 4*b3 + 2*b2 + b1 (b = lane bits); that total sits in lanes qlane(q), qlane(q) + 1.
+__device__ __forceinline__ float warp_sum16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int o = 16, n = 16; o >= 2; o >>= 1, n >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = up ? v[i] : v[i + n / 2];
+      const float keep = up ? v[i + n / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+__host__ __device__ __forceinline__ constexpr int qlane(int q) {
+  return ((q >> 3) & 1) * 16 + ((q >> 2) & 1) * 8 + ((q >> 1) & 1) * 4 + (q & 1) * 2;
+}
+}  // namespace fastloss
+
+template <class TD, int MINB>
+__global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
+    const float* __restrict__ out, const int32_t* __restrict__ act,
+    const uint8_t* __restrict__ head_on, const uint8_t* __restrict__ avail,
+    const float* __restrict__ logp_old, const float* __restrict__ adv,
+    const float* __restrict__ ret, const uint8_t* __restrict__ valid,
+    const float* __restrict__ aux_label, LossParams p, TD* __restrict__ dout,
+    float* __restrict__ logp, float* __restrict__ partials) {
+  using namespace fastloss;
+  __shared__ float red[8][PPO_STATS];
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int n0 = sz(0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int A = p.A;
+  float acc[PPO_STATS] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  uint32_t flags = 0;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.N; row += (int64_t)gridDim.x * 8) {
+    const float* yr = out + row * A;
+    const float* yl = yr + lane;
+    // ---- per-row metadata: lane k < 7 holds head k's action and read flag
+    const int a_l = lane < NH ? act[row * NH + lane] : 0;
+    const uint32_t on_l = lane < NH ? head_on[row * NH + lane] : 0u;
+    const uint32_t amask = __ballot_sync(FULL, lane < n0 && avail[row * n0 + (lane < n0 ? lane : 0)] != 0);
+    const float w = valid ? (float)valid[row] : 1.f;
+    const float lo = logp_old[row], At = adv[row], Rt = ret[row];
+    // ---- the row's logits into registers (masked primary entries -> NEG).  After
+    // unrolling, hd/ix/off/lim are constants: one base pointer, immediate offsets.
+    float y[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      bool ok = lim(s) >= 32 || lane < lim(s);
+      if (hd(s) == 0) ok = ok && ((amask >> lane) & 1u);
+      y[s] = ok ? __ldcs(yl + off(hd(s)) + 32 * ix(s)) : NEG;
+    }
+    // ---- per-head max (one CREDUX each), then sum e and sum e*y (one SFU exp per element)
+    float mx[NH], mb[NH], v[16];
+#pragma unroll
+    for (int k = 0; k < NH; ++k) mx[k] = NEG;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mx[hd(s)] = fmaxf(mx[hd(s)], y[s]);
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      mx[k] = warp_max_redux(mx[k]);
+      mb[k] = mx[k] * L2E;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = 0.f;   // v[k] = sum e, v[8 + k] = sum e*y
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int k = hd(s);
+      const float e = ex2(fmaf(y[s], L2E, -mb[k]));
+      v[k] += e;
+      v[8 + k] = fmaf(e, y[s], v[8 + k]);
+    }
+    // reduce-scatter: lane of sum index q holds it; the sum-e lanes take sum e*y from lane+16
+    const float tot = warp_sum16(v, lane);
+    const float toty = __shfl_xor_sync(FULL, tot, 16);
+    const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                  ((lane >> 1) & 1);
+    float mq = NEG;
+#pragma unroll
+    for (int k = 0; k < NH; ++k) mq = q == k ? mx[k] : mq;
+    const bool emptyq = mq <= NEG;             // nothing allowed (empty avail)
+    const float lse_q = emptyq ? 0.f : mq + lg2(tot) * LN2;
+    const float H_q = emptyq ? 0.f : lse_q - toty / tot;
+    float lse[NH], Hk[NH];
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      lse[k] = __shfl_sync(FULL, lse_q, qlane(k));
+      Hk[k] = __shfl_sync(FULL, H_q, qlane(k));
+    }
+    // ---- log pi(a) and the entropy of the read heads: lane k takes head k
+    float lsel = 0.f, Hl = 0.f;
+    int offl = 0, nl = 1;
+#pragma unroll
+    for (int k = 0; k < NH; ++k)
+      if (lane == k) {
+        lsel = lse[k];
+        Hl = Hk[k];
+        offl = off(k);
+        nl = sz(k);
+      }
+    float ya = 0.f, lp_l = 0.f, ent_l = 0.f;
+    if (lane < NH) ya = __ldg(yr + offl + min(max(a_l, 0), nl - 1));
+    if (lane < NH && on_l) {
+      lp_l = ya - lsel;
+      ent_l = Hl;
+    }
+    const float lpi = warp_sum(lp_l), ent = warp_sum(ent_l);
+    const int a0 = __shfl_sync(FULL, a_l, 0);
+    if (w != 0.f) {
+      if (amask == 0) flags |= 4u;
+      if (a0 < 0 || a0 >= n0 || !((amask >> a0) & 1u)) flags |= 2u;
+    }
+    const float rho = __expf(lpi - lo);
+    const float s1 = rho * At;
+    const float s2 = fminf(fmaxf(rho, 1.f - p.clip_eps), 1.f + p.clip_eps) * At;
+    const bool unclipped = s1 <= s2;
+    const float pg = -fminf(s1, s2);
+    const float V = __ldg(yr + p.vcol);
+    const float vf = (V - Rt) * (V - Rt);
+    const float lrow = pg + p.c_v * vf - p.c_e * ent;
+    const float gpi = unclipped ? -At * rho * w * p.inv_denom : 0.f;
+    const float ce = p.c_e * w * p.inv_denom;
+    // ---- dL/dlogits of the read heads: d = p (ce (y - lse + H) - gpi), + gpi at the taken
+    // action (stored afterwards by lane k for head k); unread heads and masked entries 0
+    TD* dr = dout + row * A;
+    TD* dl = dr + lane;
+    float lb[NH], cek[NH], c1[NH];   // per head: exp shift, and d = p (cek y + c1) (0 if unread)
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      const float onf = __shfl_sync(FULL, on_l, k) != 0u ? 1.f : 0.f;
+      lb[k] = lse[k] * L2E;
+      cek[k] = onf * ce;
+      c1[k] = onf * (ce * (Hk[k] - lse[k]) - gpi);
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int k = hd(s);
+      const float d = ex2(fmaf(y[s], L2E, -lb[k])) * fmaf(cek[k], y[s], c1[k]);
+      if (lim(s) >= 32 || lane < lim(s)) dl[off(k) + 32 * ix(s)] = from_f<TD>(d);
+    }
+    __syncwarp();
+    if (lane < NH && on_l) {
+      const int a = a_l;
+      if (a >= 0 && a < nl && (lane != 0 || ((amask >> a) & 1u))) {
+        const float pa = ex2(fmaf(ya, L2E, -lsel * L2E));
+        dr[offl + a] = from_f<TD>(pa * fmaf(ce, ya, ce * (Hl - lsel) - gpi) + gpi);
+      }
+    }
+    // ---- NEXT-4 aux heads (as loss_kernel): logistic columns lane-parallel, rank softmax
+    float laux = 0.f;
+    if (p.n_aux) {
+      const float* lab = aux_label + row * p.n_aux;
+      const int c0 = p.vcol + 1, r0 = p.n_win, r1 = p.n_win + p.n_rank;
+      const float wd = w * p.inv_denom;
+      for (int j = lane; j < p.n_aux; j += 32) {
+        if (j >= r0 && j < r1) continue;
+        const float z = yr[c0 + j], t = lab[j];
+        const float cw = j < r0 ? p.c_win : p.c_bld;
+        laux += cw * (fmaxf(z, 0.f) + log1pf(expf(-fabsf(z))) - t * z);
+        const float dd = cw * wd * (1.f / (1.f + expf(-z)) - t);
+        dr[c0 + j] = from_f<TD>(j < r0 ? dd * p.win_scale : dd);
+      }
+      if (p.n_rank) {
+        const bool in = lane < p.n_rank;
+        const float z = in ? yr[c0 + r0 + lane] : -INFINITY;
+        const float t = in ? lab[r0 + lane] : 0.f;
+        const float m = warp_max(z);
+        const float e = in ? expf(z - m) : 0.f;
+        const float sz_ = warp_sum(e), ty = warp_sum(t);
+        const float l = m + logf(sz_);
+        if (in) {
+          laux += p.c_rank * (-t * (z - l));
+          dr[c0 + r0 + lane] = from_f<TD>(p.c_rank * wd * (e / sz_ * ty - t));
+        }
+      }
+      laux = warp_sum(laux);
+    }
+    if (lane == 0) {
+      dr[p.vcol] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
+      if (logp) logp[row] = lpi;
+      if (w != 0.f) {
+        if (!isfinite(lrow) || !isfinite(laux)) flags |= 1u;
+        acc[0] += w * (lrow + laux);
+        acc[PPO_STAT_AUX] += w * laux;
+        acc[1] += w * pg;
+        acc[2] += w * vf;
+        acc[3] += w * ent;
+        acc[4] += w * (lo - lpi);
+        acc[5] += unclipped ? 0.f : w;
+        acc[6] += w;
+      }
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < PPO_STATS; ++i) red[warp][i] = acc[i];
+    red[warp][PPO_STAT_FLAGS] = __uint_as_float(flags);
+  }
+  __syncthreads();
+  if (threadIdx.x < PPO_STATS) {
+    const int i = threadIdx.x;
+    float v = 0.f;
+    uint32_t f = 0;
+    for (int wi = 0; wi < 8; ++wi) {
+      if (i != PPO_STAT_FLAGS) v += red[wi][i];
+      else f |= __float_as_uint(red[wi][i]);
+    }
+    partials[blockIdx.x * PPO_STATS + i] = i != PPO_STAT_FLAGS ? v : __uint_as_float(f);
+  }
+}
+
 __global__ void loss_finalize_kernel(const float* __restrict__ partials, int nblocks,
                                      float inv_denom, float* __restrict__ stats) {
   __shared__ float sv[256];
@@ -919,7 +1187,28 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
                 void* dout, float* logp, float* stats, cudaStream_t st) {
   const size_t smem = 8 * (size_t)p.A_pad * sizeof(float);
   float* partials = stats + PPO_STATS;
-  {
+  // the paper's head layout takes the register-resident half-warp kernel
+  bool fast = p.nh == fastloss::NH && p.vcol == fastloss::off(fastloss::NH);
+  for (int k = 0; k <= p.nh && fast; ++k) fast = p.off[k] == fastloss::off(k);
+  if (const char* e = getenv("PPO_LOSS_GENERIC")) fast = fast && !atoi(e);
+  if (fast) {
+    ProfScope _prof("loss", st);
+    const char* mb = getenv("PPO_LOSS_MINB");   // experiment knob: blocks per SM (3 or 4)
+    const bool four = mb && atoi(mb) == 4;
+    if (bf16 && four)
+      loss_fast_kernel<__nv_bfloat16, 4><<<PPO_LOSS_BLOCKS, 256, 0, st>>>(
+          out, act, head_on, avail, logp_old, adv, ret, valid, aux_label, p,
+          (__nv_bfloat16*)dout, logp, partials);
+    else if (bf16)
+      loss_fast_kernel<__nv_bfloat16, 3><<<PPO_LOSS_BLOCKS, 256, 0, st>>>(
+          out, act, head_on, avail, logp_old, adv, ret, valid, aux_label, p,
+          (__nv_bfloat16*)dout, logp, partials);
+    else
+      loss_fast_kernel<float, 3><<<PPO_LOSS_BLOCKS, 256, 0, st>>>(
+          out, act, head_on, avail, logp_old, adv, ret, valid, aux_label, p, (float*)dout, logp,
+          partials);
+    PPO_LAUNCH_CHECK("loss_fast_kernel");
+  } else {
   ProfScope _prof("loss", st);
   if (bf16)
     loss_kernel<__nv_bfloat16><<<PPO_LOSS_BLOCKS, 256, smem, st>>>(
