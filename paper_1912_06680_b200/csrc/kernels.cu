@@ -184,12 +184,15 @@ __device__ __forceinline__ void store_floats(float* p, const float (&v)[NV]) {
   }
 }
 
-// One warp per rollout stream; 256-step windows from the end; each lane owns 8 steps and
-// the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
-// across lanes with a reverse shuffle scan of affine maps (oracle O2).
+// One warp per rollout stream; windows of 32*CH steps from the end; each lane owns CH steps
+// and the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
+// across lanes with a reverse shuffle scan of affine maps (oracle O2).  CH = 8 when there are
+// enough streams to fill the GPU; CH = 16 doubles the loads in flight per warp otherwise.
+template <int CH>
 __global__ void gae_kernel(const float* __restrict__ rew, const float* __restrict__ val,
                            const uint8_t* __restrict__ done, int64_t R, int64_t L, float gamma,
-                           float lam, int seq_T, float* __restrict__ adv, float* __restrict__ ret) {
+                           float lam, int seq_T, float* __restrict__ adv, float* __restrict__ ret,
+                           bool vec) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const float gl = gamma * lam;
@@ -200,25 +203,56 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
     const float* vv = val + r * (L + 1);
     const uint8_t* dd = done + r * L;
     float carry = 0.f;
-    for (int64_t w_end = L; w_end > 0; w_end -= 256) {
-      const int64_t w_start = w_end > 256 ? w_end - 256 : 0;
-      const int64_t t0 = w_start + 8 * lane;
-      const int n = (int)max((int64_t)0, min((int64_t)8, w_end - t0));
-      float delta[8], cf[8];
-      if (n == 8) {
-        float rv[8], v[9];
-        load_floats<8>(rr + t0, rv, rew + R * L);
-        load_floats<9>(vv + t0, v, val + R * (L + 1));
+    // Windows of <= W = 32*CH steps from the end.  Lane chunks sit on global multiples of 8
+    // steps (window starts are rounded up to them; the row's first window starts its lane 0
+    // early and masks the steps before the row), so every full chunk is 32-byte aligned in
+    // r, A, R and 8-byte aligned in d, whatever L is.  (V has row stride L + 1: shifted
+    // loads.)  Steps outside [w_start, w_end) are identities (delta 0, c 1).
+    constexpr int W = 32 * CH;
+    const int64_t g0 = r * L;
+    const int64_t sh0 = g0 & 7;
+    int64_t w_end = L;
+    while (w_end > 0) {
+      int64_t w_start = w_end - W;
+      if (w_start <= 0 && w_end + sh0 <= W) {
+        w_start = 0;
+      } else {
+        if (w_start < 8) w_start = 8;
+        w_start += (8 - ((g0 + w_start) & 7)) & 7;
+      }
+      const int64_t t0 = w_start - ((g0 + w_start) & 7) + CH * lane;   // chunk [t0, t0 + CH)
+      const int i_lo = (int)min((int64_t)CH, max((int64_t)0, w_start - t0));
+      const int i_hi = (int)max((int64_t)0, min((int64_t)CH, w_end - t0));
+      const int n = i_hi;     // (kept for the store path: valid steps are [i_lo, i_hi))
+      const bool full = vec && i_lo == 0 && i_hi == CH;   // vec: bases allow the alignment
+      float delta[CH], cf[CH], vkeep[CH];
+      if (full) {
+        float rv[CH], v[CH + 1];
+        const float4* r4 = reinterpret_cast<const float4*>(rr + t0);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float nd = dd[t0 + i] ? 0.f : 1.f;
+        for (int q = 0; q < CH / 4; ++q) {
+          const float4 a4 = __ldcs(r4 + q);
+          rv[4 * q] = a4.x;
+          rv[4 * q + 1] = a4.y;
+          rv[4 * q + 2] = a4.z;
+          rv[4 * q + 3] = a4.w;
+        }
+        load_floats<CH + 1>(vv + t0, v, val + R * (L + 1));
+        uint2 dw[CH / 8];
+#pragma unroll
+        for (int q = 0; q < CH / 8; ++q) dw[q] = __ldcs(reinterpret_cast<const uint2*>(dd + t0) + q);
+        const uint8_t* db = reinterpret_cast<const uint8_t*>(dw);
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const float nd = db[i] ? 0.f : 1.f;
           delta[i] = rv[i] + gamma * nd * v[i + 1] - v[i];
           cf[i] = gl * nd;
+          vkeep[i] = v[i];
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (i < n) {
+        for (int i = 0; i < CH; ++i) {
+          if (i >= i_lo && i < i_hi) {
             const int64_t t = t0 + i;
             const float nd = dd[t] ? 0.f : 1.f;
             delta[i] = rr[t] + gamma * nd * vv[t + 1] - vv[t];
@@ -231,7 +265,7 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
       }
       float P = 0.f, Q = 1.f;  // A_first = P + Q * A_after
 #pragma unroll
-      for (int i = 7; i >= 0; --i) {
+      for (int i = CH - 1; i >= 0; --i) {
         P = delta[i] + cf[i] * P;
         Q = cf[i] * Q;
       }
@@ -247,23 +281,22 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
       const float a_first = P + Q * carry;
       float a = __shfl_down_sync(0xffffffffu, a_first, 1);
       if (lane == 31) a = carry;
-      float Aout[8];
+      float Aout[CH];
 #pragma unroll
-      for (int i = 7; i >= 0; --i) {
+      for (int i = CH - 1; i >= 0; --i) {
         a = delta[i] + cf[i] * a;
         Aout[i] = a;
       }
-      if (seq_T == 0 && n == 8) {
-        float vr[8], Rout[8];
-        load_floats<8>(vv + t0, vr, val + R * (L + 1));
+      if (seq_T == 0 && full) {
+        float Rout[CH];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) Rout[i] = Aout[i] + vr[i];
-        store_floats<8>(adv + r * L + t0, Aout);
-        store_floats<8>(ret + r * L + t0, Rout);
+        for (int i = 0; i < CH; ++i) Rout[i] = Aout[i] + vkeep[i];
+        store_floats<CH>(adv + r * L + t0, Aout);
+        store_floats<CH>(ret + r * L + t0, Rout);
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (i < n) {
+        for (int i = 0; i < CH; ++i) {
+          if (i >= i_lo && i < n) {
             const int64_t t = t0 + i;
             int64_t o;
             if (seq_T > 0) {
@@ -278,6 +311,7 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
         }
       }
       carry = __shfl_sync(0xffffffffu, a_first, 0);
+      w_end = w_start;
     }
   }
 }
@@ -1142,7 +1176,8 @@ int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, con
   return PPO_OK;
 }
 // Warp-per-stream kernel when streams are short or numerous enough to fill the GPU.
-static bool gae_use_short(int64_t R, int64_t L) { return L <= kGaeShortL || R >= 16384; }
+// warp-per-stream kernel unless the streams are too few to fill the GPU with warps
+static bool gae_use_short(int64_t R, int64_t L) { return L <= kGaeShortL || R >= 600; }
 
 size_t gae_scratch_bytes(int64_t R, int64_t L) {
   if (gae_use_short(R, L)) return 0;
@@ -1166,7 +1201,14 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
   ProfScope _prof("gae", st);
   if (gae_use_short(R, L)) {
     const int64_t threads = R * 32;
-    gae_kernel<<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret);
+    // the aligned-chunk path needs 32-byte aligned r, A, R bases and an 8-byte aligned d base
+    const bool vec = aligned(rew, 32) && aligned(done, 8) && aligned(adv, 32) && aligned(ret, 32);
+    if (R >= 4736 || L <= 256)   // >= 32 warps per SM, or short rows: 8-step lane chunks
+      gae_kernel<8><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
+                                                            seq_T, adv, ret, vec);
+    else
+      gae_kernel<16><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
+                                                             seq_T, adv, ret, vec);
     PPO_LAUNCH_CHECK("gae_kernel");
     return PPO_OK;
   }

@@ -54,6 +54,10 @@ def test_tc_gemm_vs_torch(L, mode, M, N, K):
 # ------------------------------------------------------------------ GAE
 @pytest.mark.parametrize("R,Lr,seq_T,p_done", [
     (2, 256, 16, 0.01), (2400, 256, 16, 1 / 20000), (3, 1350, 0, 0.002), (5, 1, 0, 0.5),
+    # row starts off the 8-step grid: shifted first windows, window rounding (L % 8 != 0)
+    (11, 1350, 0, 0.01), (13, 257, 0, 0.01), (9, 263, 0, 0.02), (17, 7, 0, 0.1),
+    # 600 <= R < 4736 streams: 16-step lane chunks (512-step windows)
+    (700, 3000, 0, 1e-3), (1000, 2112, 16, 1e-3), (1000, 300, 0, 0.05),
     (1, 6300, 0, 0.0), (7, 300, 0, 0.05), (4, 512, 16, 0.0),
     # long rollouts: chunk-parallel look-back kernel (chunks of 8192 steps), ragged tails
     (1, 20000, 0, 1 / 20000), (3, 100001, 0, 1e-4), (2, 8193, 0, 0.0), (5, 40960, 16, 0.001),
@@ -73,6 +77,30 @@ def test_gae_parity(L, R, Lr, seq_T, p_done):
     scratch = torch.empty(nb, dtype=torch.uint8, device="cuda") if nb else None
     L.ppo_gae(dev(ro["r"]), dev(ro["V"]), dev(ro["done"]), gamma, lam, adv, ret, seq_T=seq_T,
               scratch=scratch)
+    torch.cuda.synchronize()
+    ok, worst = elementwise_ok(adv.cpu().numpy(), A, 1e-5)
+    assert ok, worst
+    ok, worst = elementwise_ok(ret.cpu().numpy(), Rt, 1e-5)
+    assert ok, worst
+
+
+def test_gae_misaligned_bases(L):
+    """Buffers that start off the 32-byte grid take the scalar path (same results)."""
+    R, Lr = 6, 1000
+    ro = synth.make_rollouts(R, Lr, seed=3, p_done=0.01)
+    gamma = float(np.float32(oracle.gamma_from_horizon(180.0)))
+    lam = float(np.float32(0.95))
+    A, Rt = oracle.gae(ro["r"], ro["V"], ro["done"], gamma, lam)
+    def shifted(a, dtype):
+        t = torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+        buf = torch.empty(t.numel() + 1, dtype=t.dtype, device="cuda")
+        v = buf[1:].view(t.shape)
+        v.copy_(t)
+        return v
+    adv = torch.empty(R * Lr + 1, device="cuda")[1:].view(R, Lr)
+    ret = torch.empty(R * Lr + 1, device="cuda")[1:].view(R, Lr)
+    L.ppo_gae(shifted(ro["r"], None), shifted(ro["V"], None), shifted(ro["done"], None), gamma,
+              lam, adv, ret)
     torch.cuda.synchronize()
     ok, worst = elementwise_ok(adv.cpu().numpy(), A, 1e-5)
     assert ok, worst
