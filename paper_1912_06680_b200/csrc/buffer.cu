@@ -168,12 +168,23 @@ namespace {
 
 constexpr int kRewardBlocks = 148 * 4;
 
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {   // 32-byte aligned
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {   // 32-byte aligned
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
 __global__ void __launch_bounds__(128) reward_gae_kernel(
     const float* __restrict__ shaped, const float* __restrict__ win,
     const int32_t* __restrict__ step0, int64_t G, int64_t L, const float* __restrict__ val,
     const uint8_t* __restrict__ done, ppo_reward_cfg cfg, const double* __restrict__ stats,
     float gamma, float lam, int seq_T, float* __restrict__ rew_out, float* __restrict__ adv,
-    float* __restrict__ ret, double* __restrict__ partials) {
+    float* __restrict__ ret, double* __restrict__ partials, bool vec) {
   constexpr int NH = 10;
   __shared__ double red[4][3];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -196,15 +207,47 @@ __global__ void __launch_bounds__(128) reward_gae_kernel(
       const int64_t w_start = w_end > 256 ? w_end - 256 : 0;
       const int64_t t0 = w_start + 8 * lane;
       const int n = (int)max((int64_t)0, min((int64_t)8, w_end - t0));
-      // per step: decay, team means of the decayed raw rewards, GAE coefficient
+      // per step: decay, team means of the decayed raw rewards, GAE coefficient.  Full
+      // chunks on a 32-byte grid (vec: L % 8 == 0 and aligned bases) load 16-byte vectors.
+      const bool full = vec && n == 8;
       float cf[8], dec[8], mA[8], mB[8], nds[8];
+      const float st0 = (float)step0[g];
+      if (full) {
+        const uint2 dw = __ldcs(reinterpret_cast<const uint2*>(done + g * L + t0));
+        const uint8_t* db = reinterpret_cast<const uint8_t*>(&dw);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          nds[e] = db[e] ? 0.f : 1.f;
+          cf[e] = gl * nds[e];
+          dec[e] = exp2f(dk * (st0 + (float)(t0 + e)));
+          mA[e] = 0.f;
+          mB[e] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+          float sh[8], wn[8];
+          load8(shaped + (s0 + i) * L + t0, sh);
+          load8(win + (s0 + i) * L + t0, wn);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float rho = sh[e] * dec[e] + wn[e];
+            if (i < 5) mA[e] += rho;
+            else mB[e] += rho;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          mA[e] *= 0.2f;
+          mB[e] *= 0.2f;
+        }
+      } else {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const bool ok = e < n;
         const int64_t t = t0 + e;
         nds[e] = ok && !done[g * L + t] ? 1.f : 0.f;
         cf[e] = ok ? gl * nds[e] : 1.f;
-        dec[e] = ok ? exp2f(dk * (float)(step0[g] + t)) : 0.f;
+        dec[e] = ok ? exp2f(dk * (st0 + (float)t)) : 0.f;
         float a = 0.f, b = 0.f;
         if (ok) {
 #pragma unroll
@@ -217,17 +260,25 @@ __global__ void __launch_bounds__(128) reward_gae_kernel(
         mA[e] = 0.2f * a;
         mB[e] = 0.2f * b;
       }
+      }
 #pragma unroll 1
       for (int i = 0; i < NH; ++i) {
         const float* vv = val + (s0 + i) * (L + 1);
-        float delta[8];
+        float delta[8], vk[9], sh[8], wn[8];
+        if (full) {
+          load8(shaped + (s0 + i) * L + t0, sh);
+          load8(win + (s0 + i) * L + t0, wn);
+          load_floats<9>(vv + t0, vk, val + S * (L + 1));
+        }
+        float rr[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const bool ok = e < n;
           const int64_t t = t0 + e;
           float dl = 0.f;
           if (ok) {
-            const float rho = shaped[(s0 + i) * L + t] * dec[e] + win[(s0 + i) * L + t];
+            const float rho = full ? sh[e] * dec[e] + wn[e]
+                                   : shaped[(s0 + i) * L + t] * dec[e] + win[(s0 + i) * L + t];
             const float mt = i < 5 ? mA[e] : mB[e], me = i < 5 ? mB[e] : mA[e];
             float r = (1.f - tau) * rho + tau * mt;
             if (cfg.zero_sum) r -= me;
@@ -235,10 +286,20 @@ __global__ void __launch_bounds__(128) reward_gae_kernel(
             pss += (double)r * r;
             pn += 1.0;
             r *= inv_sigma;
-            if (rew_out) rew_out[(s0 + i) * L + t] = r;
-            dl = r + gamma * nds[e] * vv[t + 1] - vv[t];
+            rr[e] = r;
+            dl = full ? r + gamma * nds[e] * vk[e + 1] - vk[e]
+                      : r + gamma * nds[e] * vv[t + 1] - vv[t];
           }
           delta[e] = dl;
+        }
+        if (rew_out) {
+          if (full) {
+            store8(rew_out + (s0 + i) * L + t0, rr);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (e < n) rew_out[(s0 + i) * L + t0 + e] = rr[e];
+          }
         }
         float P = 0.f, Q = 1.f;
 #pragma unroll
@@ -258,6 +319,17 @@ __global__ void __launch_bounds__(128) reward_gae_kernel(
         const float a_first = P + Q * carry[i];
         float a = __shfl_down_sync(0xffffffffu, a_first, 1);
         if (lane == 31) a = carry[i];
+        if (full && seq_T == 0) {
+          float Ao[8], Ro[8];
+#pragma unroll
+          for (int e = 7; e >= 0; --e) {
+            a = delta[e] + cf[e] * a;
+            Ao[e] = a;
+            Ro[e] = a + vk[e];
+          }
+          store8(adv + (s0 + i) * L + t0, Ao);
+          store8(ret + (s0 + i) * L + t0, Ro);
+        } else {
 #pragma unroll
         for (int e = 7; e >= 0; --e) {
           if (e < n) {
@@ -273,6 +345,7 @@ __global__ void __launch_bounds__(128) reward_gae_kernel(
             adv[o] = a;
             ret[o] = a + vv[t];
           }
+        }
         }
         carry[i] = __shfl_sync(0xffffffffu, a_first, 0);
       }
@@ -349,9 +422,12 @@ int ppo_reward_gae(const float* shaped, const float* win, const int32_t* step0, 
   double* partials = static_cast<double*>(scratch);
   {
     ProfScope _prof("reward_gae", st);
+    // 16-byte vectors for full 8-step chunks: L % 8 == 0 and 32-byte aligned bases
+    const bool vec = L % 8 == 0 && aligned(shaped, 32) && aligned(win, 32) && aligned(done, 8) &&
+                     aligned(adv, 32) && aligned(ret, 32) && (!rew_out || aligned(rew_out, 32));
     reward_gae_kernel<<<kRewardBlocks, 128, 0, st>>>(shaped, win, step0, G, L, val, done, *cfg,
                                                      stats, gamma, lam, seq_T, rew_out, adv, ret,
-                                                     partials);
+                                                     partials, vec);
     PPO_LAUNCH_CHECK("reward_gae_kernel");
   }
   ProfScope _prof("reward_stats", st);

@@ -143,47 +143,6 @@ __global__ void __launch_bounds__(256) pack_state_kernel(Shape s, int64_t B,
 
 // ============================================================================ GAE
 
-// NV consecutive floats from an arbitrarily aligned p, using aligned 16-byte loads (streaming,
-// evict-first); falls back to scalar loads where the aligned window would pass `end`.
-template <int NV>
-__device__ __forceinline__ void load_floats(const float* p, float (&v)[NV], const float* end) {
-  constexpr int NQ = (NV + 6) / 4;
-  const int m = static_cast<int>((reinterpret_cast<uintptr_t>(p) >> 2) & 3);
-  const float4* b = reinterpret_cast<const float4*>(p - m);
-  if (reinterpret_cast<const float*>(b + NQ) <= end) {
-    float buf[NQ * 4];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) reinterpret_cast<float4*>(buf)[q] = __ldcs(b + q);
-    switch (m) {
-#define PPO_SHIFT_CASE(M)                                  \
-  case M:                                                  \
-    _Pragma("unroll") for (int i = 0; i < NV; ++i) v[i] = buf[i + M]; \
-    break;
-      PPO_SHIFT_CASE(0)
-      PPO_SHIFT_CASE(1)
-      PPO_SHIFT_CASE(2)
-      PPO_SHIFT_CASE(3)
-#undef PPO_SHIFT_CASE
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = p[i];
-  }
-}
-template <int NV>
-__device__ __forceinline__ void store_floats(float* p, const float (&v)[NV]) {
-  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-#pragma unroll
-    for (int q = 0; q < NV / 4; ++q)
-      reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-#pragma unroll
-    for (int i = (NV / 4) * 4; i < NV; ++i) p[i] = v[i];
-  } else {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) p[i] = v[i];
-  }
-}
-
 // One warp per rollout stream; windows of 32*CH steps from the end; each lane owns CH steps
 // and the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
 // across lanes with a reverse shuffle scan of affine maps (oracle O2).  CH = 8 when there are
