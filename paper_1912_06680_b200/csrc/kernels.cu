@@ -1162,12 +1162,15 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
     const int64_t threads = R * 32;
     // the aligned-chunk path needs 32-byte aligned r, A, R bases and an 8-byte aligned d base
     const bool vec = aligned(rew, 32) && aligned(done, 8) && aligned(adv, 32) && aligned(ret, 32);
-    if (R >= 4736 || L <= 256)   // >= 32 warps per SM, or short rows: 8-step lane chunks
+    // >= 32 warps per SM (or short rows): 8-step lane chunks; fewer streams: 16-step chunks
+    // keep twice the loads in flight per warp (32-step chunks measured slower), and 2-warp
+    // blocks spread the few warps over all SMs
+    if (R >= 4736 || L <= 256)
       gae_kernel<8><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
                                                             seq_T, adv, ret, vec);
     else
-      gae_kernel<16><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
-                                                             seq_T, adv, ret, vec);
+      gae_kernel<16><<<grid_for(threads, 64), 64, 0, st>>>(rew, val, done, R, L, gamma, lam,
+                                                           seq_T, adv, ret, vec);
     PPO_LAUNCH_CHECK("gae_kernel");
     return PPO_OK;
   }

@@ -57,7 +57,7 @@ def test_tc_gemm_vs_torch(L, mode, M, N, K):
     # row starts off the 8-step grid: shifted first windows, window rounding (L % 8 != 0)
     (11, 1350, 0, 0.01), (13, 257, 0, 0.01), (9, 263, 0, 0.02), (17, 7, 0, 0.1),
     # 600 <= R < 4736 streams: 16-step lane chunks (512-step windows)
-    (700, 3000, 0, 1e-3), (1000, 2112, 16, 1e-3), (1000, 300, 0, 0.05),
+    (700, 3000, 0, 1e-3), (1000, 2112, 16, 1e-3), (1000, 300, 0, 0.05), (2100, 520, 0, 0.01),
     (1, 6300, 0, 0.0), (7, 300, 0, 0.05), (4, 512, 16, 0.0),
     # long rollouts: chunk-parallel look-back kernel (chunks of 8192 steps), ragged tails
     (1, 20000, 0, 1 / 20000), (3, 100001, 0, 1e-4), (2, 8193, 0, 0.0), (5, 40960, 16, 0.001),
