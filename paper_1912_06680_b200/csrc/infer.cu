@@ -124,12 +124,13 @@ __global__ void __launch_bounds__(256) infer_cell_kernel(Shape s, int64_t B, int
 // One block per row b: y = sum_s Yp[s][b][.]; warp k samples head k by Gumbel-max over its
 // allowed logits (primary: avail) with ties to the smallest index and computes its
 // log-softmax at the draw; thread 0 then applies the target-type table.
-__global__ void __launch_bounds__(256) infer_sample_kernel(
+constexpr int kSampleThreads = 1024;   // one thread per output column in the first phase
+__global__ void __launch_bounds__(kSampleThreads) infer_sample_kernel(
     Shape s, int64_t B, int S, const float* __restrict__ yp, const uint8_t* __restrict__ avail,
     const uint8_t* __restrict__ table, uint64_t base, int32_t* __restrict__ act,
     uint8_t* __restrict__ head_on, float* __restrict__ logp, float* __restrict__ value,
     float* __restrict__ out) {
-  extern __shared__ float ys[];
+  extern __shared__ float ys[];          // [A] outputs, then [n_logits] Gumbel noise
   __shared__ int sact[PPO_MAX_HEADS];
   __shared__ float slp[PPO_MAX_HEADS];
   __shared__ uint8_t sav[64];   // primary head <= 64 actions (check_dims)
@@ -148,9 +149,12 @@ __global__ void __launch_bounds__(256) infer_sample_kernel(
     for (int sp = 0; sp < kMaxSplitK; ++sp) acc += v[sp];   // split order; +0 beyond S
     ys[k] = acc;
     if (out) out[b * A + k] = acc;
+    // the noise of every logit, drawn by the whole block (not by the 7 head warps)
+    if (k < s.vcol) ys[A + k] = gumbel_noise(base, b, k);
   }
   for (int k = threadIdx.x; k < s.head_off[1]; k += blockDim.x) sav[k] = avail[b * s.head_off[1] + k];
   __syncthreads();
+  const float* gs = ys + A;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int hk = warp; hk < s.n_heads; hk += blockDim.x >> 5) {
     const int off = s.head_off[hk], n = s.head_off[hk + 1] - off;
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(256) infer_sample_kernel(
     for (int k = lane; k < n; k += 32) {
       if (hk == 0 && !sav[k]) continue;
       const float y = ys[off + k];
-      const float sc = y + gumbel_noise(base, b, off + k);
+      const float sc = y + gs[off + k];
       if (sc > best || (sc == best && k < bi)) {
         best = sc;
         bi = k;
@@ -293,12 +297,15 @@ int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h,
   InferLayout L = infer_layout(s, B);
   if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small (ppo_infer_ws_bytes)");
   if ((rc = check_tc_device())) return rc;
+  // experiment knob (timing breakdowns only; results are wrong when set): skip kernels by bit
+  // 1 pack, 2 gates GEMM, 4 cell, 8 heads GEMM, 16 sample
+  static const int skip = getenv("PPO_INFER_SKIP") ? atoi(getenv("PPO_INFER_SKIP")) : 0;
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   auto* xh = reinterpret_cast<__nv_bfloat16*>(wsb + L.xh);
   auto* ho = reinterpret_cast<__nv_bfloat16*>(wsb + L.ho);
   auto* zp = reinterpret_cast<float*>(wsb + L.zp);
   auto* yp = reinterpret_cast<float*>(wsb + L.yp);
-  {
+  if (!(skip & 1)) {
     ProfScope _prof("infer_pack", st);
     PPO_CUDA_CHECK(launch_pdl(infer_pack_kernel, dim3((unsigned)((B * (s.Kx / 8 + 8) + 255) / 256)),
                               dim3(256), 0, st, s, B, static_cast<const __nv_bfloat16*>(x),
@@ -306,20 +313,20 @@ int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h,
     PPO_LAUNCH_CHECK("infer_pack_kernel");
   }
   int S = 1;
-  if ((rc = tc_infer_gates(s, B, w, xh, zp, &S, st))) return rc;
-  {
+  if (!(skip & 2) && (rc = tc_infer_gates(s, B, w, xh, zp, &S, st))) return rc;
+  if (!(skip & 4)) {
     ProfScope _prof("infer_cell", st);
     PPO_CUDA_CHECK(launch_pdl(infer_cell_kernel, dim3((unsigned)((B * s.H + 255) / 256)), dim3(256),
                               0, st, s, B, S, (const float*)zp, h, c, ho));
     PPO_LAUNCH_CHECK("infer_cell_kernel");
   }
   int S2 = 1;
-  if ((rc = tc_infer_heads(s, B, w, ho, yp, &S2, st))) return rc;
-  {
+  if (!(skip & 8) && (rc = tc_infer_heads(s, B, w, ho, yp, &S2, st))) return rc;
+  if (!(skip & 16)) {
     ProfScope _prof("infer_sample", st);
     const uint64_t base = seed + (step << 32);
-    PPO_CUDA_CHECK(launch_pdl(infer_sample_kernel, dim3((unsigned)B), dim3(256),
-                              s.A * sizeof(float), st, s, B, S2, (const float*)yp, avail,
+    PPO_CUDA_CHECK(launch_pdl(infer_sample_kernel, dim3((unsigned)B), dim3(kSampleThreads),
+                              (s.A + s.vcol) * sizeof(float), st, s, B, S2, (const float*)yp, avail,
                               head_table, base, act, head_on, logp, value, out));
     PPO_LAUNCH_CHECK("infer_sample_kernel");
   }

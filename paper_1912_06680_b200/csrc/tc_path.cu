@@ -344,19 +344,20 @@ int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx,
 // tile), K split so the units fill whole waves of the SMs.  Deterministic fp32 partials
 // out[split][b][m] (transposed store); the consumer kernel sums them in split order.
 namespace {
-int infer_split(int tiles, int nkb, int min_kb) {
-  const char* e = getenv("PPO_INFER_SPLIT");
+int infer_split(int tiles, int nkb, int min_kb, const char* knob = "PPO_INFER_SPLIT") {
+  const char* e = getenv(knob);
   if (e && atoi(e) > 0) return std::min(std::min(atoi(e), kMaxSplitK), nkb);
   const int sms = num_sms();
+  if (tiles >= sms) return 1;   // the tiles alone fill the machine
   int best = 1;
   double best_eff = 0.0;
+  // best wave fill; among (near-)ties the larger split (more CTAs streaming the weights).
+  // Each split keeps >= min_kb k-blocks, which bounds the fp32 partials the consumer reads.
   for (int sp = 1; sp <= kMaxSplitK && nkb / sp >= min_kb; ++sp) {
     const int units = tiles * sp;
     const double eff = (double)units / ((double)((units + sms - 1) / sms) * sms);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best = sp;
-    }
+    if (eff > best_eff + 0.02) best_eff = eff;
+    if (eff >= best_eff - 0.02) best = sp;
   }
   return best;
 }
@@ -377,7 +378,11 @@ int infer_gemm_bn(const char* tag, int slot, const void* W, int64_t M, int64_t K
     return rc;
   if ((rc = map_kmajor(&mb, act, K, B, ld_act, 1, 0, BN))) return rc;
   const int tiles = cdiv(M, tc::BM) * cdiv(B, BN);
-  const int sp = infer_split(tiles, nkb, 4);
+  // gates: >= 32 k-blocks per split (4 splits of W_xh at the paper's size: the cell kernel
+  // reads 4 partials); heads: >= 8 (8 splits of the small W_o)
+  const bool heads = slot == kSchedInferHeads;
+  const int sp = infer_split(tiles, nkb, heads ? 8 : 32,
+                             heads ? "PPO_INFER_SPLIT_HEADS" : "PPO_INFER_SPLIT");
   tc::TileShape sh{(int)M, (int)B, nkb, 0, 0, 0, 0, 0, 1, 0};
   sh.ksplit = sp;
   sh.sched = sched_counter(slot);
