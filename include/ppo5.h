@@ -306,6 +306,13 @@ int ppo_reward_gae(const float* shaped, const float* win, const int32_t* step0, 
  * pointers; w, x, h, c 16-byte aligned; ws 1024-byte aligned, >= ppo_infer_ws_bytes.
  * bf16 precision only (PPO_E_ARG otherwise); PPO_E_UNSUPPORTED off sm_100.
  * Asynchronous on the stream. */
+/* Same step with the counter on the device: this call draws with step = *step_ctr and leaves
+ * *step_ctr + 1 (device uint64, 8-byte aligned), so a captured CUDA graph of inference steps
+ * draws fresh noise on every replay. */
+int ppo_infer_step_ctr(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
+                       const uint8_t* avail, const uint8_t* head_table, uint64_t seed,
+                       uint64_t* step_ctr, int64_t B, void* ws, size_t ws_bytes, int32_t* act,
+                       uint8_t* head_on, float* logp, float* value, float* out, ppo_stream_t s);
 int ppo_infer_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes /* host out */);
 /* The served weights, re-laid out once per published version for streaming: every
  * [128 rows][64 k] block of W_xh_aug and W_o_aug becomes one contiguous 16 KB tile (rows past

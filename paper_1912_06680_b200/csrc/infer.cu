@@ -51,9 +51,12 @@ __global__ void __launch_bounds__(256) infer_pack_kernel(Shape s, int64_t B,
                                                          const __nv_bfloat16* __restrict__ x,
                                                          const float* __restrict__ h,
                                                          __nv_bfloat16* __restrict__ xh,
-                                                         __nv_bfloat16* __restrict__ ho) {
+                                                         __nv_bfloat16* __restrict__ ho,
+                                                         unsigned long long* __restrict__ step_ctr) {
   pdl_launch_dependents();
   pdl_wait();
+  // device step counter (graph replays): this step is *ctr; the sample kernel reads *ctr - 1
+  if (step_ctr && blockIdx.x == 0 && threadIdx.x == 0) *step_ctr += 1ull;
   const int64_t per_row = s.Kx / 8 + 8;   // XH row in 8-column groups + the 64-column HO pad
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= B * per_row) return;
@@ -127,7 +130,8 @@ __global__ void __launch_bounds__(256) infer_cell_kernel(Shape s, int64_t B, int
 constexpr int kSampleThreads = 1024;   // one thread per output column in the first phase
 __global__ void __launch_bounds__(kSampleThreads) infer_sample_kernel(
     Shape s, int64_t B, int S, const float* __restrict__ yp, const uint8_t* __restrict__ avail,
-    const uint8_t* __restrict__ table, uint64_t base, int32_t* __restrict__ act,
+    const uint8_t* __restrict__ table, uint64_t seed, uint64_t step,
+    const unsigned long long* __restrict__ step_ctr, int32_t* __restrict__ act,
     uint8_t* __restrict__ head_on, float* __restrict__ logp, float* __restrict__ value,
     float* __restrict__ out) {
   extern __shared__ float ys[];          // [A] outputs, then [n_logits] Gumbel noise
@@ -139,6 +143,7 @@ __global__ void __launch_bounds__(kSampleThreads) infer_sample_kernel(
   const int64_t b = blockIdx.x;
   const int A = (int)s.A;
   const size_t slab = (size_t)A * B;
+  const uint64_t base = seed + ((step_ctr ? (uint64_t)(*step_ctr - 1ull) : step) << 32);
   for (int k = threadIdx.x; k < A; k += blockDim.x) {
     const float* p = yp + b * A + k;
     float v[kMaxSplitK];
@@ -279,10 +284,11 @@ int ppo_infer_pack_weights(const ppo_dims* dims, const void* w, void* wt, size_t
   return PPO_OK;
 }
 
-int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
-                   const uint8_t* avail, const uint8_t* head_table, uint64_t seed, uint64_t step,
-                   int64_t B, void* ws, size_t ws_bytes, int32_t* act, uint8_t* head_on,
-                   float* logp, float* value, float* out, ppo_stream_t st_) {
+static int infer_impl(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
+                      const uint8_t* avail, const uint8_t* head_table, uint64_t seed,
+                      uint64_t step, unsigned long long* step_ctr, int64_t B, void* ws,
+                      size_t ws_bytes, int32_t* act, uint8_t* head_on, float* logp,
+                      float* value, float* out, ppo_stream_t st_) {
   cudaStream_t st = (cudaStream_t)st_;
   Shape s;
   int rc = check_dims(dims, &s);
@@ -309,7 +315,7 @@ int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h,
     ProfScope _prof("infer_pack", st);
     PPO_CUDA_CHECK(launch_pdl(infer_pack_kernel, dim3((unsigned)((B * (s.Kx / 8 + 8) + 255) / 256)),
                               dim3(256), 0, st, s, B, static_cast<const __nv_bfloat16*>(x),
-                              (const float*)h, xh, ho));
+                              (const float*)h, xh, ho, step_ctr));
     PPO_LAUNCH_CHECK("infer_pack_kernel");
   }
   int S = 1;
@@ -324,13 +330,32 @@ int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h,
   if (!(skip & 8) && (rc = tc_infer_heads(s, B, w, ho, yp, &S2, st))) return rc;
   if (!(skip & 16)) {
     ProfScope _prof("infer_sample", st);
-    const uint64_t base = seed + (step << 32);
     PPO_CUDA_CHECK(launch_pdl(infer_sample_kernel, dim3((unsigned)B), dim3(kSampleThreads),
                               (s.A + s.vcol) * sizeof(float), st, s, B, S2, (const float*)yp, avail,
-                              head_table, base, act, head_on, logp, value, out));
+                              head_table, seed, step, (const unsigned long long*)step_ctr, act,
+                              head_on, logp, value, out));
     PPO_LAUNCH_CHECK("infer_sample_kernel");
   }
   return PPO_OK;
+}
+
+int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
+                   const uint8_t* avail, const uint8_t* head_table, uint64_t seed, uint64_t step,
+                   int64_t B, void* ws, size_t ws_bytes, int32_t* act, uint8_t* head_on,
+                   float* logp, float* value, float* out, ppo_stream_t st) {
+  return infer_impl(dims, w, x, h, c, avail, head_table, seed, step, nullptr, B, ws, ws_bytes,
+                    act, head_on, logp, value, out, st);
+}
+
+int ppo_infer_step_ctr(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
+                       const uint8_t* avail, const uint8_t* head_table, uint64_t seed,
+                       uint64_t* step_ctr, int64_t B, void* ws, size_t ws_bytes, int32_t* act,
+                       uint8_t* head_on, float* logp, float* value, float* out,
+                       ppo_stream_t st) {
+  if (!step_ctr || !aligned(step_ctr, 8)) return fail(PPO_E_ARG, "step_ctr must be a device u64");
+  return infer_impl(dims, w, x, h, c, avail, head_table, seed, 0,
+                    reinterpret_cast<unsigned long long*>(step_ctr), B, ws, ws_bytes, act,
+                    head_on, logp, value, out, st);
 }
 
 }  // extern "C"

@@ -666,6 +666,11 @@ __host__ __device__ __forceinline__ constexpr int hd(int s) {   // head of slot 
 __host__ __device__ __forceinline__ constexpr int ix(int s) { return s - sb(hd(s)); }
 // slot s of lane l holds logit off(hd(s)) + l + 32 ix(s); it exists iff l < lim(s)
 __host__ __device__ __forceinline__ constexpr int lim(int s) { return sz(hd(s)) - 32 * ix(s); }
+// packed pairs: slots (s, s+1) of one head with ix(s) even
+__host__ __device__ __forceinline__ constexpr bool pair_first(int s) {
+  return ix(s) % 2 == 0 && ix(s) + 1 < ni(hd(s));
+}
+__host__ __device__ __forceinline__ constexpr bool pair_second(int s) { return ix(s) % 2 == 1; }
 static_assert(off(1) == sz(0) && off(2) == off(1) + sz(1) && off(3) == off(2) + sz(2) &&
               off(4) == off(3) + sz(3) && off(5) == off(4) + sz(4) &&
               off(6) == off(5) + sz(5) && off(7) == off(6) + sz(6), "offsets");
@@ -758,12 +763,32 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = 0.f;   // v[k] = sum e, v[8 + k] = sum e*y
+    // slots of one head in pairs through the packed fp32x2 pipe (FFMA2/FADD2), odd tails alone
+    float2 se2[NH], sey2[NH];
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      se2[k] = make_float2(0.f, 0.f);
+      sey2[k] = make_float2(0.f, 0.f);
+    }
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const int k = hd(s);
-      const float e = ex2(fmaf(y[s], L2E, -mb[k]));
-      v[k] += e;
-      v[8 + k] = fmaf(e, y[s], v[8 + k]);
+      if (pair_first(s)) {
+        const float2 y2 = make_float2(y[s], y[s + 1]);
+        const float2 a2 = __ffma2_rn(y2, make_float2(L2E, L2E), make_float2(-mb[k], -mb[k]));
+        const float2 e2 = make_float2(ex2(a2.x), ex2(a2.y));
+        se2[k] = __fadd2_rn(se2[k], e2);
+        sey2[k] = __ffma2_rn(e2, y2, sey2[k]);
+      } else if (!pair_second(s)) {
+        const float e = ex2(fmaf(y[s], L2E, -mb[k]));
+        v[k] += e;
+        v[8 + k] = fmaf(e, y[s], v[8 + k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      v[k] += se2[k].x + se2[k].y;
+      v[8 + k] += sey2[k].x + sey2[k].y;
     }
     // reduce-scatter: lane of sum index q holds it; the sum-e lanes take sum e*y from lane+16
     const float tot = warp_sum16(v, lane);
@@ -830,8 +855,17 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const int k = hd(s);
-      const float d = ex2(fmaf(y[s], L2E, -lb[k])) * fmaf(cek[k], y[s], c1[k]);
-      if (lim(s) >= 32 || lane < lim(s)) dl[off(k) + 32 * ix(s)] = from_f<TD>(d);
+      if (pair_first(s)) {
+        const float2 y2 = make_float2(y[s], y[s + 1]);
+        const float2 a2 = __ffma2_rn(y2, make_float2(L2E, L2E), make_float2(-lb[k], -lb[k]));
+        const float2 t2 = __ffma2_rn(make_float2(cek[k], cek[k]), y2, make_float2(c1[k], c1[k]));
+        const float2 d2 = __fmul2_rn(make_float2(ex2(a2.x), ex2(a2.y)), t2);
+        if (lim(s) >= 32 || lane < lim(s)) dl[off(k) + 32 * ix(s)] = from_f<TD>(d2.x);
+        if (lim(s + 1) >= 32 || lane < lim(s + 1)) dl[off(k) + 32 * ix(s + 1)] = from_f<TD>(d2.y);
+      } else if (!pair_second(s)) {
+        const float d = ex2(fmaf(y[s], L2E, -lb[k])) * fmaf(cek[k], y[s], c1[k]);
+        if (lim(s) >= 32 || lane < lim(s)) dl[off(k) + 32 * ix(s)] = from_f<TD>(d);
+      }
     }
     __syncwarp();
     if (lane < NH && on_l) {

@@ -37,6 +37,9 @@ class PolicyServer:
         self.value = torch.empty(B, device=dev)
         self.out = torch.empty(B, self.A, device=dev)
         self.seed, self.t = seed, 0
+        # the step counter lives on the device (ppo_infer_step_ctr): a captured CUDA graph of
+        # steps draws fresh noise on every replay
+        self.step_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def load(self, weights: torch.Tensor, stream=None):
         """a published bf16 parameter vector (PPOOptimizer.shadow layout) -> tiled copy"""
@@ -44,15 +47,18 @@ class PolicyServer:
             raise ValueError("expected the bf16 parameter vector of ppo_param_layout")
         L.ppo_infer_pack_weights(self.dims, weights, self.wt, stream)
 
-    def reset(self, h0=None, c0=None):
+    def reset(self, h0=None, c0=None, step: int | None = None):
         self.h.copy_(h0) if h0 is not None else self.h.zero_()
         self.c.copy_(c0) if c0 is not None else self.c.zero_()
+        if step is not None:
+            self.step_ctr.fill_(step)
+            self.t = step
 
     def step(self, x: torch.Tensor, avail: torch.Tensor, want_out: bool = True, stream=None):
         """x [B][D] bf16, avail [B][n_primary] uint8 -> (act, head_on, logp, value); the
         recurrent state advances in place."""
-        L.ppo_infer_step(self.dims, self.wt, x, self.h, self.c, avail, self.head_table,
-                         self.seed, self.t, self.B, self.ws, self.act, self.head_on, self.logp,
-                         self.value, self.out if want_out else None, stream)
-        self.t += 1
+        L.ppo_infer_step_ctr(self.dims, self.wt, x, self.h, self.c, avail, self.head_table,
+                             self.seed, self.step_ctr, self.B, self.ws, self.act, self.head_on,
+                             self.logp, self.value, self.out if want_out else None, stream)
+        self.t += 1   # host mirror (eager calls only; graph replays advance step_ctr alone)
         return self.act, self.head_on, self.logp, self.value

@@ -114,3 +114,54 @@ def test_infer_deterministic_and_counter():
     torch.cuda.synchronize()
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
     assert torch.equal(outs[0][2], outs[1][2])
+
+
+def test_graph_replay_draws_fresh_noise():
+    """A captured CUDA graph of 3 inference steps, replayed twice, equals 6 eager steps (the
+    device step counter advances inside the graph), bit for bit."""
+    cfg = synth.Config(H=128, D=128, B=40, T=6)
+    prm = {k: synth.round_bf16(v) for k, v in synth.make_params(cfg, 2, bo_scale=0.3).items()}
+    s = synth.make_sequences(cfg, 3)
+    table = synth.heads_on_table(cfg.head_sizes)
+    xs = [dev(s["x"][t]).bfloat16() for t in range(cfg.T)]
+    avs = [dev(s["avail"][t]) for t in range(cfg.T)]
+    eager = _server(cfg, cfg.B, prm, table, seed=9)
+    eager.reset(dev(s["h0"]), dev(s["c0"]))
+    ref = []
+    for t in range(cfg.T):
+        a, _, lp, _ = eager.step(xs[t], avs[t])
+        ref.append((a.clone(), lp.clone()))
+    g_srv = _server(cfg, cfg.B, prm, table, seed=9)
+    g_srv.reset(dev(s["h0"]), dev(s["c0"]), step=0)
+    xin = torch.empty_like(xs[0])
+    ain = torch.empty_like(avs[0])
+    acts = [torch.empty_like(ref[0][0]) for _ in range(3)]
+    lps = [torch.empty_like(ref[0][1]) for _ in range(3)]
+    xbuf = [torch.empty_like(xs[0]) for _ in range(3)]
+    abuf = [torch.empty_like(avs[0]) for _ in range(3)]
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st):
+        # warm the library's lazy set-up outside the capture (state restored below)
+        g_srv.step(xs[0], avs[0])
+        torch.cuda.synchronize()
+        g_srv.reset(dev(s["h0"]), dev(s["c0"]), step=0)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=st):
+            for i in range(3):
+                a, _, lp, _ = g_srv.step(xbuf[i], abuf[i])
+                acts[i].copy_(a)
+                lps[i].copy_(lp)
+    torch.cuda.current_stream().wait_stream(st)
+    for rep in range(2):
+        for i in range(3):
+            xbuf[i].copy_(xs[3 * rep + i])
+            abuf[i].copy_(avs[3 * rep + i])
+        graph.replay()
+        torch.cuda.synchronize()
+        for i in range(3):
+            t = 3 * rep + i
+            assert torch.equal(acts[i], ref[t][0]), t
+            assert torch.equal(lps[i], ref[t][1]), t
+    assert int(g_srv.step_ctr.item()) == 6
