@@ -637,11 +637,15 @@ def main():
         # End to end through the public API with HOST inputs: every step's inputs are copied
         # from pinned host memory (H2D) and its stats read back (D2H) inside the timed region.
         # Inputs are double-buffered on the device: the H2D of step k+1 runs on a copy stream
-        # while step k computes (the first step's copy is not overlapped).
-        # x goes straight from pinned host memory into the x rows of one of two workspaces
-        # (ppo_copy_x); the other inputs into double-buffered device tensors.
-        keys = ("h0", "c0", "act", "head_on", "avail", "logp_old", "rew", "val", "done") + \
+        # while step k computes (the first step's copy overlaps only its own forward).
+        # x goes straight from pinned host memory into the x rows of one of two workspaces,
+        # one time slice at a time (ppo_copy_x_slice), and the forward's step t waits only for
+        # slice t (lstm_bptt_fwd_ev); GAE's and the state's inputs go first, the loss's last.
+        # The other inputs are double-buffered device tensors.
+        keys_first = ("h0", "c0", "rew", "val", "done") + \
             (("last", "outcome", "rank", "events", "boot") if args.aux else ())
+        keys_rest = ("act", "head_on", "avail", "logp_old")
+        keys = keys_first + keys_rest
         host = {k: batch[k].cpu().pin_memory() for k in keys}
         host_x = x_dev.cpu().pin_memory()
         del x_dev
@@ -651,26 +655,33 @@ def main():
         st_host = torch.empty(8, dtype=torch.float32).pin_memory()
         d2h = st_host.numel() * 4
         copy_stream = torch.cuda.Stream(device=device)
-        h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_first = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_x = [[torch.cuda.Event() for _ in range(T)] for _ in range(2)]
+        ev_rest = [torch.cuda.Event(), torch.cuda.Event()]
         used = [torch.cuda.Event(), torch.cuda.Event()]
 
         def upload(slot):
             copy_stream.wait_event(used[slot])
             with torch.cuda.stream(copy_stream):
-                for k in keys:
+                for k in keys_first:
                     bufs[slot][k].copy_(host[k], non_blocking=True)
-                opt.put_x(host_x, ws=slot, stream=copy_stream)
-            h2d_done[slot].record(copy_stream)
+                ev_first[slot].record(copy_stream)
+                for t in range(T):
+                    L.ppo_copy_x_slice(opt.dims, B, t, host_x[t], opt.ws_list[slot], copy_stream)
+                    ev_x[slot][t].record(copy_stream)
+                for k in keys_rest:
+                    bufs[slot][k].copy_(host[k], non_blocking=True)
+                ev_rest[slot].record(copy_stream)
 
         def run(nsteps):
             upload(0)
             for i in range(nsteps):
                 cur = i % 2
-                stream.wait_event(h2d_done[cur])
                 if i + 1 < nsteps:
                     upload(1 - cur)
+                stream.wait_event(ev_first[cur])
                 opt.select_ws(cur)
-                opt.step(bufs[cur], dx=dx)
+                opt.step_streamed(bufs[cur], ev_x[cur], ev_rest[cur], dx=dx)
                 used[cur].record(stream)
                 st_host.copy_(opt.stats[:8], non_blocking=True)
 
@@ -688,7 +699,8 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / args.steps,
                "overlap": "H2D of step k+1 on a copy stream during step k (double-buffered "
-                          "inputs; x straight into the workspace of step k+1)"}
+                          "inputs; x straight into the workspace of step k+1, one time slice "
+                          "at a time; step t of the forward waits only for slice t)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -160,6 +160,17 @@ int lstm_ws_x(const ppo_dims* dims, int64_t B, void* ws, void** x /* host out */
 int ppo_copy_x(const ppo_dims* dims, int64_t B, const void* src, int64_t src_ld, void* ws,
                size_t ws_bytes, ppo_stream_t s);
 
+/* Streaming inputs: copy time slice t of x (B rows [B][D], row stride src_ld elements; pinned
+ * host or device) into the workspace, and run the forward with x already there while the
+ * later slices are still in flight: lstm_bptt_fwd_ev waits on x_ready[t] (a cudaEvent_t
+ * recorded after slice t's copy; NULL entries or a NULL array = no wait) before step t.
+ * h0, c0 as in lstm_bptt_fwd with x == NULL. */
+int ppo_copy_x_slice(const ppo_dims* dims, int64_t B, int32_t t, const void* src,
+                     int64_t src_ld, void* ws, size_t ws_bytes, ppo_stream_t s);
+int lstm_bptt_fwd_ev(const ppo_dims* dims, const void* w, const float* h0, const float* c0,
+                     int64_t B, void* ws, size_t ws_bytes, float* out,
+                     void* const* x_ready /* host array of T cudaEvent_t */, ppo_stream_t s);
+
 /* ---- a5: PPO loss and its gradient (O6, O7) --
  * out [T·B][A] fp32 (row = t*B + b); act [T·B][n_heads] int32; head_on [T·B][n_heads] u8
  * (heads read by the taken primary action, Table target types P:350-368); avail

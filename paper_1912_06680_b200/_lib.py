@@ -93,6 +93,10 @@ _lib_fns = dict(
     lstm_bptt_fwd=([_D, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_size_t,
                     c_void_p, c_void_p], c_int),
     lstm_ws_x=([_D, c_int64, c_void_p, POINTER(c_void_p), POINTER(c_int64)], c_int),
+    ppo_copy_x_slice=([_D, c_int64, c_int32, c_void_p, c_int64, c_void_p, c_size_t, c_void_p],
+                      c_int),
+    lstm_bptt_fwd_ev=([_D, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_size_t, c_void_p,
+                       POINTER(c_void_p), c_void_p], c_int),
     ppo_copy_x=([_D, c_int64, c_void_p, c_int64, c_void_p, c_size_t, c_void_p], c_int),
     ppo_loss_grad=([_D] + [c_void_p] * 9 + [c_int64, POINTER(ppo_loss_cfg), c_void_p, c_void_p,
                                              c_void_p, c_void_p], c_int),
@@ -228,6 +232,20 @@ def ppo_copy_x(dims, B, src, ws, stream=None):
     """src: contiguous [T][B][D] tensor (pinned host or device)"""
     _check(_lib.ppo_copy_x(ctypes.byref(dims), B, _p(src), src.shape[-1], _p(ws),
                            ws.numel() * ws.element_size(), _s(stream)))
+
+
+def ppo_copy_x_slice(dims, B, t, src, ws, stream=None):
+    """src: [B][D] contiguous (pinned host or device): time slice t of x"""
+    _check(_lib.ppo_copy_x_slice(ctypes.byref(dims), B, t, _p(src), src.shape[-1], _p(ws),
+                                 ws.numel() * ws.element_size(), _s(stream)))
+
+
+def lstm_bptt_fwd_ev(dims, w, h0, c0, B, ws, out, events, stream=None):
+    """events: list of T torch.cuda.Event (or None entries)"""
+    arr = (c_void_p * len(events))(*[None if e is None else c_void_p(e.cuda_event)
+                                     for e in events])
+    _check(_lib.lstm_bptt_fwd_ev(ctypes.byref(dims), _p(w), _p(h0), _p(c0), B, _p(ws),
+                                 ws.numel() * ws.element_size(), _p(out), arr, _s(stream)))
 
 
 def ppo_loss_grad(dims, out, act, head_on, avail, logp_old, adv, ret, valid, B, cfg, dout, logp,

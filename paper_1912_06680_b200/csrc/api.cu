@@ -249,9 +249,9 @@ int lstm_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes) {
   return PPO_OK;
 }
 
-int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const float* h0,
-                  const float* c0, int64_t B, void* ws, size_t ws_bytes, float* out,
-                  ppo_stream_t st_) {
+static int fwd_impl(const ppo_dims* dims, const void* w, const void* x, const float* h0,
+                    const float* c0, int64_t B, void* ws, size_t ws_bytes, float* out,
+                    const cudaEvent_t* x_ready, ppo_stream_t st_) {
   cudaStream_t st = (cudaStream_t)st_;
   Shape s;
   int rc = check_dims(dims, &s);
@@ -281,7 +281,7 @@ int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const floa
   }
   if (s.bf16) {
     if ((rc = check_tc_device())) return rc;
-    return tc_forward(s, B, w, ws, out, st);
+    return tc_forward(s, B, w, ws, out, x_ready, st);
   }
   // ---- SIMT fp32 reference path
   const float* W = static_cast<const float*>(w);
@@ -290,6 +290,7 @@ int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const floa
   float* G = reinterpret_cast<float*>(wsb + L.g);
   float* raw = reinterpret_cast<float*>(wsb + L.raw);
   for (int64_t t = 0; t < s.T; ++t) {
+    if (x_ready && x_ready[t]) PPO_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready[t], 0));
     SimtOp a{{XH + t * B * s.Kx, nullptr}, {s.Kx, 0}, {B, 0}, {s.Kx, 0}, s.Kx, false};
     SimtOp b{{W, nullptr}, {s.Kx, 0}, {s.G4, 0}, {s.Kx, 0}, s.Kx, false};
     if ((rc = launch_simt_gemm(a, b, B, s.G4, s.Kx, raw, s.G4, st))) return rc;
@@ -300,6 +301,37 @@ int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const floa
   SimtOp a{{XH + B * s.Kx + s.D, nullptr}, {s.Kx, 0}, {s.T * B, 0}, {s.Ko, 0}, s.Ko, false};
   SimtOp b{{Wo, nullptr}, {s.Ko, 0}, {s.A, 0}, {s.Ko, 0}, s.Ko, false};
   return launch_simt_gemm(a, b, s.T * B, s.A, s.Ko, out, s.A, st);
+}
+
+int lstm_bptt_fwd(const ppo_dims* dims, const void* w, const void* x, const float* h0,
+                  const float* c0, int64_t B, void* ws, size_t ws_bytes, float* out,
+                  ppo_stream_t st) {
+  return fwd_impl(dims, w, x, h0, c0, B, ws, ws_bytes, out, nullptr, st);
+}
+
+int lstm_bptt_fwd_ev(const ppo_dims* dims, const void* w, const float* h0, const float* c0,
+                     int64_t B, void* ws, size_t ws_bytes, float* out,
+                     void* const* x_ready, ppo_stream_t st) {
+  return fwd_impl(dims, w, nullptr, h0, c0, B, ws, ws_bytes, out,
+                  reinterpret_cast<const cudaEvent_t*>(x_ready), st);
+}
+
+int ppo_copy_x_slice(const ppo_dims* dims, int64_t B, int32_t t, const void* src,
+                     int64_t src_ld, void* ws, size_t ws_bytes, ppo_stream_t st) {
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (B < 1 || t < 0 || t >= s.T) return fail(PPO_E_SHAPE, "need B >= 1 and 0 <= t < T");
+  if (!src || !ws) return fail(PPO_E_ARG, "NULL pointer");
+  if (src_ld < s.D) return fail(PPO_E_ARG, "src_ld < D");
+  WsLayout L = ws_layout(s, B);
+  if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small");
+  const size_t esz = s.bf16 ? 2 : 4;
+  ProfScope _prof("copy_x", (cudaStream_t)st);
+  PPO_CUDA_CHECK(cudaMemcpy2DAsync(static_cast<uint8_t*>(ws) + L.xh + (size_t)t * B * s.Kx * esz,
+                                   s.Kx * esz, src, src_ld * esz, s.D * esz, B,
+                                   cudaMemcpyDefault, (cudaStream_t)st));
+  return PPO_OK;
 }
 
 int lstm_ws_x(const ppo_dims* dims, int64_t B, void* ws, void** x, int64_t* ld) {

@@ -62,7 +62,8 @@ int launch_simt_cell_bwd(const Shape& s, int64_t B, const float* dh, float* gz, 
 int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cudaStream_t st);
 
 // tcgen05 bf16 path (tc_path.cu)
-int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, cudaStream_t st);
+int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
+               const cudaEvent_t* x_ready, cudaStream_t st);
 int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
                 cudaStream_t st);
 // Standalone test GEMM (exported for tests): C = A B^T variants on bf16 inputs.

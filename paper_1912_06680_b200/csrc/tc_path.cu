@@ -189,7 +189,8 @@ WsPtrs ws_ptrs(const Shape& s, int64_t B, void* ws) {
 }  // namespace
 
 // ---------------------------------------------------------------- forward (a2-a4)
-int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, cudaStream_t st) {
+int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
+               const cudaEvent_t* x_ready, cudaStream_t st) {
   WsPtrs P = ws_ptrs(s, B, ws);
   const __nv_bfloat16* wxh = static_cast<const __nv_bfloat16*>(w);
   const __nv_bfloat16* wo = wxh + s.G4 * s.Kx;
@@ -202,6 +203,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out, c
   if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 128))) return rc;
   if ((rc = map_kmajor(&mB1, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
   for (int t = 0; t < s.T; ++t) {
+    if (x_ready && x_ready[t]) PPO_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready[t], 0));
     tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8, 1};
     raster(sh, "FWD", 8, 1);
     sh.sched = sched_counter(kSchedFwd);

@@ -123,6 +123,30 @@ class PPOOptimizer:
                          batch["events"], batch["boot"], g2, batch["aux_label"], seq_T=self.T,
                          stream=stream)
 
+    def forward_streamed(self, batch, x_events, stream=None):
+        """a2-a4 with x arriving in the workspace slice by slice (ppo_copy_x_slice): step t
+        waits on x_events[t] (lstm_bptt_fwd_ev)"""
+        L.lstm_bptt_fwd_ev(self.dims, self.weights, batch["h0"], batch["c0"], self.B, self.ws,
+                           self.out, x_events, stream)
+
+    def step_streamed(self, batch, x_events, rest_event, stream=None, dx=None):
+        """The step with host inputs still streaming in: GAE and the forward start as soon as
+        their inputs land (x per time step); the loss waits on rest_event (act, head_on,
+        avail, logp_old ...)."""
+        import torch
+        self.gae(batch, stream)
+        if sum(self.aux) and "events" in batch:
+            self.aux_labels(batch, stream)
+        self.forward_streamed(batch, x_events, stream)
+        (stream or torch.cuda.current_stream()).wait_event(rest_event)
+        self.loss(batch, stream=stream)
+        self.backward(stream)
+        if dx is not None:
+            self.input_grad(dx, stream)
+        self.allreduce(stream)
+        self.apply(stream)
+        return self.stats[:L.PPO_STATS]
+
     def forward(self, batch, stream=None):
         """a2-a4; batch["x"] None = x already in the workspace (put_x / ppo_gather)"""
         L.lstm_bptt_fwd(self.dims, self.weights, batch.get("x"), batch["h0"], batch["c0"], self.B,

@@ -175,6 +175,19 @@ def test_zero_copy_x_matches_packed(precision):
         opt.forward(dict(batch, x=None))
         torch.cuda.synchronize()
         assert torch.equal(opt.out, ref), ws
+    # streamed: x slice by slice on a side stream, the forward waits per time step
+    side = torch.cuda.Stream()
+    evs = [torch.cuda.Event() for _ in range(cfg.T)]
+    opt.out.zero_()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for t in range(cfg.T):
+            L.ppo_copy_x_slice(opt.dims, cfg.B, t, xh[t], opt.ws_list[1], side)
+            evs[t].record(side)
+    opt.select_ws(1)
+    opt.forward_streamed(dict(batch, x=None), evs)
+    torch.cuda.synchronize()
+    assert torch.equal(opt.out, ref)
     p, ld = L.lstm_ws_x(opt.dims, cfg.B, opt.ws_list[1])
     assert p == opt.ws_list[1].data_ptr() and ld == cfg.D + cfg.H + 64
     with pytest.raises(RuntimeError):
