@@ -621,7 +621,7 @@ def main():
               key=lambda k: kernels[k]["ms_per_step"])
     d = kernels[dom]
     n_launch = sum(n for n, _ in prof.values())
-    step_flop = sum(w for k, (kind, w) in alg.items() if kind == "flop")
+    step_flop = sum(w for k, (kind, w) in alg.items() if kind == "flop" and k in prof)
     roofline = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": d["unit"], "frac": d["frac"],
                 "traffic": traffic.get(dom, {}).get("dram_bytes_per_launch") if B == 38400 else None,
@@ -630,6 +630,13 @@ def main():
                 "peak_source": pk["source"] + (" sustained" if d["bound"] == "tensor" else ""),
                 "step_tflops": step_flop / (ms_step / 1e3) / 1e12,
                 "step_frac_of_sustained_bf16": step_flop / (ms_step / 1e3) / 1e12 / pk["bf16_tflops_sustained"]}
+    # whole-step roofline: every GEMM at the sustained bf16 peak plus every
+    # HBM-bound kernel at the measured HBM bandwidth, against the measured step time
+    step_bytes = sum(w for k, (kind, w) in alg.items() if kind == "byte" and k in prof)
+    t_roof = step_flop / (pk["bf16_tflops_sustained"] * 1e12) + step_bytes / (pk["hbm_gbs"] * 1e9)
+    roofline["step"] = {"T_roof_ms": t_roof * 1e3, "ms_per_step": ms_step,
+                        "frac": t_roof * 1e3 / ms_step,
+                        "flop": step_flop, "hbm_bytes": step_bytes}
 
     # ---- end to end through the public API with host buffers
     e2e = None
