@@ -474,8 +474,15 @@ def run_infer(args):
         g_us = gates[1] / gates[0] * 1e3
         kern = {k: {"launches_per_step": c // nsteps, "us_per_step": t / nsteps * 1e3}
                 for k, (c, t) in prof.items()}
+        step_flop = 2.0 * B * (G4 * Kx + A * Ko)
+        t_roof = max(step_bytes / (pk["hbm_gbs"] * 1e9),
+                     step_flop / (pk["bf16_tflops_sustained"] * 1e12))
         rows.append({
             "B": B, "us_per_step": us, "us_per_step_graph": us_graph,
+            # the bound flips from the weights' HBM stream to the tensor pipe as B grows
+            "bound": "hbm" if step_bytes / (pk["hbm_gbs"] * 1e9) >= step_flop / (
+                pk["bf16_tflops_sustained"] * 1e12) else "tensor",
+            "roofline_frac": t_roof / (us_graph * 1e-6),
             "steps_per_s": 1e6 / us_graph, "hero_actions_per_s": B * 1e6 / us_graph,
             "achieved_GB_s": step_bytes / (us_graph * 1e-6) / 1e9,
             "frac": step_bytes / (us_graph * 1e-6) / 1e9 / pk["hbm_gbs"],

@@ -299,7 +299,8 @@ int ppo_reward_gae(const float* shaped, const float* win, const int32_t* step0, 
 /* ---- NEXT-3: forward-pass inference step ---------------------------------------
  * "a separate pool of GPU machines which run forward passes in larger batches of
  * approximately 60": one policy step for B heroes.
- *   z = W_xh_aug [x | h | 1]; LSTM cell -> h', c' (written back in place)
+ *   z = W_xh_aug [x | h | 1]; LSTM cell -> h', c' (written back in place);
+ *   x is read by TMA directly from the caller's buffer (rows of D*2 bytes, 16-byte aligned)
  *   y = W_o_aug [h' | 1]  (logits of the n_heads heads | value)
  *   act[b][k] = argmax over allowed j of (y_kj + g_kj), g = -log(-log u) Gumbel noise, ties
  *     to the smallest j (DESIGN reading Q22); allowed = avail[b] for the primary head (action
@@ -319,11 +320,16 @@ int ppo_reward_gae(const float* shaped, const float* win, const int32_t* step0, 
  * Asynchronous on the stream. */
 /* Same step with the counter on the device: this call draws with step = *step_ctr and leaves
  * *step_ctr + 1 (device uint64, 8-byte aligned), so a captured CUDA graph of inference steps
- * draws fresh noise on every replay. */
+ * draws fresh noise on every replay.  flags: PPO_INFER_STATE_CURRENT = the workspace still
+ * holds the bf16 copy of h written by this ws's previous step (h not modified since): the
+ * state upload is skipped.  Without it (first call, or after the caller changed h) the step
+ * re-derives the copy from h. */
+#define PPO_INFER_STATE_CURRENT 1u
 int ppo_infer_step_ctr(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
                        const uint8_t* avail, const uint8_t* head_table, uint64_t seed,
-                       uint64_t* step_ctr, int64_t B, void* ws, size_t ws_bytes, int32_t* act,
-                       uint8_t* head_on, float* logp, float* value, float* out, ppo_stream_t s);
+                       uint64_t* step_ctr, uint32_t flags, int64_t B, void* ws,
+                       size_t ws_bytes, int32_t* act, uint8_t* head_on, float* logp,
+                       float* value, float* out, ppo_stream_t s);
 int ppo_infer_ws_bytes(const ppo_dims* dims, int64_t B, size_t* bytes /* host out */);
 /* The served weights, re-laid out once per published version for streaming: every
  * [128 rows][64 k] block of W_xh_aug and W_o_aug becomes one contiguous 16 KB tile (rows past

@@ -118,8 +118,8 @@ _lib_fns = dict(
                      c_void_p, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
     lstm_input_grad=([_D, c_void_p, c_void_p, c_size_t, c_int64, c_void_p, c_void_p], c_int),
     ppo_infer_step_ctr=([_D, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                         ctypes.c_uint64, c_void_p, c_int64, c_void_p, c_size_t, c_void_p,
-                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p], c_int),
+                         ctypes.c_uint64, c_void_p, ctypes.c_uint32, c_int64, c_void_p, c_size_t,
+                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p], c_int),
     ppo_infer_ws_bytes=([_D, c_int64, POINTER(c_size_t)], c_int),
     ppo_infer_weights_bytes=([_D, POINTER(c_size_t)], c_int),
     ppo_infer_pack_weights=([_D, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
@@ -338,11 +338,14 @@ def ppo_infer_step(dims, w, x, h, c, avail, head_table, seed, step, B, ws, act, 
                                _p(value), _p(out), _s(stream)))
 
 
+PPO_INFER_STATE_CURRENT = 1
+
+
 def ppo_infer_step_ctr(dims, w, x, h, c, avail, head_table, seed, step_ctr, B, ws, act, head_on,
-                       logp, value=None, out=None, stream=None):
+                       logp, value=None, out=None, stream=None, flags=0):
     """step_ctr: device int64 tensor [1] (steps taken so far; advanced by the call)"""
     _check(_lib.ppo_infer_step_ctr(ctypes.byref(dims), _p(w), _p(x), _p(h), _p(c), _p(avail),
-                                   _p(head_table), seed, _p(step_ctr), B, _p(ws),
+                                   _p(head_table), seed, _p(step_ctr), flags, B, _p(ws),
                                    ws.numel() * ws.element_size(), _p(act), _p(head_on),
                                    _p(logp), _p(value), _p(out), _s(stream)))
 

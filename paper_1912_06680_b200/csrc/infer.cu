@@ -2,9 +2,10 @@
 // passes in larger batches of approximately 60"): LSTM step from the carried state (P:1210,
 // P:1202), the heads and masked factorised sampling (reading Q22).
 //
-//   infer_pack    XH[b] = [x_b | bf16(h_b) | 1 | 0..]; the [1 | 0..] pad of HO rows
-//   infer_gates   tcgen05 split-K GEMM: Zp[s][b][r] = W_xh_aug[r, ks] . XH[b, ks]   (tc_path.cu)
-//   infer_cell    z = sum_s Zp[s]; LSTM cell; h, c (fp32 state, in place); HO[b] = [bf16(h') | 1 | 0]
+//   infer_state   HO[b] = [bf16(h_b) | 1 | 0..] (skipped when HO already holds the state)
+//   infer_gates   tcgen05 split-K GEMM: Zp[s][b][r] = W_xh_aug[r, ks] . [x_b | HO_b][ks] -- x
+//                 read by TMA straight from the caller's buffer                  (tc_path.cu)
+//   infer_cell    z = sum_s Zp[s]; LSTM cell; h, c (fp32 state, in place); HO[b] = bf16(h')
 //   infer_heads   tcgen05 split-K GEMM: Yp[s][b][a] = W_o_aug[a, ks] . HO[b, ks]
 //   infer_sample  y = sum_s Yp[s]; Gumbel-max per head (primary masked by avail); target-type
 //                 table -> head_on; behaviour log-prob of the read heads; value.
@@ -18,13 +19,12 @@ namespace {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct InferLayout {
-  size_t xh, ho, zp, yp, total;
+  size_t ho, zp, yp, total;
 };
 InferLayout infer_layout(const Shape& s, int64_t B) {
   InferLayout L;
   const size_t S = (size_t)tc_infer_max_split();
-  L.xh = 0;
-  L.ho = align_up(L.xh + (size_t)B * s.Kx * 2, 1024);
+  L.ho = 0;
   L.zp = align_up(L.ho + (size_t)B * s.Ko * 2, 1024);
   L.yp = align_up(L.zp + S * s.G4 * B * 4, 1024);
   L.total = align_up(L.yp + S * s.A * B * 4, 1024);
@@ -45,29 +45,21 @@ __device__ __forceinline__ float gumbel_noise(uint64_t base, int64_t b, int k) {
   return -logf(-logf(u));
 }
 
-// XH[b] = [x_b | bf16(h_b) | 1 | 0...]; HO[b][H..Ko) = [1 | 0...].  One thread per 8 output
-// columns (16-byte stores), all rows in one flat grid.
-__global__ void __launch_bounds__(256) infer_pack_kernel(Shape s, int64_t B,
-                                                         const __nv_bfloat16* __restrict__ x,
-                                                         const float* __restrict__ h,
-                                                         __nv_bfloat16* __restrict__ xh,
-                                                         __nv_bfloat16* __restrict__ ho,
-                                                         unsigned long long* __restrict__ step_ctr) {
+// HO[b] = [bf16(h_b) | 1 | 0...]: the recurrent half of the gates GEMM's batch operand and the
+// heads GEMM's.  One thread per 8 columns (16-byte stores), all rows in one flat grid.
+__global__ void __launch_bounds__(256) infer_state_kernel(Shape s, int64_t B,
+                                                          const float* __restrict__ h,
+                                                          __nv_bfloat16* __restrict__ ho) {
   pdl_launch_dependents();
   pdl_wait();
-  // device step counter (graph replays): this step is *ctr; the sample kernel reads *ctr - 1
-  if (step_ctr && blockIdx.x == 0 && threadIdx.x == 0) *step_ctr += 1ull;
-  const int64_t per_row = s.Kx / 8 + 8;   // XH row in 8-column groups + the 64-column HO pad
+  const int64_t per_row = s.Ko / 8;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= B * per_row) return;
   const int64_t b = e / per_row;
-  const int64_t q = e - b * per_row;
-  const int64_t col = 8 * q;
+  const int64_t col = 8 * (e - b * per_row);
   uint4 v;
-  if (col < s.D) {
-    v = *reinterpret_cast<const uint4*>(x + b * s.D + col);
-  } else if (col < s.D + s.H) {
-    const float4* hp = reinterpret_cast<const float4*>(h + b * s.H + (col - s.D));
+  if (col < s.H) {
+    const float4* hp = reinterpret_cast<const float4*>(h + b * s.H + col);
     const float4 a = hp[0], c = hp[1];
     __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y), p1 = __floats2bfloat162_rn(a.z, a.w);
     __nv_bfloat162 p2 = __floats2bfloat162_rn(c.x, c.y), p3 = __floats2bfloat162_rn(c.z, c.w);
@@ -76,14 +68,9 @@ __global__ void __launch_bounds__(256) infer_pack_kernel(Shape s, int64_t B,
     v.z = *reinterpret_cast<uint32_t*>(&p2);
     v.w = *reinterpret_cast<uint32_t*>(&p3);
   } else {
-    // [1 | 0 ...]: bf16 1.0 = 0x3F80 in the first column of the pad
-    const bool first = col == s.D + s.H || col == s.Kx;
-    v = make_uint4(first ? 0x3F80u : 0u, 0u, 0u, 0u);
+    v = make_uint4(col == s.H ? 0x3F80u : 0u, 0u, 0u, 0u);   // [1 | 0 ...] (bf16 1.0 = 0x3F80)
   }
-  if (col < s.Kx)
-    *reinterpret_cast<uint4*>(xh + b * s.Kx + col) = v;
-  else
-    *reinterpret_cast<uint4*>(ho + b * s.Ko + s.H + (col - s.Kx)) = v;
+  *reinterpret_cast<uint4*>(ho + b * s.Ko + col) = v;
 }
 
 // z = sum_s Zp[s][b][r] for the 4 gate rows r of unit j (gate-interleaved rows: r = 256*(j/64)
@@ -93,9 +80,13 @@ __global__ void __launch_bounds__(256) infer_cell_kernel(Shape s, int64_t B, int
                                                          const float* __restrict__ zp,
                                                          float* __restrict__ h,
                                                          float* __restrict__ c,
-                                                         __nv_bfloat16* __restrict__ ho) {
+                                                         __nv_bfloat16* __restrict__ ho,
+                                                         unsigned long long* __restrict__ step_ctr) {
   pdl_launch_dependents();
   pdl_wait();
+  // device step counter (graph replays): this step draws with *ctr before the increment; the
+  // sample kernel (after this one) reads *ctr - 1
+  if (step_ctr && blockIdx.x == 0 && threadIdx.x == 0) *step_ctr += 1ull;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= B * s.H) return;
   const int64_t b = e / s.H;
@@ -286,8 +277,8 @@ int ppo_infer_pack_weights(const ppo_dims* dims, const void* w, void* wt, size_t
 
 static int infer_impl(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
                       const uint8_t* avail, const uint8_t* head_table, uint64_t seed,
-                      uint64_t step, unsigned long long* step_ctr, int64_t B, void* ws,
-                      size_t ws_bytes, int32_t* act, uint8_t* head_on, float* logp,
+                      uint64_t step, unsigned long long* step_ctr, uint32_t flags, int64_t B,
+                      void* ws, size_t ws_bytes, int32_t* act, uint8_t* head_on, float* logp,
                       float* value, float* out, ppo_stream_t st_) {
   cudaStream_t st = (cudaStream_t)st_;
   Shape s;
@@ -304,26 +295,24 @@ static int infer_impl(const ppo_dims* dims, const void* w, const void* x, float*
   if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small (ppo_infer_ws_bytes)");
   if ((rc = check_tc_device())) return rc;
   // experiment knob (timing breakdowns only; results are wrong when set): skip kernels by bit
-  // 1 pack, 2 gates GEMM, 4 cell, 8 heads GEMM, 16 sample
+  // 1 state, 2 gates GEMM, 4 cell, 8 heads GEMM, 16 sample
   static const int skip = getenv("PPO_INFER_SKIP") ? atoi(getenv("PPO_INFER_SKIP")) : 0;
   uint8_t* wsb = static_cast<uint8_t*>(ws);
-  auto* xh = reinterpret_cast<__nv_bfloat16*>(wsb + L.xh);
   auto* ho = reinterpret_cast<__nv_bfloat16*>(wsb + L.ho);
   auto* zp = reinterpret_cast<float*>(wsb + L.zp);
   auto* yp = reinterpret_cast<float*>(wsb + L.yp);
-  if (!(skip & 1)) {
-    ProfScope _prof("infer_pack", st);
-    PPO_CUDA_CHECK(launch_pdl(infer_pack_kernel, dim3((unsigned)((B * (s.Kx / 8 + 8) + 255) / 256)),
-                              dim3(256), 0, st, s, B, static_cast<const __nv_bfloat16*>(x),
-                              (const float*)h, xh, ho, step_ctr));
-    PPO_LAUNCH_CHECK("infer_pack_kernel");
+  if (!(flags & PPO_INFER_STATE_CURRENT) && !(skip & 1)) {
+    ProfScope _prof("infer_state", st);
+    PPO_CUDA_CHECK(launch_pdl(infer_state_kernel, dim3((unsigned)((B * (s.Ko / 8) + 255) / 256)),
+                              dim3(256), 0, st, s, B, (const float*)h, ho));
+    PPO_LAUNCH_CHECK("infer_state_kernel");
   }
   int S = 1;
-  if (!(skip & 2) && (rc = tc_infer_gates(s, B, w, xh, zp, &S, st))) return rc;
+  if (!(skip & 2) && (rc = tc_infer_gates(s, B, w, x, ho, zp, &S, st))) return rc;
   if (!(skip & 4)) {
     ProfScope _prof("infer_cell", st);
     PPO_CUDA_CHECK(launch_pdl(infer_cell_kernel, dim3((unsigned)((B * s.H + 255) / 256)), dim3(256),
-                              0, st, s, B, S, (const float*)zp, h, c, ho));
+                              0, st, s, B, S, (const float*)zp, h, c, ho, step_ctr));
     PPO_LAUNCH_CHECK("infer_cell_kernel");
   }
   int S2 = 1;
@@ -343,18 +332,18 @@ int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h,
                    const uint8_t* avail, const uint8_t* head_table, uint64_t seed, uint64_t step,
                    int64_t B, void* ws, size_t ws_bytes, int32_t* act, uint8_t* head_on,
                    float* logp, float* value, float* out, ppo_stream_t st) {
-  return infer_impl(dims, w, x, h, c, avail, head_table, seed, step, nullptr, B, ws, ws_bytes,
-                    act, head_on, logp, value, out, st);
+  return infer_impl(dims, w, x, h, c, avail, head_table, seed, step, nullptr, 0u, B, ws,
+                    ws_bytes, act, head_on, logp, value, out, st);
 }
 
 int ppo_infer_step_ctr(const ppo_dims* dims, const void* w, const void* x, float* h, float* c,
                        const uint8_t* avail, const uint8_t* head_table, uint64_t seed,
-                       uint64_t* step_ctr, int64_t B, void* ws, size_t ws_bytes, int32_t* act,
-                       uint8_t* head_on, float* logp, float* value, float* out,
-                       ppo_stream_t st) {
+                       uint64_t* step_ctr, uint32_t flags, int64_t B, void* ws,
+                       size_t ws_bytes, int32_t* act, uint8_t* head_on, float* logp,
+                       float* value, float* out, ppo_stream_t st) {
   if (!step_ctr || !aligned(step_ctr, 8)) return fail(PPO_E_ARG, "step_ctr must be a device u64");
   return infer_impl(dims, w, x, h, c, avail, head_table, seed, 0,
-                    reinterpret_cast<unsigned long long*>(step_ctr), B, ws, ws_bytes, act,
+                    reinterpret_cast<unsigned long long*>(step_ctr), flags, B, ws, ws_bytes, act,
                     head_on, logp, value, out, st);
 }
 

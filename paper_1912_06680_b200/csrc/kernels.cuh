@@ -70,8 +70,8 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
 // NEXT-4: dX = dz W_x over all T*B rows (bf16 path)
 int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx, cudaStream_t st);
 // NEXT-3: split-K skinny GEMMs of the inference step (weights x batch); *split = partials
-int tc_infer_gates(const Shape& s, int64_t B, const void* w, const void* xh, float* part,
-                   int* split, cudaStream_t st);
+int tc_infer_gates(const Shape& s, int64_t B, const void* w, const void* x, const void* ho,
+                   float* part, int* split, cudaStream_t st);
 int tc_infer_heads(const Shape& s, int64_t B, const void* w, const void* ho, float* part,
                    int* split, cudaStream_t st);
 int tc_infer_max_split();

@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!A_MN) {
             const int a0 = sh.a_tiled_nkb ? 0 : kk;
             const int a1 = sh.a_tiled_nkb ? 0 : mb * BM;
-            const int a2 = sh.a_tiled_nkb ? mb * sh.a_tiled_nkb + kk / BK : za;
+            const int a2 = sh.a_tiled_nkb ? mb * sh.a_tiled_nkb + kb : za;   // global k-block
             if (sh.a_evict_first)
               tma_load_3d_hint(ta, &full[stage], a_dst, a0, a1, a2, policy_evict_first());
             else

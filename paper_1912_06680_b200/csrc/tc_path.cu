@@ -367,25 +367,31 @@ int infer_split(int tiles, int nkb, int min_kb, const char* knob = "PPO_INFER_SP
 // N tile by batch size: 64 at the paper's ~60, wider tiles once the batch fills them (the
 // MMA needs N >= 128 to stop being shared-memory bound).
 // W is pre-tiled (tc_infer_tile_weights): [ceil(M/128) * nkb] tiles of [128][64] bf16.
+// The batch operand is the K-concatenation of act0 [B][K0] (ld0) and act1 [B][K - K0] (ld1)
+// (K0 = K: one source); K0 must be a multiple of 64.
 template <int BN>
 int infer_gemm_bn(const char* tag, int slot, const void* W, int64_t M, int64_t K,
-                  const void* act, int64_t B, int64_t ld_act, float* part, int* split_out,
-                  cudaStream_t st) {
-  CUtensorMap ma, mb;
+                  const void* act0, int64_t K0, int64_t ld0, const void* act1, int64_t ld1,
+                  int64_t B, float* part, int* split_out, cudaStream_t st) {
+  CUtensorMap ma, mb0, mb1;
   int rc;
   const int nkb = cdiv(K, tc::BK);
   const int64_t wtiles = (int64_t)cdiv(M, tc::BM) * nkb;
   if ((rc = make_map(&ma, W, tc::BK, tc::BM, wtiles, tc::BK * 2, tc::BK * tc::BM * 2, tc::BK,
                      tc::BM)))
     return rc;
-  if ((rc = map_kmajor(&mb, act, K, B, ld_act, 1, 0, BN))) return rc;
+  if (K0 % tc::BK) return fail(PPO_E_SHAPE, "first K source must be a multiple of 64");
+  if ((rc = map_kmajor(&mb0, act0, K0, B, ld0, 1, 0, BN))) return rc;
+  if (K0 < K && (rc = map_kmajor(&mb1, act1, K - K0, B, ld1, 1, 0, BN))) return rc;
+  if (K0 == K) mb1 = mb0;
+  const int nkb0 = (int)(K0 / tc::BK);
   const int tiles = cdiv(M, tc::BM) * cdiv(B, BN);
   // gates: >= 32 k-blocks per split (4 splits of W_xh at the paper's size: the cell kernel
   // reads 4 partials); heads: >= 8 (8 splits of the small W_o)
   const bool heads = slot == kSchedInferHeads;
   const int sp = infer_split(tiles, nkb, heads ? 8 : 32,
                              heads ? "PPO_INFER_SPLIT_HEADS" : "PPO_INFER_SPLIT");
-  tc::TileShape sh{(int)M, (int)B, nkb, 0, 0, 0, 0, 0, 1, 0};
+  tc::TileShape sh{(int)M, (int)B, nkb0, nkb - nkb0, 0, 0, 0, 0, 1, 0};
   sh.ksplit = sp;
   sh.sched = sched_counter(slot);
   const char* e = getenv("PPO_INFER_EVICT_FIRST");
@@ -394,16 +400,18 @@ int infer_gemm_bn(const char* tag, int slot, const void* W, int64_t M, int64_t K
   tc::EpiStoreF32T epi{part, M, (int)M, (int)B, M * B};
   *split_out = sp;
   constexpr int STAGES = BN == 64 ? 8 : BN == 128 ? 6 : 4;
-  return launch<BN, false, false, tc::EpiStoreF32T, STAGES>(tag, ma, ma, mb, mb, sh, epi, st,
+  return launch<BN, false, false, tc::EpiStoreF32T, STAGES>(tag, ma, ma, mb0, mb1, sh, epi, st,
                                                              true);
 }
-int infer_gemm(const char* tag, int slot, const void* W, int64_t M, int64_t K, const void* act,
-               int64_t B, int64_t ld_act, float* part, int* split_out, cudaStream_t st) {
+int infer_gemm(const char* tag, int slot, const void* W, int64_t M, int64_t K, const void* act0,
+               int64_t K0, int64_t ld0, const void* act1, int64_t ld1, int64_t B, float* part,
+               int* split_out, cudaStream_t st) {
   if (B <= 64)
-    return infer_gemm_bn<64>(tag, slot, W, M, K, act, B, ld_act, part, split_out, st);
+    return infer_gemm_bn<64>(tag, slot, W, M, K, act0, K0, ld0, act1, ld1, B, part, split_out, st);
   if (B <= 128)
-    return infer_gemm_bn<128>(tag, slot, W, M, K, act, B, ld_act, part, split_out, st);
-  return infer_gemm_bn<256>(tag, slot, W, M, K, act, B, ld_act, part, split_out, st);
+    return infer_gemm_bn<128>(tag, slot, W, M, K, act0, K0, ld0, act1, ld1, B, part, split_out,
+                              st);
+  return infer_gemm_bn<256>(tag, slot, W, M, K, act0, K0, ld0, act1, ld1, B, part, split_out, st);
 }
 
 }  // namespace
@@ -414,14 +422,17 @@ size_t tc_infer_tiled_offset_heads(const Shape& s) {
 size_t tc_infer_tiled_elems(const Shape& s) {
   return tc_infer_tiled_offset_heads(s) + (size_t)cdiv(s.A, tc::BM) * cdiv(s.Ko, tc::BK) * tc::BM * tc::BK;
 }
-int tc_infer_gates(const Shape& s, int64_t B, const void* wt, const void* xh, float* part,
-                   int* split, cudaStream_t st) {
-  return infer_gemm("infer_gates", kSchedInferGates, wt, s.G4, s.Kx, xh, B, s.Kx, part, split, st);
+int tc_infer_gates(const Shape& s, int64_t B, const void* wt, const void* x, const void* ho,
+                   float* part, int* split, cudaStream_t st) {
+  // [x | h | 1 | 0] = x [B][D] straight from the caller, then the state buffer HO [B][Ko]
+  return infer_gemm("infer_gates", kSchedInferGates, wt, s.G4, s.Kx, x, s.D, s.D, ho, s.Ko, B,
+                    part, split, st);
 }
 int tc_infer_heads(const Shape& s, int64_t B, const void* wt, const void* ho, float* part,
                    int* split, cudaStream_t st) {
   const __nv_bfloat16* wo = static_cast<const __nv_bfloat16*>(wt) + tc_infer_tiled_offset_heads(s);
-  return infer_gemm("infer_heads", kSchedInferHeads, wo, s.A, s.Ko, ho, B, s.Ko, part, split, st);
+  return infer_gemm("infer_heads", kSchedInferHeads, wo, s.A, s.Ko, ho, s.Ko, s.Ko, nullptr, 0, B,
+                    part, split, st);
 }
 int tc_infer_max_split() { return kMaxSplitK; }
 

@@ -40,6 +40,9 @@ class PolicyServer:
         # the step counter lives on the device (ppo_infer_step_ctr): a captured CUDA graph of
         # steps draws fresh noise on every replay
         self.step_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+        # the workspace's bf16 copy of h is current only after a step (reset() or an
+        # external change of h invalidates it)
+        self.state_current = False
 
     def load(self, weights: torch.Tensor, stream=None):
         """a published bf16 parameter vector (PPOOptimizer.shadow layout) -> tiled copy"""
@@ -53,12 +56,15 @@ class PolicyServer:
         if step is not None:
             self.step_ctr.fill_(step)
             self.t = step
+        self.state_current = False
 
     def step(self, x: torch.Tensor, avail: torch.Tensor, want_out: bool = True, stream=None):
         """x [B][D] bf16, avail [B][n_primary] uint8 -> (act, head_on, logp, value); the
         recurrent state advances in place."""
         L.ppo_infer_step_ctr(self.dims, self.wt, x, self.h, self.c, avail, self.head_table,
                              self.seed, self.step_ctr, self.B, self.ws, self.act, self.head_on,
-                             self.logp, self.value, self.out if want_out else None, stream)
+                             self.logp, self.value, self.out if want_out else None, stream,
+                             flags=L.PPO_INFER_STATE_CURRENT if self.state_current else 0)
+        self.state_current = True
         self.t += 1   # host mirror (eager calls only; graph replays advance step_ctr alone)
         return self.act, self.head_on, self.logp, self.value
