@@ -113,12 +113,33 @@ __device__ __forceinline__ void cell_fwd(float zi, float zf, float zg, float zo,
   h = o * tanhf(c);
 }
 
+// The tensor-core path's cell: tanh on the SFU (tanh.approx.f32, max rel. error ~2^-11, below
+// the bf16 storage of the gates and h) and sigmoid(z) = 1/2 + tanh(z/2)/2.  The fp32 reference
+// path and the inference step keep the accurate functions above.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sigmoid_fast(float z) { return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f); }
+__device__ __forceinline__ void cell_fwd_fast(float zi, float zf, float zg, float zo,
+                                              float c_prev, float& i, float& f, float& g,
+                                              float& o, float& c, float& h) {
+  i = sigmoid_fast(zi);
+  f = sigmoid_fast(zf);
+  g = tanh_fast(zg);
+  o = sigmoid_fast(zo);
+  c = f * c_prev + i * g;
+  h = o * tanh_fast(c);
+}
+
 // Backward through one cell: dh (total), carried dc, saved gates, c_t, c_{t-1}
 // -> pre-activation grads dz (i,f,g,o) and the carry dc_next = dc * f.
 __device__ __forceinline__ void cell_bwd(float dh, float dc_carry, float i, float f, float g,
                                          float o, float c, float c_prev, float& dzi, float& dzf,
-                                         float& dzg, float& dzo, float& dc_next) {
-  float tc = tanhf(c);
+                                         float& dzg, float& dzo, float& dc_next,
+                                         bool fast = false) {
+  float tc = fast ? tanh_fast(c) : tanhf(c);
   float dc = dc_carry + dh * o * (1.0f - tc * tc);
   float d_o = dh * tc;
   float di = dc * g;

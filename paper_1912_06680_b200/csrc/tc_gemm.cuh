@@ -905,6 +905,7 @@ struct EpiLstmFwd {
   float* c_out;           // C[t+1] [B][H]
   __nv_bfloat16* gates;   // G[t]   [B][4H], interleaved like the accumulator columns
   int B, H;
+  int fast;               // 1: SFU tanh/sigmoid (cell_fwd_fast)
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int split) const {
@@ -926,7 +927,8 @@ struct EpiLstmFwd {
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         float i, f, g, o;
-        cell_fwd(zi[e], zf[e], zg[e], zo[e], cp[e], i, f, g, o, c[e], h[e]);
+        if (fast) cell_fwd_fast(zi[e], zf[e], zg[e], zo[e], cp[e], i, f, g, o, c[e], h[e]);
+        else cell_fwd(zi[e], zf[e], zg[e], zo[e], cp[e], i, f, g, o, c[e], h[e]);
         zi[e] = i;
         zf[e] = f;
         zg[e] = g;
@@ -982,6 +984,7 @@ struct EpiLstmBwd {
   const float* c_prev;    // C[t]
   float* dc;              // [B][H] carry (in/out)
   int B, H;
+  int fast;               // 1: SFU tanh for tanh(c_t)
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int split) const {
@@ -1026,7 +1029,7 @@ struct EpiLstmBwd {
             const int e = 2 * w + h;
             float a, b, c, d, dn;
             cell_bwd(dh[e], dcv[e], z[0][h], z[1][h], z[2][h], z[3][h], ct[e], cp[e], a, b, c,
-                     d, dn);
+                     d, dn, fast != 0);
             z[0][h] = a;
             z[1][h] = b;
             z[2][h] = c;

@@ -173,6 +173,14 @@ bool use_pair(const char* kind, bool def) {
   return strcmp(e, "pair") == 0;
 }
 
+// Experiment knob: PPO_FAST_CELL=1 puts tanh/sigmoid of the fused LSTM epilogues on the SFU
+// (tanh.approx).  Off by default: -3% forward time, but the full-width bf16 weight gradient
+// drifts past the 2e-2 parity bar (0.022 on test_full_width_bf16).
+int fast_cell() {
+  const char* e = getenv("PPO_FAST_CELL");
+  return e ? atoi(e) != 0 : 0;
+}
+
 struct WsPtrs {
   __nv_bfloat16* xh;
   __nv_bfloat16* g;
@@ -199,9 +207,15 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
   CUtensorMap mA, mB;
   if ((rc = map_kmajor(&mA, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, tc::BM))) return rc;
   const bool pair = use_pair("FWD", true);
-  CUtensorMap mB1;
+  // experiment: PPO_VARIANT_FWD=pair2 -> 512x256 pair tiles (256 A rows per CTA, one
+  // 512-column accumulator): 25% less operand traffic per FLOP (the SMs clock ~15% higher
+  // under the power cap) but the fused epilogue is no longer overlapped: 15-25% slower
+  const char* vf = getenv("PPO_VARIANT_FWD");
+  const bool pair2 = vf && strcmp(vf, "pair2") == 0;
+  CUtensorMap mB1, mA2;
   if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 128))) return rc;
   if ((rc = map_kmajor(&mB1, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
+  if (pair2 && (rc = map_kmajor(&mA2, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, 256))) return rc;
   for (int t = 0; t < s.T; ++t) {
     if (x_ready && x_ready[t]) PPO_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready[t], 0));
     tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8, 1};
@@ -209,9 +223,12 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     sh.sched = sched_counter(kSchedFwd);
     tc::TileShape sh1 = sh;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
-                       P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
-    rc = pair ? launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st)
-              : launch<256, false, false>("lstm_fwd_step", mA, mA, mB1, mB1, sh1, epi, st);
+                       P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H,
+                       fast_cell()};
+    rc = pair2  ? launch2<false, false, tc::EpiLstmFwd, 2>("lstm_fwd_step", mA2, mA2, mB, mB, sh,
+                                                           epi, st)
+         : pair ? launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st)
+                : launch<256, false, false>("lstm_fwd_step", mA, mA, mB1, mB1, sh1, epi, st);
     if (rc) return rc;
   }
   // heads: y = [h_t | 1] W_o_aug^T over all T*B rows (XH slots 1..T, columns D..D+Ko).
@@ -259,7 +276,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     raster(sh, "BWD", 8, 1);
     sh.sched = sched_counter(kSchedBwd);
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
-                       (int)B, (int)s.H};
+                       (int)B, (int)s.H, fast_cell()};
     tc::TileShape sh1 = sh;
     rc = pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
               : launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh1, epi, st);
