@@ -230,3 +230,14 @@ def test_input_grad(precision, H, D, B, tol):
     ref = oracle.lstm_input_grad(case["params"]["Wx"], case["inter"]["dz"])
     e = normwise(dx.cpu().numpy(), ref)
     assert e < tol, e
+
+
+@pytest.mark.parametrize("precision,T,B", [("fp32", 4, 64), ("bf16", 4, 64), ("bf16", 1, 256),
+                                           ("fp32", 1, 256)])
+def test_other_unroll_lengths(precision, T, B):
+    """TBPTT over T != 16 (the paper's 16, is a parameter): T = 4, and T = 1 where the
+    backward has only the last step (no recurrent term)."""
+    cfg = synth.Config(H=128, D=128, B=B, T=T)
+    case = make_case(cfg, 12, pad_frac=0.2, wo_scale=10.0)
+    tol = 1e-4 if precision == "fp32" else 2e-2
+    _check_step(case, cfg, precision, tol, tol)
