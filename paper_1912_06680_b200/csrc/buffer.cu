@@ -179,7 +179,7 @@ __device__ __forceinline__ void store8(float* p, const float (&v)[8]) {   // 32-
   reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-__global__ void __launch_bounds__(128) reward_gae_kernel(
+__global__ void __launch_bounds__(128, 4) reward_gae_kernel(
     const float* __restrict__ shaped, const float* __restrict__ win,
     const int32_t* __restrict__ step0, int64_t G, int64_t L, const float* __restrict__ val,
     const uint8_t* __restrict__ done, ppo_reward_cfg cfg, const double* __restrict__ stats,
