@@ -10,6 +10,8 @@
 
 #include "kernels.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace ppo {
 
 static thread_local std::string g_err;
@@ -53,6 +55,7 @@ Prof& prof() {
 }  // namespace
 
 void prof_begin(const char* tag, cudaStream_t s) {
+  nvtxRangePushA(tag);   // NVTX range per library launch (no-op without an attached tool)
   Prof& P = prof();
   if (!P.on) return;
   std::lock_guard<std::mutex> g(P.mu);
@@ -62,6 +65,7 @@ void prof_begin(const char* tag, cudaStream_t s) {
   P.open.push_back((int)P.recs.size() - 1);
 }
 void prof_end(cudaStream_t s) {
+  nvtxRangePop();
   Prof& P = prof();
   if (!P.on) return;
   std::lock_guard<std::mutex> g(P.mu);

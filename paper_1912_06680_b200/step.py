@@ -95,6 +95,38 @@ class PPOOptimizer:
                             stream)
         return out
 
+    # ---------------------------------------------------------------- checkpoint / resume
+    def state_dict(self) -> dict:
+        """fp32 parameters and Adam moments in the canonical layout (gate blocks [i;f;g;o],
+        separate W_x, W_h, b, W_o, b_o: the oracle's), the Adam step t and the shapes; host
+        tensors, loadable into an optimizer of the same dims."""
+        torch.cuda.synchronize(self.device)
+        cpu = lambda d: {k: v.cpu() for k, v in d.items()}  # noqa: E731
+        return {"format": "ppo5-ckpt-1", "t": self.t, "D": self.D, "H": self.H,
+                "head_sizes": list(self.head_sizes), "aux": list(self.aux),
+                "params": cpu(self.unpack(self.theta)), "m": cpu(self.unpack(self.m)),
+                "v": cpu(self.unpack(self.v))}
+
+    def load_state_dict(self, sd: dict, stream=None):
+        if sd.get("format") != "ppo5-ckpt-1":
+            raise ValueError("not a ppo5 checkpoint")
+        if (sd["D"], sd["H"], tuple(sd["head_sizes"]), tuple(sd["aux"])) != \
+                (self.D, self.H, self.head_sizes, self.aux):
+            raise ValueError("checkpoint shapes differ from this optimizer's")
+        names = ("Wx", "Wh", "b", "Wo", "bo")
+        for key, flat in (("params", self.theta), ("m", self.m), ("v", self.v)):
+            t = [sd[key][k].to(self.device, torch.float32).contiguous() for k in names]
+            L.ppo_pack_params(self.dims, *t, flat, stream)
+        if self.bf16:
+            L.ppo_cast_bf16(self.theta, self.shadow, stream)
+        self.t = int(sd["t"])
+
+    def save(self, path: str):
+        torch.save(self.state_dict(), path)
+
+    def load(self, path: str):
+        self.load_state_dict(torch.load(path, map_location="cpu"))
+
     # ---------------------------------------------------------------- zero-copy inputs
     def select_ws(self, i: int):
         """make workspace i the one the next forward/backward use"""

@@ -241,3 +241,28 @@ def test_other_unroll_lengths(precision, T, B):
     case = make_case(cfg, 12, pad_frac=0.2, wo_scale=10.0)
     tol = 1e-4 if precision == "fp32" else 2e-2
     _check_step(case, cfg, precision, tol, tol)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_checkpoint_resume(tmp_path, precision):
+    """Save after two steps, resume into a fresh optimizer: the third step is bit-identical
+    to the uninterrupted run (params, Adam moments and t round-trip through the canonical
+    layout)."""
+    from paper_1912_06680_b200 import PPOOptimizer
+    cfg = synth.Config(H=128, D=256, B=32)
+    case = make_case(cfg, 21, pad_frac=0.1, wo_scale=10.0)
+    batch = device_batch(case, precision == "bf16")
+    a = PPOOptimizer(cfg.D, cfg.H, cfg.B, cfg.T, cfg.head_sizes, precision=precision)
+    load_params(a, case["params"])
+    a.step(batch)
+    a.step(batch)
+    path = str(tmp_path / "ckpt.pt")
+    a.save(path)
+    b = PPOOptimizer(cfg.D, cfg.H, cfg.B, cfg.T, cfg.head_sizes, precision=precision)
+    b.load(path)
+    assert b.t == 2
+    assert torch.equal(a.theta, b.theta) and torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
+    a.step(batch)
+    b.step(batch)
+    torch.cuda.synchronize()
+    assert torch.equal(a.theta, b.theta) and torch.equal(a.grad, b.grad)
