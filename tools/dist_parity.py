@@ -1,0 +1,71 @@
+"""Data-parallel equivalence on real GPUs over NCCL (SURVEY §4b "DP equivalence"): N ranks
+each take B/N sequences of one seeded minibatch, the library averages the gradients
+(grad_allreduce, ncclAvg) and applies Adam; rank 0 also runs the whole batch alone on its
+GPU.  Both gradients and updated parameters must agree (fp32 path: 1e-5 normwise -- the
+sum order differs; bf16 path: 2e-2).
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \\
+        tools/dist_parity.py --precision fp32
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+from gpu_util import device_batch, load_params, make_case  # noqa: E402
+from paper_1912_06680_b200 import PPOOptimizer  # noqa: E402
+from paper_1912_06680_b200 import dist as pdist  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--precision", default="fp32")
+a = ap.parse_args()
+rank, world, local = pdist.env()
+torch.cuda.set_device(local)
+dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+dev = torch.device("cuda", local)
+cfg = synth.Config(H=128, D=256, B=64)
+case = make_case(cfg, 5, pad_frac=0.2, wo_scale=20.0)   # same seed on every rank
+full = device_batch(case, a.precision == "bf16", device=dev)
+Bs, Rs = cfg.B // world, case["ro"]["r"].shape[0] // world
+sl, rs = slice(rank * Bs, (rank + 1) * Bs), slice(rank * Rs, (rank + 1) * Rs)
+shard = {k: (v[:, sl] if k in ("x", "act", "head_on", "avail", "valid", "logp_old")
+             else v[sl] if k in ("h0", "c0") else v[rs]).contiguous() for k, v in full.items()}
+comm = pdist.make_comm(dev)
+opt = PPOOptimizer(cfg.D, cfg.H, Bs, cfg.T, cfg.head_sizes, precision=a.precision, device=dev,
+                   comm=comm, n_buckets=4)
+load_params(opt, case["params"], device=dev)
+# each rank's loss uses its local denominator T*Bs (DESIGN Q9), so the average of the N
+# gradients is the gradient of the whole batch over T*B
+opt.step(shard)
+torch.cuda.synchronize()
+res = {}
+if rank == 0:
+    ref = PPOOptimizer(cfg.D, cfg.H, cfg.B, cfg.T, cfg.head_sizes, precision=a.precision,
+                       device=dev)
+    load_params(ref, case["params"], device=dev)
+    ref.step(full)
+    torch.cuda.synchronize()
+    nw = lambda x, y: float((x - y).norm() / y.norm())  # noqa: E731
+    res = {"world": world, "precision": a.precision, "grad_err": nw(opt.grad, ref.grad),
+           "theta_err": nw(opt.theta, ref.theta)}
+    tol = 1e-5 if a.precision == "fp32" else 2e-2
+    res["ok"] = res["grad_err"] < tol
+    print(json.dumps(res), flush=True)
+# every rank holds identical parameters after the averaged update
+th = opt.theta.clone()
+dist.broadcast(th, 0)
+same = bool(torch.equal(th, opt.theta))
+flag = torch.tensor([1 if same else 0], device=dev)
+dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+if rank == 0:
+    print(json.dumps({"replicas_identical": bool(flag.item())}), flush=True)
+from paper_1912_06680_b200 import _lib as L  # noqa: E402
+L.comm_destroy(comm)
+dist.destroy_process_group()
