@@ -302,7 +302,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
       const int kb0 = (int)((int64_t)nkb_all * c / nchunks);
       const int kb1 = (int)((int64_t)nkb_all * (c + 1) / nchunks);
       tc::TileShape sh{(int)s.G4, (int)s.Kx, kb1 - kb0, 0, 0, 0, 0, 0, 8, 0};
-      raster(sh, "WGRAD", 8, 0);
+      raster(sh, "WGRAD", 8, 1);   // n8: A/B in the step 2-3% faster than m8 (current kernels)
       sh.kb_off = kb0;
       sh.sched = sched_counter(kSchedWgrad);
       tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx, 0, c > 0 ? 1 : 0};
