@@ -781,6 +781,261 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- 2 CTA pairs, B multicast
+// Cluster of 4 = two CTA pairs stacked along M (m-tiles 2u and 2u+1, the same N tile).  Each
+// pair runs the pair kernel's 256x256 tile (K-major A and B, double-buffered accumulators),
+// but the two pairs share the B operand: every CTA loads 64 of its pair-half's 128 B rows and
+// multicasts them to the same-rank CTA of the other pair, so the L2 supplies each B tile once
+// per cluster (25% fewer L2->SM operand bytes per FLOP).  Completion is tracked per CTA (plain
+// multicast: each destination's own full barrier); the follower of each pair forwards its
+// stage completion to the pair leader, whose MMA waits for both; a stage is released when
+// both pairs' MMAs committed it (commit multicast to all 4 CTAs, count 2).
+template <int STAGES>
+struct SmemMC {
+  static constexpr int A_BYTES = BM * BK * 2;          // this CTA's 128 A rows
+  static constexpr int B_BYTES = 128 * BK * 2;         // this CTA's 128-row N-half of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (3 * STAGES + 4 + 2 * kSchedDepth) * 8 + 32 + 1024;
+};
+__device__ __forceinline__ void tma_load_3d_mc(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                               int c0, int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
+// 2-SM multicast: data lands at the same offset in every CTA of mask; complete_tx is counted on
+// the mbarrier at bar's offset in each destination CTA's pair leader (bar: a cluster address)
+__device__ __forceinline__ void tma_load_3d_pair_mc(const CUtensorMap* map, uint32_t bar_cluster,
+                                                    void* dst, int c0, int c1, int c2,
+                                                    uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+template <int STAGES, class Epi>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_gemm2mc_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap tb0,
+                      const TileShape sh, const Epi epi) {
+  constexpr int BN = 256, TM = 2 * BM;     // per-pair tile 256 x 256
+  using L = SmemMC<STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);   // this CTA's bytes
+  uint64_t* fullP = full + STAGES;                                   // leader: follower's done
+  uint64_t* empty = fullP + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* sfull = tempty + 2;
+  uint64_t* sempty = sfull + kSchedDepth;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + kSchedDepth);
+  int* ring = reinterpret_cast<int*>(tslot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pair = rank >> 1, prank = rank & 1, pl = rank & ~1u;
+  const int nclusters = gridDim.x >> 2;
+  const int num_m = (sh.M + TM - 1) / TM;          // 256-row tiles
+  const int num_mu = (num_m + 1) / 2;              // units: pairs of m-tiles
+  const int num_n = (sh.N + BN - 1) / BN;
+  const int nunits = num_mu * num_n;
+  const int nkb = sh.nkb0;
+
+  if (threadIdx.x == 0) {
+    prefetch_map(&ta0);
+    prefetch_map(&tb0);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);    // pair leader: one arrive.expect_tx for both CTAs' bytes
+      mbar_init(&fullP[s], 1);   // (unused with 2-SM multicast)
+      mbar_init(&empty[s], 2);   // one commit from each pair's MMA
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs of the pair (leader's copy)
+    }
+    for (int s = 0; s < kSchedDepth; ++s) {
+      mbar_init(&sfull[s], 1);
+      // rank 0's copy: rank0 MMA + 4 epi; ranks 1,3 producer + 4 epi; rank 2 producer + MMA
+      // + 4 epi
+      mbar_init(&sempty[s], 21);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t sempty_c0 = mapa_shared(smem_u32(&sempty[0]), 0);
+
+  // reads the next unit from this CTA's ring (rank 0's own copy, the others' written remotely)
+  auto next_unit = [&](int& sslot, uint32_t& sphase, bool arrive) -> int {
+    if (rank == 0) mbar_wait(&sfull[sslot], sphase);
+    else mbar_wait_cluster(&sfull[sslot], sphase);
+    const int u = ring[sslot];
+    if (arrive) mbar_arrive_cluster(sempty_c0 + 8 * sslot);
+    if (++sslot == kSchedDepth) {
+      sslot = 0;
+      sphase ^= 1;
+    }
+    return u;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer (all 4 CTAs); rank 0 also fetches units ==========
+      int stage = 0;
+      uint32_t phase = 0;
+      int sslot = 0;
+      uint32_t sphase = 0;
+      const uint16_t bmask = (uint16_t)((1u << prank) | (1u << (prank + 2)));
+      while (true) {
+        int unit;
+        if (rank == 0) {
+          mbar_wait(&sempty[sslot], sphase ^ 1);
+          unit = sched_fetch(sh.sched, nunits, nclusters);
+          ring[sslot] = unit;
+          mbar_arrive(&sfull[sslot]);
+#pragma unroll
+          for (uint32_t r = 1; r < 4; ++r) {
+            st_shared_cluster(mapa_shared(smem_u32(&ring[sslot]), r), unit);
+            mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[sslot]), r));
+          }
+          if (++sslot == kSchedDepth) {
+            sslot = 0;
+            sphase ^= 1;
+          }
+        } else {
+          unit = next_unit(sslot, sphase, true);
+        }
+        if (unit >= nunits) break;
+        int mu, nb;
+        tile_coords(unit, num_mu, num_n, sh.group, sh.group_n, mu, nb);
+        const int m_row = (2 * mu + (int)pair) * TM + (int)prank * BM;
+        const int n_row = nb * BN + (int)prank * 128 + (int)pair * 64;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fbar = mapa_shared(smem_u32(&full[stage]), pl);
+          if (prank == 0) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
+          const int kk = (kb + sh.kb_off) * BK;
+          tma_load_3d_pair(&ta0, fbar, sA + stage * L::A_BYTES, kk, m_row, sh.za0);
+          tma_load_3d_pair_mc(&tb0, fbar, sB + stage * L::B_BYTES + pair * (64 * 128), kk,
+                              n_row, sh.zb0, bmask);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int sslot = 0;
+    uint32_t sphase = 0;
+    int stage = 0;
+    uint32_t phase = 0;
+    if (prank == 0) {
+      // ===================== MMA issuer (pair leaders) =====================
+      constexpr uint32_t idesc = idesc_bf16(2 * BM, BN, false, false);
+      const uint64_t a_desc0 = sdesc(smem_u32(sA), 16, 1024);
+      const uint64_t b_desc0 = sdesc(smem_u32(sB), 16, 1024);
+      constexpr uint64_t a_k = 32 >> 4, b_k = 32 >> 4;
+      const uint16_t pmask = (uint16_t)(0x3u << (2 * pair));
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      while (true) {
+        const int unit = next_unit(sslot, sphase, lane == 0);
+        __syncwarp();
+        if (unit >= nunits) break;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (L::A_BYTES >> 4));
+          const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (L::B_BYTES >> 4));
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_pair(d_tmem, ad + k * a_k, bd + k * b_k, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_commit_mask(&empty[stage], (uint16_t)0xF);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit_mask(&tfull[acc], pmask);
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5 (all CTAs) =====================
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t tempty_pl0 = mapa_shared(smem_u32(&tempty[0]), pl);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int sslot = 0;
+    uint32_t sphase = 0;
+    while (true) {
+      const int unit = next_unit(sslot, sphase, lane == 0);
+      __syncwarp();
+      if (unit >= nunits) break;
+      int mu, nb;
+      tile_coords(unit, num_mu, num_n, sh.group, sh.group_n, mu, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr =
+          tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
+      epi.template apply<BN>((2 * mu + (int)pair) * TM + (int)prank * BM, nb * BN, row, taddr, 0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_pl0 + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
+                 : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- epilogues
 
 // Plain fp32 store: out[m*ldc + n] for m < M, n < N.

@@ -129,6 +129,31 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
   return PPO_OK;
 }
 
+// Two CTA pairs sharing B by multicast (cluster of 4): 512 x 256 per cluster, K-major A and B.
+template <class Epi>
+int launch2mc(const char* tag, const CUtensorMap& a0, const CUtensorMap& b0,
+              const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
+  constexpr int STAGES = 7;   // 7 x 32 KB: the two pairs release a stage only together
+  using L = tc::SmemMC<STAGES>;
+  auto kern = tc::tc_gemm2mc_kernel<STAGES, Epi>;
+  static bool configured = false;
+  if (!configured) {
+    PPO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  if (sh.nkb0 <= 0 || sh.nkb1 != 0 || sh.ksplit > 1)
+    return fail(PPO_E_SHAPE, "multicast pair kernel: one K source, no split");
+  if (!sh.sched) return fail(PPO_E_CUDA, "tile scheduler counter unavailable");
+  const int64_t num_m = (sh.M + 255) / 256;
+  const int64_t units = ((num_m + 1) / 2) * ((sh.N + 255) / 256);
+  const int clusters = (int)std::min<int64_t>(units, num_sms() / 4);
+  if (clusters <= 0) return PPO_OK;
+  ProfScope _prof(tag, st);
+  kern<<<4 * clusters, tc::kThreads, L::TOTAL, st>>>(a0, b0, sh, epi);
+  PPO_LAUNCH_CHECK("tc_gemm2mc_kernel");
+  return PPO_OK;
+}
+
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // Split-K factor in [1, kMaxSplitK] that best fills whole waves of `sms` CTAs (each split
@@ -212,10 +237,15 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
   // under the power cap) but the fused epilogue is no longer overlapped: 15-25% slower
   const char* vf = getenv("PPO_VARIANT_FWD");
   const bool pair2 = vf && strcmp(vf, "pair2") == 0;
-  CUtensorMap mB1, mA2;
+  // experiment: PPO_VARIANT_FWD=pairmc -> two CTA pairs share the weight tile by 2-SM TMA
+  // multicast (cluster of 4): the SMs clock ~10% higher (less L2->SM traffic) but the coupled
+  // pairs keep the tensor pipe only ~85% busy (ncu) -> ~8% slower in the step; off
+  const bool pairmc = vf && strcmp(vf, "pairmc") == 0;
+  CUtensorMap mB1, mA2, mBmc;
   if ((rc = map_kmajor(&mB, wxh, s.Kx, s.G4, s.Kx, 1, 0, 128))) return rc;
   if ((rc = map_kmajor(&mB1, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
   if (pair2 && (rc = map_kmajor(&mA2, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, 256))) return rc;
+  if (pairmc && (rc = map_kmajor(&mBmc, wxh, s.Kx, s.G4, s.Kx, 1, 0, 64))) return rc;
   for (int t = 0; t < s.T; ++t) {
     if (x_ready && x_ready[t]) PPO_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready[t], 0));
     tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8, 1};
@@ -225,7 +255,8 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H,
                        fast_cell()};
-    rc = pair2  ? launch2<false, false, tc::EpiLstmFwd, 2>("lstm_fwd_step", mA2, mA2, mB, mB, sh,
+    rc = pairmc ? launch2mc("lstm_fwd_step", mA, mBmc, sh, epi, st)
+         : pair2  ? launch2<false, false, tc::EpiLstmFwd, 2>("lstm_fwd_step", mA2, mA2, mB, mB, sh,
                                                            epi, st)
          : pair ? launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st)
                 : launch<256, false, false>("lstm_fwd_step", mA, mA, mB1, mB1, sh1, epi, st);
