@@ -147,8 +147,176 @@ __global__ void __launch_bounds__(256) pack_state_kernel(Shape s, int64_t B,
 // and the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
 // across lanes with a reverse shuffle scan of affine maps (oracle O2).  CH = 8 when there are
 // enough streams to fill the GPU; CH = 16 doubles the loads in flight per warp otherwise.
-template <int CH>
+template <int CH, bool PF>
 __global__ void gae_kernel(const float* __restrict__ rew, const float* __restrict__ val,
+                           const uint8_t* __restrict__ done, int64_t R, int64_t L, float gamma,
+                           float lam, int seq_T, float* __restrict__ adv, float* __restrict__ ret,
+                           bool vec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float gl = gamma * lam;
+  const int64_t spr = seq_T > 0 ? L / seq_T : 0;  // sequences per rollout
+  const int64_t nseq = R * spr;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
+    const float* rr = rew + r * L;
+    const float* vv = val + r * (L + 1);
+    const uint8_t* dd = done + r * L;
+    float carry = 0.f;
+    // Windows of <= W = 32*CH steps from the end.  Lane chunks sit on global multiples of 8
+    // steps (window starts are rounded up to them; the row's first window starts its lane 0
+    // early and masks the steps before the row), so every full chunk is 32-byte aligned in
+    // r, A, R and 8-byte aligned in d, whatever L is.  (V has row stride L + 1: shifted
+    // loads.)  Steps outside [w_start, w_end) are identities (delta 0, c 1).
+    constexpr int W = 32 * CH;
+    const int64_t g0 = r * L;
+    const int64_t sh0 = g0 & 7;
+    // window [w_start, w_end) and this lane's chunk [t0, t0 + CH) of it
+    auto window = [&](int64_t w_end, int64_t& w_start, int64_t& t0, int& i_lo, int& i_hi,
+                      bool& full) {
+      w_start = w_end - W;
+      if (w_start <= 0 && w_end + sh0 <= W) {
+        w_start = 0;
+      } else {
+        if (w_start < 8) w_start = 8;
+        w_start += (8 - ((g0 + w_start) & 7)) & 7;
+      }
+      t0 = w_start - ((g0 + w_start) & 7) + CH * lane;
+      i_lo = (int)min((int64_t)CH, max((int64_t)0, w_start - t0));
+      i_hi = (int)max((int64_t)0, min((int64_t)CH, w_end - t0));
+      full = vec && i_lo == 0 && i_hi == CH;   // vec: bases allow the alignment
+    };
+    // the next (earlier) window's r, V, d are prefetched while this one computes
+    float p_rv[CH], p_v[CH + 1];
+    uint2 p_dw[CH / 8];
+    auto prefetch = [&](int64_t t0) {
+      const float4* r4 = reinterpret_cast<const float4*>(rr + t0);
+#pragma unroll
+      for (int q = 0; q < CH / 4; ++q) {
+        const float4 a4 = __ldcs(r4 + q);
+        p_rv[4 * q] = a4.x;
+        p_rv[4 * q + 1] = a4.y;
+        p_rv[4 * q + 2] = a4.z;
+        p_rv[4 * q + 3] = a4.w;
+      }
+      load_floats<CH + 1>(vv + t0, p_v, val + R * (L + 1));
+#pragma unroll
+      for (int q = 0; q < CH / 8; ++q) p_dw[q] = __ldcs(reinterpret_cast<const uint2*>(dd + t0) + q);
+    };
+    int64_t w_end = L, w_start, t0;
+    int i_lo, i_hi;
+    bool full;
+    window(w_end, w_start, t0, i_lo, i_hi, full);
+    if (full) prefetch(t0);
+    while (w_end > 0) {
+      const int n = i_hi;     // (kept for the store path: valid steps are [i_lo, i_hi))
+      float delta[CH], cf[CH], vkeep[CH];
+      if (full) {
+        float rv[CH], v[CH + 1];
+        uint2 dw[CH / 8];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) rv[i] = p_rv[i];
+#pragma unroll
+        for (int i = 0; i <= CH; ++i) v[i] = p_v[i];
+#pragma unroll
+        for (int q = 0; q < CH / 8; ++q) dw[q] = p_dw[q];
+        const uint8_t* db = reinterpret_cast<const uint8_t*>(dw);
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const float nd = db[i] ? 0.f : 1.f;
+          delta[i] = rv[i] + gamma * nd * v[i + 1] - v[i];
+          cf[i] = gl * nd;
+          vkeep[i] = v[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          if (i >= i_lo && i < i_hi) {
+            const int64_t t = t0 + i;
+            const float nd = dd[t] ? 0.f : 1.f;
+            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vv[t];
+            cf[i] = gl * nd;
+          } else {
+            delta[i] = 0.f;
+            cf[i] = 1.f;
+          }
+        }
+      }
+      // next window: bounds now, its loads in flight during this window's scan and stores
+      const int64_t cur_t0 = t0, cur_ws = w_start;
+      const int cur_lo = i_lo;
+      const bool cur_full = full;
+      const int64_t nxt_end = w_start;
+      bool nxt_loaded = false;
+      if (nxt_end > 0) {
+        window(nxt_end, w_start, t0, i_lo, i_hi, full);
+        if (PF && full) {
+          prefetch(t0);
+          nxt_loaded = true;
+        }
+      }
+      float P = 0.f, Q = 1.f;  // A_first = P + Q * A_after
+#pragma unroll
+      for (int i = CH - 1; i >= 0; --i) {
+        P = delta[i] + cf[i] * P;
+        Q = cf[i] * Q;
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float P2 = __shfl_down_sync(0xffffffffu, P, off);
+        const float Q2 = __shfl_down_sync(0xffffffffu, Q, off);
+        if (lane + off < 32) {
+          P = P + Q * P2;
+          Q = Q * Q2;
+        }
+      }
+      const float a_first = P + Q * carry;
+      float a = __shfl_down_sync(0xffffffffu, a_first, 1);
+      if (lane == 31) a = carry;
+      float Aout[CH];
+#pragma unroll
+      for (int i = CH - 1; i >= 0; --i) {
+        a = delta[i] + cf[i] * a;
+        Aout[i] = a;
+      }
+      if (seq_T == 0 && cur_full) {
+        float Rout[CH];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) Rout[i] = Aout[i] + vkeep[i];
+        store_floats<CH>(adv + r * L + cur_t0, Aout);
+        store_floats<CH>(ret + r * L + cur_t0, Rout);
+      } else {
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          if (i >= cur_lo && i < n) {
+            const int64_t t = cur_t0 + i;
+            int64_t o;
+            if (seq_T > 0) {
+              const int64_t k = t / seq_T, tt = t - k * seq_T;
+              o = tt * nseq + r * spr + k;
+            } else {
+              o = r * L + t;
+            }
+            adv[o] = Aout[i];
+            ret[o] = Aout[i] + vv[t];
+          }
+        }
+      }
+      carry = __shfl_sync(0xffffffffu, a_first, 0);
+      (void)cur_ws;
+      (void)nxt_loaded;
+      w_end = nxt_end;
+    }
+  }
+}
+
+
+// (No-prefetch variant: fewest registers, for launches with enough warps to hide latency.)
+// One warp per rollout stream; windows of 32*CH steps from the end; each lane owns CH steps
+// and the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
+// across lanes with a reverse shuffle scan of affine maps (oracle O2).  CH = 8 when there are
+// enough streams to fill the GPU; CH = 16 doubles the loads in flight per warp otherwise.
+template <int CH>
+__global__ void gae_kernel_np(const float* __restrict__ rew, const float* __restrict__ val,
                            const uint8_t* __restrict__ done, int64_t R, int64_t L, float gamma,
                            float lam, int seq_T, float* __restrict__ adv, float* __restrict__ ret,
                            bool vec) {
@@ -1196,15 +1364,20 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
     const int64_t threads = R * 32;
     // the aligned-chunk path needs 32-byte aligned r, A, R bases and an 8-byte aligned d base
     const bool vec = aligned(rew, 32) && aligned(done, 8) && aligned(adv, 32) && aligned(ret, 32);
-    // >= 32 warps per SM (or short rows): 8-step lane chunks; fewer streams: 16-step chunks
-    // keep twice the loads in flight per warp (32-step chunks measured slower), and 2-warp
-    // blocks spread the few warps over all SMs
-    if (R >= 4736 || L <= 256)
-      gae_kernel<8><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
-                                                            seq_T, adv, ret, vec);
+    // >= 48 warps per SM (or one window per row): 8-step lane chunks, no prefetch (fewest
+    // registers, occupancy hides the latency); 32-48 warps per SM: prefetch the next window
+    // during the current one; fewer streams: 16-step chunks with prefetch (four times the
+    // loads in flight per warp; 32-step chunks measured slower) in 2-warp blocks spread over
+    // all SMs
+    if (L <= 256 || R >= 7104)
+      gae_kernel_np<8><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
+                                                               seq_T, adv, ret, vec);
+    else if (R >= 4736)
+      gae_kernel<8, true><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma,
+                                                                  lam, seq_T, adv, ret, vec);
     else
-      gae_kernel<16><<<grid_for(threads, 64), 64, 0, st>>>(rew, val, done, R, L, gamma, lam,
-                                                           seq_T, adv, ret, vec);
+      gae_kernel<16, true><<<grid_for(threads, 64), 64, 0, st>>>(rew, val, done, R, L, gamma,
+                                                                 lam, seq_T, adv, ret, vec);
     PPO_LAUNCH_CHECK("gae_kernel");
     return PPO_OK;
   }
