@@ -66,3 +66,42 @@ def test_null_pointers_rejected(lib):
     assert lib.gae_scratch_bytes(4, 256) == 0
     assert lib.gae_scratch_bytes(1, 10 ** 6) >= 16 * (10 ** 6 // 4096)
     assert lib.gae_scratch_bytes(20000, 20000) == 0  # enough streams: warp per stream
+
+
+def test_next_rows_host_checks(lib):
+    """Host-side argument checks of the §8(f) calls (no device needed)."""
+    hs = (30, 4, 189, 189, 81, 81, 81)
+    # aux heads: sizes bounded; A counts them; bad trunk weight rejected
+    d = lib.make_dims(256, 128, 16, hs, lib.PPO_PREC_BF16, (1, 5, 18), 0.01)
+    assert lib.param_layout(d).A == 656 + 24
+    with pytest.raises(lib.PPOError) as e:
+        lib.param_layout(lib.make_dims(256, 128, 16, hs, lib.PPO_PREC_BF16, (2, 5, 18), 0.01))
+    assert e.value.code == lib.PPO_E_SHAPE
+    with pytest.raises(lib.PPOError) as e:
+        lib.param_layout(lib.make_dims(256, 128, 16, hs, lib.PPO_PREC_BF16, (1, 33, 0), 0.01))
+    assert e.value.code == lib.PPO_E_SHAPE
+    with pytest.raises(lib.PPOError) as e:
+        lib.param_layout(lib.make_dims(256, 128, 16, hs, lib.PPO_PREC_BF16, (1, 5, 18), -1.0))
+    assert e.value.code == lib.PPO_E_ARG
+    # inference workspace / weights sizes are positive and grow with B
+    dims = lib.make_dims(256, 128, 1, hs)
+    assert 0 < lib.infer_ws_bytes(dims, 1) < lib.infer_ws_bytes(dims, 64)
+    assert lib.infer_weights_bytes(dims) >= 2 * (4 * 128 * (256 + 128 + 64) + 656 * (128 + 64))
+    # the inference step needs the bf16 path and non-NULL buffers
+    rc = lib._lib.ppo_infer_step(ctypes.byref(lib.make_dims(256, 128, 1, hs, lib.PPO_PREC_FP32)),
+                                 None, None, None, None, None, None, 0, 0, 60, None, 0, None, None,
+                                 None, None, None, None)
+    assert rc == lib.PPO_E_ARG
+    rc = lib._lib.ppo_infer_step(ctypes.byref(dims), None, None, None, None, None, None, 0, 0, 60,
+                                 None, 0, None, None, None, None, None, None)
+    assert rc == lib.PPO_E_ARG
+    # aux labels: L must be a multiple of seq_T
+    rc = lib._lib.ppo_aux_labels(ctypes.byref(d), 2, 250, None, None, None, None, None,
+                                 ctypes.c_float(0.999), 16, None, None)
+    assert rc == lib.PPO_E_SHAPE
+    # reward pipeline: scratch size and config checks
+    assert lib.reward_gae_scratch_bytes() > 0
+    # streamed x: slice index checked
+    rc = lib._lib.ppo_copy_x_slice(ctypes.byref(lib.make_dims(256, 128, 16, hs)), 8, 16, None, 256,
+                                   None, 0, None)
+    assert rc == lib.PPO_E_SHAPE
