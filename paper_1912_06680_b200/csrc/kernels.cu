@@ -863,27 +863,64 @@ __device__ __forceinline__ float warp_max_redux(float x) {   // sm_100a: one CRE
   asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
   return r;
 }
-// Sum 16 per-lane values over the warp by recursive halving (reduce-scatter): 31 shuffles
-// instead of 80.  Returns, in every lane, the total of value index q(lane) =
-// 8*b4 + 4*b3 + 2*b2 + b1 (b = lane bits); that total sits in lanes qlane(q), qlane(q) + 1.
-__device__ __forceinline__ float warp_sum16(float (&v)[16], int lane) {
+// Sum 16 per-lane values over the warp through a shared-memory transpose: 16 STS, 4 LDS.128,
+// 16 FADD and one SHFL (the butterfly reduce-scatter needs 16 SHFL, 30 SEL, 16 FADD).  Lane l
+// returns the total of value q = l >> 1 (so value q sits in lanes qlane(q), qlane(q) + 1).
+// sc: the warp's [16][36] scratch; row stride 36 keeps each LDS.128 phase conflict-free.
+__device__ __forceinline__ float warp_sum16(const float (&v)[16], int lane, float* sc) {
 #pragma unroll
-  for (int o = 16, n = 16; o >= 2; o >>= 1, n >>= 1) {
-    const bool up = lane & o;
-#pragma unroll
-    for (int i = 0; i < n / 2; ++i) {
-      const float send = up ? v[i] : v[i + n / 2];
-      const float keep = up ? v[i + n / 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+  for (int i = 0; i < 16; ++i) sc[i * 36 + lane] = v[i];
+  __syncwarp();
+  const float4* r = reinterpret_cast<const float4*>(sc + (lane >> 1) * 36 + (lane & 1) * 16);
+  const float4 a = r[0], b = r[1], c = r[2], d = r[3];
+  __syncwarp();                                 // scratch free for the next row
+  const float s = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w)) +
+                  (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w)));
+  return s + __shfl_xor_sync(0xffffffffu, s, 1);
 }
-__host__ __device__ __forceinline__ constexpr int qlane(int q) {
-  return ((q >> 3) & 1) * 16 + ((q >> 2) & 1) * 8 + ((q >> 1) & 1) * 4 + (q & 1) * 2;
-}
+__host__ __device__ __forceinline__ constexpr int qlane(int q) { return 2 * q; }
 }  // namespace fastloss
 
+namespace fastloss {
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// one elected lane: bulk copy (TMA, 1-D) of `bytes` into shared memory, completion counted
+// in transaction bytes on the mbarrier at `bar`
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+// one elected lane: bulk copy of `bytes` from shared memory to global (bulk async-group)
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {   // all but the newest N stores have read smem
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+constexpr int NBUF = 3;          // row buffers per warp: computing, arriving, draining
+constexpr int SCR = 16 * 36;     // per-warp transpose scratch of warp_sum16 (floats)
+}  // namespace fastloss
+
+// Each warp walks a contiguous run of rows through three shared-memory row buffers: row r+1
+// arrives by TMA bulk copy while row r is computed, and row r-1's dY drains to HBM by a TMA
+// bulk store; row r+1's metadata (actions, read flags, availability, logp_old, advantage,
+// return) is loaded into registers one row ahead.  Row r's dY is staged in its own buffer (in
+// place, once every lane holds its logits in registers).  The grid is one persistent wave
+// (SMs x MINB blocks).  Needs A % 4 == 0 and a 16-byte aligned `out` (launch_loss checks).
 template <class TD, int MINB>
 __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
     const float* __restrict__ out, const int32_t* __restrict__ act,
@@ -893,31 +930,94 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
     const float* __restrict__ aux_label, LossParams p, TD* __restrict__ dout,
     float* __restrict__ logp, float* __restrict__ partials) {
   using namespace fastloss;
+  extern __shared__ __align__(128) float lbuf[];   // [8 warps][NBUF][A], then [8][SCR]
   __shared__ float red[8][PPO_STATS];
+  __shared__ __align__(8) uint64_t mbar[8][NBUF];
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int n0 = sz(0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int A = p.A;
+  float* const wbuf = lbuf + (size_t)warp * NBUF * A;
+  float* const scr = lbuf + (size_t)8 * NBUF * A + warp * SCR;
+  const uint32_t rbytes = (uint32_t)A * 4u, obytes = (uint32_t)A * (uint32_t)sizeof(TD);
+  const uint32_t buf_s = su32(wbuf), bar_s = su32(&mbar[warp][0]);
+  const bool bstore = (obytes & 15) == 0 && (reinterpret_cast<uintptr_t>(dout) & 15) == 0;
+  // lane k < 7: head k's first logit and size
+  int offl = 0, nl = 1;
+#pragma unroll
+  for (int k = 0; k < NH; ++k)
+    if (lane == k) {
+      offl = off(k);
+      nl = sz(k);
+    }
   float acc[PPO_STATS] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   uint32_t flags = 0;
-  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.N; row += (int64_t)gridDim.x * 8) {
+  const int64_t nw = (int64_t)gridDim.x * 8, gw = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t per = (p.N + nw - 1) / nw;
+  const int64_t r_beg = min(gw * per, p.N), r_end = min(r_beg + per, p.N);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NBUF; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s + 8 * i) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (r_beg < r_end) bulk_load(buf_s, out + r_beg * A, rbytes, bar_s);
+  }
+  __syncwarp();
+  // metadata, one row ahead: per-lane pointers advance by one row per iteration
+  const int32_t* pa = act + r_beg * NH + (lane < NH ? lane : 0);
+  const uint8_t* ph = head_on + r_beg * NH + (lane < NH ? lane : 0);
+  const uint8_t* pv = avail + r_beg * n0 + (lane < n0 ? lane : 0);
+  int a_n = 0;
+  uint32_t on_n = 0, av_n = 0;
+  float w_n = 1.f, lo_n = 0.f, At_n = 0.f, Rt_n = 0.f;
+  auto meta = [&](int64_t r) {
+    a_n = lane < NH ? *pa : 0;
+    on_n = lane < NH ? *ph : 0u;
+    av_n = lane < n0 ? *pv : 0u;
+    pa += NH;
+    ph += NH;
+    pv += n0;
+    w_n = valid ? (float)valid[r] : 1.f;
+    lo_n = logp_old[r];
+    At_n = adv[r];
+    Rt_n = ret[r];
+  };
+  if (r_beg < r_end) meta(r_beg);
+  uint32_t phase = 0;                           // bit i: parity of buffer i's next completion
+  int b = 0;                                    // buffer of `row`
+  for (int64_t row = r_beg; row < r_end; ++row, b = b == NBUF - 1 ? 0 : b + 1) {
+    float* const ys = wbuf + b * A;
+    const int a_l = a_n;
+    const uint32_t on_l = on_n;
+    const uint32_t amask = __ballot_sync(FULL, av_n != 0);
+    const float w = w_n, lo = lo_n, At = At_n, Rt = Rt_n;
+    if (row + 1 < r_end) {
+      const int nb = b == NBUF - 1 ? 0 : b + 1;
+      if (lane == 0) {
+        bulk_wait_read<1>();                    // row - 2's dY store has left buffer nb
+        bulk_load(buf_s + nb * rbytes, out + (row + 1) * A, rbytes, bar_s + 8 * nb);
+      }
+      meta(row + 1);
+    }
     const float* yr = out + row * A;
-    const float* yl = yr + lane;
-    // ---- per-row metadata: lane k < 7 holds head k's action and read flag
-    const int a_l = lane < NH ? act[row * NH + lane] : 0;
-    const uint32_t on_l = lane < NH ? head_on[row * NH + lane] : 0u;
-    const uint32_t amask = __ballot_sync(FULL, lane < n0 && avail[row * n0 + (lane < n0 ? lane : 0)] != 0);
-    const float w = valid ? (float)valid[row] : 1.f;
-    const float lo = logp_old[row], At = adv[row], Rt = ret[row];
+    bar_wait(bar_s + 8 * b, (phase >> b) & 1u);
+    phase ^= 1u << b;
     // ---- the row's logits into registers (masked primary entries -> NEG).  After
     // unrolling, hd/ix/off/lim are constants: one base pointer, immediate offsets.
+    const float* yl = ys + lane;
     float y[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       bool ok = lim(s) >= 32 || lane < lim(s);
       if (hd(s) == 0) ok = ok && ((amask >> lane) & 1u);
-      y[s] = ok ? __ldcs(yl + off(hd(s)) + 32 * ix(s)) : NEG;
+      y[s] = ok ? yl[off(hd(s)) + 32 * ix(s)] : NEG;
     }
+    const float ya = lane < NH ? ys[offl + min(max(a_l, 0), nl - 1)] : 0.f;
+    const float V = ys[p.vcol];
+    __syncwarp();                               // the buffer now becomes row's dY staging
+    TD* const ds = reinterpret_cast<TD*>(ys);
+    TD* const dl = ds + lane;
+
     // ---- per-head max (one CREDUX each), then sum e and sum e*y (one SFU exp per element)
     float mx[NH], mb[NH], v[16];
 #pragma unroll
@@ -958,41 +1058,31 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
       v[k] += se2[k].x + se2[k].y;
       v[8 + k] += sey2[k].x + sey2[k].y;
     }
-    // reduce-scatter: lane of sum index q holds it; the sum-e lanes take sum e*y from lane+16
-    const float tot = warp_sum16(v, lane);
+    // lane l holds the total of value q = l >> 1; the sum-e lanes take sum e*y from lane + 16
+    const float tot = warp_sum16(v, lane, scr);
     const float toty = __shfl_xor_sync(FULL, tot, 16);
-    const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                  ((lane >> 1) & 1);
+    const int q = lane >> 1;
     float mq = NEG;
 #pragma unroll
     for (int k = 0; k < NH; ++k) mq = q == k ? mx[k] : mq;
     const bool emptyq = mq <= NEG;             // nothing allowed (empty avail)
     const float lse_q = emptyq ? 0.f : mq + lg2(tot) * LN2;
     const float H_q = emptyq ? 0.f : lse_q - toty / tot;
-    float lse[NH], Hk[NH];
-#pragma unroll
-    for (int k = 0; k < NH; ++k) {
-      lse[k] = __shfl_sync(FULL, lse_q, qlane(k));
-      Hk[k] = __shfl_sync(FULL, H_q, qlane(k));
-    }
-    // ---- log pi(a) and the entropy of the read heads: lane k takes head k
-    float lsel = 0.f, Hl = 0.f;
-    int offl = 0, nl = 1;
-#pragma unroll
-    for (int k = 0; k < NH; ++k)
-      if (lane == k) {
-        lsel = lse[k];
-        Hl = Hk[k];
-        offl = off(k);
-        nl = sz(k);
-      }
-    float ya = 0.f, lp_l = 0.f, ent_l = 0.f;
-    if (lane < NH) ya = __ldg(yr + offl + min(max(a_l, 0), nl - 1));
+    // ---- log pi(a) and the entropy of the read heads: lane k takes head k; sums over lanes
+    // 0..7 (3 butterfly levels), log pi broadcast from lane 0 (the entropy is needed there only)
+    const float lsel = __shfl_sync(FULL, lse_q, qlane(lane & 7));
+    const float Hl = __shfl_sync(FULL, H_q, qlane(lane & 7));
+    float lp_l = 0.f, ent_l = 0.f;
     if (lane < NH && on_l) {
       lp_l = ya - lsel;
       ent_l = Hl;
     }
-    const float lpi = warp_sum(lp_l), ent = warp_sum(ent_l);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      lp_l += __shfl_xor_sync(FULL, lp_l, o);
+      ent_l += __shfl_xor_sync(FULL, ent_l, o);
+    }
+    const float lpi = __shfl_sync(FULL, lp_l, 0), ent = ent_l;
     const int a0 = __shfl_sync(FULL, a_l, 0);
     if (w != 0.f) {
       if (amask == 0) flags |= 4u;
@@ -1003,22 +1093,28 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
     const float s2 = fminf(fmaxf(rho, 1.f - p.clip_eps), 1.f + p.clip_eps) * At;
     const bool unclipped = s1 <= s2;
     const float pg = -fminf(s1, s2);
-    const float V = __ldg(yr + p.vcol);
     const float vf = (V - Rt) * (V - Rt);
     const float lrow = pg + p.c_v * vf - p.c_e * ent;
     const float gpi = unclipped ? -At * rho * w * p.inv_denom : 0.f;
     const float ce = p.c_e * w * p.inv_denom;
     // ---- dL/dlogits of the read heads: d = p (ce (y - lse + H) - gpi), + gpi at the taken
-    // action (stored afterwards by lane k for head k); unread heads and masked entries 0
-    TD* dr = dout + row * A;
-    TD* dl = dr + lane;
-    float lb[NH], cek[NH], c1[NH];   // per head: exp shift, and d = p (cek y + c1) (0 if unread)
+    // action (stored afterwards by lane k for head k); unread heads and masked entries 0.
+    // Lane 2k (holding head k's lse and H) forms head k's coefficients -- exp shift lb, and
+    // d = p (cek y + c1) -- and every lane reads all seven back as smem broadcasts.
+    const uint32_t on_q = __shfl_sync(FULL, on_l, q & 7);
+    float4* const coef = reinterpret_cast<float4*>(scr);
+    if (!(lane & 1) && q < NH) {
+      const float onf = on_q != 0u ? 1.f : 0.f;
+      coef[q] = make_float4(lse_q * L2E, onf * ce, onf * (ce * (H_q - lse_q) - gpi), 0.f);
+    }
+    __syncwarp();
+    float lb[NH], cek[NH], c1[NH];
 #pragma unroll
     for (int k = 0; k < NH; ++k) {
-      const float onf = __shfl_sync(FULL, on_l, k) != 0u ? 1.f : 0.f;
-      lb[k] = lse[k] * L2E;
-      cek[k] = onf * ce;
-      c1[k] = onf * (ce * (Hk[k] - lse[k]) - gpi);
+      const float4 c = coef[k];
+      lb[k] = c.x;
+      cek[k] = c.y;
+      c1[k] = c.z;
     }
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -1040,7 +1136,7 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
       const int a = a_l;
       if (a >= 0 && a < nl && (lane != 0 || ((amask >> a) & 1u))) {
         const float pa = ex2(fmaf(ya, L2E, -lsel * L2E));
-        dr[offl + a] = from_f<TD>(pa * fmaf(ce, ya, ce * (Hl - lsel) - gpi) + gpi);
+        ds[offl + a] = from_f<TD>(pa * fmaf(ce, ya, ce * (Hl - lsel) - gpi) + gpi);
       }
     }
     // ---- NEXT-4 aux heads (as loss_kernel): logistic columns lane-parallel, rank softmax
@@ -1055,7 +1151,7 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
         const float cw = j < r0 ? p.c_win : p.c_bld;
         laux += cw * (fmaxf(z, 0.f) + log1pf(expf(-fabsf(z))) - t * z);
         const float dd = cw * wd * (1.f / (1.f + expf(-z)) - t);
-        dr[c0 + j] = from_f<TD>(j < r0 ? dd * p.win_scale : dd);
+        ds[c0 + j] = from_f<TD>(j < r0 ? dd * p.win_scale : dd);
       }
       if (p.n_rank) {
         const bool in = lane < p.n_rank;
@@ -1067,13 +1163,13 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
         const float l = m + logf(sz_);
         if (in) {
           laux += p.c_rank * (-t * (z - l));
-          dr[c0 + r0 + lane] = from_f<TD>(p.c_rank * wd * (e / sz_ * ty - t));
+          ds[c0 + r0 + lane] = from_f<TD>(p.c_rank * wd * (e / sz_ * ty - t));
         }
       }
       laux = warp_sum(laux);
     }
     if (lane == 0) {
-      dr[p.vcol] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
+      ds[p.vcol] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
       if (logp) logp[row] = lpi;
       if (w != 0.f) {
         if (!isfinite(lrow) || !isfinite(laux)) flags |= 1u;
@@ -1087,7 +1183,23 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
         acc[6] += w;
       }
     }
+    __syncwarp();
+    // ---- the staged dY row out: one TMA bulk store (its smem reads are awaited before the
+    // buffer is refilled, two rows later)
+    TD* const dr = dout + row * A;
+    if (bstore) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+      __syncwarp();
+      if (lane == 0) bulk_store(dr, buf_s + b * rbytes, obytes);
+    } else {
+      __syncwarp();
+      for (int i = lane; i < A; i += 32) dr[i] = ds[i];
+      // the next bulk load into this buffer is an async-proxy write after these generic reads
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+    }
   }
+  if (lane == 0) bulk_wait_read<0>();          // smem stays valid until every store has read it
   if (lane == 0) {
 #pragma unroll
     for (int i = 0; i < PPO_STATS; ++i) red[warp][i] = acc[i];
@@ -1392,33 +1504,56 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
   PPO_LAUNCH_CHECK("gae_long_kernel");
   return PPO_OK;
 }
+// one persistent wave (SMs x MINB blocks), two shared-memory row buffers per warp
+template <class TD, int MINB>
+static int launch_loss_fast(const LossParams& p, const float* out, const int32_t* act,
+                            const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
+                            const float* adv, const float* ret, const uint8_t* valid,
+                            const float* aux_label, void* dout, float* logp, float* partials,
+                            int& nblk, cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    PPO_CUDA_CHECK(cudaGetDevice(&dev));
+    PPO_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const size_t smem = 8 * (fastloss::NBUF * (size_t)p.A + fastloss::SCR) * sizeof(float);
+  if (smem > 227 * 1024) return fail(PPO_E_SHAPE, "loss: row too wide for the fast kernel");
+  if (smem > 48 * 1024)
+    PPO_CUDA_CHECK(cudaFuncSetAttribute(loss_fast_kernel<TD, MINB>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  nblk = std::min(PPO_LOSS_BLOCKS, sms * MINB);
+  if (const char* g = getenv("PPO_LOSS_GRID"))   // experiment knob: grid size
+    nblk = std::max(1, std::min(PPO_LOSS_BLOCKS, atoi(g)));
+  loss_fast_kernel<TD, MINB><<<nblk, 256, smem, st>>>(out, act, head_on, avail, logp_old, adv,
+                                                      ret, valid, aux_label, p, (TD*)dout, logp,
+                                                      partials);
+  PPO_LAUNCH_CHECK("loss_fast_kernel");
+  return PPO_OK;
+}
 int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t* act,
                 const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
                 const float* adv, const float* ret, const uint8_t* valid, const float* aux_label,
                 void* dout, float* logp, float* stats, cudaStream_t st) {
   const size_t smem = 8 * (size_t)p.A_pad * sizeof(float);
   float* partials = stats + PPO_STATS;
-  // the paper's head layout takes the register-resident half-warp kernel
+  int nblk = PPO_LOSS_BLOCKS;
+  // the paper's head layout takes the register-resident warp-per-row kernel
   bool fast = p.nh == fastloss::NH && p.vcol == fastloss::off(fastloss::NH);
   for (int k = 0; k <= p.nh && fast; ++k) fast = p.off[k] == fastloss::off(k);
+  // rows move by 16-byte TMA bulk copies
+  fast = fast && p.A % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   if (const char* e = getenv("PPO_LOSS_GENERIC")) fast = fast && !atoi(e);
   if (fast) {
     ProfScope _prof("loss", st);
-    const char* mb = getenv("PPO_LOSS_MINB");   // experiment knob: blocks per SM (3 or 4)
-    const bool four = mb && atoi(mb) == 4;
-    if (bf16 && four)
-      loss_fast_kernel<__nv_bfloat16, 4><<<PPO_LOSS_BLOCKS, 256, 0, st>>>(
-          out, act, head_on, avail, logp_old, adv, ret, valid, aux_label, p,
-          (__nv_bfloat16*)dout, logp, partials);
-    else if (bf16)
-      loss_fast_kernel<__nv_bfloat16, 3><<<PPO_LOSS_BLOCKS, 256, 0, st>>>(
-          out, act, head_on, avail, logp_old, adv, ret, valid, aux_label, p,
-          (__nv_bfloat16*)dout, logp, partials);
-    else
-      loss_fast_kernel<float, 3><<<PPO_LOSS_BLOCKS, 256, 0, st>>>(
-          out, act, head_on, avail, logp_old, adv, ret, valid, aux_label, p, (float*)dout, logp,
-          partials);
-    PPO_LAUNCH_CHECK("loss_fast_kernel");
+    // 2 blocks of 8 warps per SM: 126 registers and 3 row buffers per warp, no spills
+    const int rc = bf16 ? launch_loss_fast<__nv_bfloat16, 2>(p, out, act, head_on, avail,
+                                                            logp_old, adv, ret, valid, aux_label,
+                                                            dout, logp, partials, nblk, st)
+                        : launch_loss_fast<float, 2>(p, out, act, head_on, avail, logp_old, adv,
+                                                     ret, valid, aux_label, dout, logp, partials,
+                                                     nblk, st);
+    if (rc != PPO_OK) return rc;
   } else {
   ProfScope _prof("loss", st);
   if (bf16)
@@ -1432,7 +1567,7 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
   PPO_LAUNCH_CHECK("loss_kernel");
   }
   ProfScope _prof("loss_finalize", st);
-  loss_finalize_kernel<<<1, 256, 0, st>>>(partials, PPO_LOSS_BLOCKS, p.inv_denom, stats);
+  loss_finalize_kernel<<<1, 256, 0, st>>>(partials, nblk, p.inv_denom, stats);
   PPO_LAUNCH_CHECK("loss_finalize_kernel");
   return PPO_OK;
 }
