@@ -48,6 +48,10 @@ def parse():
                     help="NEXT-4: with the aux heads (win, rank, 18 buildings) and their targets")
     ap.add_argument("--dx", action="store_true",
                     help="NEXT-4: also produce dL/dx for the observation network each step")
+    ap.add_argument("--dp", choices=["nccl", "fused"], default="fused",
+                    help="N>1 gradient exchange: nccl = ncclAvg allreduce + replicated Adam; "
+                         "fused = one NVLink peer-memory kernel (reduce-scatter, Adam on 1/N, "
+                         "all-gather of theta and its bf16 shadow)")
     ap.add_argument("--infer-B", type=str, default="60,1,240,960",
                     help="--config infer: comma-separated batch sizes (first = headline)")
     ap.add_argument("--config", choices=["full", "gae", "iteration", "infer"], default="full",
@@ -215,6 +219,9 @@ def workload_config(args, n):
         "global_batch_samples": args.B * n // SEQ_PER_SAMPLE,
         "global_batch_timesteps": args.B * n * 16,
         "parallelism": f"dp{n}",
+        "dp_exchange": (None if n == 1 else
+                        "fused NVLink peer-memory reduce-scatter + Adam + all-gather"
+                        if getattr(args, "dp", "nccl") == "fused" else "NCCL allreduce (avg)"),
         "l2": "inputs larger than L2 (x alone is T*B*D*2 bytes per step)",
         "dx": bool(getattr(args, "dx", False)),
         "aux_heads": list(__import__("synth").AUX_SIZES) if getattr(args, "aux", False) else None,
@@ -541,8 +548,22 @@ def main():
     H, D, T, B = args.H, args.D, 16, args.B
     aux = synth.AUX_SIZES if args.aux else (0, 0, 0)
     cfg = synth.Config(H=H, D=D, B=B, T=T, aux=aux)
-    opt = PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16", device=device, comm=comm,
-                       n_buckets=8, n_ws=1 if args.no_e2e else 2, aux=aux)
+    mk = lambda dp: PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16",  # noqa: E731
+                                 device=device, comm=comm, n_buckets=8,
+                                 n_ws=1 if args.no_e2e else 2, aux=aux, dp=dp)
+    opt = None
+    if comm is not None and args.dp == "fused":
+        # the peer mappings (CUDA IPC) need plain cudaMalloc'd buffers; every rank must agree
+        # before the first collective step, else all fall back to the NCCL allreduce
+        try:
+            opt, ok = mk("fused"), 1.0
+        except L.PPOError as e:
+            ok = 0.0
+            print(f"[bench] fused DP exchange unavailable on rank {rank}: {e}", file=sys.stderr)
+        if -pdist.max_over_ranks(-ok, device) < 1.0:
+            opt, args.dp = None, "nccl"
+    if opt is None:
+        opt = mk("allreduce")
     prm = synth.torch_params(cfg, 0, device)          # same init on every rank
     opt.load_canonical(prm["Wx"], prm["Wh"], prm["b"], prm["Wo"], prm["bo"])
     del prm

@@ -231,6 +231,35 @@ int ppo_comm_init(const uint8_t id[PPO_COMM_ID_BYTES] /* host */, int rank, int 
 int grad_allreduce(ppo_comm* comm, float* g, size_t n, int32_t n_buckets, ppo_stream_t s);
 int ppo_comm_destroy(ppo_comm* comm);
 
+/* ---- a9+a10 fused over NVLink peer memory (SURVEY §8(e) option: reduce-scatter -> Adam on
+ * 1/N of theta -> all-gather; "averaged ... before being synchronously applied").
+ * Rank r owns the shard [r s, min(n, (r+1) s)) with s = ppo_dp_shard(n, world).  One kernel
+ * per rank reads its shard of every rank's gradient over NVLink (CUDA IPC mappings), sums it
+ * in rank order (so the average is the same bits wherever it is formed), scales by 1/world,
+ * applies a10 to its shard of theta, m and v, and stores what the forward reads into every
+ * rank's copy: the bf16 shadow when there is one (theta, m, v then stay sharded -- current on
+ * each rank's own shard only, until ppo_dp_allgather), else theta (fp32 path).  A 1-float NCCL allreduce before and after the
+ * kernel orders it against the peers' backward and next forward (stream-ordered; no spinning
+ * kernel).  The all-gathered copies are bitwise identical on all ranks. */
+#define PPO_DP_MAX_RANKS 8
+/* floats per shard (a multiple of 64) */
+size_t ppo_dp_shard(size_t n, int world);
+/* Collective, synchronous, once per comm: maps every rank's grad g [n] fp32, theta p [n] fp32
+ * and shadow p_bf16 [n] bf16 (nullable; the same on every rank) into this process.  The
+ * buffers must be cudaMalloc'd device memory (torch's default allocator qualifies; not
+ * expandable segments), 16-byte aligned, and stay allocated until ppo_comm_destroy (which
+ * closes the mappings).  world == 1: records the pointers only. */
+int ppo_dp_attach(ppo_comm* comm, float* g, float* p, uint16_t* p_bf16, size_t n);
+/* a9 + a10 for this rank's shard (same arguments and arithmetic as adam_step).  Collective:
+ * every rank calls it once per step, after its backward, on the attached buffers.  m, v:
+ * [n] fp32, 16-byte aligned; only this rank's shard is read and written. */
+int ppo_dp_adam_step(ppo_comm* comm, float* m, float* v, int64_t t, double lr, double b1,
+                     double b2, double eps, double clip_sigma, ppo_stream_t s);
+/* Collective: in-place all-gather of a sharded fp32 vector (m, v, theta before a checkpoint).
+ * buf holds world * ppo_dp_shard(n, world) floats (n = the attached length; the slack past n
+ * is scratch). */
+int ppo_dp_allgather(ppo_comm* comm, float* buf, ppo_stream_t s);
+
 /* ---- a10: Adam with the +-clip_sigma sqrt(v) clip (O10, Q3, Q4) --
  *   v <- b2 v + (1-b2) g^2;  g_c = clamp(g, +-clip_sigma sqrt(v));  m <- b1 m + (1-b1) g_c
  *   p <- p - lr sqrt(1-b2^t)/(1-b1^t) * m / (sqrt(v) + eps)

@@ -107,6 +107,11 @@ _lib_fns = dict(
     ppo_comm_init=([POINTER(c_uint8), c_int, c_int, POINTER(c_void_p)], c_int),
     grad_allreduce=([c_void_p, c_void_p, c_size_t, c_int32, c_void_p], c_int),
     ppo_comm_destroy=([c_void_p], c_int),
+    ppo_dp_shard=([c_size_t, c_int], c_size_t),
+    ppo_dp_attach=([c_void_p, c_void_p, c_void_p, c_void_p, c_size_t], c_int),
+    ppo_dp_adam_step=([c_void_p, c_void_p, c_void_p, c_int64, c_double, c_double, c_double,
+                       c_double, c_double, c_void_p], c_int),
+    ppo_dp_allgather=([c_void_p, c_void_p, c_void_p], c_int),
     adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_double,
                 c_double, c_double, c_double, c_double, c_void_p], c_int),
     ppo_sample_indices=([c_int64, c_int64, ctypes.c_uint64, ctypes.c_uint64, c_void_p, c_void_p], c_int),
@@ -369,6 +374,25 @@ def grad_allreduce(comm, g, n_buckets=1, stream=None):
 
 def comm_destroy(comm):
     _check(_lib.ppo_comm_destroy(comm))
+
+
+def dp_shard(n: int, world: int) -> int:
+    """floats per rank shard of the fused a9+a10 path (a multiple of 64)"""
+    return int(_lib.ppo_dp_shard(n, world))
+
+
+def dp_attach(comm, g, p, p_bf16, n: int):
+    """collective: map every rank's grad / theta / shadow for ppo_dp_adam_step"""
+    _check(_lib.ppo_dp_attach(comm, _p(g), _p(p), _p(p_bf16), n))
+
+
+def dp_adam_step(comm, m, v, t, lr, b1, b2, eps, clip_sigma, stream=None):
+    _check(_lib.ppo_dp_adam_step(comm, _p(m), _p(v), t, lr, b1, b2, eps, clip_sigma,
+                                 _s(stream)))
+
+
+def dp_allgather(comm, buf, stream=None):
+    _check(_lib.ppo_dp_allgather(comm, _p(buf), _s(stream)))
 
 
 def prof_start():

@@ -1,15 +1,33 @@
 // comm.cu -- a9: data-parallel gradient average ("Gradients are averaged across the
 // pool using NCCL2 allreduce before being synchronously applied").  libppo5 owns its NCCL
 // communicator; the unique id travels over the caller's torch process group.
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <nccl.h>
 
 #include <string>
+#include <vector>
 
 #include "common.cuh"
+#include "kernels.cuh"
+
+// a9+a10 over NVLink peer memory (SURVEY §8(e) option): the buffers every rank's fused
+// kernel reads or writes on its peers, mapped through CUDA IPC by ppo_dp_attach.
+struct DpPeers {
+  const float* g[PPO_DP_MAX_RANKS];
+  float* p[PPO_DP_MAX_RANKS];
+  __nv_bfloat16* pb[PPO_DP_MAX_RANKS];
+};
 
 struct ppo_comm {
   ncclComm_t comm;
   int rank, world;
+  // ppo_dp_attach state
+  bool attached = false;
+  size_t n = 0;
+  DpPeers peers{};
+  std::vector<void*> mapped;   // IPC mappings to close
+  float* sync = nullptr;       // 1-float device scratch for the stream-ordered barriers
 };
 
 namespace {
@@ -69,10 +87,245 @@ int grad_allreduce(ppo_comm* c, float* g, size_t n, int32_t n_buckets, ppo_strea
 
 int ppo_comm_destroy(ppo_comm* c) {
   if (!c) return PPO_OK;
+  for (void* m : c->mapped) cudaIpcCloseMemHandle(m);
+  if (c->sync) cudaFree(c->sync);
   ncclResult_t r = ncclCommDestroy(c->comm);
   delete c;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return PPO_OK;
+}
+
+size_t ppo_dp_shard(size_t n, int world) {
+  if (world < 1) return 0;
+  const size_t per = (n + (size_t)world - 1) / (size_t)world;
+  return (per + 63) / 64 * 64;
+}
+
+namespace {
+using GetRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+// base of the allocation holding ptr (IPC handles name whole cudaMalloc allocations)
+int alloc_base(const void* ptr, char** base) {
+  static GetRangeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    PPO_CUDA_CHECK(cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000,
+                                                    cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f)
+      return ppo::fail(PPO_E_CUDA, "cuMemGetAddressRange entry point not found");
+    fn = reinterpret_cast<GetRangeFn>(f);
+  }
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return ppo::fail(PPO_E_ARG, "pointer is not device memory from cudaMalloc");
+  *base = reinterpret_cast<char*>(b);
+  return PPO_OK;
+}
+
+struct IpcRecord {          // what one rank publishes for one buffer
+  cudaIpcMemHandle_t h;
+  uint64_t off;
+  uint64_t present;
+};
+
+// a9 + a10 on the rank's shard: peers' grads in, the updated shard out to every rank
+__global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int rank,
+                                                      size_t lo, size_t hi, float* __restrict__ m,
+                                                      float* __restrict__ v, ppo::AdamParams ap,
+                                                      float inv_world) {
+  const float alpha = ap.alpha, b1 = ap.b1, b2 = ap.b2, omb1 = ap.omb1, omb2 = ap.omb2;
+  const float eps = ap.eps, clip = ap.clip;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t lo4 = lo / 4, hi4 = hi / 4;           // lo is a multiple of 64
+  auto adam1 = [&](float gi, float& pi, float& mi, float& vi) {
+    vi = b2 * vi + omb2 * gi * gi;
+    const float sv = sqrtf(vi);
+    const float gc = clip > 0.f ? fminf(fmaxf(gi, -clip * sv), clip * sv) : gi;
+    mi = b1 * mi + omb1 * gc;
+    pi = pi - alpha * mi / (sv + eps);
+  };
+  for (size_t i = lo4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hi4; i += stride) {
+    // g = (1/N) sum over ranks in rank order: the same bits on every rank's shard owner
+    float4 gs = reinterpret_cast<const float4*>(pe.g[0])[i];
+    for (int j = 1; j < world; ++j) {
+      const float4 gj = reinterpret_cast<const float4*>(pe.g[j])[i];
+      gs.x += gj.x;
+      gs.y += gj.y;
+      gs.z += gj.z;
+      gs.w += gj.w;
+    }
+    float4 pp = reinterpret_cast<const float4*>(pe.p[rank])[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    adam1(gs.x * inv_world, pp.x, mm.x, vv.x);
+    adam1(gs.y * inv_world, pp.y, mm.y, vv.y);
+    adam1(gs.z * inv_world, pp.z, mm.z, vv.z);
+    adam1(gs.w * inv_world, pp.w, mm.w, vv.w);
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    uint2 u;
+    if (pe.pb[rank]) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(pp.x, pp.y), b = __floats2bfloat162_rn(pp.z, pp.w);
+      u.x = *reinterpret_cast<uint32_t*>(&a);
+      u.y = *reinterpret_cast<uint32_t*>(&b);
+    }
+    // all-gather over NVLink of what the forward reads: the bf16 shadow when there is one
+    // (theta then stays sharded like m, v), else theta itself
+    if (pe.pb[rank]) {
+      reinterpret_cast<float4*>(pe.p[rank])[i] = pp;
+      for (int j = 0; j < world; ++j) reinterpret_cast<uint2*>(pe.pb[j])[i] = u;
+    } else {
+      for (int j = 0; j < world; ++j) reinterpret_cast<float4*>(pe.p[j])[i] = pp;
+    }
+  }
+  // scalar tail (n % 4) on the last shard
+  for (size_t i = hi4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hi; i += stride) {
+    float gi = pe.g[0][i];
+    for (int j = 1; j < world; ++j) gi += pe.g[j][i];
+    float pi = pe.p[rank][i], mi = m[i], vi = v[i];
+    adam1(gi * inv_world, pi, mi, vi);
+    m[i] = mi;
+    v[i] = vi;
+    if (pe.pb[rank]) {
+      pe.p[rank][i] = pi;
+      for (int j = 0; j < world; ++j) pe.pb[j][i] = __float2bfloat16_rn(pi);
+    } else {
+      for (int j = 0; j < world; ++j) pe.p[j][i] = pi;
+    }
+  }
+  __threadfence_system();
+}
+
+int barrier(ppo_comm* c, cudaStream_t st) {   // stream-ordered: a 1-float NCCL allreduce
+  ncclResult_t r = ncclAllReduce(c->sync, c->sync, 1, ncclFloat32, ncclSum, c->comm, st);
+  return r == ncclSuccess ? PPO_OK : nccl_fail(r, "ncclAllReduce (barrier)");
+}
+}  // namespace
+
+int ppo_dp_attach(ppo_comm* c, float* g, float* p, uint16_t* p_bf16, size_t n) {
+  if (!c) return ppo::fail(PPO_E_ARG, "comm is NULL");
+  if (!g || !p) return ppo::fail(PPO_E_ARG, "g or p is NULL");
+  if (c->attached) return ppo::fail(PPO_E_ARG, "buffers already attached to this comm");
+  if (c->world > PPO_DP_MAX_RANKS) return ppo::fail(PPO_E_SHAPE, "world exceeds PPO_DP_MAX_RANKS");
+  if (!ppo::aligned(g, 16) || !ppo::aligned(p, 16) || (p_bf16 && !ppo::aligned(p_bf16, 16)))
+    return ppo::fail(PPO_E_ALIGN, "dp buffers must be 16-byte aligned");
+  const int W = c->world;
+  void* bufs[3] = {g, p, p_bf16};
+  IpcRecord mine[3];
+  memset(mine, 0, sizeof(mine));
+  for (int k = 0; k < 3; ++k) {
+    if (!bufs[k] || W == 1) continue;
+    char* base = nullptr;
+    int rc = alloc_base(bufs[k], &base);
+    if (rc != PPO_OK) return rc;
+    PPO_CUDA_CHECK(cudaIpcGetMemHandle(&mine[k].h, base));
+    mine[k].off = (uint64_t)(static_cast<char*>(bufs[k]) - base);
+    mine[k].present = 1;
+  }
+  // all-gather the records over NCCL (device staging, synchronous)
+  const size_t rec = sizeof(mine);
+  std::vector<uint8_t> all(rec * W);
+  if (W > 1) {
+    uint8_t* dbuf = nullptr;
+    cudaStream_t st;
+    PPO_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    PPO_CUDA_CHECK(cudaMalloc(&dbuf, rec * W));
+    PPO_CUDA_CHECK(cudaMemcpyAsync(dbuf + rec * c->rank, mine, rec, cudaMemcpyHostToDevice, st));
+    ncclResult_t r = ncclAllGather(dbuf + rec * c->rank, dbuf, rec, ncclUint8, c->comm, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather (ipc handles)");
+    PPO_CUDA_CHECK(cudaMemcpyAsync(all.data(), dbuf, rec * W, cudaMemcpyDeviceToHost, st));
+    PPO_CUDA_CHECK(cudaStreamSynchronize(st));
+    PPO_CUDA_CHECK(cudaFree(dbuf));
+    PPO_CUDA_CHECK(cudaStreamDestroy(st));
+  }
+  DpPeers pe{};
+  for (int j = 0; j < W; ++j) {
+    if (j == c->rank) {
+      pe.g[j] = g;
+      pe.p[j] = p;
+      pe.pb[j] = reinterpret_cast<__nv_bfloat16*>(p_bf16);
+      continue;
+    }
+    const IpcRecord* r = reinterpret_cast<const IpcRecord*>(all.data() + rec * j);
+    char* mapped[3] = {nullptr, nullptr, nullptr};
+    for (int k = 0; k < 3; ++k) {
+      if (!r[k].present) continue;
+      // one mapping per distinct allocation of rank j
+      for (int q = 0; q < k && !mapped[k]; ++q)
+        if (r[q].present && !memcmp(&r[q].h, &r[k].h, sizeof(r[k].h)))
+          mapped[k] = mapped[q] - r[q].off;
+      if (!mapped[k]) {
+        void* m = nullptr;
+        PPO_CUDA_CHECK(cudaIpcOpenMemHandle(&m, r[k].h, cudaIpcMemLazyEnablePeerAccess));
+        c->mapped.push_back(m);
+        mapped[k] = static_cast<char*>(m);
+      }
+      mapped[k] += r[k].off;
+    }
+    pe.g[j] = reinterpret_cast<const float*>(mapped[0]);
+    pe.p[j] = reinterpret_cast<float*>(mapped[1]);
+    pe.pb[j] = reinterpret_cast<__nv_bfloat16*>(mapped[2]);
+    if (!pe.g[j] || !pe.p[j] || (p_bf16 && !pe.pb[j]))
+      return ppo::fail(PPO_E_ARG, "ranks disagree on which dp buffers exist");
+  }
+  if (!c->sync) PPO_CUDA_CHECK(cudaMalloc(&c->sync, 16));
+  PPO_CUDA_CHECK(cudaMemset(c->sync, 0, 16));
+  c->peers = pe;
+  c->n = n;
+  c->attached = true;
+  return PPO_OK;
+}
+
+int ppo_dp_adam_step(ppo_comm* c, float* m, float* v, int64_t t, double lr, double b1,
+                     double b2, double eps, double clip_sigma, ppo_stream_t s) {
+  if (!c) return ppo::fail(PPO_E_ARG, "comm is NULL");
+  if (!c->attached) return ppo::fail(PPO_E_ARG, "ppo_dp_attach was not called on this comm");
+  if (!m || !v) return ppo::fail(PPO_E_ARG, "m or v is NULL");
+  if (!ppo::aligned(m, 16) || !ppo::aligned(v, 16))
+    return ppo::fail(PPO_E_ALIGN, "m and v must be 16-byte aligned");
+  if (t < 1) return ppo::fail(PPO_E_ARG, "t must be >= 1");
+  if (!(b1 >= 0.0 && b1 < 1.0 && b2 >= 0.0 && b2 < 1.0)) return ppo::fail(PPO_E_ARG, "bad betas");
+  ppo::AdamParams ap;
+  ap.alpha = (float)(lr * sqrt(1.0 - pow(b2, (double)t)) / (1.0 - pow(b1, (double)t)));
+  ap.b1 = (float)b1;
+  ap.omb1 = (float)(1.0 - b1);
+  ap.b2 = (float)b2;
+  ap.omb2 = (float)(1.0 - b2);
+  ap.eps = (float)eps;
+  ap.clip = (clip_sigma > 0.0 && isfinite(clip_sigma)) ? (float)clip_sigma : 0.f;
+  const size_t sh = ppo_dp_shard(c->n, c->world);
+  const size_t lo = std::min(c->n, sh * (size_t)c->rank), hi = std::min(c->n, lo + sh);
+  cudaStream_t st = (cudaStream_t)s;
+  int rc = PPO_OK;
+  if (c->world > 1 && (rc = barrier(c, st)) != PPO_OK) return rc;   // every grad is final
+  {
+    ppo::ProfScope _prof("dp_adam", st);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t units = (hi - lo) / 4 + 1;
+    const int grid = (int)std::min<size_t>((size_t)sms * 8, (units + 255) / 256);
+    dp_adam_kernel<<<std::max(grid, 1), 256, 0, st>>>(c->peers, c->world, c->rank, lo, hi, m, v,
+                                                      ap, 1.0f / (float)c->world);
+    PPO_LAUNCH_CHECK("dp_adam_kernel");
+  }
+  // every rank's writes into this rank's theta/shadow have landed, and no rank still reads
+  // this rank's grad, before the caller's next step
+  if (c->world > 1 && (rc = barrier(c, st)) != PPO_OK) return rc;
+  return PPO_OK;
+}
+
+int ppo_dp_allgather(ppo_comm* c, float* buf, ppo_stream_t s) {
+  if (!c) return ppo::fail(PPO_E_ARG, "comm is NULL");
+  if (!c->attached) return ppo::fail(PPO_E_ARG, "ppo_dp_attach was not called on this comm");
+  if (!buf) return ppo::fail(PPO_E_ARG, "buf is NULL");
+  if (c->world == 1) return PPO_OK;
+  const size_t sh = ppo_dp_shard(c->n, c->world);
+  ncclResult_t r = ncclAllGather(buf + sh * (size_t)c->rank, buf, sh, ncclFloat32, c->comm,
+                                 (cudaStream_t)s);
+  return r == ncclSuccess ? PPO_OK : nccl_fail(r, "ncclAllGather");
 }
 
 }  // extern "C"

@@ -33,7 +33,8 @@ class PPOOptimizer:
 
     def __init__(self, D: int, H: int, B: int, T: int = 16, head_sizes=HEAD_SIZES,
                  precision: str = "bf16", device="cuda", hyper: dict | None = None,
-                 comm=None, n_buckets: int = 1, n_ws: int = 1, aux=(0, 0, 0)):
+                 comm=None, n_buckets: int = 1, n_ws: int = 1, aux=(0, 0, 0),
+                 dp: str = "allreduce"):
         self.D, self.H, self.B, self.T = D, H, B, T
         self.head_sizes = tuple(head_sizes)
         self.aux = tuple(aux)           # NEXT-4 (n_win, n_rank, n_bld) heads after the value
@@ -48,11 +49,28 @@ class PPOOptimizer:
         n = self.layout.n_total
         dev = self.device
         f32 = dict(dtype=torch.float32, device=dev)
-        self.theta = torch.zeros(n, **f32)
-        self.m = torch.zeros(n, **f32)
-        self.v = torch.zeros(n, **f32)
+        # dp = "fused" (with a comm): a9+a10 as one NVLink peer-memory kernel per rank
+        # (ppo_dp_adam_step); m, v (and theta, when the bf16 shadow is what is all-gathered)
+        # are then sharded, padded to world x shard for the in-place all-gather that brings
+        # them up to date for a checkpoint
+        if dp not in ("allreduce", "fused"):
+            raise ValueError("dp must be 'allreduce' or 'fused'")
+        self.dp = dp if comm is not None else "allreduce"
+        world = 1
+        if self.dp == "fused":
+            import torch.distributed as dist
+            world = dist.get_world_size() if dist.is_initialized() else 1
+        n_mv = world * L.dp_shard(n, world) if self.dp == "fused" else n
+        self._theta_full = torch.zeros(n_mv, **f32)
+        self.theta = self._theta_full[:n]
+        self._m_full = torch.zeros(n_mv, **f32)
+        self._v_full = torch.zeros(n_mv, **f32)
+        self.m = self._m_full[:n]
+        self.v = self._v_full[:n]
         self.grad = torch.zeros(n, **f32)
         self.shadow = torch.zeros(n, dtype=torch.bfloat16, device=dev) if self.bf16 else None
+        if self.dp == "fused":
+            L.dp_attach(comm, self.grad, self.theta, self.shadow, n)
         # activation workspaces; n_ws = 2 lets the next step's x be uploaded into one while
         # the current step runs in the other
         self.ws_list = [_aligned_empty(L.ws_bytes(self.dims, B), dev) for _ in range(n_ws)]
@@ -99,7 +117,9 @@ class PPOOptimizer:
     def state_dict(self) -> dict:
         """fp32 parameters and Adam moments in the canonical layout (gate blocks [i;f;g;o],
         separate W_x, W_h, b, W_o, b_o: the oracle's), the Adam step t and the shapes; host
-        tensors, loadable into an optimizer of the same dims."""
+        tensors, loadable into an optimizer of the same dims.  Collective when
+        dp = "fused" (the sharded moments are all-gathered first)."""
+        self.gather_sharded()
         torch.cuda.synchronize(self.device)
         cpu = lambda d: {k: v.cpu() for k, v in d.items()}  # noqa: E731
         return {"format": "ppo5-ckpt-1", "t": self.t, "D": self.D, "H": self.H,
@@ -200,16 +220,29 @@ class PPOOptimizer:
         L.lstm_input_grad(self.dims, self.weights, self.ws, self.B, dx, stream)
 
     def allreduce(self, stream=None):
-        """a9"""
-        if self.comm is not None:
+        """a9 (dp = "fused": folded into apply)"""
+        if self.comm is not None and self.dp == "allreduce":
             L.grad_allreduce(self.comm, self.grad, self.n_buckets, stream)
 
     def apply(self, stream=None):
-        """a10"""
+        """a10 (dp = "fused": a9 + a10 on this rank's shard, theta and shadow all-gathered)"""
         h = self.hyper
         self.t += 1
+        if self.dp == "fused":
+            L.dp_adam_step(self.comm, self.m, self.v, self.t, h["lr"], h["beta1"], h["beta2"],
+                           h["adam_eps"], h["clip_sigma"], stream)
+            return
         L.adam_step(self.theta, self.shadow, self.grad, self.m, self.v, self.t, h["lr"],
                     h["beta1"], h["beta2"], h["adam_eps"], h["clip_sigma"], stream)
+
+    def gather_sharded(self, stream=None):
+        """dp = "fused": bring every rank's m, v (and theta, on the bf16 path) up to date from
+        the owners' shards (collective; state_dict calls it)"""
+        if self.dp == "fused":
+            L.dp_allgather(self.comm, self._m_full, stream)
+            L.dp_allgather(self.comm, self._v_full, stream)
+            if self.bf16:
+                L.dp_allgather(self.comm, self._theta_full, stream)
 
     def step(self, batch, stream=None, dx=None):
         """One full optimizer step a1-a10 on this rank; returns the device stats tensor.

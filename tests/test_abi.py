@@ -105,3 +105,17 @@ def test_next_rows_host_checks(lib):
     rc = lib._lib.ppo_copy_x_slice(ctypes.byref(lib.make_dims(256, 128, 16, hs)), 8, 16, None, 256,
                                    None, 0, None)
     assert rc == lib.PPO_E_SHAPE
+
+
+def test_dp_fused_host_checks(lib):
+    """The fused a9+a10 exchange (ppo_dp_*): shard arithmetic and host-side argument checks."""
+    for n in (1, 63, 64, 1000, 135_917_728, 135_917_729):
+        for world in (1, 2, 3, 4, 8):
+            s = lib.dp_shard(n, world)
+            assert s % 64 == 0 and world * s >= n and s - -(-n // world) < 64, (n, world, s)
+    assert lib.dp_shard(10, 0) == 0
+    assert lib._lib.ppo_dp_attach(None, None, None, None, 10) == lib.PPO_E_ARG
+    assert lib._lib.ppo_dp_adam_step(None, None, None, 1, 1e-3, 0.9, 0.999, 1e-8, 5.0,
+                                     None) == lib.PPO_E_ARG
+    assert lib._lib.ppo_dp_allgather(None, None, None) == lib.PPO_E_ARG
+    assert "comm is NULL" in lib.last_error()

@@ -25,6 +25,8 @@ from paper_1912_06680_b200 import dist as pdist  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--precision", default="fp32")
+ap.add_argument("--dp", default="allreduce", choices=("allreduce", "fused"))
+ap.add_argument("--steps", type=int, default=1)
 a = ap.parse_args()
 rank, world, local = pdist.env()
 torch.cuda.set_device(local)
@@ -39,29 +41,41 @@ shard = {k: (v[:, sl] if k in ("x", "act", "head_on", "avail", "valid", "logp_ol
              else v[sl] if k in ("h0", "c0") else v[rs]).contiguous() for k, v in full.items()}
 comm = pdist.make_comm(dev)
 opt = PPOOptimizer(cfg.D, cfg.H, Bs, cfg.T, cfg.head_sizes, precision=a.precision, device=dev,
-                   comm=comm, n_buckets=4)
+                   comm=comm, n_buckets=4, dp=a.dp)
 load_params(opt, case["params"], device=dev)
 # each rank's loss uses its local denominator T*Bs (DESIGN Q9), so the average of the N
 # gradients is the gradient of the whole batch over T*B
-opt.step(shard)
+for _ in range(a.steps):
+    opt.step(shard)
+opt.gather_sharded()
 torch.cuda.synchronize()
 res = {}
 if rank == 0:
     ref = PPOOptimizer(cfg.D, cfg.H, cfg.B, cfg.T, cfg.head_sizes, precision=a.precision,
                        device=dev)
     load_params(ref, case["params"], device=dev)
-    ref.step(full)
+    th0 = ref.theta.clone()
+    for _ in range(a.steps):
+        ref.step(full)
     torch.cuda.synchronize()
     nw = lambda x, y: float((x - y).norm() / y.norm())  # noqa: E731
-    res = {"world": world, "precision": a.precision, "grad_err": nw(opt.grad, ref.grad),
-           "theta_err": nw(opt.theta, ref.theta)}
+    res = {"world": world, "precision": a.precision, "dp": a.dp, "steps": a.steps,
+           "theta_err": nw(opt.theta, ref.theta),
+           "update_err": nw(opt.theta - th0, ref.theta - th0),
+           "m_err": nw(opt.m, ref.m), "v_err": nw(opt.v, ref.v)}
+    if a.dp == "allreduce":   # the fused path leaves each rank's own (unaveraged) gradient
+        res["grad_err"] = nw(opt.grad, ref.grad)
     tol = 1e-5 if a.precision == "fp32" else 2e-2
-    res["ok"] = res["grad_err"] < tol
+    res["ok"] = max(res.get("grad_err", 0.0), res["m_err"]) < tol
     print(json.dumps(res), flush=True)
 # every rank holds identical parameters after the averaged update
 th = opt.theta.clone()
 dist.broadcast(th, 0)
 same = bool(torch.equal(th, opt.theta))
+if opt.shadow is not None:
+    sh = opt.shadow.clone()
+    dist.broadcast(sh, 0)
+    same = same and bool(torch.equal(sh, opt.shadow))
 flag = torch.tensor([1 if same else 0], device=dev)
 dist.all_reduce(flag, op=dist.ReduceOp.MIN)
 if rank == 0:
