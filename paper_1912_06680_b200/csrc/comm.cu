@@ -135,17 +135,8 @@ __global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int
                                                       size_t lo, size_t hi, float* __restrict__ m,
                                                       float* __restrict__ v, ppo::AdamParams ap,
                                                       float inv_world) {
-  const float alpha = ap.alpha, b1 = ap.b1, b2 = ap.b2, omb1 = ap.omb1, omb2 = ap.omb2;
-  const float eps = ap.eps, clip = ap.clip;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t lo4 = lo / 4, hi4 = hi / 4;           // lo is a multiple of 64
-  auto adam1 = [&](float gi, float& pi, float& mi, float& vi) {
-    vi = b2 * vi + omb2 * gi * gi;
-    const float sv = sqrtf(vi);
-    const float gc = clip > 0.f ? fminf(fmaxf(gi, -clip * sv), clip * sv) : gi;
-    mi = b1 * mi + omb1 * gc;
-    pi = pi - alpha * mi / (sv + eps);
-  };
   for (size_t i = lo4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hi4; i += stride) {
     // g = (1/N) sum over ranks in rank order: the same bits on every rank's shard owner
     float4 gs = reinterpret_cast<const float4*>(pe.g[0])[i];
@@ -159,10 +150,10 @@ __global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int
     float4 pp = reinterpret_cast<const float4*>(pe.p[rank])[i];
     float4 mm = reinterpret_cast<float4*>(m)[i];
     float4 vv = reinterpret_cast<float4*>(v)[i];
-    adam1(gs.x * inv_world, pp.x, mm.x, vv.x);
-    adam1(gs.y * inv_world, pp.y, mm.y, vv.y);
-    adam1(gs.z * inv_world, pp.z, mm.z, vv.z);
-    adam1(gs.w * inv_world, pp.w, mm.w, vv.w);
+    ppo::adam_elem(ap, __fmul_rn(gs.x, inv_world), pp.x, mm.x, vv.x);
+    ppo::adam_elem(ap, __fmul_rn(gs.y, inv_world), pp.y, mm.y, vv.y);
+    ppo::adam_elem(ap, __fmul_rn(gs.z, inv_world), pp.z, mm.z, vv.z);
+    ppo::adam_elem(ap, __fmul_rn(gs.w, inv_world), pp.w, mm.w, vv.w);
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
     uint2 u;
@@ -185,7 +176,7 @@ __global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int
     float gi = pe.g[0][i];
     for (int j = 1; j < world; ++j) gi += pe.g[j][i];
     float pi = pe.p[rank][i], mi = m[i], vi = v[i];
-    adam1(gi * inv_world, pi, mi, vi);
+    ppo::adam_elem(ap, __fmul_rn(gi, inv_world), pi, mi, vi);
     m[i] = mi;
     v[i] = vi;
     if (pe.pb[rank]) {

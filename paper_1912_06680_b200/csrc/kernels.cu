@@ -1253,8 +1253,6 @@ __global__ void loss_finalize_kernel(const float* __restrict__ partials, int nbl
 __global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p16,
                             const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, size_t n, AdamParams ap) {
-  const float alpha = ap.alpha, b1 = ap.b1, b2 = ap.b2, omb1 = ap.omb1, omb2 = ap.omb2;
-  const float eps = ap.eps, clip = ap.clip;
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -1267,16 +1265,7 @@ __global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p
     float* me = &mm.x;
     float* ve = &vv.x;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float gi = ge[e];
-      const float vi = b2 * ve[e] + omb2 * gi * gi;
-      const float sv = sqrtf(vi);
-      const float gc = clip > 0.f ? fminf(fmaxf(gi, -clip * sv), clip * sv) : gi;
-      const float mi = b1 * me[e] + omb1 * gc;
-      pe[e] = pe[e] - alpha * mi / (sv + eps);
-      me[e] = mi;
-      ve[e] = vi;
-    }
+    for (int e = 0; e < 4; ++e) adam_elem(ap, ge[e], pe[e], me[e], ve[e]);
     reinterpret_cast<float4*>(p)[i] = pp;
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
@@ -1290,15 +1279,12 @@ __global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p
     }
   }
   for (size_t i = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const float gi = g[i];
-    const float vi = b2 * v[i] + omb2 * gi * gi;
-    const float sv = sqrtf(vi);
-    const float gc = clip > 0.f ? fminf(fmaxf(gi, -clip * sv), clip * sv) : gi;
-    const float mi = b1 * m[i] + omb1 * gc;
-    p[i] = p[i] - alpha * mi / (sv + eps);
+    float pi = p[i], mi = m[i], vi = v[i];
+    adam_elem(ap, g[i], pi, mi, vi);
+    p[i] = pi;
     m[i] = mi;
     v[i] = vi;
-    if (p16) p16[i] = __float2bfloat16_rn(p[i]);
+    if (p16) p16[i] = __float2bfloat16_rn(pi);
   }
 }
 

@@ -49,6 +49,17 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
 struct AdamParams {
   float alpha, b1, omb1, b2, omb2, eps, clip;
 };
+// a10 on one element (O10): every rounding explicit, so adam_kernel and the
+// fused DP kernel (comm.cu) produce the same bits from the same gradient
+__device__ __forceinline__ void adam_elem(const AdamParams& ap, float g, float& p, float& m,
+                                          float& v) {
+  v = __fadd_rn(__fmul_rn(ap.b2, v), __fmul_rn(__fmul_rn(ap.omb2, g), g));
+  const float sv = __fsqrt_rn(v);
+  const float gc = ap.clip > 0.f ? fminf(fmaxf(g, -__fmul_rn(ap.clip, sv)), __fmul_rn(ap.clip, sv))
+                                 : g;
+  m = __fadd_rn(__fmul_rn(ap.b1, m), __fmul_rn(ap.omb1, gc));
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(ap.alpha, m), __fadd_rn(sv, ap.eps)));
+}
 int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n,
                 const AdamParams& ap, cudaStream_t st);
 int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int64_t K, float* C,
