@@ -123,9 +123,12 @@ def test_gae_lambda_edge_cases(L):
 
 # ------------------------------------------------------------------ PPO loss
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
-@pytest.mark.parametrize("seed,pad", [(0, 0.0), (1, 0.5), (2, 0.0)])
-def test_loss_parity(L, precision, seed, pad):
-    T, B = 16, 40
+# B = 643 and 4,000: several rows per warp of the persistent loss kernel (its buffer
+# rotation, one-row-ahead metadata and bulk stores) with a ragged last run
+@pytest.mark.parametrize("seed,pad,B", [(0, 0.0, 40), (1, 0.5, 40), (2, 0.0, 40), (3, 0.3, 643),
+                                        (4, 0.1, 4000)])
+def test_loss_parity(L, precision, seed, pad, B):
+    T = 16
     cfg = synth.Config(H=64, D=64, B=B, T=T)
     s = synth.make_sequences(cfg, seed, pad_frac=pad)
     N = T * B
