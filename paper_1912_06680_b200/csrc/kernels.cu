@@ -1255,27 +1255,28 @@ __global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p
                             float* __restrict__ v, size_t n, AdamParams ap) {
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
+  // every byte is touched once per step: streaming (evict-first) loads and stores
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
-    float4 pp = reinterpret_cast<float4*>(p)[i];
-    const float4 gg = reinterpret_cast<const float4*>(g)[i];
-    float4 mm = reinterpret_cast<float4*>(m)[i];
-    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float4 pp = __ldcs(reinterpret_cast<const float4*>(p) + i);
+    const float4 gg = __ldcs(reinterpret_cast<const float4*>(g) + i);
+    float4 mm = __ldcs(reinterpret_cast<const float4*>(m) + i);
+    float4 vv = __ldcs(reinterpret_cast<const float4*>(v) + i);
     float* pe = &pp.x;
     const float* ge = &gg.x;
     float* me = &mm.x;
     float* ve = &vv.x;
 #pragma unroll
     for (int e = 0; e < 4; ++e) adam_elem(ap, ge[e], pe[e], me[e], ve[e]);
-    reinterpret_cast<float4*>(p)[i] = pp;
-    reinterpret_cast<float4*>(m)[i] = mm;
-    reinterpret_cast<float4*>(v)[i] = vv;
+    __stcs(reinterpret_cast<float4*>(p) + i, pp);
+    __stcs(reinterpret_cast<float4*>(m) + i, mm);
+    __stcs(reinterpret_cast<float4*>(v) + i, vv);
     if (p16) {
       __nv_bfloat162 lo = __floats2bfloat162_rn(pp.x, pp.y);
       __nv_bfloat162 hi = __floats2bfloat162_rn(pp.z, pp.w);
       uint2 u;
       u.x = *reinterpret_cast<uint32_t*>(&lo);
       u.y = *reinterpret_cast<uint32_t*>(&hi);
-      reinterpret_cast<uint2*>(p16)[i] = u;
+      __stcs(reinterpret_cast<uint2*>(p16) + i, u);
     }
   }
   for (size_t i = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
