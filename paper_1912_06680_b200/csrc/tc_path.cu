@@ -320,12 +320,12 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&wa, P.g, s.G4, rows, s.G4))) return rc;
   if ((rc = map_mnmajor(&wb, P.xh, s.Kx, rows, s.Kx))) return rc;
   {
-    // K = T*B is long (614,400 at the full config): run it as K-chunks of ~76,800 rows, each
+    // K = T*B is long (614,400 at the full config): run it as K-chunks of ~153,600 rows, each
     // a separate launch that accumulates into dW.  The tiles of one launch start together and
     // drift apart little over a chunk, so the shared operand panels stay in L2 (DRAM traffic
     // and hence power drop; the step is power-capped).  PPO_WGRAD_CHUNK overrides the rows.
     const int nkb_all = cdiv(rows, tc::BK);
-    int chunk_kb = 1200;
+    int chunk_kb = 2400;   // 153,600 rows: A/B on two boxes, dW_xh 4.6% faster than 76,800
     if (const char* e = getenv("PPO_WGRAD_CHUNK")) chunk_kb = std::max(1, atoi(e) / tc::BK);
     const int nchunks = std::max(1, (nkb_all + chunk_kb - 1) / chunk_kb);
     const bool pair = use_pair("WGRAD", true);
