@@ -248,7 +248,9 @@ size_t ppo_dp_shard(size_t n, int world);
  * and shadow p_bf16 [n] bf16 (nullable; the same on every rank) into this process.  The
  * buffers must be cudaMalloc'd device memory (torch's default allocator qualifies; not
  * expandable segments), 16-byte aligned, and stay allocated until ppo_comm_destroy (which
- * closes the mappings).  world == 1: records the pointers only. */
+ * closes the mappings).  world == 1: records the pointers only.  Errors are per rank: if any
+ * rank's call fails, no rank may use ppo_dp_adam_step on this comm (agree over the caller's
+ * process group first, as bench.py does, and fall back to grad_allreduce + adam_step). */
 int ppo_dp_attach(ppo_comm* comm, float* g, float* p, uint16_t* p_bf16, size_t n);
 /* a9 + a10 for this rank's shard (same arguments and arithmetic as adam_step).  Collective:
  * every rank calls it once per step, after its backward, on the attached buffers.  m, v:
