@@ -48,10 +48,12 @@ def parse():
                     help="NEXT-4: with the aux heads (win, rank, 18 buildings) and their targets")
     ap.add_argument("--dx", action="store_true",
                     help="NEXT-4: also produce dL/dx for the observation network each step")
-    ap.add_argument("--dp", choices=["nccl", "fused"], default="fused",
+    ap.add_argument("--dp", choices=["nccl", "fused", "fused-pull"], default="fused",
                     help="N>1 gradient exchange: nccl = ncclAvg allreduce + replicated Adam; "
-                         "fused = one NVLink peer-memory kernel (reduce-scatter, Adam on 1/N, "
-                         "all-gather of theta and its bf16 shadow)")
+                         "fused = the backward's epilogues push the gradient shards to their "
+                         "owners over NVLink, one kernel per rank applies Adam to its shard and "
+                         "all-gathers the bf16 shadow; fused-pull = the owners read the shards "
+                         "after the backward instead")
     ap.add_argument("--infer-B", type=str, default="60,1,240,960",
                     help="--config infer: comma-separated batch sizes (first = headline)")
     ap.add_argument("--config", choices=["full", "gae", "iteration", "infer"], default="full",
@@ -220,8 +222,12 @@ def workload_config(args, n):
         "global_batch_timesteps": args.B * n * 16,
         "parallelism": f"dp{n}",
         "dp_exchange": (None if n == 1 else
-                        "fused NVLink peer-memory reduce-scatter + Adam + all-gather"
-                        if getattr(args, "dp", "nccl") == "fused" else "NCCL allreduce (avg)"),
+                        "fused: gradient shards pushed to their owners over NVLink from the "
+                        "backward's epilogues + Adam on 1/N + bf16 all-gather"
+                        if getattr(args, "dp", "nccl") == "fused" else
+                        "fused-pull: NVLink peer-memory reduce-scatter + Adam on 1/N + bf16 "
+                        "all-gather" if getattr(args, "dp", "nccl") == "fused-pull"
+                        else "NCCL allreduce (avg)"),
         "l2": "inputs larger than L2 (x alone is T*B*D*2 bytes per step)",
         "dx": bool(getattr(args, "dx", False)),
         "aux_heads": list(__import__("synth").AUX_SIZES) if getattr(args, "aux", False) else None,
@@ -552,11 +558,11 @@ def main():
                                  device=device, comm=comm, n_buckets=8,
                                  n_ws=1 if args.no_e2e else 2, aux=aux, dp=dp)
     opt = None
-    if comm is not None and args.dp == "fused":
+    if comm is not None and args.dp.startswith("fused"):
         # the peer mappings (CUDA IPC) need plain cudaMalloc'd buffers; every rank must agree
         # before the first collective step, else all fall back to the NCCL allreduce
         try:
-            opt, ok = mk("fused"), 1.0
+            opt, ok = mk(args.dp), 1.0
         except L.PPOError as e:
             ok = 0.0
             print(f"[bench] fused DP exchange unavailable on rank {rank}: {e}", file=sys.stderr)

@@ -254,9 +254,21 @@ size_t ppo_dp_shard(size_t n, int world);
 int ppo_dp_attach(ppo_comm* comm, float* g, float* p, uint16_t* p_bf16, size_t n);
 /* a9 + a10 for this rank's shard (same arguments and arithmetic as adam_step).  Collective:
  * every rank calls it once per step, after its backward, on the attached buffers.  m, v:
- * [n] fp32, 16-byte aligned; only this rank's shard is read and written. */
+ * [n] fp32, 16-byte aligned; only this rank's shard is read and written.  staged = 0 (pull
+ * mode): the shard of every rank's gradient is read over NVLink; staged = 1 (push mode):
+ * from this rank's staging, filled by every rank's lstm_bptt_bwd_dp of this step. */
 int ppo_dp_adam_step(ppo_comm* comm, float* m, float* v, int64_t t, double lr, double b1,
-                     double b2, double eps, double clip_sigma, ppo_stream_t s);
+                     double b2, double eps, double clip_sigma, int32_t staged, ppo_stream_t s);
+/* Push mode (staged = 1 in ppo_dp_adam_step): the backward itself delivers the gradients --
+ * lstm_bptt_bwd, plus: the epilogues of the tiles that produce final weight gradients (the
+ * last K-chunk of dW_xh, dW_o's split-K reduction) also store each 4-element group over
+ * NVLink into its owner's staging slot for this rank (a library-owned buffer of world x shard
+ * floats per rank, mapped by ppo_dp_attach), so the reduce-scatter overlaps the GEMM tile by
+ * tile and ppo_dp_adam_step reads only local memory.  Same bits as pull mode.  grad still
+ * receives this rank's own gradient.  bf16 path without the win-head trunk route only
+ * (PPO_E_UNSUPPORTED otherwise: use lstm_bptt_bwd + staged = 0); comm attached, world > 1. */
+int lstm_bptt_bwd_dp(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
+                     const void* dout, int64_t B, float* grad, ppo_comm* comm, ppo_stream_t s);
 /* Collective: in-place all-gather of a sharded fp32 vector (m, v, theta before a checkpoint).
  * buf holds world * ppo_dp_shard(n, world) floats (n = the attached length; the slack past n
  * is scratch). */

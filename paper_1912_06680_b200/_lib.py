@@ -110,7 +110,9 @@ _lib_fns = dict(
     ppo_dp_shard=([c_size_t, c_int], c_size_t),
     ppo_dp_attach=([c_void_p, c_void_p, c_void_p, c_void_p, c_size_t], c_int),
     ppo_dp_adam_step=([c_void_p, c_void_p, c_void_p, c_int64, c_double, c_double, c_double,
-                       c_double, c_double, c_void_p], c_int),
+                       c_double, c_double, c_int32, c_void_p], c_int),
+    lstm_bptt_bwd_dp=([_D, c_void_p, c_void_p, c_size_t, c_void_p, c_int64, c_void_p, c_void_p,
+                       c_void_p], c_int),
     ppo_dp_allgather=([c_void_p, c_void_p, c_void_p], c_int),
     adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_double,
                 c_double, c_double, c_double, c_double, c_void_p], c_int),
@@ -386,9 +388,15 @@ def dp_attach(comm, g, p, p_bf16, n: int):
     _check(_lib.ppo_dp_attach(comm, _p(g), _p(p), _p(p_bf16), n))
 
 
-def dp_adam_step(comm, m, v, t, lr, b1, b2, eps, clip_sigma, stream=None):
+def dp_adam_step(comm, m, v, t, lr, b1, b2, eps, clip_sigma, staged=False, stream=None):
     _check(_lib.ppo_dp_adam_step(comm, _p(m), _p(v), t, lr, b1, b2, eps, clip_sigma,
-                                 _s(stream)))
+                                 1 if staged else 0, _s(stream)))
+
+
+def lstm_bptt_bwd_dp(dims, w, ws, dout, B, grad, comm, stream=None):
+    """backward that also pushes the final weight gradients to the DP owners' staging"""
+    _check(_lib.lstm_bptt_bwd_dp(ctypes.byref(dims), _p(w), _p(ws), ws.numel() * ws.element_size(),
+                                 _p(dout), B, _p(grad), comm, _s(stream)))
 
 
 def dp_allgather(comm, buf, stream=None):

@@ -180,6 +180,10 @@ int check_tc_device() {
 
 using namespace ppo;
 
+// comm.cu: the push-mode staging of an attached comm (C++ linkage, library-internal)
+const ppo::DpStage* ppo_comm_dp_stage(const ppo_comm* c);
+size_t ppo_comm_dp_n(const ppo_comm* c);
+
 extern "C" {
 
 const char* ppo_last_error(void) { return g_err.c_str(); }
@@ -402,6 +406,29 @@ int ppo_loss_grad(const ppo_dims* dims, const float* out, const int32_t* act,
   if (s.A > 6 * 128) return fail(PPO_E_SHAPE, "loss kernel supports A <= 768");
   return launch_loss(p, s.bf16, out, act, head_on, avail, logp_old, adv, ret, valid, aux_label,
                      dout, logp, stats, (cudaStream_t)st);
+}
+
+int lstm_bptt_bwd_dp(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
+                     const void* dout, int64_t B, float* grad, ppo_comm* comm,
+                     ppo_stream_t st_) {
+  if (!comm) return fail(PPO_E_ARG, "comm is NULL");
+  const ppo::DpStage* dp = ppo_comm_dp_stage(comm);
+  if (!dp) return fail(PPO_E_ARG, "comm has no attached dp buffers (ppo_dp_attach, world > 1)");
+  Shape s;
+  int rc = check_dims(dims, &s);
+  if (rc) return rc;
+  if (!s.bf16) return fail(PPO_E_UNSUPPORTED, "push-mode dp exchange needs the bf16 path");
+  if (s.win_pass) return fail(PPO_E_UNSUPPORTED, "push-mode dp exchange: no win-head trunk scale");
+  if (ppo_comm_dp_n(comm) != (size_t)(s.G4 * s.Kx + s.A * s.Ko))
+    return fail(PPO_E_SHAPE, "attached dp length differs from this model's theta");
+  if (B < 1) return fail(PPO_E_SHAPE, "B must be >= 1");
+  NEED(w);
+  NEED(dout);
+  NEED(grad);
+  if (!ws || !aligned(ws, 1024)) return fail(PPO_E_ALIGN, "ws must be 1024-byte aligned");
+  if (ws_bytes < ws_layout(s, B).total) return fail(PPO_E_ARG, "workspace too small");
+  if ((rc = check_tc_device())) return rc;
+  return tc_backward(s, B, w, ws, dout, grad, (cudaStream_t)st_, dp);
 }
 
 int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,

@@ -28,6 +28,8 @@ struct ppo_comm {
   DpPeers peers{};
   std::vector<void*> mapped;   // IPC mappings to close
   float* sync = nullptr;       // 1-float device scratch for the stream-ordered barriers
+  float* stage = nullptr;      // push mode: world x shard floats, slot j = rank j's gradient
+  ppo::DpStage dst{};          // every rank's staging, as the backward's epilogues see it
 };
 
 namespace {
@@ -89,11 +91,22 @@ int ppo_comm_destroy(ppo_comm* c) {
   if (!c) return PPO_OK;
   for (void* m : c->mapped) cudaIpcCloseMemHandle(m);
   if (c->sync) cudaFree(c->sync);
+  if (c->stage) cudaFree(c->stage);
   ncclResult_t r = ncclCommDestroy(c->comm);
   delete c;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return PPO_OK;
 }
+
+}  // extern "C"
+
+// the push-mode staging map of an attached comm with world > 1 (NULL otherwise); api.cu
+const ppo::DpStage* ppo_comm_dp_stage(const ppo_comm* c) {
+  return c && c->attached && c->world > 1 ? &c->dst : nullptr;
+}
+size_t ppo_comm_dp_n(const ppo_comm* c) { return c ? c->n : 0; }
+
+extern "C" {
 
 size_t ppo_dp_shard(size_t n, int world) {
   if (world < 1) return 0;
@@ -131,17 +144,24 @@ struct IpcRecord {          // what one rank publishes for one buffer
 };
 
 // a9 + a10 on the rank's shard: peers' grads in, the updated shard out to every rank
+// stage (push mode, nullable): the owner's staging, slot j = rank j's gradient of the shard
+// (written by the backward's epilogues); else (pull mode) the peers' gradients over NVLink
 __global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int rank,
                                                       size_t lo, size_t hi, float* __restrict__ m,
                                                       float* __restrict__ v, ppo::AdamParams ap,
-                                                      float inv_world) {
+                                                      float inv_world,
+                                                      const float* __restrict__ stage,
+                                                      size_t shard) {
+  auto gsrc = [&](int j, size_t e) -> const float* {   // rank j's gradient element e
+    return stage ? stage + (size_t)j * shard + (e - lo) : pe.g[j] + e;
+  };
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t lo4 = lo / 4, hi4 = hi / 4;           // lo is a multiple of 64
   for (size_t i = lo4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hi4; i += stride) {
     // g = (1/N) sum over ranks in rank order: the same bits on every rank's shard owner
-    float4 gs = reinterpret_cast<const float4*>(pe.g[0])[i];
+    float4 gs = *reinterpret_cast<const float4*>(gsrc(0, 4 * i));
     for (int j = 1; j < world; ++j) {
-      const float4 gj = reinterpret_cast<const float4*>(pe.g[j])[i];
+      const float4 gj = *reinterpret_cast<const float4*>(gsrc(j, 4 * i));
       gs.x += gj.x;
       gs.y += gj.y;
       gs.z += gj.z;
@@ -173,8 +193,8 @@ __global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int
   }
   // scalar tail (n % 4) on the last shard
   for (size_t i = hi4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hi; i += stride) {
-    float gi = pe.g[0][i];
-    for (int j = 1; j < world; ++j) gi += pe.g[j][i];
+    float gi = *gsrc(0, i);
+    for (int j = 1; j < world; ++j) gi += *gsrc(j, i);
     float pi = pe.p[rank][i], mi = m[i], vi = v[i];
     ppo::adam_elem(ap, __fmul_rn(gi, inv_world), pi, mi, vi);
     m[i] = mi;
@@ -203,10 +223,13 @@ int ppo_dp_attach(ppo_comm* c, float* g, float* p, uint16_t* p_bf16, size_t n) {
   if (!ppo::aligned(g, 16) || !ppo::aligned(p, 16) || (p_bf16 && !ppo::aligned(p_bf16, 16)))
     return ppo::fail(PPO_E_ALIGN, "dp buffers must be 16-byte aligned");
   const int W = c->world;
-  void* bufs[3] = {g, p, p_bf16};
-  IpcRecord mine[3];
+  const size_t sh = ppo_dp_shard(n, W);
+  // push-mode staging, owned by the comm (the backward's epilogues write into the owners')
+  if (W > 1) PPO_CUDA_CHECK(cudaMalloc(&c->stage, (size_t)W * sh * sizeof(float)));
+  void* bufs[4] = {g, p, p_bf16, c->stage};
+  IpcRecord mine[4];
   memset(mine, 0, sizeof(mine));
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     if (!bufs[k] || W == 1) continue;
     char* base = nullptr;
     int rc = alloc_base(bufs[k], &base);
@@ -232,16 +255,21 @@ int ppo_dp_attach(ppo_comm* c, float* g, float* p, uint16_t* p_bf16, size_t n) {
     PPO_CUDA_CHECK(cudaStreamDestroy(st));
   }
   DpPeers pe{};
+  ppo::DpStage ds{};
+  ds.world = W;
+  ds.rank = c->rank;
+  ds.shard = (int64_t)sh;
   for (int j = 0; j < W; ++j) {
     if (j == c->rank) {
       pe.g[j] = g;
       pe.p[j] = p;
       pe.pb[j] = reinterpret_cast<__nv_bfloat16*>(p_bf16);
+      ds.stage[j] = c->stage;
       continue;
     }
     const IpcRecord* r = reinterpret_cast<const IpcRecord*>(all.data() + rec * j);
-    char* mapped[3] = {nullptr, nullptr, nullptr};
-    for (int k = 0; k < 3; ++k) {
+    char* mapped[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int k = 0; k < 4; ++k) {
       if (!r[k].present) continue;
       // one mapping per distinct allocation of rank j
       for (int q = 0; q < k && !mapped[k]; ++q)
@@ -258,19 +286,21 @@ int ppo_dp_attach(ppo_comm* c, float* g, float* p, uint16_t* p_bf16, size_t n) {
     pe.g[j] = reinterpret_cast<const float*>(mapped[0]);
     pe.p[j] = reinterpret_cast<float*>(mapped[1]);
     pe.pb[j] = reinterpret_cast<__nv_bfloat16*>(mapped[2]);
-    if (!pe.g[j] || !pe.p[j] || (p_bf16 && !pe.pb[j]))
+    ds.stage[j] = reinterpret_cast<float*>(mapped[3]);
+    if (!pe.g[j] || !pe.p[j] || (p_bf16 && !pe.pb[j]) || !ds.stage[j])
       return ppo::fail(PPO_E_ARG, "ranks disagree on which dp buffers exist");
   }
   if (!c->sync) PPO_CUDA_CHECK(cudaMalloc(&c->sync, 16));
   PPO_CUDA_CHECK(cudaMemset(c->sync, 0, 16));
   c->peers = pe;
+  c->dst = W > 1 ? ds : ppo::DpStage{};
   c->n = n;
   c->attached = true;
   return PPO_OK;
 }
 
 int ppo_dp_adam_step(ppo_comm* c, float* m, float* v, int64_t t, double lr, double b1,
-                     double b2, double eps, double clip_sigma, ppo_stream_t s) {
+                     double b2, double eps, double clip_sigma, int32_t staged, ppo_stream_t s) {
   if (!c) return ppo::fail(PPO_E_ARG, "comm is NULL");
   if (!c->attached) return ppo::fail(PPO_E_ARG, "ppo_dp_attach was not called on this comm");
   if (!m || !v) return ppo::fail(PPO_E_ARG, "m or v is NULL");
@@ -298,8 +328,9 @@ int ppo_dp_adam_step(ppo_comm* c, float* m, float* v, int64_t t, double lr, doub
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t units = (hi - lo) / 4 + 1;
     const int grid = (int)std::min<size_t>((size_t)sms * 8, (units + 255) / 256);
-    dp_adam_kernel<<<std::max(grid, 1), 256, 0, st>>>(c->peers, c->world, c->rank, lo, hi, m, v,
-                                                      ap, 1.0f / (float)c->world);
+    dp_adam_kernel<<<std::max(grid, 1), 256, 0, st>>>(
+        c->peers, c->world, c->rank, lo, hi, m, v, ap, 1.0f / (float)c->world,
+        staged && c->world > 1 ? c->stage : nullptr, sh);
     PPO_LAUNCH_CHECK("dp_adam_kernel");
   }
   // every rank's writes into this rank's theta/shadow have landed, and no rank still reads

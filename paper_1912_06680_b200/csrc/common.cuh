@@ -14,6 +14,22 @@
 
 namespace ppo {
 
+// Fused DP exchange, push mode (comm.cu): where the final gradient of rank `rank` goes --
+// element i of theta to stage[i / shard] + rank * shard + i % shard, the owner's slot for
+// this rank (CUDA IPC mappings; stage[j] is rank j's staging buffer, world x shard floats).
+struct DpStage {
+  int world = 0, rank = 0;
+  int64_t shard = 0;
+  float* stage[PPO_DP_MAX_RANKS] = {};
+  __host__ __device__ __forceinline__ float* slot(int64_t i) const {
+    const int64_t r = i / shard;
+    float* base = stage[0];   // select, not a dynamic index (keeps the param array off the stack)
+#pragma unroll
+    for (int j = 1; j < PPO_DP_MAX_RANKS; ++j) base = r == j ? stage[j] : base;
+    return base + rank * shard + (i - r * shard);
+  }
+};
+
 // ---- error plumbing (ppo_last_error is thread-local) -----------------------------------
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);

@@ -1379,7 +1379,7 @@ __global__ void simt_cell_bwd_kernel(Shape s, int64_t B, const float* __restrict
 
 // ============================================================================ split-K reduce
 __global__ void splitk_reduce_kernel(const float4* __restrict__ part, int nsplit, size_t n4,
-                                     float4* __restrict__ out) {
+                                     float4* __restrict__ out, DpStage dp, int64_t dp_base) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
        i += (size_t)gridDim.x * blockDim.x) {
     float4 a = part[i];
@@ -1391,6 +1391,7 @@ __global__ void splitk_reduce_kernel(const float4* __restrict__ part, int nsplit
       a.w += b.w;
     }
     out[i] = a;
+    if (dp.world) *reinterpret_cast<float4*>(dp.slot(dp_base + 4 * (int64_t)i)) = a;
   }
 }
 
@@ -1576,10 +1577,12 @@ int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t 
   PPO_LAUNCH_CHECK("adam_kernel");
   return PPO_OK;
 }
-int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cudaStream_t st) {
+int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cudaStream_t st,
+                         const DpStage* dp, int64_t dp_base) {
   ProfScope _prof("splitk_reduce", st);
   splitk_reduce_kernel<<<grid_for((int64_t)(n / 4)), 256, 0, st>>>(
-      reinterpret_cast<const float4*>(part), nsplit, n / 4, reinterpret_cast<float4*>(out));
+      reinterpret_cast<const float4*>(part), nsplit, n / 4, reinterpret_cast<float4*>(out),
+      dp ? *dp : DpStage{}, dp_base);
   PPO_LAUNCH_CHECK("splitk_reduce_kernel");
   return PPO_OK;
 }

@@ -70,13 +70,16 @@ int launch_simt_cell_bwd(const Shape& s, int64_t B, const float* dh, float* gz, 
                          const float* c_prev, float* dc, cudaStream_t st);
 
 // out[i] = sum_{s < nsplit} part[s * n + i] in fixed order (deterministic split-K reduction)
-int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cudaStream_t st);
+// dp (nullable): also push the sums to the DP owners' staging (element i = theta dp_base + i)
+int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cudaStream_t st,
+                         const DpStage* dp = nullptr, int64_t dp_base = 0);
 
 // tcgen05 bf16 path (tc_path.cu)
 int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
                const cudaEvent_t* x_ready, cudaStream_t st);
+// dp (nullable): push the final weight gradients to the DP owners' staging (fused exchange)
 int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
-                cudaStream_t st);
+                cudaStream_t st, const DpStage* dp = nullptr);
 // Standalone test GEMM (exported for tests): C = A B^T variants on bf16 inputs.
 // NEXT-4: dX = dz W_x over all T*B rows (bf16 path)
 int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx, cudaStream_t st);

@@ -1045,6 +1045,10 @@ struct EpiStoreF32 {
   int M, N;
   int64_t split_stride;  // elements between split-K partial outputs
   int accumulate;        // 1: out += acc (K-chunked launches after the first)
+  // final values also pushed to the DP owners' staging (fused exchange, push mode): element
+  // (m, n) is theta element dp_base + m * ldc + n; dp.world == 0: off
+  ppo::DpStage dp{};
+  int64_t dp_base = 0;
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int split) const {
@@ -1056,7 +1060,8 @@ struct EpiStoreF32 {
       tmem_ld16(taddr + c * 16, v);
       const int n0 = n_base + c * 16;
       if (m >= M || n0 >= N) continue;
-      float* dst = out + split * split_stride + static_cast<int64_t>(m) * ldc + n0;
+      const int64_t e0 = static_cast<int64_t>(m) * ldc + n0;
+      float* dst = out + split * split_stride + e0;
       if (vec && n0 + 16 <= N) {
         float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
@@ -1070,11 +1075,17 @@ struct EpiStoreF32 {
             o.w += p.w;
           }
           d4[q] = o;
+          // over NVLink to the owner of these 4 elements (shards are multiples of 64)
+          if (dp.world) *reinterpret_cast<float4*>(dp.slot(dp_base + e0 + 4 * q)) = o;
         }
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          if (n0 + i < N) dst[i] = accumulate ? dst[i] + v[i] : v[i];
+          if (n0 + i < N) {
+            const float o = accumulate ? dst[i] + v[i] : v[i];
+            dst[i] = o;
+            if (dp.world) *dp.slot(dp_base + e0 + i) = o;
+          }
       }
     }
   }

@@ -280,7 +280,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
 
 // ---------------------------------------------------------------- backward (a6-a8)
 int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
-                cudaStream_t st) {
+                cudaStream_t st, const DpStage* dp) {
   WsPtrs P = ws_ptrs(s, B, ws);
   const __nv_bfloat16* wxh = static_cast<const __nv_bfloat16*>(w);
   const __nv_bfloat16* wo = wxh + s.G4 * s.Kx;
@@ -337,6 +337,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
       sh.kb_off = kb0;
       sh.sched = sched_counter(kSchedWgrad);
       tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx, 0, c > 0 ? 1 : 0};
+      // the last chunk's tiles are final: their epilogues push them to the DP owners over
+      // NVLink while the remaining tiles are still being multiplied
+      if (dp && c == nchunks - 1) epi.dp = *dp;
       rc = pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
                 : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st);
       if (rc) return rc;
@@ -358,10 +361,15 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
                                                               ws_layout(s, B).splitk)
                                 : dwo;
     tc::EpiStoreF32 epi{part, s.Ko, (int)s.A, (int)s.Ko, n_o};
+    if (dp && sh.ksplit == 1) {
+      epi.dp = *dp;
+      epi.dp_base = s.G4 * s.Kx;
+    }
     rc = pair_o ? launch2<true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st)
                 : launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st);
     if (rc) return rc;
-    if (sh.ksplit > 1 && (rc = launch_splitk_reduce(part, sh.ksplit, (size_t)n_o, dwo, st)))
+    if (sh.ksplit > 1 &&
+        (rc = launch_splitk_reduce(part, sh.ksplit, (size_t)n_o, dwo, st, dp, s.G4 * s.Kx)))
       return rc;
     if (s.win_pass &&  // dout's win column carries win_trunk x the gradient (Q26)
         (rc = launch_scale(dwo + (int64_t)(s.vcol + 1) * s.Ko, s.Ko, 1.f / s.win_trunk, st)))

@@ -53,9 +53,9 @@ class PPOOptimizer:
         # (ppo_dp_adam_step); m, v (and theta, when the bf16 shadow is what is all-gathered)
         # are then sharded, padded to world x shard for the in-place all-gather that brings
         # them up to date for a checkpoint
-        if dp not in ("allreduce", "fused"):
-            raise ValueError("dp must be 'allreduce' or 'fused'")
-        self.dp = dp if comm is not None else "allreduce"
+        if dp not in ("allreduce", "fused", "fused-pull"):
+            raise ValueError("dp must be 'allreduce', 'fused' or 'fused-pull'")
+        self.dp = "fused" if comm is not None and dp.startswith("fused") else "allreduce"
         world = 1
         if self.dp == "fused":
             import torch.distributed as dist
@@ -69,6 +69,11 @@ class PPOOptimizer:
         self.v = self._v_full[:n]
         self.grad = torch.zeros(n, **f32)
         self.shadow = torch.zeros(n, dtype=torch.bfloat16, device=dev) if self.bf16 else None
+        # push mode: the backward's epilogues deliver the gradient shards to their owners
+        # over NVLink (bf16 path without the win-head trunk route); "fused-pull" forces the
+        # owners to read them after the backward instead
+        self.dp_push = (self.dp == "fused" and dp != "fused-pull" and world > 1 and self.bf16
+                        and sum(self.aux) == 0)
         if self.dp == "fused":
             L.dp_attach(comm, self.grad, self.theta, self.shadow, n)
         # activation workspaces; n_ws = 2 lets the next step's x be uploaded into one while
@@ -212,7 +217,11 @@ class PPOOptimizer:
                         self.stats, stream, aux_label=batch.get("aux_label"))
 
     def backward(self, stream=None):
-        """a6-a8"""
+        """a6-a8 (dp push mode: + the reduce-scatter of the final weight gradients)"""
+        if self.dp_push:
+            L.lstm_bptt_bwd_dp(self.dims, self.weights, self.ws, self.dout, self.B, self.grad,
+                               self.comm, stream)
+            return
         L.lstm_bptt_bwd(self.dims, self.weights, self.ws, self.dout, self.B, self.grad, stream)
 
     def input_grad(self, dx: torch.Tensor, stream=None):
@@ -230,7 +239,7 @@ class PPOOptimizer:
         self.t += 1
         if self.dp == "fused":
             L.dp_adam_step(self.comm, self.m, self.v, self.t, h["lr"], h["beta1"], h["beta2"],
-                           h["adam_eps"], h["clip_sigma"], stream)
+                           h["adam_eps"], h["clip_sigma"], staged=self.dp_push, stream=stream)
             return
         L.adam_step(self.theta, self.shadow, self.grad, self.m, self.v, self.t, h["lr"],
                     h["beta1"], h["beta2"], h["adam_eps"], h["clip_sigma"], stream)

@@ -115,7 +115,11 @@ def test_dp_fused_host_checks(lib):
             assert s % 64 == 0 and world * s >= n and s - -(-n // world) < 64, (n, world, s)
     assert lib.dp_shard(10, 0) == 0
     assert lib._lib.ppo_dp_attach(None, None, None, None, 10) == lib.PPO_E_ARG
-    assert lib._lib.ppo_dp_adam_step(None, None, None, 1, 1e-3, 0.9, 0.999, 1e-8, 5.0,
+    assert lib._lib.ppo_dp_adam_step(None, None, None, 1, 1e-3, 0.9, 0.999, 1e-8, 5.0, 0,
+                                     None) == lib.PPO_E_ARG
+    hs = (30, 4, 189, 189, 81, 81, 81)
+    d = lib.make_dims(256, 128, 16, hs)
+    assert lib._lib.lstm_bptt_bwd_dp(ctypes.byref(d), None, None, 0, None, 32, None, None,
                                      None) == lib.PPO_E_ARG
     assert lib._lib.ppo_dp_allgather(None, None, None) == lib.PPO_E_ARG
     assert "comm is NULL" in lib.last_error()

@@ -25,7 +25,7 @@ from paper_1912_06680_b200 import dist as pdist  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--precision", default="fp32")
-ap.add_argument("--dp", default="allreduce", choices=("allreduce", "fused"))
+ap.add_argument("--dp", default="allreduce", choices=("allreduce", "fused", "fused-pull"))
 ap.add_argument("--steps", type=int, default=1)
 a = ap.parse_args()
 rank, world, local = pdist.env()
@@ -63,7 +63,7 @@ if rank == 0:
            "theta_err": nw(opt.theta, ref.theta),
            "update_err": nw(opt.theta - th0, ref.theta - th0),
            "m_err": nw(opt.m, ref.m), "v_err": nw(opt.v, ref.v)}
-    if a.dp == "allreduce":   # the fused path leaves each rank's own (unaveraged) gradient
+    if a.dp == "allreduce":   # the fused paths leave each rank's own (unaveraged) gradient
         res["grad_err"] = nw(opt.grad, ref.grad)
     tol = 1e-5 if a.precision == "fp32" else 2e-2
     res["ok"] = max(res.get("grad_err", 0.0), res["m_err"]) < tol
@@ -81,5 +81,25 @@ dist.all_reduce(flag, op=dist.ReduceOp.MIN)
 if rank == 0:
     print(json.dumps({"replicas_identical": bool(flag.item())}), flush=True)
 from paper_1912_06680_b200 import _lib as L  # noqa: E402
+if a.dp == "fused" and opt.dp_push:
+    # push mode (gradient shards delivered by the backward's epilogues) against pull mode
+    # (owners read them after the backward) on a second communicator: the same bits
+    comm2 = pdist.make_comm(dev)
+    opt2 = PPOOptimizer(cfg.D, cfg.H, Bs, cfg.T, cfg.head_sizes, precision=a.precision,
+                        device=dev, comm=comm2, dp="fused-pull")
+    load_params(opt2, case["params"], device=dev)
+    for _ in range(a.steps):
+        opt2.step(shard)
+    opt2.gather_sharded()
+    torch.cuda.synchronize()
+    eq = all(torch.equal(getattr(opt, k), getattr(opt2, k)) for k in ("theta", "m", "v", "grad"))
+    if opt.shadow is not None:
+        eq = eq and torch.equal(opt.shadow, opt2.shadow)
+    flag = torch.tensor([1 if eq else 0], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"push_equals_pull": bool(flag.item())}), flush=True)
+    del opt2
+    L.comm_destroy(comm2)
 L.comm_destroy(comm)
 dist.destroy_process_group()
