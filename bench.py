@@ -48,12 +48,11 @@ def parse():
                     help="NEXT-4: with the aux heads (win, rank, 18 buildings) and their targets")
     ap.add_argument("--dx", action="store_true",
                     help="NEXT-4: also produce dL/dx for the observation network each step")
-    ap.add_argument("--dp", choices=["nccl", "fused", "fused-pull"], default="fused",
+    ap.add_argument("--dp", choices=["nccl", "fused", "fused-push"], default="fused",
                     help="N>1 gradient exchange: nccl = ncclAvg allreduce + replicated Adam; "
-                         "fused = the backward's epilogues push the gradient shards to their "
-                         "owners over NVLink, one kernel per rank applies Adam to its shard and "
-                         "all-gathers the bf16 shadow; fused-pull = the owners read the shards "
-                         "after the backward instead")
+                         "fused = one NVLink peer-memory kernel per rank (reduce-scatter of the "
+                         "gradient shards, Adam on 1/N, all-gather of the bf16 shadow); "
+                         "fused-push = the backward's epilogues push the shards to their owners")
     ap.add_argument("--infer-B", type=str, default="60,1,240,960",
                     help="--config infer: comma-separated batch sizes (first = headline)")
     ap.add_argument("--config", choices=["full", "gae", "iteration", "infer"], default="full",
@@ -222,11 +221,11 @@ def workload_config(args, n):
         "global_batch_timesteps": args.B * n * 16,
         "parallelism": f"dp{n}",
         "dp_exchange": (None if n == 1 else
-                        "fused: gradient shards pushed to their owners over NVLink from the "
-                        "backward's epilogues + Adam on 1/N + bf16 all-gather"
+                        "fused: NVLink peer-memory reduce-scatter + Adam on 1/N + bf16 all-gather"
                         if getattr(args, "dp", "nccl") == "fused" else
-                        "fused-pull: NVLink peer-memory reduce-scatter + Adam on 1/N + bf16 "
-                        "all-gather" if getattr(args, "dp", "nccl") == "fused-pull"
+                        "fused-push: gradient shards pushed to their owners over NVLink from the "
+                        "backward's epilogues + Adam on 1/N + bf16 all-gather"
+                        if getattr(args, "dp", "nccl") == "fused-push"
                         else "NCCL allreduce (avg)"),
         "l2": "inputs larger than L2 (x alone is T*B*D*2 bytes per step)",
         "dx": bool(getattr(args, "dx", False)),

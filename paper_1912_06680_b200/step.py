@@ -53,8 +53,8 @@ class PPOOptimizer:
         # (ppo_dp_adam_step); m, v (and theta, when the bf16 shadow is what is all-gathered)
         # are then sharded, padded to world x shard for the in-place all-gather that brings
         # them up to date for a checkpoint
-        if dp not in ("allreduce", "fused", "fused-pull"):
-            raise ValueError("dp must be 'allreduce', 'fused' or 'fused-pull'")
+        if dp not in ("allreduce", "fused", "fused-push"):
+            raise ValueError("dp must be 'allreduce', 'fused' or 'fused-push'")
         self.dp = "fused" if comm is not None and dp.startswith("fused") else "allreduce"
         world = 1
         if self.dp == "fused":
@@ -69,10 +69,10 @@ class PPOOptimizer:
         self.v = self._v_full[:n]
         self.grad = torch.zeros(n, **f32)
         self.shadow = torch.zeros(n, dtype=torch.bfloat16, device=dev) if self.bf16 else None
-        # push mode: the backward's epilogues deliver the gradient shards to their owners
-        # over NVLink (bf16 path without the win-head trunk route); "fused-pull" forces the
-        # owners to read them after the backward instead
-        self.dp_push = (self.dp == "fused" and dp != "fused-pull" and world > 1 and self.bf16
+        # "fused-push": the backward's epilogues deliver the gradient shards to their owners
+        # over NVLink (bf16 path without the win-head trunk route); "fused" (pull): the owners
+        # read them after the backward -- the default, 1-1.5% faster per step in the A/B
+        self.dp_push = (self.dp == "fused" and dp == "fused-push" and world > 1 and self.bf16
                         and sum(self.aux) == 0)
         if self.dp == "fused":
             L.dp_attach(comm, self.grad, self.theta, self.shadow, n)

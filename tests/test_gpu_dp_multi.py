@@ -19,10 +19,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs 2 GPUs")
-@pytest.mark.parametrize("dp", ["fused", "fused-pull", "allreduce"])
+@pytest.mark.parametrize("dp", ["fused", "fused-push", "allreduce"])
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_dp_two_ranks(dp, precision):
-    port = 29600 + ["fused", "fused-pull", "allreduce"].index(dp) * 10 + (precision == "bf16")
+    port = 29600 + ["fused", "fused-push", "allreduce"].index(dp) * 10 + (precision == "bf16")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tools", "dist_parity.py"), "--precision", precision, "--dp", dp,
@@ -35,5 +35,5 @@ def test_dp_two_ranks(dp, precision):
     tol = 1e-5 if precision == "fp32" else 2e-2
     assert res["ok"] and res["theta_err"] < tol and res["m_err"] < tol, res
     assert rep["replicas_identical"]
-    if dp == "fused" and precision == "bf16":   # push mode ran: it must equal pull mode bitwise
+    if dp == "fused-push" and precision == "bf16":   # push ran: it must equal pull bitwise
         assert next(x for x in lines if "push_equals_pull" in x)["push_equals_pull"]

@@ -25,7 +25,7 @@ from paper_1912_06680_b200 import dist as pdist  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--precision", default="fp32")
-ap.add_argument("--dp", default="allreduce", choices=("allreduce", "fused", "fused-pull"))
+ap.add_argument("--dp", default="allreduce", choices=("allreduce", "fused", "fused-push"))
 ap.add_argument("--steps", type=int, default=1)
 a = ap.parse_args()
 rank, world, local = pdist.env()
@@ -81,12 +81,12 @@ dist.all_reduce(flag, op=dist.ReduceOp.MIN)
 if rank == 0:
     print(json.dumps({"replicas_identical": bool(flag.item())}), flush=True)
 from paper_1912_06680_b200 import _lib as L  # noqa: E402
-if a.dp == "fused" and opt.dp_push:
+if a.dp == "fused-push" and opt.dp_push:
     # push mode (gradient shards delivered by the backward's epilogues) against pull mode
     # (owners read them after the backward) on a second communicator: the same bits
     comm2 = pdist.make_comm(dev)
     opt2 = PPOOptimizer(cfg.D, cfg.H, Bs, cfg.T, cfg.head_sizes, precision=a.precision,
-                        device=dev, comm=comm2, dp="fused-pull")
+                        device=dev, comm=comm2, dp="fused")
     load_params(opt2, case["params"], device=dev)
     for _ in range(a.steps):
         opt2.step(shard)
