@@ -1045,6 +1045,49 @@ struct EpiStoreF32 {
   int M, N;
   int64_t split_stride;  // elements between split-K partial outputs
   int accumulate;        // 1: out += acc (K-chunked launches after the first)
+  template <int BN>
+  __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
+                                        int split) const {
+    const int m = m_base + row;
+    const bool vec = (N % 4 == 0) && (ldc % 4 == 0);
+#pragma unroll 1
+    for (int c = 0; c < BN / 16; ++c) {
+      float v[16];
+      tmem_ld16(taddr + c * 16, v);
+      const int n0 = n_base + c * 16;
+      if (m >= M || n0 >= N) continue;
+      float* dst = out + split * split_stride + static_cast<int64_t>(m) * ldc + n0;
+      if (vec && n0 + 16 <= N) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          if (accumulate) {
+            const float4 p = d4[q];
+            o.x += p.x;
+            o.y += p.y;
+            o.z += p.z;
+            o.w += p.w;
+          }
+          d4[q] = o;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (n0 + i < N) dst[i] = accumulate ? dst[i] + v[i] : v[i];
+      }
+    }
+  }
+};
+
+// EpiStoreF32 whose final values also go to the DP owners' staging (fused exchange, push
+// mode; a separate type so the default launches keep the lean epilogue)
+struct EpiStoreF32Dp {
+  float* out;
+  int64_t ldc;
+  int M, N;
+  int64_t split_stride;  // elements between split-K partial outputs
+  int accumulate;        // 1: out += acc (K-chunked launches after the first)
   // final values also pushed to the DP owners' staging (fused exchange, push mode): element
   // (m, n) is theta element dp_base + m * ldc + n; dp.world == 0: off
   ppo::DpStage dp{};

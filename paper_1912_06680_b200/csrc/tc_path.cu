@@ -337,11 +337,18 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
       sh.kb_off = kb0;
       sh.sched = sched_counter(kSchedWgrad);
       tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx, 0, c > 0 ? 1 : 0};
-      // the last chunk's tiles are final: their epilogues push them to the DP owners over
-      // NVLink while the remaining tiles are still being multiplied
-      if (dp && c == nchunks - 1) epi.dp = *dp;
-      rc = pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
-                : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st);
+      if (dp && c == nchunks - 1) {
+        // the last chunk's tiles are final: their epilogues push them to the DP owners over
+        // NVLink while the remaining tiles are still being multiplied
+        tc::EpiStoreF32Dp epd{grad, s.Kx, (int)s.G4, (int)s.Kx, 0, c > 0 ? 1 : 0};
+        epd.dp = *dp;
+        rc = pair ? launch2<true, true, tc::EpiStoreF32Dp, 2>("wgrad_xh", wa, wa, wb, wb, sh, epd,
+                                                             st)
+                  : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epd, st);
+      } else {
+        rc = pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
+                  : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st);
+      }
       if (rc) return rc;
     }
   }
@@ -362,11 +369,15 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
                                 : dwo;
     tc::EpiStoreF32 epi{part, s.Ko, (int)s.A, (int)s.Ko, n_o};
     if (dp && sh.ksplit == 1) {
-      epi.dp = *dp;
-      epi.dp_base = s.G4 * s.Kx;
+      tc::EpiStoreF32Dp epd{part, s.Ko, (int)s.A, (int)s.Ko, n_o};
+      epd.dp = *dp;
+      epd.dp_base = s.G4 * s.Kx;
+      rc = pair_o ? launch2<true, true>("wgrad_o", oa, oa, ob, ob, sh, epd, st)
+                  : launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epd, st);
+    } else {
+      rc = pair_o ? launch2<true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st)
+                  : launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st);
     }
-    rc = pair_o ? launch2<true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st)
-                : launch<256, true, true>("wgrad_o", oa, oa, ob, ob, sh, epi, st);
     if (rc) return rc;
     if (sh.ksplit > 1 &&
         (rc = launch_splitk_reduce(part, sh.ksplit, (size_t)n_o, dwo, st, dp, s.G4 * s.Kx)))
