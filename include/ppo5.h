@@ -238,9 +238,10 @@ int ppo_comm_destroy(ppo_comm* comm);
  * in rank order (so the average is the same bits wherever it is formed), scales by 1/world,
  * applies a10 to its shard of theta, m and v, and stores what the forward reads into every
  * rank's copy: the bf16 shadow when there is one (theta, m, v then stay sharded -- current on
- * each rank's own shard only, until ppo_dp_allgather), else theta (fp32 path).  A 1-float NCCL allreduce before and after the
- * kernel orders it against the peers' backward and next forward (stream-ordered; no spinning
- * kernel).  The all-gathered copies are bitwise identical on all ranks. */
+ * each rank's own shard only, until ppo_dp_allgather), else theta (fp32 path).  A 1-float
+ * NCCL allreduce before and after the kernel orders it against the peers' backward and next
+ * forward (stream-ordered; no spinning kernel).  The all-gathered copies are bitwise
+ * identical on all ranks. */
 #define PPO_DP_MAX_RANKS 8
 /* floats per shard (a multiple of 64) */
 size_t ppo_dp_shard(size_t n, int world);
@@ -267,8 +268,9 @@ int ppo_dp_adam_step(ppo_comm* comm, float* m, float* v, int64_t t, double lr, d
  * tile and ppo_dp_adam_step reads only local memory.  Same bits as pull mode.  grad still
  * receives this rank's own gradient (measured: Adam 0.4-0.55 ms instead of 0.75-1.0 ms, but
  * the whole step 1-1.5% slower than pull mode).  bf16 path without the win-head
- * trunk route only
- * (PPO_E_UNSUPPORTED otherwise: use lstm_bptt_bwd + staged = 0); comm attached, world > 1. */
+ * trunk route only (PPO_E_UNSUPPORTED otherwise: use lstm_bptt_bwd + staged = 0); comm
+ * attached with world > 1 (PPO_E_ARG otherwise); the attached n must be this model's theta
+ * length (PPO_E_SHAPE).  Asynchronous on s, like lstm_bptt_bwd. */
 int lstm_bptt_bwd_dp(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
                      const void* dout, int64_t B, float* grad, ppo_comm* comm, ppo_stream_t s);
 /* Collective: in-place all-gather of a sharded fp32 vector (m, v, theta before a checkpoint).
