@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libppo5.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_1912_06680_b200.build` "
+    raise ImportError(f"{LIB_PATH} is not built; run `python paper_1912_06680_b200/build.py` "
                       "(or __graft_entry__.build()).  There is no CPU fallback.")
 
 import torch  # noqa: E402,F401  -- load torch (and its NCCL) before libppo5 links against it
