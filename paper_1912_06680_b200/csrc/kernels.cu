@@ -233,11 +233,14 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
           if (i >= i_lo && i < i_hi) {
             const int64_t t = t0 + i;
             const float nd = dd[t] ? 0.f : 1.f;
-            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vv[t];
+            const float vt = vv[t];
+            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vt;
             cf[i] = gl * nd;
+            vkeep[i] = vt;
           } else {
             delta[i] = 0.f;
             cf[i] = 1.f;
+            vkeep[i] = 0.f;
           }
         }
       }
@@ -297,7 +300,7 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
               o = r * L + t;
             }
             adv[o] = Aout[i];
-            ret[o] = Aout[i] + vv[t];
+            ret[o] = Aout[i] + vkeep[i];   // V_t as loaded (no second read)
           }
         }
       }
@@ -382,11 +385,14 @@ __global__ void gae_kernel_np(const float* __restrict__ rew, const float* __rest
           if (i >= i_lo && i < i_hi) {
             const int64_t t = t0 + i;
             const float nd = dd[t] ? 0.f : 1.f;
-            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vv[t];
+            const float vt = vv[t];
+            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vt;
             cf[i] = gl * nd;
+            vkeep[i] = vt;
           } else {
             delta[i] = 0.f;
             cf[i] = 1.f;
+            vkeep[i] = 0.f;
           }
         }
       }
@@ -433,7 +439,7 @@ __global__ void gae_kernel_np(const float* __restrict__ rew, const float* __rest
               o = r * L + t;
             }
             adv[o] = Aout[i];
-            ret[o] = Aout[i] + vv[t];
+            ret[o] = Aout[i] + vkeep[i];   // V_t as loaded (no second read)
           }
         }
       }
