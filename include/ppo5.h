@@ -17,6 +17,9 @@
  *     them after synchronising and aborts the step.
  *   - Results are deterministic for fixed inputs and world size (no float atomics).
  *   - bf16 values are passed as uint16_t bit patterns.
+ *   - Empty inputs: elementwise calls (ppo_gae with R*L = 0, adam_step with n = 0) are
+ *     no-ops returning PPO_OK before any pointer check; the LSTM and loss calls need
+ *     B >= 1 (PPO_E_SHAPE otherwise).
  */
 #ifndef PPO5_H
 #define PPO5_H

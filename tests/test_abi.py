@@ -123,3 +123,21 @@ def test_dp_fused_host_checks(lib):
                                      None) == lib.PPO_E_ARG
     assert lib._lib.ppo_dp_allgather(None, None, None) == lib.PPO_E_ARG
     assert "comm is NULL" in lib.last_error()
+
+
+def test_empty_and_degenerate_sizes(lib):
+    """Empty elementwise inputs are no-ops (before any pointer check); B = 0 is rejected by
+    the LSTM and loss calls (include/ppo5.h, conventions) -- all decided on the host."""
+    assert lib._lib.adam_step(None, None, None, None, None, 0, 1, 1e-3, 0.9, 0.999, 1e-8, 5.0,
+                              None) == lib.PPO_OK
+    assert lib._lib.ppo_gae(None, None, None, 3, 0, 0.99, 0.95, 0, None, None, None, 0,
+                            None) == lib.PPO_OK
+    assert lib._lib.ppo_gae(None, None, None, -1, 4, 0.99, 0.95, 0, None, None, None, 0,
+                            None) == lib.PPO_E_SHAPE
+    assert lib.gae_scratch_bytes(0, 10 ** 6) == 0
+    d = lib.make_dims(256, 128, 16, (30, 4, 189, 189, 81, 81, 81))
+    rc = lib._lib.lstm_bptt_bwd(ctypes.byref(d), None, None, 0, None, 0, None, None)
+    assert rc == lib.PPO_E_SHAPE and "B must be >= 1" in lib.last_error()
+    rc = lib._lib.ppo_loss_grad(ctypes.byref(d), None, None, None, None, None, None, None, None,
+                                None, 0, None, None, None, None, None)
+    assert rc == lib.PPO_E_SHAPE and "B must be >= 1" in lib.last_error()
