@@ -1,5 +1,7 @@
 """Parity at BASELINE.json's full size, in the launch configuration bench.py times
-(H=4096, D=4032, T=16, B=38,400 sequences, bf16 tcgen05 path), on sampled outputs.
+(H=4096, D=4032, T=16, B=38,400 sequences, bf16 tcgen05 path), on sampled outputs -- and
+again at the maximum minibatch that fits 180 GB (B_max = 123,648 sequences, 170 GB,
+profiles/r01_sweep_B_v3.jsonl), the largest launch the library supports on one B200.
 
 The GPU runs the whole step over all 38,400 sequences.  Per-sequence quantities (GAE of a
 rollout stream, the forward pass of a sequence, the loss gradient of a row) are checked one
@@ -7,6 +9,8 @@ by one against the float64 oracle.  For the weight gradients, every row outside 
 sequences is masked (valid = 0): their dL/dy is exactly zero, so dW is the sum over the sampled
 sequences only, which the oracle computes with the same denominator T*B.  Adam is checked on
 sampled elements of the GPU's own gradient."""
+import gc
+
 import numpy as np
 import pytest
 import torch
@@ -18,16 +22,25 @@ from oracle.step import loss_and_grads
 
 pytestmark = pytest.mark.gpu
 
-CFG = synth.Config(H=4096, D=4032, B=38400)
-SAMPLE_SEQ = (0, 12345, 38399)          # sampled sequences (first, middle, last tile)
-SAMPLE_STREAMS = (0, 771, 2399)          # rollout streams of 256 steps (16 sequences each)
+B_BENCH, B_MAX = 38400, 123648
 
 
-@pytest.fixture(scope="module")
-def run():
+@pytest.fixture(scope="module", params=[B_BENCH, B_MAX], ids=["B38400", "Bmax123648"])
+def run(request):
+    res = _run(request.param)
+    yield res
+    res.clear()
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def _run(B_total):
     from paper_1912_06680_b200 import PPOOptimizer
     dev = "cuda"
-    cfg = CFG
+    cfg = synth.Config(H=4096, D=4032, B=B_total)
+    # sampled sequences (first, middle, last tile); rollout streams of 256 steps (16 sequences)
+    SAMPLE_SEQ = (0, 12345, B_total - 1)
+    SAMPLE_STREAMS = (0, 771, B_total // 16 - 1)
     T, B, H, D = cfg.T, cfg.B, cfg.H, cfg.D
     prm = synth.torch_params(cfg, 3, dev, bo_scale=0.05)
     prm["Wo"] *= 5.0
@@ -78,12 +91,12 @@ def run():
     Lref, gref, st, inter = loss_and_grads(p64, hseq, lp_old_s.astype(np.float64), adv_s, ret_s,
                                            cfg.head_sizes, HYPER["clip_eps"], HYPER["c_v"],
                                            HYPER["c_e"], denom=float(T * B))
-    return dict(opt=opt, batch=batch, theta0=theta0, gae_ref=gae_ref, gref=gref, st=st,
+    return dict(cfg=cfg, opt=opt, batch=batch, theta0=theta0, gae_ref=gae_ref, gref=gref, st=st,
                 inter=inter, sidx=sidx, adv_s=adv_s, ret_s=ret_s, lp_old_s=lp_old_s)
 
 
 def test_gae_sampled_streams(run):
-    opt, T = run["opt"], CFG.T
+    opt, T = run["opt"], run["cfg"].T
     adv = opt.adv.cpu().numpy()
     ret = opt.ret.cpu().numpy()
     for r, (A, R) in run["gae_ref"].items():
@@ -96,7 +109,7 @@ def test_gae_sampled_streams(run):
 
 
 def test_forward_sampled_sequences(run):
-    opt, T, B = run["opt"], CFG.T, CFG.B
+    opt, T, B = run["opt"], run["cfg"].T, run["cfg"].B
     Y = opt.out.view(T, B, -1)[:, run["sidx"]].cpu().numpy().reshape(T * len(run["sidx"]), -1)
     e = normwise(Y, run["inter"]["Y"])
     assert e < 2e-2, e
@@ -105,14 +118,14 @@ def test_forward_sampled_sequences(run):
 def test_loss_rows_sampled(run):
     """dL/dy of the sampled rows from the oracle loss fed the GPU's own head outputs (the
     loss is row-local given y), with the full-batch denominator."""
-    opt, T, B = run["opt"], CFG.T, CFG.B
+    opt, T, B = run["opt"], run["cfg"].T, run["cfg"].B
     sidx = run["sidx"]
     Y = opt.out.view(T, B, -1)[:, sidx].cpu().numpy().reshape(T * len(sidx), -1)
     b = run["batch"]
     pick = lambda k: b[k][:, sidx].cpu().numpy().reshape(T * len(sidx), -1)
     _, dYref, _, lpref = oracle.ppo_loss(Y, pick("act"), pick("head_on"), pick("avail"),
                                          run["lp_old_s"].reshape(-1), run["adv_s"].reshape(-1),
-                                         run["ret_s"].reshape(-1), None, CFG.head_sizes,
+                                         run["ret_s"].reshape(-1), None, run["cfg"].head_sizes,
                                          HYPER["clip_eps"], HYPER["c_v"], HYPER["c_e"],
                                          denom=float(T * B))
     d = opt.dout.view(T, B, -1)[:, sidx].float().cpu().numpy().reshape(T * len(sidx), -1)
@@ -123,7 +136,9 @@ def test_loss_rows_sampled(run):
     # every other row is masked: exactly zero gradient
     mask = torch.ones(B, dtype=torch.bool, device="cuda")
     mask[sidx] = False
-    assert int(torch.count_nonzero(opt.dout.view(T, B, -1)[:, mask])) == 0
+    dout = opt.dout.view(T, B, -1)
+    for t in range(T):  # one time slice at a time: no multi-GB temporary at B_max
+        assert int(torch.count_nonzero(dout[t, mask])) == 0, t
 
 
 def test_weight_gradients_masked_batch(run):
