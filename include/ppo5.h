@@ -16,6 +16,10 @@
  *     action, empty availability row) set bits in stats[PPO_STAT_FLAGS]; the caller checks
  *     them after synchronising and aborts the step.
  *   - Results are deterministic for fixed inputs and world size (no float atomics).
+ *   - A workspace (lstm_ws_bytes / ppo_infer_ws_bytes) serves one call at a time: it holds
+ *     the saved activations and the tile-scheduler counters of the GEMMs launched on it.
+ *     Calls in flight concurrently (two streams, two optimizers) must use distinct
+ *     workspaces; nothing else in the library is shared between streams.
  *   - bf16 values are passed as uint16_t bit patterns.
  *   - Empty inputs: elementwise calls (ppo_gae with R*L = 0, adam_step with n = 0) are
  *     no-ops returning PPO_OK before any pointer check; the LSTM and loss calls need
@@ -280,6 +284,23 @@ int lstm_bptt_bwd_dp(const ppo_dims* dims, const void* w, void* ws, size_t ws_by
  * buf holds world * ppo_dp_shard(n, world) floats (n = the attached length; the slack past n
  * is scratch). */
 int ppo_dp_allgather(ppo_comm* comm, float* buf, ppo_stream_t s);
+
+/* Test hook (not part of the step): the fused kernel of ppo_dp_adam_step, run for `world`
+ * (1..PPO_DP_MAX_RANKS) VIRTUAL ranks on the current device, so the reduce-scatter / Adam /
+ * all-gather arithmetic at world 2, 4 and 8 is checkable on a one-GPU box.  Every argument
+ * but n and the scalars is a HOST array of `world` device pointers, entry j = virtual rank
+ * j's buffer: g [n] fp32 gradients; p [n] fp32 theta; p_bf16 [n] bf16 shadows (the array, or
+ * its entry 0, NULL = fp32 path); m, v [n] fp32 moments; stage (array nullable = pull mode):
+ * rank j's push-mode staging of world x ppo_dp_shard(n, world) floats, slot i = rank i's
+ * gradient over rank j's shard (what lstm_bptt_bwd_dp delivers).  The kernel is launched once
+ * per virtual rank r, in rank order on s, with r's shard [r s, min(n, (r+1) s)); the stream
+ * order replaces the two NCCL barriers.  Afterwards, exactly as on `world` GPUs: m[r], v[r]
+ * (and p[r] when there is a shadow) are updated on r's shard only; every p_bf16[j] (fp32
+ * path: every p[j]) holds the whole updated vector.  16-byte aligned; asynchronous. */
+int ppo_test_dp_adam(int32_t world, const float* const* g, float* const* p,
+                     uint16_t* const* p_bf16, float* const* m, float* const* v,
+                     const float* const* stage, size_t n, int64_t t, double lr, double b1,
+                     double b2, double eps, double clip_sigma, ppo_stream_t s);
 
 /* ---- a10: Adam with the +-clip_sigma sqrt(v) clip (O10, Q3, Q4) --
  *   v <- b2 v + (1-b2) g^2;  g_c = clamp(g, +-clip_sigma sqrt(v));  m <- b1 m + (1-b1) g_c

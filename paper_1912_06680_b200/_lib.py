@@ -114,6 +114,8 @@ _lib_fns = dict(
     lstm_bptt_bwd_dp=([_D, c_void_p, c_void_p, c_size_t, c_void_p, c_int64, c_void_p, c_void_p,
                        c_void_p], c_int),
     ppo_dp_allgather=([c_void_p, c_void_p, c_void_p], c_int),
+    ppo_test_dp_adam=([c_int32] + [POINTER(c_void_p)] * 6 + [c_size_t, c_int64, c_double,
+                      c_double, c_double, c_double, c_double, c_void_p], c_int),
     adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_double,
                 c_double, c_double, c_double, c_double, c_void_p], c_int),
     ppo_sample_indices=([c_int64, c_int64, ctypes.c_uint64, ctypes.c_uint64, c_void_p, c_void_p], c_int),
@@ -401,6 +403,17 @@ def lstm_bptt_bwd_dp(dims, w, ws, dout, B, grad, comm, stream=None):
 
 def dp_allgather(comm, buf, stream=None):
     _check(_lib.ppo_dp_allgather(comm, _p(buf), _s(stream)))
+
+
+def test_dp_adam(g, p, p_bf16, m, v, t, lr, b1, b2, eps, clip_sigma, stage=None, stream=None):
+    """the fused a9+a10 kernel for len(g) virtual ranks on this device (lists of tensors;
+    p_bf16 / stage None = fp32 path / pull mode)"""
+    W = len(g)
+
+    def arr(ts):
+        return None if ts is None else (c_void_p * W)(*[t.data_ptr() for t in ts])
+    _check(_lib.ppo_test_dp_adam(W, arr(g), arr(p), arr(p_bf16), arr(m), arr(v), arr(stage),
+                                 g[0].numel(), t, lr, b1, b2, eps, clip_sigma, _s(stream)))
 
 
 def prof_start():

@@ -28,6 +28,11 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
 if _NCCL:
     FLAGS.append("-I" + os.path.join(_NCCL, "include"))
+# A/B timing builds only: PPO_EXPERIMENTS=1 compiles in the PPO_* environment overrides
+# (common.cuh knob()); a release build reads no environment variable
+if os.environ.get("PPO_EXPERIMENTS", "0") not in ("", "0"):
+    FLAGS.append("-DPPO_EXPERIMENTS")
+STAMP = os.path.join(CSRC, ".build_flags")
 
 
 def _stale(obj, deps):
@@ -38,6 +43,14 @@ def _stale(obj, deps):
 
 
 def build(verbose: bool = False, jobs: int = 4) -> str:
+    flags = " ".join(FLAGS)
+    if not os.path.exists(STAMP) or open(STAMP).read() != flags:
+        # other flags than the last build (e.g. an experiments build): rebuild everything
+        for f in os.listdir(CSRC):
+            if f.endswith(".o"):
+                os.remove(os.path.join(CSRC, f))
+        if os.path.exists(OUT):
+            os.remove(OUT)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "ppo5.h"))
     objs, procs = [], []
@@ -67,6 +80,8 @@ def build(verbose: bool = False, jobs: int = 4) -> str:
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs,
                *link]
         subprocess.run(cmd, check=True)
+    with open(STAMP, "w") as f:
+        f.write(flags)
     return OUT
 
 

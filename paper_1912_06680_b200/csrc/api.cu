@@ -141,6 +141,8 @@ WsLayout ws_layout(const Shape& s, int64_t B) {
   if (!s.bf16) off = align_up(off + (size_t)B * s.G4 * 4, 1024);
   L.splitk = off;  // split-K partials of dW_o (bf16 path)
   if (s.bf16) off = align_up(off + (size_t)kMaxSplitK * s.A * s.Ko * 4, 1024);
+  L.sched = off;   // tile-scheduler counters of this workspace's GEMMs
+  off = align_up(off + kSchedBytes, 1024);
   L.total = off;
   return L;
 }
@@ -533,14 +535,7 @@ int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, si
   if (p_bf16 && !aligned(p_bf16, 16)) return fail(PPO_E_ALIGN, "p_bf16 is not 16-byte aligned");
   if (t < 1) return fail(PPO_E_ARG, "t must be >= 1");
   if (!(b1 >= 0.0 && b1 < 1.0 && b2 >= 0.0 && b2 < 1.0)) return fail(PPO_E_ARG, "bad betas");
-  AdamParams ap;
-  ap.alpha = (float)(lr * sqrt(1.0 - pow(b2, (double)t)) / (1.0 - pow(b1, (double)t)));
-  ap.b1 = (float)b1;
-  ap.omb1 = (float)(1.0 - b1);
-  ap.b2 = (float)b2;
-  ap.omb2 = (float)(1.0 - b2);
-  ap.eps = (float)eps;
-  ap.clip = (clip_sigma > 0.0 && isfinite(clip_sigma)) ? (float)clip_sigma : 0.f;
+  const AdamParams ap = make_adam_params(t, lr, b1, b2, eps, clip_sigma);
   return launch_adam(p, p_bf16, g, m, v, n, ap, (cudaStream_t)st);
 }
 

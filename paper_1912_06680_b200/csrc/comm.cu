@@ -209,6 +209,21 @@ __global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int
   __threadfence_system();
 }
 
+int launch_dp_adam(const DpPeers& pe, int world, int rank, size_t lo, size_t hi, float* m,
+                   float* v, const ppo::AdamParams& ap, const float* stage, size_t shard,
+                   cudaStream_t st) {
+  ppo::ProfScope _prof("dp_adam", st);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t units = (hi - lo) / 4 + 1;
+  const int grid = (int)std::min<size_t>((size_t)sms * 8, (units + 255) / 256);
+  dp_adam_kernel<<<std::max(grid, 1), 256, 0, st>>>(pe, world, rank, lo, hi, m, v, ap,
+                                                    1.0f / (float)world, stage, shard);
+  PPO_LAUNCH_CHECK("dp_adam_kernel");
+  return PPO_OK;
+}
+
 int barrier(ppo_comm* c, cudaStream_t st) {   // stream-ordered: a 1-float NCCL allreduce
   ncclResult_t r = ncclAllReduce(c->sync, c->sync, 1, ncclFloat32, ncclSum, c->comm, st);
   return r == ncclSuccess ? PPO_OK : nccl_fail(r, "ncclAllReduce (barrier)");
@@ -308,31 +323,15 @@ int ppo_dp_adam_step(ppo_comm* c, float* m, float* v, int64_t t, double lr, doub
     return ppo::fail(PPO_E_ALIGN, "m and v must be 16-byte aligned");
   if (t < 1) return ppo::fail(PPO_E_ARG, "t must be >= 1");
   if (!(b1 >= 0.0 && b1 < 1.0 && b2 >= 0.0 && b2 < 1.0)) return ppo::fail(PPO_E_ARG, "bad betas");
-  ppo::AdamParams ap;
-  ap.alpha = (float)(lr * sqrt(1.0 - pow(b2, (double)t)) / (1.0 - pow(b1, (double)t)));
-  ap.b1 = (float)b1;
-  ap.omb1 = (float)(1.0 - b1);
-  ap.b2 = (float)b2;
-  ap.omb2 = (float)(1.0 - b2);
-  ap.eps = (float)eps;
-  ap.clip = (clip_sigma > 0.0 && isfinite(clip_sigma)) ? (float)clip_sigma : 0.f;
+  const ppo::AdamParams ap = ppo::make_adam_params(t, lr, b1, b2, eps, clip_sigma);
   const size_t sh = ppo_dp_shard(c->n, c->world);
   const size_t lo = std::min(c->n, sh * (size_t)c->rank), hi = std::min(c->n, lo + sh);
   cudaStream_t st = (cudaStream_t)s;
   int rc = PPO_OK;
   if (c->world > 1 && (rc = barrier(c, st)) != PPO_OK) return rc;   // every grad is final
-  {
-    ppo::ProfScope _prof("dp_adam", st);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t units = (hi - lo) / 4 + 1;
-    const int grid = (int)std::min<size_t>((size_t)sms * 8, (units + 255) / 256);
-    dp_adam_kernel<<<std::max(grid, 1), 256, 0, st>>>(
-        c->peers, c->world, c->rank, lo, hi, m, v, ap, 1.0f / (float)c->world,
-        staged && c->world > 1 ? c->stage : nullptr, sh);
-    PPO_LAUNCH_CHECK("dp_adam_kernel");
-  }
+  rc = launch_dp_adam(c->peers, c->world, c->rank, lo, hi, m, v, ap,
+                      staged && c->world > 1 ? c->stage : nullptr, sh, st);
+  if (rc != PPO_OK) return rc;
   // every rank's writes into this rank's theta/shadow have landed, and no rank still reads
   // this rank's grad, before the caller's next step
   if (c->world > 1 && (rc = barrier(c, st)) != PPO_OK) return rc;
@@ -348,6 +347,43 @@ int ppo_dp_allgather(ppo_comm* c, float* buf, ppo_stream_t s) {
   ncclResult_t r = ncclAllGather(buf + sh * (size_t)c->rank, buf, sh, ncclFloat32, c->comm,
                                  (cudaStream_t)s);
   return r == ncclSuccess ? PPO_OK : nccl_fail(r, "ncclAllGather");
+}
+
+int ppo_test_dp_adam(int32_t world, const float* const* g, float* const* p,
+                     uint16_t* const* p_bf16, float* const* m, float* const* v,
+                     const float* const* stage, size_t n, int64_t t, double lr, double b1,
+                     double b2, double eps, double clip_sigma, ppo_stream_t s) {
+  if (world < 1 || world > PPO_DP_MAX_RANKS) return ppo::fail(PPO_E_ARG, "world out of range");
+  if (!g || !p || !m || !v) return ppo::fail(PPO_E_ARG, "NULL pointer array");
+  if (t < 1) return ppo::fail(PPO_E_ARG, "t must be >= 1");
+  if (!(b1 >= 0.0 && b1 < 1.0 && b2 >= 0.0 && b2 < 1.0)) return ppo::fail(PPO_E_ARG, "bad betas");
+  if (n == 0) return PPO_OK;
+  DpPeers pe{};
+  const bool shadow = p_bf16 && p_bf16[0];
+  for (int j = 0; j < world; ++j) {
+    if (!g[j] || !p[j] || !m[j] || !v[j] || (shadow && !p_bf16[j]) || (stage && !stage[j]))
+      return ppo::fail(PPO_E_ARG, "NULL buffer of a virtual rank");
+    if (!ppo::aligned(g[j], 16) || !ppo::aligned(p[j], 16) || !ppo::aligned(m[j], 16) ||
+        !ppo::aligned(v[j], 16) || (shadow && !ppo::aligned(p_bf16[j], 16)) ||
+        (stage && !ppo::aligned(stage[j], 16)))
+      return ppo::fail(PPO_E_ALIGN, "dp buffers must be 16-byte aligned");
+    pe.g[j] = g[j];
+    pe.p[j] = p[j];
+    pe.pb[j] = shadow ? reinterpret_cast<__nv_bfloat16*>(p_bf16[j]) : nullptr;
+  }
+  const ppo::AdamParams ap = ppo::make_adam_params(t, lr, b1, b2, eps, clip_sigma);
+  const size_t sh = ppo_dp_shard(n, world);
+  // every virtual rank's launch, in rank order on one stream: the stream order stands in for
+  // the two NCCL barriers of ppo_dp_adam_step (all gradients final before, all peer stores
+  // landed after)
+  for (int r = 0; r < world; ++r) {
+    const size_t lo = std::min(n, sh * (size_t)r), hi = std::min(n, lo + sh);
+    if (lo == hi) continue;
+    const int rc = launch_dp_adam(pe, world, r, lo, hi, m[r], v[r], ap,
+                                  stage && world > 1 ? stage[r] : nullptr, sh, (cudaStream_t)s);
+    if (rc != PPO_OK) return rc;
+  }
+  return PPO_OK;
 }
 
 }  // extern "C"

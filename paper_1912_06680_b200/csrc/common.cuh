@@ -12,6 +12,8 @@
 
 #include <algorithm>
 
+#include <cstdlib>
+
 namespace ppo {
 
 // Fused DP exchange, push mode (comm.cu): where the final gradient of rank `rank` goes --
@@ -46,6 +48,20 @@ int cuda_fail(cudaError_t e, const char* what);
     cudaError_t _e = cudaGetLastError();                        \
     if (_e != cudaSuccess) return ::ppo::cuda_fail(_e, what);   \
   } while (0)
+
+// Experiment knobs (A/B timing builds only).  A release build -- the default, what
+// build.py produces -- reads no environment variable: knob() is constant NULL and every
+// default below is what runs.  Build with -DPPO_EXPERIMENTS (PPO_EXPERIMENTS=1 python
+// build.py) to re-enable the PPO_* overrides the tools/ab_variants.py A/B runs use.
+#ifdef PPO_EXPERIMENTS
+inline const char* knob(const char* name) { return getenv(name); }
+#else
+inline const char* knob(const char*) { return nullptr; }
+#endif
+inline int knob_int(const char* name, int def) {
+  const char* e = knob(name);
+  return e ? atoi(e) : def;
+}
 
 inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
@@ -101,8 +117,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // Workspace regions (byte offsets from ws base); esz = activation element size.
 constexpr int kMaxSplitK = 16;
 struct WsLayout {
-  size_t xh, g, c, dc, raw, splitk, total;
+  size_t xh, g, c, dc, raw, splitk, sched, total;
 };
+// Dynamic tile-scheduler counters live in the caller's workspace (2 x u32 per GEMM call site),
+// so launches on different workspaces -- two optimizers, two streams -- never share one.  The
+// call that launches them zeroes them on its stream first; each kernel leaves its pair zero.
+enum SchedSlot { kSchedFwd = 0, kSchedHeads, kSchedBwd, kSchedWgrad, kSchedWgradO, kSchedDx,
+                 kSchedLstmSlots };
+enum InferSchedSlot { kSchedInferGates = 0, kSchedInferHeads, kSchedInferSlots };
+constexpr size_t kSchedBytes = 64;   // >= 2 * 4 * max(kSchedLstmSlots, kSchedInferSlots)
 WsLayout ws_layout(const Shape& s, int64_t B);
 
 // ---- activation storage type ---------------------------------------------------------------

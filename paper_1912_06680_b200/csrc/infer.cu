@@ -19,7 +19,7 @@ namespace {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct InferLayout {
-  size_t ho, zp, yp, total;
+  size_t ho, zp, yp, sched, total;
 };
 InferLayout infer_layout(const Shape& s, int64_t B) {
   InferLayout L;
@@ -27,7 +27,8 @@ InferLayout infer_layout(const Shape& s, int64_t B) {
   L.ho = 0;
   L.zp = align_up(L.ho + (size_t)B * s.Ko * 2, 1024);
   L.yp = align_up(L.zp + S * s.G4 * B * 4, 1024);
-  L.total = align_up(L.yp + S * s.A * B * 4, 1024);
+  L.sched = align_up(L.yp + S * s.A * B * 4, 1024);
+  L.total = align_up(L.sched + kSchedBytes, 1024);
   return L;
 }
 
@@ -294,9 +295,13 @@ static int infer_impl(const ppo_dims* dims, const void* w, const void* x, float*
   InferLayout L = infer_layout(s, B);
   if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small (ppo_infer_ws_bytes)");
   if ((rc = check_tc_device())) return rc;
+#ifdef PPO_EXPERIMENTS
   // experiment knob (timing breakdowns only; results are wrong when set): skip kernels by bit
-  // 1 state, 2 gates GEMM, 4 cell, 8 heads GEMM, 16 sample
-  static const int skip = getenv("PPO_INFER_SKIP") ? atoi(getenv("PPO_INFER_SKIP")) : 0;
+  // 1 state, 2 gates GEMM, 4 cell, 8 heads GEMM, 16 sample.  Not in release builds.
+  static const int skip = knob_int("PPO_INFER_SKIP", 0);
+#else
+  constexpr int skip = 0;
+#endif
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   auto* ho = reinterpret_cast<__nv_bfloat16*>(wsb + L.ho);
   auto* zp = reinterpret_cast<float*>(wsb + L.zp);
@@ -307,8 +312,15 @@ static int infer_impl(const ppo_dims* dims, const void* w, const void* x, float*
                               dim3(256), 0, st, s, B, (const float*)h, ho));
     PPO_LAUNCH_CHECK("infer_state_kernel");
   }
+  auto* sched = reinterpret_cast<unsigned int*>(wsb + L.sched);
+  if (!(flags & PPO_INFER_STATE_CURRENT)) {
+    // first step on this workspace (or state re-derived): zero its tile-scheduler counters;
+    // afterwards every GEMM leaves its own pair zero, so steady-state steps need no reset
+    ProfScope _prof("sched_reset", st);
+    PPO_CUDA_CHECK(cudaMemsetAsync(sched, 0, kSchedBytes, st));
+  }
   int S = 1;
-  if (!(skip & 2) && (rc = tc_infer_gates(s, B, w, x, ho, zp, &S, st))) return rc;
+  if (!(skip & 2) && (rc = tc_infer_gates(s, B, w, x, ho, zp, &S, sched, st))) return rc;
   if (!(skip & 4)) {
     ProfScope _prof("infer_cell", st);
     PPO_CUDA_CHECK(launch_pdl(infer_cell_kernel, dim3((unsigned)((B * s.H + 255) / 256)), dim3(256),
@@ -316,7 +328,7 @@ static int infer_impl(const ppo_dims* dims, const void* w, const void* x, float*
     PPO_LAUNCH_CHECK("infer_cell_kernel");
   }
   int S2 = 1;
-  if (!(skip & 8) && (rc = tc_infer_heads(s, B, w, ho, yp, &S2, st))) return rc;
+  if (!(skip & 8) && (rc = tc_infer_heads(s, B, w, ho, yp, &S2, sched, st))) return rc;
   if (!(skip & 16)) {
     ProfScope _prof("infer_sample", st);
     PPO_CUDA_CHECK(launch_pdl(infer_sample_kernel, dim3((unsigned)B), dim3(kSampleThreads),

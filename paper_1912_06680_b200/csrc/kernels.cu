@@ -147,6 +147,9 @@ __global__ void __launch_bounds__(256) pack_state_kernel(Shape s, int64_t B,
 // and the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
 // across lanes with a reverse shuffle scan of affine maps (oracle O2).  CH = 8 when there are
 // enough streams to fill the GPU; CH = 16 doubles the loads in flight per warp otherwise.
+// PF = true: the next (earlier) window's loads are issued before this window's scan (more
+// registers, more bytes in flight per warp); PF = false: each window loads just before use
+// (fewest registers, for launches with enough warps to hide the latency).
 template <int CH, bool PF>
 __global__ void gae_kernel(const float* __restrict__ rew, const float* __restrict__ val,
                            const uint8_t* __restrict__ done, int64_t R, int64_t L, float gamma,
@@ -206,11 +209,12 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
     int i_lo, i_hi;
     bool full;
     window(w_end, w_start, t0, i_lo, i_hi, full);
-    if (full) prefetch(t0);
+    if (PF && full) prefetch(t0);
     while (w_end > 0) {
       const int n = i_hi;     // (kept for the store path: valid steps are [i_lo, i_hi))
       float delta[CH], cf[CH], vkeep[CH];
       if (full) {
+        if (!PF) prefetch(t0);
         float rv[CH], v[CH + 1];
         uint2 dw[CH / 8];
 #pragma unroll
@@ -308,143 +312,6 @@ __global__ void gae_kernel(const float* __restrict__ rew, const float* __restric
       (void)cur_ws;
       (void)nxt_loaded;
       w_end = nxt_end;
-    }
-  }
-}
-
-
-// (No-prefetch variant: fewest registers, for launches with enough warps to hide latency.)
-// One warp per rollout stream; windows of 32*CH steps from the end; each lane owns CH steps
-// and the affine recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lam (1-d_t)) is combined
-// across lanes with a reverse shuffle scan of affine maps (oracle O2).  CH = 8 when there are
-// enough streams to fill the GPU; CH = 16 doubles the loads in flight per warp otherwise.
-template <int CH>
-__global__ void gae_kernel_np(const float* __restrict__ rew, const float* __restrict__ val,
-                           const uint8_t* __restrict__ done, int64_t R, int64_t L, float gamma,
-                           float lam, int seq_T, float* __restrict__ adv, float* __restrict__ ret,
-                           bool vec) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const float gl = gamma * lam;
-  const int64_t spr = seq_T > 0 ? L / seq_T : 0;  // sequences per rollout
-  const int64_t nseq = R * spr;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
-    const float* rr = rew + r * L;
-    const float* vv = val + r * (L + 1);
-    const uint8_t* dd = done + r * L;
-    float carry = 0.f;
-    // Windows of <= W = 32*CH steps from the end.  Lane chunks sit on global multiples of 8
-    // steps (window starts are rounded up to them; the row's first window starts its lane 0
-    // early and masks the steps before the row), so every full chunk is 32-byte aligned in
-    // r, A, R and 8-byte aligned in d, whatever L is.  (V has row stride L + 1: shifted
-    // loads.)  Steps outside [w_start, w_end) are identities (delta 0, c 1).
-    constexpr int W = 32 * CH;
-    const int64_t g0 = r * L;
-    const int64_t sh0 = g0 & 7;
-    int64_t w_end = L;
-    while (w_end > 0) {
-      int64_t w_start = w_end - W;
-      if (w_start <= 0 && w_end + sh0 <= W) {
-        w_start = 0;
-      } else {
-        if (w_start < 8) w_start = 8;
-        w_start += (8 - ((g0 + w_start) & 7)) & 7;
-      }
-      const int64_t t0 = w_start - ((g0 + w_start) & 7) + CH * lane;   // chunk [t0, t0 + CH)
-      const int i_lo = (int)min((int64_t)CH, max((int64_t)0, w_start - t0));
-      const int i_hi = (int)max((int64_t)0, min((int64_t)CH, w_end - t0));
-      const int n = i_hi;     // (kept for the store path: valid steps are [i_lo, i_hi))
-      const bool full = vec && i_lo == 0 && i_hi == CH;   // vec: bases allow the alignment
-      float delta[CH], cf[CH], vkeep[CH];
-      if (full) {
-        float rv[CH], v[CH + 1];
-        const float4* r4 = reinterpret_cast<const float4*>(rr + t0);
-#pragma unroll
-        for (int q = 0; q < CH / 4; ++q) {
-          const float4 a4 = __ldcs(r4 + q);
-          rv[4 * q] = a4.x;
-          rv[4 * q + 1] = a4.y;
-          rv[4 * q + 2] = a4.z;
-          rv[4 * q + 3] = a4.w;
-        }
-        load_floats<CH + 1>(vv + t0, v, val + R * (L + 1));
-        uint2 dw[CH / 8];
-#pragma unroll
-        for (int q = 0; q < CH / 8; ++q) dw[q] = __ldcs(reinterpret_cast<const uint2*>(dd + t0) + q);
-        const uint8_t* db = reinterpret_cast<const uint8_t*>(dw);
-#pragma unroll
-        for (int i = 0; i < CH; ++i) {
-          const float nd = db[i] ? 0.f : 1.f;
-          delta[i] = rv[i] + gamma * nd * v[i + 1] - v[i];
-          cf[i] = gl * nd;
-          vkeep[i] = v[i];
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < CH; ++i) {
-          if (i >= i_lo && i < i_hi) {
-            const int64_t t = t0 + i;
-            const float nd = dd[t] ? 0.f : 1.f;
-            const float vt = vv[t];
-            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vt;
-            cf[i] = gl * nd;
-            vkeep[i] = vt;
-          } else {
-            delta[i] = 0.f;
-            cf[i] = 1.f;
-            vkeep[i] = 0.f;
-          }
-        }
-      }
-      float P = 0.f, Q = 1.f;  // A_first = P + Q * A_after
-#pragma unroll
-      for (int i = CH - 1; i >= 0; --i) {
-        P = delta[i] + cf[i] * P;
-        Q = cf[i] * Q;
-      }
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const float P2 = __shfl_down_sync(0xffffffffu, P, off);
-        const float Q2 = __shfl_down_sync(0xffffffffu, Q, off);
-        if (lane + off < 32) {
-          P = P + Q * P2;
-          Q = Q * Q2;
-        }
-      }
-      const float a_first = P + Q * carry;
-      float a = __shfl_down_sync(0xffffffffu, a_first, 1);
-      if (lane == 31) a = carry;
-      float Aout[CH];
-#pragma unroll
-      for (int i = CH - 1; i >= 0; --i) {
-        a = delta[i] + cf[i] * a;
-        Aout[i] = a;
-      }
-      if (seq_T == 0 && full) {
-        float Rout[CH];
-#pragma unroll
-        for (int i = 0; i < CH; ++i) Rout[i] = Aout[i] + vkeep[i];
-        store_floats<CH>(adv + r * L + t0, Aout);
-        store_floats<CH>(ret + r * L + t0, Rout);
-      } else {
-#pragma unroll
-        for (int i = 0; i < CH; ++i) {
-          if (i >= i_lo && i < n) {
-            const int64_t t = t0 + i;
-            int64_t o;
-            if (seq_T > 0) {
-              const int64_t k = t / seq_T, tt = t - k * seq_T;
-              o = tt * nseq + r * spr + k;
-            } else {
-              o = r * L + t;
-            }
-            adv[o] = Aout[i];
-            ret[o] = Aout[i] + vkeep[i];   // V_t as loaded (no second read)
-          }
-        }
-      }
-      carry = __shfl_sync(0xffffffffu, a_first, 0);
-      w_end = w_start;
     }
   }
 }
@@ -1476,7 +1343,7 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
     // loads in flight per warp; 32-step chunks measured slower) in 2-warp blocks spread over
     // all SMs
     if (L <= 256 || R >= 7104)
-      gae_kernel_np<8><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
+      gae_kernel<8, false><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
                                                                seq_T, adv, ret, vec);
     else if (R >= 4736)
       gae_kernel<8, true><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma,
@@ -1517,7 +1384,7 @@ static int launch_loss_fast(const LossParams& p, const float* out, const int32_t
     PPO_CUDA_CHECK(cudaFuncSetAttribute(loss_fast_kernel<TD, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   nblk = std::min(PPO_LOSS_BLOCKS, sms * MINB);
-  if (const char* g = getenv("PPO_LOSS_GRID"))   // experiment knob: grid size
+  if (const char* g = knob("PPO_LOSS_GRID"))   // experiment knob: grid size
     nblk = std::max(1, std::min(PPO_LOSS_BLOCKS, atoi(g)));
   loss_fast_kernel<TD, MINB><<<nblk, 256, smem, st>>>(out, act, head_on, avail, logp_old, adv,
                                                       ret, valid, aux_label, p, (TD*)dout, logp,
@@ -1537,7 +1404,7 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
   for (int k = 0; k <= p.nh && fast; ++k) fast = p.off[k] == fastloss::off(k);
   // rows move by 16-byte TMA bulk copies
   fast = fast && p.A % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  if (const char* e = getenv("PPO_LOSS_GENERIC")) fast = fast && !atoi(e);
+  if (const char* e = knob("PPO_LOSS_GENERIC")) fast = fast && !atoi(e);
   if (fast) {
     ProfScope _prof("loss", st);
     // 2 blocks of 8 warps per SM: 126 registers and 3 row buffers per warp, no spills

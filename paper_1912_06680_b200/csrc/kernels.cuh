@@ -60,6 +60,19 @@ __device__ __forceinline__ void adam_elem(const AdamParams& ap, float g, float& 
   m = __fadd_rn(__fmul_rn(ap.b1, m), __fmul_rn(ap.omb1, gc));
   p = __fsub_rn(p, __fdiv_rn(__fmul_rn(ap.alpha, m), __fadd_rn(sv, ap.eps)));
 }
+// host: alpha_t, 1-b1 and 1-b2 formed in double and rounded once to fp32 (ppo5.h adam_step)
+inline AdamParams make_adam_params(int64_t t, double lr, double b1, double b2, double eps,
+                                   double clip_sigma) {
+  AdamParams ap;
+  ap.alpha = (float)(lr * sqrt(1.0 - pow(b2, (double)t)) / (1.0 - pow(b1, (double)t)));
+  ap.b1 = (float)b1;
+  ap.omb1 = (float)(1.0 - b1);
+  ap.b2 = (float)b2;
+  ap.omb2 = (float)(1.0 - b2);
+  ap.eps = (float)eps;
+  ap.clip = (clip_sigma > 0.0 && isfinite(clip_sigma)) ? (float)clip_sigma : 0.f;
+  return ap;
+}
 int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n,
                 const AdamParams& ap, cudaStream_t st);
 int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int64_t K, float* C,
@@ -85,9 +98,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
 int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx, cudaStream_t st);
 // NEXT-3: split-K skinny GEMMs of the inference step (weights x batch); *split = partials
 int tc_infer_gates(const Shape& s, int64_t B, const void* w, const void* x, const void* ho,
-                   float* part, int* split, cudaStream_t st);
+                   float* part, int* split, unsigned int* sched, cudaStream_t st);
 int tc_infer_heads(const Shape& s, int64_t B, const void* w, const void* ho, float* part,
-                   int* split, cudaStream_t st);
+                   int* split, unsigned int* sched, cudaStream_t st);
 int tc_infer_max_split();
 // pre-tiled inference weights: [128][64] bf16 tiles, gates then heads (elements)
 size_t tc_infer_tiled_offset_heads(const Shape& s);

@@ -1270,7 +1270,7 @@ __device__ __forceinline__ void bwd_load(BwdRaw& r, const __nv_bfloat16* gp, con
   for (int q = 0; q < 2; ++q) {
     r.ct[q] = reinterpret_cast<const float4*>(ct)[q];
     r.cp[q] = reinterpret_cast<const float4*>(cp)[q];
-    r.dc[q] = reinterpret_cast<const float4*>(dc)[q];
+    r.dc[q] = dc ? reinterpret_cast<const float4*>(dc)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
@@ -1294,6 +1294,7 @@ struct EpiLstmBwd {
   float* dc;              // [B][H] carry (in/out)
   int B, H;
   int fast;               // 1: SFU tanh for tanh(c_t)
+  int first;              // 1: t = T-1, the incoming carry is zero (not read; no memset)
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int split) const {
@@ -1309,7 +1310,9 @@ struct EpiLstmBwd {
       return (j0 >> 6) * 256 + (j0 & 63);
     };
     BwdRaw cur, nxt;
-    if (ok && nch > 0) bwd_load(cur, grow + goff(0), c_t + crow, c_prev + crow, dc + crow);
+    const float* dcin = first ? nullptr : dc;
+    if (ok && nch > 0)
+      bwd_load(cur, grow + goff(0), c_t + crow, c_prev + crow, dcin ? dcin + crow : nullptr);
 #pragma unroll 1
     for (int cc = 0; cc < BN / CW; ++cc) {
       float dh[8];
@@ -1317,7 +1320,7 @@ struct EpiLstmBwd {
       if (cc >= nch) continue;
       if (ok && cc + 1 < nch) {
         const int64_t o = crow + (cc + 1) * CW;
-        bwd_load(nxt, grow + goff(cc + 1), c_t + o, c_prev + o, dc + o);
+        bwd_load(nxt, grow + goff(cc + 1), c_t + o, c_prev + o, dcin ? dcin + o : nullptr);
       }
       if (ok) {
         // in place: each 32-bit gate word holds units (2w, 2w+1); dz overwrites the gates

@@ -10,25 +10,21 @@
 namespace ppo {
 namespace {
 
-// Dynamic tile-scheduler counters (zero-initialised; each kernel resets its pair on exit).
-// One slot per GEMM call site, so stream-ordered launches never share a live counter.
-enum SchedSlot {
-  kSchedFwd = 0, kSchedHeads, kSchedBwd, kSchedWgrad, kSchedWgradO, kSchedTest,
-  kSchedInferGates, kSchedInferHeads, kSchedDx, kSchedSlots
-};
-__device__ unsigned int g_sched_ctr[2 * kSchedSlots];
+// Tile-scheduler counters of the standalone test GEMM (ppo_test_tc_gemm, tests only); the
+// step's GEMMs use the counters in their workspace (common.cuh SchedSlot).
+__device__ unsigned int g_test_sched_ctr[2];
 
-unsigned int* sched_counter(int slot) {
+unsigned int* test_sched_counter() {
   static unsigned int* base[64] = {nullptr};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return nullptr;
   if (!base[dev]) {
     void* p = nullptr;
-    if (cudaGetSymbolAddress(&p, g_sched_ctr) != cudaSuccess) return nullptr;
+    if (cudaGetSymbolAddress(&p, g_test_sched_ctr) != cudaSuccess) return nullptr;
     base[dev] = static_cast<unsigned int*>(p);
   }
-  return base[dev] + 2 * slot;
+  return base[dev];
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -88,7 +84,7 @@ int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const 
   if (sh.nkb0 + sh.nkb1 <= 0) return fail(PPO_E_SHAPE, "GEMM with empty K");
   if (!sh.sched) return fail(PPO_E_CUDA, "tile scheduler counter unavailable");
   const int64_t ntiles = (int64_t)((sh.M + tc::BM - 1) / tc::BM) * ((sh.N + BN - 1) / BN);
-  const bool all_tiles = getenv("PPO_GRID_ALL_TILES") && atoi(getenv("PPO_GRID_ALL_TILES"));
+  const bool all_tiles = knob_int("PPO_GRID_ALL_TILES", 0) != 0;
   const int grid = (int)std::min<int64_t>(ntiles * std::max(sh.ksplit, 1),
                                           all_tiles ? (int64_t)1 << 30 : num_sms());
   if (grid <= 0) return PPO_OK;
@@ -120,7 +116,7 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
   const int64_t ntiles = (int64_t)((sh.M + 256 * MB - 1) / (256 * MB)) * ((sh.N + BN - 1) / BN) *
                          std::max(sh.ksplit, 1);
   // PPO_GRID_ALL_TILES=1: one cluster per tile (hardware-ordered dispatch; experiment knob)
-  const bool all_tiles = getenv("PPO_GRID_ALL_TILES") && atoi(getenv("PPO_GRID_ALL_TILES"));
+  const bool all_tiles = knob_int("PPO_GRID_ALL_TILES", 0) != 0;
   const int clusters = (int)std::min<int64_t>(ntiles, all_tiles ? (int64_t)1 << 30 : num_sms() / 2);
   if (clusters <= 0) return PPO_OK;
   ProfScope _prof(tag, st);
@@ -180,7 +176,7 @@ void raster(tc::TileShape& sh, const char* kind, int def_group, int def_n) {
   sh.group_n = def_n;
   char name[64];
   snprintf(name, sizeof(name), "PPO_RASTER_%s", kind);
-  const char* e = getenv(name);
+  const char* e = knob(name);
   if (e && (e[0] == 'm' || e[0] == 'n') && atoi(e + 1) > 0) {
     sh.group_n = e[0] == 'n';
     sh.group = atoi(e + 1);
@@ -193,17 +189,21 @@ void raster(tc::TileShape& sh, const char* kind, int def_group, int def_n) {
 bool use_pair(const char* kind, bool def) {
   char name[64];
   snprintf(name, sizeof(name), "PPO_VARIANT_%s", kind);
-  const char* e = getenv(name);
+  const char* e = knob(name);
   if (!e) return def;
   return strcmp(e, "pair") == 0;
 }
 
-// Experiment knob: PPO_FAST_CELL=1 puts tanh/sigmoid of the fused LSTM epilogues on the SFU
-// (tanh.approx).  Off by default: -3% forward time, but the full-width bf16 weight gradient
-// drifts past the 2e-2 parity bar (0.022 on test_full_width_bf16).
+// Experiment knob (PPO_EXPERIMENTS builds only): PPO_FAST_CELL=1 puts tanh/sigmoid of the
+// fused LSTM epilogues on the SFU (tanh.approx): -3% forward time, but the full-width bf16
+// weight gradient drifts past the 2e-2 parity bar (0.022 on test_full_width_bf16), so a
+// release build always takes the accurate functions.
 int fast_cell() {
-  const char* e = getenv("PPO_FAST_CELL");
-  return e ? atoi(e) != 0 : 0;
+#ifdef PPO_EXPERIMENTS
+  return knob_int("PPO_FAST_CELL", 0) != 0;
+#else
+  return 0;
+#endif
 }
 
 struct WsPtrs {
@@ -211,12 +211,21 @@ struct WsPtrs {
   __nv_bfloat16* g;
   float* c;
   float* dc;
+  unsigned int* sched;   // this workspace's tile-scheduler counters, 2 per SchedSlot
+  unsigned int* slot(int k) const { return sched + 2 * k; }
 };
 WsPtrs ws_ptrs(const Shape& s, int64_t B, void* ws) {
   WsLayout L = ws_layout(s, B);
   uint8_t* p = static_cast<uint8_t*>(ws);
   return {reinterpret_cast<__nv_bfloat16*>(p + L.xh), reinterpret_cast<__nv_bfloat16*>(p + L.g),
-          reinterpret_cast<float*>(p + L.c), reinterpret_cast<float*>(p + L.dc)};
+          reinterpret_cast<float*>(p + L.c), reinterpret_cast<float*>(p + L.dc),
+          reinterpret_cast<unsigned int*>(p + L.sched)};
+}
+// zero the workspace's counters on the stream before its GEMMs (fresh memory is arbitrary)
+int sched_reset(const WsPtrs& P, cudaStream_t st) {
+  ProfScope _prof("sched_reset", st);
+  PPO_CUDA_CHECK(cudaMemsetAsync(P.sched, 0, kSchedBytes, st));
+  return PPO_OK;
 }
 
 }  // namespace
@@ -228,6 +237,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
   const __nv_bfloat16* wxh = static_cast<const __nv_bfloat16*>(w);
   const __nv_bfloat16* wo = wxh + s.G4 * s.Kx;
   int rc;
+  if ((rc = sched_reset(P, st))) return rc;
   // z_t = [x_t | h_{t-1} | 1] W_xh_aug^T : A = XH (3-D, slot t), B = W_xh_aug.
   CUtensorMap mA, mB;
   if ((rc = map_kmajor(&mA, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, tc::BM))) return rc;
@@ -235,7 +245,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
   // experiment: PPO_VARIANT_FWD=pair2 -> 512x256 pair tiles (256 A rows per CTA, one
   // 512-column accumulator): 25% less operand traffic per FLOP (the SMs clock ~15% higher
   // under the power cap) but the fused epilogue is no longer overlapped: 15-25% slower
-  const char* vf = getenv("PPO_VARIANT_FWD");
+  const char* vf = knob("PPO_VARIANT_FWD");
   const bool pair2 = vf && strcmp(vf, "pair2") == 0;
   // experiment: PPO_VARIANT_FWD=pairmc -> two CTA pairs share the weight tile by 2-SM TMA
   // multicast (cluster of 4): the SMs clock ~10% higher (less L2->SM traffic) but the coupled
@@ -250,7 +260,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     if (x_ready && x_ready[t]) PPO_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready[t], 0));
     tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8, 1};
     raster(sh, "FWD", 8, 1);
-    sh.sched = sched_counter(kSchedFwd);
+    sh.sched = P.slot(kSchedFwd);
     tc::TileShape sh1 = sh;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H,
@@ -271,7 +281,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
   if ((rc = map_kmajor(&hB, wo, s.Ko, s.A, s.Ko, 1, 0, pair_h ? 112 : 224))) return rc;
   tc::TileShape sh{(int)(s.T * B), (int)s.A, cdiv(s.Ko, tc::BK), 0, 0, 0, 0, 0, 3, 1};
   raster(sh, "HEADS", 3, 1);
-  sh.sched = sched_counter(kSchedHeads);
+  sh.sched = P.slot(kSchedHeads);
   tc::EpiStoreF32 epi{out, s.A, (int)(s.T * B), (int)s.A};
   if (pair_h)
     return launch2<false, false, tc::EpiStoreF32, 1, 224>("heads_fwd", hA, hA, hB, hB, sh, epi, st);
@@ -286,10 +296,8 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   const __nv_bfloat16* wo = wxh + s.G4 * s.Kx;
   const __nv_bfloat16* dY = static_cast<const __nv_bfloat16*>(dout);
   int rc;
-  {
-    ProfScope _prof("memset_dc", st);
-    PPO_CUDA_CHECK(cudaMemsetAsync(P.dc, 0, B * s.H * sizeof(float), st));
-  }
+  // (the dc carry needs no memset: the t = T-1 epilogue takes it as zero, EpiLstmBwd::first)
+  if ((rc = sched_reset(P, st))) return rc;
   // dh_t = dz_{t+1} W_h + dy_t W_o : A = [G (3-D, slot t+1) | dY (3-D, slot t)] (K-major),
   // B = [W_xh_aug[:, D:D+H] | W_o_aug[:, :H]] read MN-major (K = gate row / head output).
   CUtensorMap a0, a1, b0, b1;
@@ -305,9 +313,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A_pass, tc::BK),
                      t + 1, t, 0, 0, 8, 1};
     raster(sh, "BWD", 8, 1);   // n8: A/B with the current kernels, backward GEMM 0.7-2 ms faster than n4
-    sh.sched = sched_counter(kSchedBwd);
+    sh.sched = P.slot(kSchedBwd);
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
-                       (int)B, (int)s.H, fast_cell()};
+                       (int)B, (int)s.H, fast_cell(), last ? 1 : 0};
     tc::TileShape sh1 = sh;
     rc = pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
               : launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh1, epi, st);
@@ -326,7 +334,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     // and hence power drop; the step is power-capped).  PPO_WGRAD_CHUNK overrides the rows.
     const int nkb_all = cdiv(rows, tc::BK);
     int chunk_kb = 2400;   // 153,600 rows: A/B on two boxes, dW_xh 4.6% faster than 76,800
-    if (const char* e = getenv("PPO_WGRAD_CHUNK")) chunk_kb = std::max(1, atoi(e) / tc::BK);
+    if (const char* e = knob("PPO_WGRAD_CHUNK")) chunk_kb = std::max(1, atoi(e) / tc::BK);
     const int nchunks = std::max(1, (nkb_all + chunk_kb - 1) / chunk_kb);
     const bool pair = use_pair("WGRAD", true);
     for (int c = 0; c < nchunks; ++c) {
@@ -335,7 +343,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
       tc::TileShape sh{(int)s.G4, (int)s.Kx, kb1 - kb0, 0, 0, 0, 0, 0, 8, 0};
       raster(sh, "WGRAD", 8, 1);   // n8: A/B in the step 2-3% faster than m8 (current kernels)
       sh.kb_off = kb0;
-      sh.sched = sched_counter(kSchedWgrad);
+      sh.sched = P.slot(kSchedWgrad);
       tc::EpiStoreF32 epi{grad, s.Kx, (int)s.G4, (int)s.Kx, 0, c > 0 ? 1 : 0};
       if (dp && c == nchunks - 1) {
         // the last chunk's tiles are final: their epilogues push them to the DP owners over
@@ -361,7 +369,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     const bool pair_o = use_pair("WGRAD_O", true);
     const int tiles = pair_o ? cdiv(s.A, 256) * cdiv(s.Ko, 256) : cdiv(s.A, tc::BM) * cdiv(s.Ko, 256);
     sh.ksplit = pick_split(tiles, pair_o ? num_sms() / 2 : num_sms(), cdiv(rows, tc::BK));
-    sh.sched = sched_counter(kSchedWgradO);
+    sh.sched = P.slot(kSchedWgradO);
     float* dwo = grad + s.G4 * s.Kx;
     const int64_t n_o = s.A * s.Ko;
     float* part = sh.ksplit > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) +
@@ -400,9 +408,10 @@ int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx,
   int rc;
   if ((rc = map_kmajor(&ma, P.g, s.G4, rows, s.G4, 1, 0, tc::BM))) return rc;
   if ((rc = map_mnmajor(&mb, wxh, s.D, s.G4, s.Kx))) return rc;
+  if ((rc = sched_reset(P, st))) return rc;
   tc::TileShape sh{(int)rows, (int)s.D, cdiv(s.G4, tc::BK), 0, 0, 0, 0, 0, 8, 0};
   raster(sh, "DX", 8, 0);
-  sh.sched = sched_counter(kSchedDx);
+  sh.sched = P.slot(kSchedDx);
   tc::EpiStoreF32 epi{dx, s.D, (int)rows, (int)s.D};
   return launch2<false, true>("input_grad", ma, ma, mb, mb, sh, epi, st);
 }
@@ -414,7 +423,7 @@ int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx,
 // out[split][b][m] (transposed store); the consumer kernel sums them in split order.
 namespace {
 int infer_split(int tiles, int nkb, int min_kb, const char* knob = "PPO_INFER_SPLIT") {
-  const char* e = getenv(knob);
+  const char* e = ppo::knob(knob);
   if (e && atoi(e) > 0) return std::min(std::min(atoi(e), kMaxSplitK), nkb);
   const int sms = num_sms();
   if (tiles >= sms) return 1;   // the tiles alone fill the machine
@@ -439,7 +448,7 @@ int infer_split(int tiles, int nkb, int min_kb, const char* knob = "PPO_INFER_SP
 template <int BN>
 int infer_gemm_bn(const char* tag, int slot, const void* W, int64_t M, int64_t K,
                   const void* act0, int64_t K0, int64_t ld0, const void* act1, int64_t ld1,
-                  int64_t B, float* part, int* split_out, cudaStream_t st) {
+                  int64_t B, float* part, int* split_out, unsigned int* sched, cudaStream_t st) {
   CUtensorMap ma, mb0, mb1;
   int rc;
   const int nkb = cdiv(K, tc::BK);
@@ -460,8 +469,8 @@ int infer_gemm_bn(const char* tag, int slot, const void* W, int64_t M, int64_t K
                              heads ? "PPO_INFER_SPLIT_HEADS" : "PPO_INFER_SPLIT");
   tc::TileShape sh{(int)M, (int)B, nkb0, nkb - nkb0, 0, 0, 0, 0, 1, 0};
   sh.ksplit = sp;
-  sh.sched = sched_counter(slot);
-  const char* e = getenv("PPO_INFER_EVICT_FIRST");
+  sh.sched = sched + 2 * slot;
+  const char* e = knob("PPO_INFER_EVICT_FIRST");
   sh.a_evict_first = e ? atoi(e) : 1;
   sh.a_tiled_nkb = nkb;
   tc::EpiStoreF32T epi{part, M, (int)M, (int)B, M * B};
@@ -472,13 +481,15 @@ int infer_gemm_bn(const char* tag, int slot, const void* W, int64_t M, int64_t K
 }
 int infer_gemm(const char* tag, int slot, const void* W, int64_t M, int64_t K, const void* act0,
                int64_t K0, int64_t ld0, const void* act1, int64_t ld1, int64_t B, float* part,
-               int* split_out, cudaStream_t st) {
+               int* split_out, unsigned int* sched, cudaStream_t st) {
   if (B <= 64)
-    return infer_gemm_bn<64>(tag, slot, W, M, K, act0, K0, ld0, act1, ld1, B, part, split_out, st);
+    return infer_gemm_bn<64>(tag, slot, W, M, K, act0, K0, ld0, act1, ld1, B, part, split_out,
+                             sched, st);
   if (B <= 128)
     return infer_gemm_bn<128>(tag, slot, W, M, K, act0, K0, ld0, act1, ld1, B, part, split_out,
-                              st);
-  return infer_gemm_bn<256>(tag, slot, W, M, K, act0, K0, ld0, act1, ld1, B, part, split_out, st);
+                              sched, st);
+  return infer_gemm_bn<256>(tag, slot, W, M, K, act0, K0, ld0, act1, ld1, B, part, split_out,
+                            sched, st);
 }
 
 }  // namespace
@@ -490,16 +501,16 @@ size_t tc_infer_tiled_elems(const Shape& s) {
   return tc_infer_tiled_offset_heads(s) + (size_t)cdiv(s.A, tc::BM) * cdiv(s.Ko, tc::BK) * tc::BM * tc::BK;
 }
 int tc_infer_gates(const Shape& s, int64_t B, const void* wt, const void* x, const void* ho,
-                   float* part, int* split, cudaStream_t st) {
+                   float* part, int* split, unsigned int* sched, cudaStream_t st) {
   // [x | h | 1 | 0] = x [B][D] straight from the caller, then the state buffer HO [B][Ko]
   return infer_gemm("infer_gates", kSchedInferGates, wt, s.G4, s.Kx, x, s.D, s.D, ho, s.Ko, B,
-                    part, split, st);
+                    part, split, sched, st);
 }
 int tc_infer_heads(const Shape& s, int64_t B, const void* wt, const void* ho, float* part,
-                   int* split, cudaStream_t st) {
+                   int* split, unsigned int* sched, cudaStream_t st) {
   const __nv_bfloat16* wo = static_cast<const __nv_bfloat16*>(wt) + tc_infer_tiled_offset_heads(s);
   return infer_gemm("infer_heads", kSchedInferHeads, wo, s.A, s.Ko, ho, s.Ko, s.Ko, nullptr, 0, B,
-                    part, split, st);
+                    part, split, sched, st);
 }
 int tc_infer_max_split() { return kMaxSplitK; }
 
@@ -520,7 +531,7 @@ int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N
   if (rc) return rc;
   tc::TileShape sh{M, N, cdiv(K, tc::BK), 0, 0, 0, 0, 0, 16, 0};
   raster(sh, "TEST", 16, 0);
-  sh.sched = sched_counter(kSchedTest);
+  sh.sched = test_sched_counter();
   tc::EpiStoreF32 epi{C, N, M, N};
   const bool wide = mode & 16, n224p = mode & 32;
   if (pair && n224p) {

@@ -164,8 +164,20 @@ class PPOOptimizer:
 
     # ---------------------------------------------------------------- the step
     def gae(self, batch, stream=None):
-        """a1: advantages/returns written time-major [T][B] for the minibatch"""
+        """a1: advantages/returns written time-major [T][B] for the minibatch.  The rollouts
+        must cover exactly this optimizer's B sequences: rew, done [R][L], val [R][L+1],
+        L % T == 0 and R * L / T == B (ppo_gae writes R*L advantages)."""
         h = self.hyper
+        rew, val, done = batch["rew"], batch["val"], batch["done"]
+        if rew.dim() != 2 or tuple(done.shape) != tuple(rew.shape):
+            raise ValueError(f"rew and done must both be [R][L]; got {tuple(rew.shape)}, "
+                             f"{tuple(done.shape)}")
+        R, Lr = rew.shape
+        if tuple(val.shape) != (R, Lr + 1):
+            raise ValueError(f"val must be [R][L+1] = {(R, Lr + 1)}; got {tuple(val.shape)}")
+        if Lr % self.T or R * (Lr // self.T) != self.B:
+            raise ValueError(f"rollouts [{R}][{Lr}] do not hold exactly B = {self.B} sequences "
+                             f"of T = {self.T} steps")
         L.ppo_gae(batch["rew"], batch["val"], batch["done"], self.gamma, h["lam"], self.adv,
                   self.ret, seq_T=self.T, stream=stream)
 

@@ -163,9 +163,137 @@ def test_loss_parity(L, precision, seed, pad, B):
     assert np.all(d[:, :30][av == 0] == 0.0)
     assert np.all(d[valid == 0] == 0.0)
     sv = stats[:8].cpu().numpy()
-    for i, k in enumerate(("loss", "pg", "vf", "ent", "approx_kl", "clipfrac", "n_valid")):
-        assert abs(sv[i] - st[k]) <= 1e-5 * (abs(st[k]) + 1.0), (k, sv[i], st[k])
+    check_loss_stats(sv, st, lpref, logp_old, adv, Y[:, -1], ret, valid, N)
+
+
+def check_loss_stats(sv, st, lpref, logp_old, adv, V, ret, valid, denom, clip_rows=None):
+    """Loss statistics vs the oracle, relative: |x - x_ref| <= 1e-5 |x_ref| + 2^-22 S, where S
+    = sum_rows w |term| / denom is the scale of the terms the statistic sums (the fp32 / SFU
+    lg2 rounding of each term, 2^-22 relative, is what a sum that cancels -- pg,
+    approx_kl -- cannot resolve below).  clipfrac and n_valid are counts: exact."""
+    w = np.asarray(valid, np.float64).reshape(-1)
+    lo = np.asarray(logp_old, np.float64).reshape(-1)
+    lp = np.asarray(lpref, np.float64).reshape(-1)
+    rho = np.exp(lp - lo)
+    s_pg = np.sum(w * np.abs(rho * np.asarray(adv, np.float64).reshape(-1))) / denom
+    s_vf = np.sum(w * (np.asarray(V, np.float64) - np.asarray(ret, np.float64).reshape(-1)) ** 2) / denom
+    scale = dict(pg=s_pg, vf=s_vf, ent=abs(st["ent"]), loss=s_pg + s_vf + 0.01 * abs(st["ent"]),
+                 approx_kl=np.sum(w * (np.abs(lo) + np.abs(lp))) / denom)
+    for i, k in enumerate(("loss", "pg", "vf", "ent", "approx_kl")):
+        tol = 1e-5 * abs(st[k]) + 2.0 ** -22 * scale[k]
+        assert abs(sv[i] - st[k]) <= tol, (k, float(sv[i]), st[k], tol)
+    n_clip = sv[5] * denom if clip_rows is None else clip_rows
+    assert round(float(sv[5]) * denom) == round(st["clipfrac"] * denom) == round(n_clip), \
+        (sv[5] * denom, st["clipfrac"] * denom)
+    assert sv[6] == st["n_valid"]
     assert int(sv[7]) == st["flags"] == 0
+
+
+def _loss_call(L, cfg, T, B, Y, act, on, av, logp_old, adv, ret, valid, clip_eps, bf16=False):
+    dims = L.make_dims(64, 64, T, cfg.head_sizes, L.PPO_PREC_BF16 if bf16 else L.PPO_PREC_FP32)
+    N = T * B
+    dout = torch.full((N, cfg.A), float("nan"), device="cuda",
+                      dtype=torch.bfloat16 if bf16 else torch.float32)
+    logp = torch.empty(N, device="cuda")
+    stats = torch.zeros(L.PPO_STATS_BUF, device="cuda")
+    L.ppo_loss_grad(dims, dev(Y), dev(act), dev(on), dev(av), dev(logp_old), dev(adv), dev(ret),
+                    None if valid is None else dev(valid), B,
+                    L.ppo_loss_cfg(clip_eps, 1.0, 0.01, 0.0), dout, logp, stats)
+    torch.cuda.synchronize()
+    return dout.float().cpu().numpy(), logp.cpu().numpy(), stats[:8].cpu().numpy()
+
+
+def test_loss_clip_tie_exact(L):
+    """DESIGN Q8 at an exact tie: clip_eps = 0 and rho = 1 exactly on every row (each side's
+    logp_old is its OWN log pi -- the oracle's fp64 value, the GPU's fp32 value -- so
+    exp(0) = 1 on both), hence rho A == clip(rho) A.  Ties take the unclipped branch: the
+    policy gradient flows on every row and clipfrac is exactly 0 (a strict '<' would zero it)."""
+    T, B = 16, 40
+    cfg = synth.Config(H=64, D=64, B=B, T=T)
+    s = synth.make_sequences(cfg, 21)
+    N = T * B
+    Y = synth.make_logits(N, cfg.A, 21, scale=1.5)
+    rng = np.random.default_rng(21)
+    adv = rng.standard_normal(N).astype(np.float32)
+    ret = rng.standard_normal(N).astype(np.float32)
+    act, on, av = (s[k].reshape(N, -1) for k in ("act", "head_on", "avail"))
+    lp_o = oracle.ppo_loss(Y, act, on, av, np.zeros(N), adv, ret, None, cfg.head_sizes)[3]
+    _, dYref, st, _ = oracle.ppo_loss(Y, act, on, av, lp_o, adv, ret, None, cfg.head_sizes,
+                                      0.0, 1.0, 0.01)
+    assert st["clipfrac"] == 0.0
+    z = np.zeros(N, np.float32)
+    _, lp_g, _ = _loss_call(L, cfg, T, B, Y, act, on, av, z, adv, ret, None, 0.0)
+    d, lp2, sv = _loss_call(L, cfg, T, B, Y, act, on, av, lp_g, adv, ret, None, 0.0)
+    assert np.array_equal(lp2, lp_g)                       # rho = exp(0) = 1 on the GPU
+    assert sv[5] == 0.0, sv[5]
+    ok, worst = elementwise_ok(d, dYref, 1e-5)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("side", [+1, -1])
+def test_loss_clip_edges(L, side):
+    """rho placed on the clip edges 1 +- eps (logp_old = log pi - log(1 +- eps), each side
+    from its own log pi).  At the edge rho is an fp32 rounding away from 1 +- eps, so the
+    branch taken there is not unique: each edge row must equal the oracle's unclipped-branch
+    gradient (rows with A as given) or its clipped-branch gradient (the same row with the
+    policy term removed, i.e. A = 0), and clipfrac must count exactly the rows that took the
+    clipped branch.  Rows 1e-3 inside / outside the edge must take the unique branch."""
+    T, B = 16, 40
+    eps = 0.2
+    cfg = synth.Config(H=64, D=64, B=B, T=T)
+    s = synth.make_sequences(cfg, 30 + side)
+    N = T * B
+    Y = synth.make_logits(N, cfg.A, 30 + side, scale=1.5)
+    rng = np.random.default_rng(30 + side)
+    # A > 0 clips above 1 + eps, A < 0 below 1 - eps: put each row's A on its edge's side
+    adv = (side * np.abs(rng.standard_normal(N)) + side * 0.1).astype(np.float32)
+    ret = rng.standard_normal(N).astype(np.float32)
+    act, on, av = (s[k].reshape(N, -1) for k in ("act", "head_on", "avail"))
+    # row kinds: 0 on the edge, 1 inside by 1e-3 (unclipped), 2 outside by 1e-3 (clipped)
+    kind = np.arange(N) % 3
+    target = 1.0 + side * eps + side * np.where(kind == 1, -1e-3, np.where(kind == 2, 1e-3, 0.0))
+    shift = np.log(target)
+    z = np.zeros(N, np.float32)
+    lp_o = oracle.ppo_loss(Y, act, on, av, z, adv, ret, None, cfg.head_sizes)[3]
+    lo_o = lp_o - shift
+    _, dY_unc, _, _ = oracle.ppo_loss(Y, act, on, av, lo_o, adv, ret, None, cfg.head_sizes, 1e9,
+                                      1.0, 0.01)            # eps = 1e9: nothing clips
+    _, dY_clp, _, _ = oracle.ppo_loss(Y, act, on, av, lo_o, z, ret, None, cfg.head_sizes, eps,
+                                      1.0, 0.01)            # A = 0: no policy term
+    _, lp_g, _ = _loss_call(L, cfg, T, B, Y, act, on, av, z, adv, ret, None, eps)
+    lo_g = (lp_g.astype(np.float64) - shift).astype(np.float32)
+    d, _, sv = _loss_call(L, cfg, T, B, Y, act, on, av, lo_g, adv, ret, None, eps)
+
+    def rows_match(ref):
+        rms = np.sqrt(np.mean(ref * ref))
+        return np.all(np.abs(d - ref) <= 1e-5 * (np.abs(ref) + rms), axis=1)
+    unc, clp = rows_match(dY_unc), rows_match(dY_clp)
+    assert not np.any(unc & clp)         # |A| >= 0.1: the two branches differ on every row
+    assert np.all(unc | clp)             # every row took one of the two valid branches
+    assert np.all(unc[kind == 1]) and np.all(clp[kind == 2])
+    assert round(float(sv[5]) * N) == int(np.sum(clp))      # clipfrac counts those rows
+
+
+def test_loss_nonfinite_flag(L):
+    """PPO_STAT_FLAGS bit0 (ppo5.h): a non-finite loss on a VALID row raises it, as the
+    oracle's FLAG_NONFINITE does; the same NaN on an invalid (w = 0) row does not."""
+    T, B = 1, 64
+    cfg = synth.Config(H=64, D=64, B=B, T=T)
+    s = synth.make_sequences(cfg, 5)
+    N = T * B
+    act, on, av = (s[k].reshape(N, -1) for k in ("act", "head_on", "avail"))
+    rng = np.random.default_rng(5)
+    adv = rng.standard_normal(N).astype(np.float32)
+    ret = rng.standard_normal(N).astype(np.float32)
+    for bad_row_valid in (1, 0):
+        Y = synth.make_logits(N, cfg.A, 5)
+        Y[9, -1] = np.nan                                     # the value output of row 9
+        valid = np.ones(N, np.uint8)
+        valid[9] = bad_row_valid
+        st = oracle.ppo_loss(Y, act, on, av, np.zeros(N), adv, ret, valid, cfg.head_sizes)[2]
+        _, _, sv = _loss_call(L, cfg, T, B, Y, act, on, av, np.zeros(N, np.float32), adv, ret,
+                              valid, 0.2)
+        assert (int(sv[7]) & 1) == (st["flags"] & 1) == bad_row_valid, (sv[7], st["flags"])
 
 
 def test_loss_flags(L):

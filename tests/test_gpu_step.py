@@ -16,6 +16,9 @@ from gpu_util import HYPER, device_batch, elementwise_ok, load_params, make_case
 pytestmark = pytest.mark.gpu
 
 KEYS = ("Wx", "Wh", "b", "Wo", "bo")
+# bf16 path: the share of entries whose gradient sign the GPU resolves (|g_ref| > 3|g - g_ref|);
+# measured 0.984-1.000 over every tensor of the bf16 step tests (profiles/r02_gpu_tests_v1.txt)
+BF16_FIRM_FLOOR = 0.95
 
 
 def _run(case, cfg, precision):
@@ -77,6 +80,7 @@ def _check_step(case, cfg, precision, tol_fwd, tol_grad):
             # first Adam step ~ -alpha/2 sign(g): compare where the sign is resolved
             gerr = np.abs(g[k] - case["grads"][k])
             firm = np.abs(case["grads"][k]) > 3 * gerr + 1e-6
+            assert firm.mean() > BF16_FIRM_FLOOR, (k, firm.mean())
             e = normwise(d_got[firm], d_ref[firm])
             assert e < 2e-2, (k, e, firm.mean())
     return opt

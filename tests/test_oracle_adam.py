@@ -70,3 +70,25 @@ def test_lr_zero_keeps_params_moments_advance():
         th, m, v = oracle.adam_clip(th, rng.standard_normal(10), m, v, t, 0.0)
     assert np.array_equal(th, th0)
     assert np.all(v > 0) and np.all(m != 0)
+
+
+def test_eps_placement_where_it_matters():
+    """DESIGN Q4 pinned by a case where eps dominates: first step, g = 1e-8, m = v = 0,
+    lr = 1e-3, clip off.  Hand evaluation (eps = 1e-8 on the RAW sqrt(v), bias factors
+    folded into alpha_t, Kingma & Ba §2 last paragraph / TF1's AdamOptimizer):
+        v = 0.001 * 1e-16 = 1e-19,  sqrt(v) = 3.16227766e-10,  m = 0.1 * 1e-8 = 1e-9,
+        alpha_1 = 1e-3 * sqrt(0.001) / 0.1 = 3.16227766e-4,
+        delta = -3.16227766e-4 * 1e-9 / (3.16227766e-10 + 1e-8) = -3.0653430e-5.
+    The other placement (eps on the bias-corrected sqrt(v_hat) = 1e-8, m_hat = 1e-8, as in
+    torch.optim.Adam) gives -1e-3 * 1e-8 / 2e-8 = -5.0e-4: 16x larger, so either a moved eps
+    or a dropped bias factor fails here."""
+    th, m, v = oracle.adam_clip(np.zeros(1), np.array([1e-8]), np.zeros(1), np.zeros(1), 1,
+                                1e-3, clip_sigma=0.0)
+    assert abs(th[0] - (-3.0653430e-5)) < 1e-12
+    assert abs(th[0] - (-5.0e-4)) > 1e-4
+    # and torch.optim.Adam (eps on sqrt(v_hat)) really is the other reading
+    p = torch.nn.Parameter(torch.zeros(1, dtype=torch.float64))
+    opt = torch.optim.Adam([p], lr=1e-3, betas=(0.9, 0.999), eps=1e-8)
+    p.grad = torch.tensor([1e-8], dtype=torch.float64)
+    opt.step()
+    assert abs(p.item() - (-5.0e-4)) < 1e-12
