@@ -55,9 +55,12 @@ def parse():
                          "fused-push = the backward's epilogues push the shards to their owners")
     ap.add_argument("--infer-B", type=str, default="60,1,240,960",
                     help="--config infer: comma-separated batch sizes (first = headline)")
-    ap.add_argument("--config", choices=["full", "gae", "iteration", "infer"], default="full",
+    ap.add_argument("--config", choices=["full", "gae", "iteration", "infer", "tiny", "paper-mb"],
+                    default="full",
                     help="full: the PPO step (default); gae: GAE-only HBM sweep (configs[3]); "
-                         "iteration: NEXT-1, steps drawn from a device experience buffer")
+                         "iteration: NEXT-1, steps drawn from a device experience buffer; "
+                         "tiny: configs[0] (H=128, D=256, B=32) latency, eager and CUDA graph; "
+                         "paper-mb: the paper's per-GPU minibatch (B=600, P:667), eager and graph")
     return ap.parse_args()
 
 
@@ -517,8 +520,127 @@ def run_infer(args):
         "sweep": rows}), flush=True)
 
 
+def run_small(args):
+    """Latency-bound step configs on one GPU, timed eager and as one CUDA-graph replay per
+    step (PPOOptimizer.capture): configs[0] tiny (H=128, D=256, 32 sequences) and the paper's
+    own per-GPU minibatch (B = 600 sequences = 120 samples) at full width.  L2
+    is flushed (a 256 MB write) between timed steps, outside the timed events."""
+    import torch
+    import synth
+    from paper_1912_06680_b200 import PPOOptimizer, _lib as L
+    dev = torch.device("cuda", 0)
+    if args.config == "tiny":
+        H, D, B = 128, 256, 32
+    else:
+        H, D, B = args.H, args.D, 600
+    T = 16
+    cfg = synth.Config(H=H, D=D, B=B, T=T)
+    opt = PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16", device=dev)
+    prm = synth.torch_params(cfg, 0, dev)
+    opt.load_canonical(prm["Wx"], prm["Wh"], prm["b"], prm["Wo"], prm["bo"])
+    seq = synth.torch_sequences(cfg, 1000, dev)
+    # rollout segments of 256 steps (P:1266) when B*T fills whole segments (tiny: 2 x 256);
+    # B = 600 x 16 steps = 37.5 segments, so there 60 segments of 160 steps
+    Lseg = 256 if (B * T) % 256 == 0 else 160
+    ro = synth.torch_rollouts(B * T // Lseg, Lseg, 1000, dev)
+    batch = dict(x=seq["x"], h0=seq["h0"], c0=seq["c0"], act=seq["act"], head_on=seq["head_on"],
+                 avail=seq["avail"], rew=ro["rew"], val=ro["val"], done=ro["done"])
+    batch["logp_old"] = opt.current_logp(batch) + seq["logp_noise"]
+    opt.put_x(batch["x"])
+    x_dev = batch.pop("x")
+    opt.use_device_t()
+    for _ in range(max(args.warmup, 1)):
+        opt.step(batch)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, n):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(n)]
+        for a, b in ev:
+            flush.fill_(1)                       # L2 flush, outside the timed region
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in ev]
+
+    clocks = Clocks(0)
+    clocks.start()
+    time.sleep(0.2)
+    L.prof_start()
+    eager = timed(lambda: opt.step(batch), args.steps)
+    prof = L.prof_stop()
+    graph = opt.capture(batch)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    replay = timed(graph.replay, args.steps)
+    clk = clocks.stop()
+    ms_e, ms_g = statistics.median(eager), statistics.median(replay)
+    pk = peaks()
+    alg = algorithmic(H, D, T, B, cfg.A, opt.layout.n_total)
+    flop = sum(w for k, (kind, w) in alg.items() if kind == "flop" and k in prof)
+    hbm = sum(w for k, (kind, w) in alg.items() if kind == "byte" and k in prof)
+    t_roof = flop / (pk["bf16_tflops_sustained"] * 1e12) + hbm / (pk["hbm_gbs"] * 1e9)
+    kernels = {k: {"launches_per_step": n // args.steps, "us_per_step": t / args.steps * 1e3}
+               for k, (n, t) in prof.items()}
+    n_launch = sum(n for n, _ in prof.values())
+    # end to end: inputs from pinned host memory each step (x into the workspace), stats back
+    keys = ("h0", "c0", "rew", "val", "done", "act", "head_on", "avail", "logp_old")
+    host = {k: batch[k].cpu().pin_memory() for k in keys}
+    host_x = x_dev.cpu().pin_memory()
+    st_host = torch.empty(8, dtype=torch.float32).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in host.values()) + \
+        host_x.numel() * host_x.element_size()
+
+    def e2e_step():
+        for k in keys:
+            batch[k].copy_(host[k], non_blocking=True)
+        opt.put_x(host_x)
+        graph.replay()
+        st_host.copy_(opt.stats[:8], non_blocking=True)
+    e2e = timed(e2e_step, args.steps)
+    ms_x = statistics.median(e2e)
+    tiny = args.config == "tiny"
+    line = {
+        "metric": ("PPO step latency, tiny config (configs[0])" if tiny else
+                   "PPO train samples/s at the paper's per-GPU minibatch (B=600, P:667)"),
+        "value": ms_g * 1e3 if tiny else B / (ms_g / 1e3) / SEQ_PER_SAMPLE,
+        "unit": "us/step" if tiny else UNIT, "higher_is_better": not tiny,
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_g,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded; paper-shaped rollouts, random-init weights)",
+        "config": {"workload": (f"{'tiny' if tiny else 'paper minibatch'} PPO step: H={H}, D={D}, "
+                                f"T=16, B={B} sequences ({B // SEQ_PER_SAMPLE} paper samples), "
+                                f"GAE over {Lseg}-step segments + TBPTT fwd/bwd + loss + Adam"),
+                   "H": H, "D": D, "T": T, "B_per_gpu": B, "parallelism": "dp1",
+                   "l2": "flushed between timed steps (256 MB write outside the timed events)",
+                   "timing": "median of per-step CUDA events; value from the CUDA-graph replay"},
+        "eager": {"ms_per_step": ms_e, "samples_per_s": B / (ms_e / 1e3) / SEQ_PER_SAMPLE},
+        "graph": {"ms_per_step": ms_g, "samples_per_s": B / (ms_g / 1e3) / SEQ_PER_SAMPLE},
+        "roofline": {"bound": "tensor", "kernel": "whole step (graph replay)",
+                     "achieved": flop / (ms_g / 1e3) / 1e12, "unit": "TFLOP/s",
+                     "peak": pk["bf16_tflops_sustained"],
+                     "frac": flop / (ms_g / 1e3) / 1e12 / pk["bf16_tflops_sustained"],
+                     "traffic": None, "step": {"T_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms_g,
+                                               "flop": flop, "hbm_bytes": hbm}},
+        "e2e": {"value": ms_x * 1e3 if tiny else B / (ms_x / 1e3) / SEQ_PER_SAMPLE,
+                "unit": "us/step" if tiny else UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": st_host.numel() * 4, "ms_per_step": ms_x,
+                "note": "inputs copied from pinned host memory, then the graph replay, then the "
+                        "stats read back, all inside the timed events"},
+        "cpu_baseline": None, "gpu_launches": n_launch, "clocks": clk, "kernels": kernels,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.config in ("tiny", "paper-mb"):
+        run_small(args)
+        return
     if args.config == "infer":
         run_infer(args)
         return

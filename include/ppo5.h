@@ -313,6 +313,17 @@ int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, si
               int64_t t, double lr, double b1, double b2, double eps, double clip_sigma,
               ppo_stream_t s);
 
+/* a10 with the step number on the device, so a captured CUDA graph of the whole step applies
+ * the right bias correction on every replay.  ctr: 16 bytes of 16-byte
+ * aligned device memory: int64 at byte 0 = steps taken so far (0 before the first step; the
+ * call advances it to t), float at byte 8 = scratch (this step's alpha_t).  alpha_t =
+ * lr sqrt(1-b2^t)/(1-b1^t) is formed in double on the device and rounded once to fp32 (the
+ * same expression as adam_step's host path); otherwise identical to adam_step.  n = 0 is a
+ * no-op (the counter does not advance).  Asynchronous; one extra 1-thread launch. */
+int adam_step_ctr(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, size_t n,
+                  int64_t* ctr, double lr, double b1, double b2, double eps, double clip_sigma,
+                  ppo_stream_t s);
+
 /* ---- NEXT-1: experience buffer and minibatch gather ----------
  * The optimizer's experience buffer holds `capacity` sequences (one hero's 16-step sample,
  * P:924) in sequence-major slots, all arrays device memory owned by the caller:

@@ -118,6 +118,8 @@ _lib_fns = dict(
                       c_double, c_double, c_double, c_double, c_void_p], c_int),
     adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_double,
                 c_double, c_double, c_double, c_double, c_void_p], c_int),
+    adam_step_ctr=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
+                    c_double, c_double, c_double, c_double, c_double, c_void_p], c_int),
     ppo_sample_indices=([c_int64, c_int64, ctypes.c_uint64, ctypes.c_uint64, c_void_p, c_void_p], c_int),
     ppo_gather=([_D, POINTER(ppo_buffer), c_void_p, c_int64, c_void_p, c_size_t] + [c_void_p] * 8,
                 c_int),
@@ -280,6 +282,12 @@ def lstm_bptt_bwd(dims, w, ws, dout, B, grad, stream=None):
 def adam_step(p, p_bf16, g, m, v, t, lr, b1, b2, eps, clip_sigma, stream=None):
     _check(_lib.adam_step(_p(p), _p(p_bf16), _p(g), _p(m), _p(v), p.numel(), t, lr, b1, b2, eps,
                           clip_sigma, _s(stream)))
+
+
+def adam_step_ctr(p, p_bf16, g, m, v, ctr, lr, b1, b2, eps, clip_sigma, stream=None):
+    """ctr: int64 device tensor of >= 2 elements, 16-byte aligned (steps taken; scratch)"""
+    _check(_lib.adam_step_ctr(_p(p), _p(p_bf16), _p(g), _p(m), _p(v), p.numel(), _p(ctr), lr, b1,
+                              b2, eps, clip_sigma, _s(stream)))
 
 
 def make_buffer(t: dict, capacity: int) -> ppo_buffer:

@@ -539,6 +539,22 @@ int adam_step(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, si
   return launch_adam(p, p_bf16, g, m, v, n, ap, (cudaStream_t)st);
 }
 
+int adam_step_ctr(float* p, uint16_t* p_bf16, const float* g, float* m, float* v, size_t n,
+                  int64_t* ctr, double lr, double b1, double b2, double eps, double clip_sigma,
+                  ppo_stream_t st) {
+  NEED(ctr);
+  if (!aligned(ctr, 16)) return fail(PPO_E_ALIGN, "ctr is not 16-byte aligned");
+  if (n == 0) return PPO_OK;
+  NEED(p);
+  NEED(g);
+  NEED(m);
+  NEED(v);
+  if (p_bf16 && !aligned(p_bf16, 16)) return fail(PPO_E_ALIGN, "p_bf16 is not 16-byte aligned");
+  if (!(b1 >= 0.0 && b1 < 1.0 && b2 >= 0.0 && b2 < 1.0)) return fail(PPO_E_ARG, "bad betas");
+  const AdamParams ap = make_adam_params(1, lr, b1, b2, eps, clip_sigma);   // alpha: device
+  return launch_adam(p, p_bf16, g, m, v, n, ap, (cudaStream_t)st, ctr, lr);
+}
+
 int ppo_prof_start(void) {
   Prof& P = prof();
   std::lock_guard<std::mutex> g(P.mu);

@@ -1123,9 +1123,13 @@ __global__ void loss_finalize_kernel(const float* __restrict__ partials, int nbl
 
 // ============================================================================ Adam + clip
 // 30 B/param: read p, g, m, v; write p, m, v, bf16 shadow (oracle O10).
+// alpha_dev (nullable): alpha_t from the device step counter (adam_tick_kernel), so a
+// captured CUDA graph of the step applies the right bias correction on every replay
 __global__ void adam_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ p16,
                             const float* __restrict__ g, float* __restrict__ m,
-                            float* __restrict__ v, size_t n, AdamParams ap) {
+                            float* __restrict__ v, size_t n, AdamParams ap,
+                            const float* __restrict__ alpha_dev) {
+  if (alpha_dev) ap.alpha = *alpha_dev;
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   // every byte is touched once per step: streaming (evict-first) loads and stores
@@ -1443,10 +1447,26 @@ int launch_scale(float* x, int64_t n, float f, cudaStream_t st) {
   PPO_LAUNCH_CHECK("scale_kernel");
   return PPO_OK;
 }
+// the device step counter of adam_step_ctr: t = ++ctr[0]; alpha_t (O10) formed in double
+// and rounded once to fp32, like the host path (ppo5.h adam_step), into the float at ctr + 8 B
+__global__ void adam_tick_kernel(long long* ctr, double lr, double b1, double b2) {
+  const long long t = ctr[0] + 1;
+  ctr[0] = t;
+  *reinterpret_cast<float*>(ctr + 1) =
+      (float)(lr * sqrt(1.0 - pow(b2, (double)t)) / (1.0 - pow(b1, (double)t)));
+}
 int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n,
-                const AdamParams& ap, cudaStream_t st) {
+                const AdamParams& ap, cudaStream_t st, int64_t* ctr, double lr) {
+  if (ctr) {
+    ProfScope _prof("adam_tick", st);
+    adam_tick_kernel<<<1, 1, 0, st>>>(reinterpret_cast<long long*>(ctr), lr, (double)ap.b1_d,
+                                      (double)ap.b2_d);
+    PPO_LAUNCH_CHECK("adam_tick_kernel");
+  }
   ProfScope _prof("adam", st);
-  adam_kernel<<<grid_for((int64_t)(n / 4 + 1)), 256, 0, st>>>(p, (__nv_bfloat16*)p16, g, m, v, n, ap);
+  adam_kernel<<<grid_for((int64_t)(n / 4 + 1)), 256, 0, st>>>(
+      p, (__nv_bfloat16*)p16, g, m, v, n, ap,
+      ctr ? reinterpret_cast<const float*>(ctr + 1) : nullptr);
   PPO_LAUNCH_CHECK("adam_kernel");
   return PPO_OK;
 }

@@ -48,6 +48,7 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
                 void* dout, float* logp, float* stats, cudaStream_t st);
 struct AdamParams {
   float alpha, b1, omb1, b2, omb2, eps, clip;
+  double b1_d, b2_d;   // host copies for the device alpha_t (adam_step_ctr)
 };
 // a10 on one element (O10): every rounding explicit, so adam_kernel and the
 // fused DP kernel (comm.cu) produce the same bits from the same gradient
@@ -71,10 +72,13 @@ inline AdamParams make_adam_params(int64_t t, double lr, double b1, double b2, d
   ap.omb2 = (float)(1.0 - b2);
   ap.eps = (float)eps;
   ap.clip = (clip_sigma > 0.0 && isfinite(clip_sigma)) ? (float)clip_sigma : 0.f;
+  ap.b1_d = b1;
+  ap.b2_d = b2;
   return ap;
 }
+// ctr (nullable, device, 16 B): the graph-capturable step counter of adam_step_ctr
 int launch_adam(float* p, void* p16, const float* g, float* m, float* v, size_t n,
-                const AdamParams& ap, cudaStream_t st);
+                const AdamParams& ap, cudaStream_t st, int64_t* ctr = nullptr, double lr = 0.0);
 int launch_simt_gemm(const SimtOp& a, const SimtOp& b, int64_t M, int64_t N, int64_t K, float* C,
                      int64_t ldc, cudaStream_t st);
 int launch_simt_cell_fwd(const Shape& s, int64_t B, const float* z, const float* c_prev,

@@ -1295,6 +1295,8 @@ struct EpiLstmBwd {
   int B, H;
   int fast;               // 1: SFU tanh for tanh(c_t)
   int first;              // 1: t = T-1, the incoming carry is zero (not read; no memset)
+  int exp;                // PPO_EXPERIMENTS builds only (timing A/B, wrong results):
+                          // bit0 skip the saved-activation loads, bit1 skip the stores
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int split) const {
@@ -1311,14 +1313,20 @@ struct EpiLstmBwd {
     };
     BwdRaw cur, nxt;
     const float* dcin = first ? nullptr : dc;
-    if (ok && nch > 0)
+#ifdef PPO_EXPERIMENTS
+    const bool no_ld = exp & 1, no_st = exp & 2;
+#else
+    constexpr bool no_ld = false, no_st = false;
+#endif
+    if (no_ld) cur = BwdRaw{};
+    if (ok && nch > 0 && !no_ld)
       bwd_load(cur, grow + goff(0), c_t + crow, c_prev + crow, dcin ? dcin + crow : nullptr);
 #pragma unroll 1
     for (int cc = 0; cc < BN / CW; ++cc) {
       float dh[8];
       tmem_ld8(taddr + cc * CW, dh);
       if (cc >= nch) continue;
-      if (ok && cc + 1 < nch) {
+      if (ok && cc + 1 < nch && !no_ld) {
         const int64_t o = crow + (cc + 1) * CW;
         bwd_load(nxt, grow + goff(cc + 1), c_t + o, c_prev + o, dcin ? dcin + o : nullptr);
       }
@@ -1354,14 +1362,18 @@ struct EpiLstmBwd {
             reinterpret_cast<uint32_t*>(&cur.g[q])[w] = *reinterpret_cast<const uint32_t*>(&pk);
           }
         }
-        __nv_bfloat16* gp = gz + static_cast<int64_t>(m) * G4 + goff(cc);
+        if (!no_st) {
+          __nv_bfloat16* gp = gz + static_cast<int64_t>(m) * G4 + goff(cc);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(gp + q * 64) = cur.g[q];
-        float4* d4 = reinterpret_cast<float4*>(dc + crow + cc * CW);
-        d4[0] = cur.dc[0];
-        d4[1] = cur.dc[1];
+          for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(gp + q * 64) = cur.g[q];
+          float4* d4 = reinterpret_cast<float4*>(dc + crow + cc * CW);
+          d4[0] = cur.dc[0];
+          d4[1] = cur.dc[1];
+        } else if (cur.dc[0].x == 1234.5f) {   // keep the math live
+          dc[crow] = cur.dc[1].y + __uint_as_float(cur.g[0].x);
+        }
       }
-      cur = nxt;
+      if (!no_ld) cur = nxt;
     }
   }
 };

@@ -315,7 +315,8 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     raster(sh, "BWD", 8, 1);   // n8: A/B with the current kernels, backward GEMM 0.7-2 ms faster than n4
     sh.sched = P.slot(kSchedBwd);
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
-                       (int)B, (int)s.H, fast_cell(), last ? 1 : 0};
+                       (int)B, (int)s.H, fast_cell(), last ? 1 : 0,
+                       knob_int("PPO_EXP_BWD_EPI", 0)};
     tc::TileShape sh1 = sh;
     rc = pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
               : launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh1, epi, st);

@@ -89,6 +89,10 @@ class PPOOptimizer:
         self.adv = torch.empty(T, B, **f32)
         self.ret = torch.empty(T, B, **f32)
         self.t = 0
+        # graph mode (capture()): the Adam step number lives on the device (adam_step_ctr):
+        # int64 steps taken + a float scratch, 16-byte aligned
+        self.device_t = False
+        self._ctr = torch.zeros(2, dtype=torch.int64, device=dev)
         self.comm = comm
         self.n_buckets = n_buckets
         h = self.hyper
@@ -127,7 +131,7 @@ class PPOOptimizer:
         self.gather_sharded()
         torch.cuda.synchronize(self.device)
         cpu = lambda d: {k: v.cpu() for k, v in d.items()}  # noqa: E731
-        return {"format": "ppo5-ckpt-1", "t": self.t, "D": self.D, "H": self.H,
+        return {"format": "ppo5-ckpt-1", "t": self.sync_t(), "D": self.D, "H": self.H,
                 "head_sizes": list(self.head_sizes), "aux": list(self.aux),
                 "params": cpu(self.unpack(self.theta)), "m": cpu(self.unpack(self.m)),
                 "v": cpu(self.unpack(self.v))}
@@ -145,6 +149,7 @@ class PPOOptimizer:
         if self.bf16:
             L.ppo_cast_bf16(self.theta, self.shadow, stream)
         self.t = int(sd["t"])
+        self._ctr[0] = self.t
 
     def save(self, path: str):
         torch.save(self.state_dict(), path)
@@ -249,6 +254,10 @@ class PPOOptimizer:
         """a10 (dp = "fused": a9 + a10 on this rank's shard, theta and shadow all-gathered)"""
         h = self.hyper
         self.t += 1
+        if self.device_t:
+            L.adam_step_ctr(self.theta, self.shadow, self.grad, self.m, self.v, self._ctr, h["lr"],
+                            h["beta1"], h["beta2"], h["adam_eps"], h["clip_sigma"], stream)
+            return
         if self.dp == "fused":
             L.dp_adam_step(self.comm, self.m, self.v, self.t, h["lr"], h["beta1"], h["beta2"],
                            h["adam_eps"], h["clip_sigma"], staged=self.dp_push, stream=stream)
@@ -279,6 +288,37 @@ class PPOOptimizer:
         self.allreduce(stream)
         self.apply(stream)
         return self.stats[:L.PPO_STATS]
+
+    # ---------------------------------------------------------------- CUDA graphs
+    def use_device_t(self):
+        """Switch Adam to the device step counter (adam_step_ctr), continuing from self.t."""
+        if not self.device_t:
+            self._ctr[0] = self.t
+            self.device_t = True
+
+    def sync_t(self) -> int:
+        """host copy of the step count (graph replays advance only the device counter)"""
+        if self.device_t:
+            self.t = int(self._ctr[0].item())
+        return self.t
+
+    def capture(self, batch, dx=None) -> "torch.cuda.CUDAGraph":
+        """Capture one whole optimizer step a1-a10 on `batch` (its tensors stay the step's
+        inputs: refill them in place between replays) into a CUDA graph; each replay() is one
+        step (the step's ~100 launches cost one graph launch).  Adam then
+        takes its step number from the device counter.  Run at least one eager step() first
+        (kernel attributes and modules are set up outside the capture).  Single-rank or
+        NCCL-allreduce exchange only (the fused exchange's IPC barriers are not captured)."""
+        if self.dp == "fused":
+            raise ValueError("capture(): the fused DP exchange is not graph-capturable; "
+                             "use dp='allreduce'")
+        self.use_device_t()
+        t_host = self.t
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(batch, dx=dx)
+        self.t = t_host           # capturing records the launches, it does not run them
+        return g
 
     def current_logp(self, batch, stream=None) -> torch.Tensor:
         """log pi_theta(a) for the batch (forward + loss pass); used to synthesise behaviour
