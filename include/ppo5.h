@@ -425,6 +425,15 @@ int ppo_infer_step(const ppo_dims* dims, const void* w, const void* x, float* h,
                    uint64_t step, int64_t B, void* ws, size_t ws_bytes, int32_t* act,
                    uint8_t* head_on, float* logp, float* value, float* out, ppo_stream_t s);
 
+/* ---- device topology (diagnostics) ---------------------------------------------------------
+ * SMs of the current device and how they split over its dies (B200: two dies; an address is
+ * homed on one of them, and the CTA-pair GEMMs give each die its own tile queue so the tiles
+ * sharing operand panels run on one die).  Measured once per device by a latency probe
+ * (~1 ms, on first use); *die0 = *die1 = 0 when no two-die split was found (then one queue).
+ * Synchronous; not callable during stream capture (returns the cached result or zeros). */
+int ppo_device_info(int32_t* n_sms /* host */, int32_t* die0_sms /* host */,
+                    int32_t* die1_sms /* host */);
+
 /* ---- tracing: CUDA events around every kernel launch ------------------------
  * ppo_prof_start() enables recording (clears previous records); every library launch then
  * records a start/end event pair on its stream.  ppo_prof_stop() synchronises those events,

@@ -137,6 +137,7 @@ _lib_fns = dict(
     ppo_infer_step=([_D, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                      ctypes.c_uint64, ctypes.c_uint64, c_int64, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
                      c_void_p, c_void_p, c_void_p], c_int),
+    ppo_device_info=([POINTER(c_int32)] * 3, c_int),
     ppo_prof_start=([], c_int),
     ppo_prof_stop=([POINTER(ppo_prof_entry), c_int32, POINTER(c_int32)], c_int),
     ppo_test_tc_gemm=([c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p], c_int),
@@ -422,6 +423,13 @@ def test_dp_adam(g, p, p_bf16, m, v, t, lr, b1, b2, eps, clip_sigma, stage=None,
         return None if ts is None else (c_void_p * W)(*[t.data_ptr() for t in ts])
     _check(_lib.ppo_test_dp_adam(W, arr(g), arr(p), arr(p_bf16), arr(m), arr(v), arr(stage),
                                  g[0].numel(), t, lr, b1, b2, eps, clip_sigma, _s(stream)))
+
+
+def device_info() -> dict:
+    """{'sms', 'die0_sms', 'die1_sms'} of the current device (die split 0/0 = none found)"""
+    a, b, c = c_int32(), c_int32(), c_int32()
+    _check(_lib.ppo_device_info(ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return {"sms": a.value, "die0_sms": b.value, "die1_sms": c.value}
 
 
 def prof_start():

@@ -32,6 +32,8 @@ if _NCCL:
 # (common.cuh knob()); a release build reads no environment variable
 if os.environ.get("PPO_EXPERIMENTS", "0") not in ("", "0"):
     FLAGS.append("-DPPO_EXPERIMENTS")
+# extra nvcc flags for experiment builds (e.g. -DPPO_SUSPEND_HINT_NS=2000)
+FLAGS += os.environ.get("PPO_NVCC_EXTRA", "").split()
 STAMP = os.path.join(CSRC, ".build_flags")
 
 

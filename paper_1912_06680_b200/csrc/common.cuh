@@ -125,7 +125,12 @@ struct WsLayout {
 enum SchedSlot { kSchedFwd = 0, kSchedHeads, kSchedBwd, kSchedWgrad, kSchedWgradO, kSchedDx,
                  kSchedLstmSlots };
 enum InferSchedSlot { kSchedInferGates = 0, kSchedInferHeads, kSchedInferSlots };
-constexpr size_t kSchedBytes = 64;   // >= 2 * 4 * max(kSchedLstmSlots, kSchedInferSlots)
+constexpr int kSchedWords = 4;       // u32 per slot: die-0 queue, exits, die-1 queue, pad
+constexpr size_t kSchedBytes = 128;  // >= kSchedWords * 4 * max(kSchedLstmSlots, kSchedInferSlots)
+// SM -> die map of the current device (B200: two dies of ~74 SMs; an L2 line is homed on one
+// of them), measured once by a latency probe (tc_path.cu).  NULL if it could not be
+// established; *n0 / *n1 = SMs on die 0 / 1.
+const uint8_t* sm_die_map(int* n0, int* n1);
 WsLayout ws_layout(const Shape& s, int64_t B);
 
 // ---- activation storage type ---------------------------------------------------------------
@@ -152,24 +157,41 @@ __device__ __forceinline__ void cell_fwd(float zi, float zf, float zg, float zo,
   h = o * tanhf(c);
 }
 
-// The tensor-core path's cell: tanh on the SFU (tanh.approx.f32, max rel. error ~2^-11, below
-// the bf16 storage of the gates and h) and sigmoid(z) = 1/2 + tanh(z/2)/2.  The fp32 reference
-// path and the inference step keep the accurate functions above.
-__device__ __forceinline__ float tanh_fast(float x) {
+// The tensor-core path's cell: the same functions built from the SFU's ex2/rcp (2 MUFU
+// instructions each instead of libm's ~25-instruction expf/tanhf and IEEE division), accurate
+// to a few 1e-7 -- far below the bf16 storage of the gates and h (2^-9).  tanh takes the odd
+// polynomial x - x^3/3 + 2x^5/15 below |x| = 0.1 (error < 6e-9 there), where 1 - e^{-2|x|}
+// would cancel.  The fp32 reference path and the inference step keep the libm functions.
+__device__ __forceinline__ float ex2_approx(float x) {
   float r;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ float sigmoid_fast(float z) { return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f); }
-__device__ __forceinline__ void cell_fwd_fast(float zi, float zf, float zg, float zo,
-                                              float c_prev, float& i, float& f, float& g,
-                                              float& o, float& c, float& h) {
-  i = sigmoid_fast(zi);
-  f = sigmoid_fast(zf);
-  g = tanh_fast(zg);
-  o = sigmoid_fast(zo);
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sigmoid_tc(float z) {
+  return rcp_approx(1.0f + ex2_approx(-1.4426950408889634f * z));
+}
+__device__ __forceinline__ float tanh_tc(float x) {
+  const float a = fabsf(x);
+  const float e = ex2_approx(-2.8853900817779268f * a);        // e^{-2|x|}
+  const float t = (1.0f - e) * rcp_approx(1.0f + e);
+  const float x2 = a * a;
+  const float p = a * fmaf(x2, fmaf(x2, 0.13333333333f, -0.33333333333f), 1.0f);
+  return copysignf(a < 0.1f ? p : t, x);
+}
+__device__ __forceinline__ void cell_fwd_tc(float zi, float zf, float zg, float zo, float c_prev,
+                                            float& i, float& f, float& g, float& o, float& c,
+                                            float& h) {
+  i = sigmoid_tc(zi);
+  f = sigmoid_tc(zf);
+  g = tanh_tc(zg);
+  o = sigmoid_tc(zo);
   c = f * c_prev + i * g;
-  h = o * tanh_fast(c);
+  h = o * tanh_tc(c);
 }
 
 // Backward through one cell: dh (total), carried dc, saved gates, c_t, c_{t-1}
@@ -177,8 +199,8 @@ __device__ __forceinline__ void cell_fwd_fast(float zi, float zf, float zg, floa
 __device__ __forceinline__ void cell_bwd(float dh, float dc_carry, float i, float f, float g,
                                          float o, float c, float c_prev, float& dzi, float& dzf,
                                          float& dzg, float& dzo, float& dc_next,
-                                         bool fast = false) {
-  float tc = fast ? tanh_fast(c) : tanhf(c);
+                                         bool tc_math = false) {
+  float tc = tc_math ? tanh_tc(c) : tanhf(c);
   float dc = dc_carry + dh * o * (1.0f - tc * tc);
   float d_o = dh * tc;
   float di = dc * g;

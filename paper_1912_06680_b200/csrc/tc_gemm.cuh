@@ -40,6 +40,8 @@ struct TileShape {
   int a_tiled_nkb;      // > 0: A is pre-tiled (16 KB [128 rows][64 k] tiles, tile index
                         // m_tile * a_tiled_nkb + k_block, map dims {64, 128, tiles}) so every
                         // TMA box is one contiguous DRAM stream
+  const uint8_t* sm_die;  // CTA-pair kernel: SM -> die map (nullable = one queue)
+  int die_split;          // > 0: units [0, die_split) are die 0's queue (sched_fetch_die)
 };
 constexpr int kSchedDepth = 4;  // tile-index ring between the fetcher and the consumers
 
@@ -244,7 +246,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   } while (!done);
 }
 // Fetch the next work unit from the global counter; the fetcher that observes the end last
-// resets the counter for the next launch.
+// resets the counter for the next launch.  ctr[0] = next unit, ctr[1] = exited fetchers.
 __device__ __forceinline__ int sched_fetch(unsigned int* ctr, int nunits, unsigned int nfetchers) {
   const int u = static_cast<int>(atomicAdd(ctr, 1u));
   if (u >= nunits && atomicAdd(ctr + 1, 1u) == nfetchers - 1) {
@@ -253,6 +255,51 @@ __device__ __forceinline__ int sched_fetch(unsigned int* ctr, int nunits, unsign
   }
   return u;
 }
+// Die-aware variant (split > 0): units [0, split) are die 0's queue (ctr[0]), [split, nunits)
+// die 1's (ctr[2]); each fetcher takes from its own die's queue in raster order, so the tiles
+// that share operand panels run on one die and the panels are fetched into that die's L2
+// (fewer cross-die fabric transfers); an exhausted queue steals from the other one.
+__device__ __forceinline__ int sched_fetch_die(unsigned int* ctr, int nunits,
+                                               unsigned int nfetchers, int die, int split) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int d = die ^ k;
+    const int u = static_cast<int>(atomicAdd(ctr + 2 * d, 1u));
+    if (u < (d ? nunits - split : split)) return (d ? split : 0) + u;
+  }
+  if (atomicAdd(ctr + 1, 1u) == nfetchers - 1) {
+    atomicExch(ctr, 0u);
+    atomicExch(ctr + 1, 0u);
+    atomicExch(ctr + 2, 0u);
+  }
+  return nunits;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// ---------------------------------------------------------------- phase trace (experiments)
+// Built with -DPPO_TRACE only: per CTA, clock64() at phase points relative to kernel entry
+// (slot 0 holds %globaltimer at entry), read back by ppo_trace_read (tools/trace_gemm.py).
+#ifdef PPO_TRACE
+__device__ unsigned long long g_tc_trace[512][32];
+__device__ __forceinline__ void tc_trace(int i, long long t0) {
+  g_tc_trace[blockIdx.x][i] = (unsigned long long)(clock64() - t0);
+}
+#define TC_TRACE(i) tc_trace((i), trace_t0)
+#define TC_TRACE_BEGIN()                                                 \
+  const long long trace_t0 = clock64();                                  \
+  if (threadIdx.x == 0) g_tc_trace[blockIdx.x][0] = globaltimer_ns()
+#else
+#define TC_TRACE(i) \
+  do {              \
+  } while (0)
+#define TC_TRACE_BEGIN() \
+  do {                   \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- the kernel
 template <int BN, bool A_MN, bool B_MN, int STAGES>
@@ -541,6 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   static_assert(BN % 32 == 0 && BN <= 256, "pair UMMA N: multiple of 16 per CTA half");
   static_assert(!B_MN || (BN / 2) % 64 == 0, "MN-major B needs 64-wide panels per CTA half");
   using L = Smem2<A_MN, B_MN, STAGES, MB, BN>;
+  TC_TRACE_BEGIN();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -599,6 +647,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) TC_TRACE(1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -612,11 +661,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t sempty_l0 = mapa_shared(smem_u32(&sempty[0]), 0);
       const uint32_t sfull_f0 = mapa_shared(smem_u32(&sfull[0]), 1);
       const uint32_t ring_f0 = mapa_shared(smem_u32(&ring[0]), 1);
+      const int die = sh.die_split > 0 ? sh.sm_die[smid()] : 0;
       while (true) {
         int tile;
         if (leader) {
           mbar_wait(&sempty[sslot], sphase ^ 1);
-          tile = sched_fetch(sh.sched, nunits, nclusters);
+          tile = sh.die_split > 0 ? sched_fetch_die(sh.sched, nunits, nclusters, die, sh.die_split)
+                                  : sched_fetch(sh.sched, nunits, nclusters);
           ring[sslot] = tile;
           st_shared_cluster(ring_f0 + 4 * sslot, tile);
           mbar_arrive(&sfull[sslot]);
@@ -631,6 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           sphase ^= 1;
         }
         if (tile >= nunits) break;
+        if (sslot == 1 && sphase == 0) TC_TRACE(2);
         const int split = tile / ntiles;
         tile -= split * ntiles;
         const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
@@ -670,6 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+      TC_TRACE(10);
     }
   } else if (warp == 1) {
     if (leader) {
@@ -704,6 +757,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (lane == 0 && kb == kb_lo && sslot == 1 && sphase == 0) TC_TRACE(4);
           const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (L::A_BYTES >> 4));
           const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (L::B_BYTES >> 4));
           if (elect_one()) {
@@ -723,11 +777,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) umma_commit_pair(&tfull[acc]);
         __syncwarp();
+        if (lane == 0 && sslot == 1 && sphase == 0) TC_TRACE(5);
         if (++acc == NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
+      if (lane == 0) TC_TRACE(11);
     }
   } else {
     // ===================== epilogue warps 2..5 (both CTAs) =====================
@@ -755,12 +811,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile - split * ntiles, num_m, num_n, sh.group, sh.group_n, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (threadIdx.x == 64 && sslot == 1 && sphase == 0) TC_TRACE(6);
+      if (lane == 0 && sslot == 1 && sphase == 0) TC_TRACE(16 + quarter);
       const uint32_t taddr =
           tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
 #pragma unroll 1
       for (int b = 0; b < MB; ++b)
         epi.template apply<BN>(mb * TM + rank * BM * MB + b * BM, nb * BN, row, taddr + b * 256,
                                split);
+      if (threadIdx.x == 64 && sslot == 1 && sphase == 0) TC_TRACE(7);
+      if (lane == 0 && sslot == 1 && sphase == 0) TC_TRACE(20 + quarter);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
@@ -769,8 +829,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) TC_TRACE(12 + quarter);
   }
 
+  if (threadIdx.x == 0) TC_TRACE(8);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -778,6 +840,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncwarp();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
                  : "memory");
+    if (lane == 0) TC_TRACE(9);
   }
 }
 
@@ -1214,7 +1277,6 @@ struct EpiLstmFwd {
   float* c_out;           // C[t+1] [B][H]
   __nv_bfloat16* gates;   // G[t]   [B][4H], interleaved like the accumulator columns
   int B, H;
-  int fast;               // 1: SFU tanh/sigmoid (cell_fwd_fast)
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int split) const {
@@ -1236,8 +1298,7 @@ struct EpiLstmFwd {
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         float i, f, g, o;
-        if (fast) cell_fwd_fast(zi[e], zf[e], zg[e], zo[e], cp[e], i, f, g, o, c[e], h[e]);
-        else cell_fwd(zi[e], zf[e], zg[e], zo[e], cp[e], i, f, g, o, c[e], h[e]);
+        cell_fwd_tc(zi[e], zf[e], zg[e], zo[e], cp[e], i, f, g, o, c[e], h[e]);
         zi[e] = i;
         zf[e] = f;
         zg[e] = g;
@@ -1293,7 +1354,6 @@ struct EpiLstmBwd {
   const float* c_prev;    // C[t]
   float* dc;              // [B][H] carry (in/out)
   int B, H;
-  int fast;               // 1: SFU tanh for tanh(c_t)
   int first;              // 1: t = T-1, the incoming carry is zero (not read; no memset)
   int exp;                // PPO_EXPERIMENTS builds only (timing A/B, wrong results):
                           // bit0 skip the saved-activation loads, bit1 skip the stores
@@ -1311,7 +1371,9 @@ struct EpiLstmBwd {
       const int j0 = n_base + cc * CW;
       return (j0 >> 6) * 256 + (j0 & 63);
     };
-    BwdRaw cur, nxt;
+    // the saved activations are loaded two chunks ahead (cur = chunk cc, nxt = cc + 1,
+    // nx2 = cc + 2 in flight), so a chunk's math overlaps ~2 chunks of HBM latency
+    BwdRaw cur, nxt, nx2;
     const float* dcin = first ? nullptr : dc;
 #ifdef PPO_EXPERIMENTS
     const bool no_ld = exp & 1, no_st = exp & 2;
@@ -1319,17 +1381,20 @@ struct EpiLstmBwd {
     constexpr bool no_ld = false, no_st = false;
 #endif
     if (no_ld) cur = BwdRaw{};
-    if (ok && nch > 0 && !no_ld)
-      bwd_load(cur, grow + goff(0), c_t + crow, c_prev + crow, dcin ? dcin + crow : nullptr);
+    auto load_chunk = [&](BwdRaw& r, int cc) {
+      const int64_t o = crow + cc * CW;
+      bwd_load(r, grow + goff(cc), c_t + o, c_prev + o, dcin ? dcin + o : nullptr);
+    };
+    if (ok && !no_ld) {
+      if (nch > 0) load_chunk(cur, 0);
+      if (nch > 1) load_chunk(nxt, 1);
+    }
 #pragma unroll 1
     for (int cc = 0; cc < BN / CW; ++cc) {
       float dh[8];
       tmem_ld8(taddr + cc * CW, dh);
       if (cc >= nch) continue;
-      if (ok && cc + 1 < nch && !no_ld) {
-        const int64_t o = crow + (cc + 1) * CW;
-        bwd_load(nxt, grow + goff(cc + 1), c_t + o, c_prev + o, dcin ? dcin + o : nullptr);
-      }
+      if (ok && cc + 2 < nch && !no_ld) load_chunk(nx2, cc + 2);
       if (ok) {
         // in place: each 32-bit gate word holds units (2w, 2w+1); dz overwrites the gates
         float* ct = reinterpret_cast<float*>(cur.ct);
@@ -1349,7 +1414,7 @@ struct EpiLstmBwd {
             const int e = 2 * w + h;
             float a, b, c, d, dn;
             cell_bwd(dh[e], dcv[e], z[0][h], z[1][h], z[2][h], z[3][h], ct[e], cp[e], a, b, c,
-                     d, dn, fast != 0);
+                     d, dn, true);
             z[0][h] = a;
             z[1][h] = b;
             z[2][h] = c;
@@ -1373,7 +1438,10 @@ struct EpiLstmBwd {
           dc[crow] = cur.dc[1].y + __uint_as_float(cur.g[0].x);
         }
       }
-      if (!no_ld) cur = nxt;
+      if (!no_ld) {
+        cur = nxt;
+        nxt = nx2;
+      }
     }
   }
 };

@@ -2,7 +2,11 @@
 // the GEMM launches for forward (a2-a4) and backward (a6-a8).  DESIGN.md "Data layout".
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cmath>
 #include <mutex>
+#include <string>
+#include <vector>
 
 #include "kernels.cuh"
 #include "tc_gemm.cuh"
@@ -12,7 +16,7 @@ namespace {
 
 // Tile-scheduler counters of the standalone test GEMM (ppo_test_tc_gemm, tests only); the
 // step's GEMMs use the counters in their workspace (common.cuh SchedSlot).
-__device__ unsigned int g_test_sched_ctr[2];
+__device__ unsigned int g_test_sched_ctr[kSchedWords];
 
 unsigned int* test_sched_counter() {
   static unsigned int* base[64] = {nullptr};
@@ -26,6 +30,100 @@ unsigned int* test_sched_counter() {
   }
   return base[dev];
 }
+
+// ---- SM -> die map (B200: 2 dies; every 2 KB of address space is homed on one of them, and an
+// SM reads a line homed on its own die ~70 cycles faster).  Probe: each SM times chains of
+// dependent L2 hits on kDieLines lines 2 KB apart; per line the SMs split into a fast and a
+// slow group, and each SM's pattern over the lines correlates +-1 with a reference SM's.
+constexpr int kDieLines = 64, kDieReps = 24, kDieMaxSm = 256;
+__global__ void die_probe_kernel(const unsigned* buf, unsigned long long* out) {
+  if (threadIdx.x != 0) return;
+  unsigned v = 0;
+  const uint32_t sm = tc::smid();
+  for (int l = 0; l < kDieLines; ++l) {
+    const unsigned* a = buf + (size_t)l * 512;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(a + v));
+    const long long t0 = clock64();
+    for (int r = 0; r < kDieReps; ++r)
+      asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(a + v));
+    const long long t1 = clock64();
+    out[(size_t)blockIdx.x * kDieLines + l] =
+        (unsigned long long)(t1 - t0) | ((unsigned long long)sm << 48);
+  }
+  if (v == 0xFFFFFFFFu) out[0] = 0;   // keep the chain live (buf is zero)
+}
+
+struct DieMap {
+  uint8_t* dev = nullptr;
+  int n0 = 0, n1 = 0;
+  bool done = false;
+};
+
+int probe_die_map(DieMap& dm) {
+  int sms = num_sms();
+  if (sms > kDieMaxSm) return PPO_E_UNSUPPORTED;
+  const int nb = 4 * sms;
+  unsigned* buf = nullptr;
+  unsigned long long* out = nullptr;
+  PPO_CUDA_CHECK(cudaMalloc(&buf, (size_t)kDieLines * 2048));
+  PPO_CUDA_CHECK(cudaMalloc(&out, (size_t)nb * kDieLines * 8));
+  PPO_CUDA_CHECK(cudaMemset(buf, 0, (size_t)kDieLines * 2048));
+  for (int rep = 0; rep < 2; ++rep) die_probe_kernel<<<nb, 32>>>(buf, out);
+  std::vector<unsigned long long> h((size_t)nb * kDieLines);
+  const cudaError_t e = cudaMemcpy(h.data(), out, h.size() * 8, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  cudaFree(out);
+  if (e != cudaSuccess) return fail(PPO_E_CUDA, cudaGetErrorString(e));
+  std::vector<double> lat((size_t)sms * kDieLines, 0.0);
+  std::vector<int> cnt(sms, 0);
+  for (int b = 0; b < nb; ++b) {
+    const int sm = (int)(h[(size_t)b * kDieLines] >> 48);
+    if (sm < 0 || sm >= sms) continue;
+    ++cnt[sm];
+    for (int l = 0; l < kDieLines; ++l)
+      lat[(size_t)sm * kDieLines + l] += (double)(h[(size_t)b * kDieLines + l] & 0xFFFFFFFFFFFFull);
+  }
+  // per line: SMs faster than the midpoint of the line's fastest and slowest SM are on the
+  // line's home die; align every line's split to line 0's (a line homed on the other die
+  // flips it) and give each SM its majority.  A misassigned SM costs locality, not results.
+  std::vector<int> votes(sms, 0), ref;
+  double gap = 0.0;
+  for (int l = 0; l < kDieLines; ++l) {
+    double lo = 1e30, hi = 0.0;
+    for (int s = 0; s < sms; ++s) {
+      if (!cnt[s]) continue;
+      const double x = lat[(size_t)s * kDieLines + l] / cnt[s];
+      lo = std::min(lo, x);
+      hi = std::max(hi, x);
+    }
+    gap += (hi - lo) / kDieReps / kDieLines;
+    const double mid = 0.5 * (lo + hi);
+    std::vector<int> fast(sms, 0);
+    for (int s = 0; s < sms; ++s) fast[s] = cnt[s] && lat[(size_t)s * kDieLines + l] / cnt[s] < mid;
+    if (ref.empty()) ref = fast;
+    int agree = 0;
+    for (int s = 0; s < sms; ++s) agree += fast[s] == ref[s];
+    const bool flip = 2 * agree < sms;
+    for (int s = 0; s < sms; ++s) votes[s] += (fast[s] ^ (int)flip) ? 1 : -1;
+  }
+  if (gap < 20.0) return PPO_E_UNSUPPORTED;   // no near/far split (one die)
+  std::vector<uint8_t> die(sms, 0);
+  int n0 = 0;
+  for (int s = 0; s < sms; ++s) {
+    die[s] = votes[s] > 0 ? 0 : 1;
+    n0 += die[s] == 0;
+  }
+  if (n0 < sms / 4 || n0 > sms - sms / 4) return PPO_E_UNSUPPORTED;
+  PPO_CUDA_CHECK(cudaMalloc(&dm.dev, kDieMaxSm));
+  PPO_CUDA_CHECK(cudaMemset(dm.dev, 0, kDieMaxSm));
+  PPO_CUDA_CHECK(cudaMemcpy(dm.dev, die.data(), sms, cudaMemcpyHostToDevice));
+  dm.n0 = n0;
+  dm.n1 = sms - n0;
+  return PPO_OK;
+}
+
+// die-aware tile queues for the CTA-pair GEMMs (PPO_DIE_SCHED=0/1 overrides in experiment builds)
+bool die_sched() { return knob_int("PPO_DIE_SCHED", 1) != 0; }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -119,8 +217,19 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
   const bool all_tiles = knob_int("PPO_GRID_ALL_TILES", 0) != 0;
   const int clusters = (int)std::min<int64_t>(ntiles, all_tiles ? (int64_t)1 << 30 : num_sms() / 2);
   if (clusters <= 0) return PPO_OK;
+  tc::TileShape shd = sh;
+  if (die_sched()) {
+    // die-aware queues: each die gets a share of the raster sequence proportional to the CTA
+    // pairs it hosts (clusters are placed within one die)
+    int n0 = 0, n1 = 0;
+    const uint8_t* map = sm_die_map(&n0, &n1);
+    if (map && ntiles >= 2 * clusters) {
+      shd.sm_die = map;
+      shd.die_split = (int)((ntiles * (n0 / 2) + (n0 / 2 + n1 / 2) / 2) / (n0 / 2 + n1 / 2));
+    }
+  }
   ProfScope _prof(tag, st);
-  kern<<<2 * clusters, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, sh, epi);
+  kern<<<2 * clusters, tc::kThreads, L::TOTAL, st>>>(a0, a1, b0, b1, shd, epi);
   PPO_LAUNCH_CHECK("tc_gemm2_kernel");
   return PPO_OK;
 }
@@ -194,25 +303,13 @@ bool use_pair(const char* kind, bool def) {
   return strcmp(e, "pair") == 0;
 }
 
-// Experiment knob (PPO_EXPERIMENTS builds only): PPO_FAST_CELL=1 puts tanh/sigmoid of the
-// fused LSTM epilogues on the SFU (tanh.approx): -3% forward time, but the full-width bf16
-// weight gradient drifts past the 2e-2 parity bar (0.022 on test_full_width_bf16), so a
-// release build always takes the accurate functions.
-int fast_cell() {
-#ifdef PPO_EXPERIMENTS
-  return knob_int("PPO_FAST_CELL", 0) != 0;
-#else
-  return 0;
-#endif
-}
-
 struct WsPtrs {
   __nv_bfloat16* xh;
   __nv_bfloat16* g;
   float* c;
   float* dc;
   unsigned int* sched;   // this workspace's tile-scheduler counters, 2 per SchedSlot
-  unsigned int* slot(int k) const { return sched + 2 * k; }
+  unsigned int* slot(int k) const { return sched + kSchedWords * k; }
 };
 WsPtrs ws_ptrs(const Shape& s, int64_t B, void* ws) {
   WsLayout L = ws_layout(s, B);
@@ -229,6 +326,27 @@ int sched_reset(const WsPtrs& P, cudaStream_t st) {
 }
 
 }  // namespace
+
+// Measured once per device, outside stream capture (a capture that needs it runs without);
+// NULL when the probe did not find a clean two-die split.
+const uint8_t* sm_die_map(int* n0, int* n1) {
+  static DieMap maps[64];
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  DieMap& dm = maps[dev];
+  if (!dm.done) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(cudaStreamLegacy, &cs);   // (any capture in progress: retry later)
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    if (probe_die_map(dm) != PPO_OK) dm.dev = nullptr;   // (no map: one queue)
+    dm.done = true;
+  }
+  if (n0) *n0 = dm.n0;
+  if (n1) *n1 = dm.n1;
+  return dm.dev;
+}
 
 // ---------------------------------------------------------------- forward (a2-a4)
 int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
@@ -263,8 +381,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     sh.sched = P.slot(kSchedFwd);
     tc::TileShape sh1 = sh;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
-                       P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H,
-                       fast_cell()};
+                       P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
     rc = pairmc ? launch2mc("lstm_fwd_step", mA, mBmc, sh, epi, st)
          : pair2  ? launch2<false, false, tc::EpiLstmFwd, 2>("lstm_fwd_step", mA2, mA2, mB, mB, sh,
                                                            epi, st)
@@ -315,7 +432,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     raster(sh, "BWD", 8, 1);   // n8: A/B with the current kernels, backward GEMM 0.7-2 ms faster than n4
     sh.sched = P.slot(kSchedBwd);
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
-                       (int)B, (int)s.H, fast_cell(), last ? 1 : 0,
+                       (int)B, (int)s.H, last ? 1 : 0,
                        knob_int("PPO_EXP_BWD_EPI", 0)};
     tc::TileShape sh1 = sh;
     rc = pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
@@ -470,7 +587,7 @@ int infer_gemm_bn(const char* tag, int slot, const void* W, int64_t M, int64_t K
                              heads ? "PPO_INFER_SPLIT_HEADS" : "PPO_INFER_SPLIT");
   tc::TileShape sh{(int)M, (int)B, nkb0, nkb - nkb0, 0, 0, 0, 0, 1, 0};
   sh.ksplit = sp;
-  sh.sched = sched + 2 * slot;
+  sh.sched = sched + kSchedWords * slot;
   const char* e = knob("PPO_INFER_EVICT_FIRST");
   sh.a_evict_first = e ? atoi(e) : 1;
   sh.a_tiled_nkb = nkb;
@@ -564,3 +681,28 @@ int tc_test_gemm(int mode, const void* A, const void* Bm, float* C, int M, int N
 }
 
 }  // namespace ppo
+
+extern "C" int ppo_device_info(int32_t* n_sms, int32_t* die0_sms, int32_t* die1_sms) {
+  if (!n_sms || !die0_sms || !die1_sms) return ppo::fail(PPO_E_ARG, "NULL pointer");
+  int n0 = 0, n1 = 0;
+  const uint8_t* m = ppo::sm_die_map(&n0, &n1);
+  *n_sms = ppo::num_sms();
+  *die0_sms = m ? n0 : 0;
+  *die1_sms = m ? n1 : 0;
+  return PPO_OK;
+}
+
+#ifdef PPO_TRACE
+// experiments build only: the phase trace of the last pair-GEMM launch (tc_gemm.cuh)
+extern "C" int ppo_trace_read(unsigned long long* out, int n) {
+  n = std::min(n, 512 * 32);
+  return cudaMemcpyFromSymbol(out, ppo::tc::g_tc_trace, n * sizeof(unsigned long long)) ==
+                 cudaSuccess
+             ? PPO_OK
+             : PPO_E_CUDA;
+}
+extern "C" int ppo_trace_clear(void) {
+  static unsigned long long z[512 * 32] = {};
+  return cudaMemcpyToSymbol(ppo::tc::g_tc_trace, z, sizeof(z)) == cudaSuccess ? PPO_OK : PPO_E_CUDA;
+}
+#endif

@@ -25,7 +25,8 @@ opt = PPOOptimizer(a.D, a.H, a.B, 16, cfg.head_sizes, precision="bf16")
 p = synth.torch_params(cfg, 0, "cuda")
 opt.load_canonical(p["Wx"], p["Wh"], p["b"], p["Wo"], p["bo"])
 seq = synth.torch_sequences(cfg, 1, "cuda")
-ro = synth.torch_rollouts(a.B * 16 // 256, 256, 1, "cuda")
+Lseg = 256 if (a.B * 16) % 256 == 0 else 160   # B = 600: 60 segments of 160 steps
+ro = synth.torch_rollouts(a.B * 16 // Lseg, Lseg, 1, "cuda")
 batch = dict(x=seq["x"], h0=seq["h0"], c0=seq["c0"], act=seq["act"], head_on=seq["head_on"],
              avail=seq["avail"], rew=ro["rew"], val=ro["val"], done=ro["done"])
 batch["logp_old"] = opt.current_logp(batch) + seq["logp_noise"]
