@@ -141,8 +141,10 @@ WsLayout ws_layout(const Shape& s, int64_t B) {
   if (!s.bf16) off = align_up(off + (size_t)B * s.G4 * 4, 1024);
   L.splitk = off;  // split-K partials of dW_o (bf16 path)
   if (s.bf16) off = align_up(off + (size_t)kMaxSplitK * s.A * s.Ko * 4, 1024);
-  L.sched = off;   // tile-scheduler counters of this workspace's GEMMs
-  off = align_up(off + kSchedBytes, 1024);
+  L.sched = off;   // tile-scheduler counters of this workspace's GEMMs, then the per-step
+                   // row-block ready counters of a multi-step launch (T x ceil(B / 256))
+  L.ready = off + kSchedBytes;
+  off = align_up(L.ready + (size_t)s.T * ((B + 255) / 256) * 4, 1024);
   L.total = off;
   return L;
 }

@@ -117,7 +117,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // Workspace regions (byte offsets from ws base); esz = activation element size.
 constexpr int kMaxSplitK = 16;
 struct WsLayout {
-  size_t xh, g, c, dc, raw, splitk, sched, total;
+  size_t xh, g, c, dc, raw, splitk, sched, ready, total;
 };
 // Dynamic tile-scheduler counters live in the caller's workspace (2 x u32 per GEMM call site),
 // so launches on different workspaces -- two optimizers, two streams -- never share one.  The

@@ -42,7 +42,57 @@ struct TileShape {
                         // TMA box is one contiguous DRAM stream
   const uint8_t* sm_die;  // CTA-pair kernel: SM -> die map (nullable = one queue)
   int die_split;          // > 0: units [0, die_split) are die 0's queue (sched_fetch_die)
+  // CTA-pair kernel, persistent multi-step launch (tsteps > 1): the T recurrent steps of the
+  // LSTM in one launch, units = tsteps x tiles in step order (unit step s is passed to the
+  // epilogue as `split`).  Step s reads the A sources at 3rd coordinate za{0,1} + s za_step{0,1},
+  // takes nkb0_s0 (>= 0) source-0 k-blocks on step 0, and its k-blocks from dep_kb on wait
+  // until every tile of step s-1 in the same row block has signalled ready[(s-1) num_m + mb]
+  // (2 per tile: both CTAs of the pair, after their epilogue's stores).
+  int tsteps;
+  int za_step0, za_step1;
+  int nkb0_s0;
+  int dep_kb;
+  unsigned int* ready;
 };
+
+// One work unit of a launch: a tile and (split-K) its k-range or (multi-step) its step.
+struct UnitInfo {
+  int split, tile, kb_lo, kb_hi, nkb0, za0, za1;
+};
+__device__ __forceinline__ UnitInfo decode_unit(const TileShape& sh, int u, int ntiles) {
+  UnitInfo r;
+  r.split = u / ntiles;
+  r.tile = u - r.split * ntiles;
+  if (sh.tsteps > 1) {
+    r.nkb0 = (r.split == 0 && sh.nkb0_s0 >= 0) ? sh.nkb0_s0 : sh.nkb0;
+    r.kb_lo = 0;
+    r.kb_hi = r.nkb0 + sh.nkb1;
+    r.za0 = sh.za0 + r.split * sh.za_step0;
+    r.za1 = sh.za1 + r.split * sh.za_step1;
+  } else {
+    const int nsplit = sh.ksplit > 1 ? sh.ksplit : 1, nkb = sh.nkb0 + sh.nkb1;
+    r.nkb0 = sh.nkb0;
+    r.kb_lo = r.split * nkb / nsplit;
+    r.kb_hi = (r.split + 1) * nkb / nsplit;
+    r.za0 = sh.za0;
+    r.za1 = sh.za1;
+  }
+  return r;
+}
+// Multi-step dependencies: spin (acquire, with back-off) until *p >= target.  async = the
+// caller then reads the data by TMA (async proxy): order those reads after the acquire.
+__device__ __forceinline__ void wait_ready(const unsigned int* p, unsigned int target,
+                                           bool async) {
+  unsigned int v;
+  uint32_t spins = 0;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (v >= target) break;
+    __nanosleep(128);
+    if (++spins == (1u << 26)) asm volatile("trap;");   // watchdog (~10 s)
+  }
+  if (async) asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 constexpr int kSchedDepth = 4;  // tile-index ring between the fetcher and the consumers
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -610,9 +660,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int num_m = (sh.M + TM - 1) / TM;
   const int num_n = (sh.N + BN - 1) / BN;
   const int ntiles = num_m * num_n;
-  const int nkb = sh.nkb0 + sh.nkb1;
   const int nsplit = sh.ksplit > 1 ? sh.ksplit : 1;
-  const int nunits = ntiles * nsplit;  // split-K: unit = split * ntiles + tile
+  // split-K: unit = split * ntiles + tile; multi-step: unit = step * ntiles + tile
+  const int nunits = ntiles * (sh.tsteps > 1 ? sh.tsteps : nsplit);
 
   if (threadIdx.x == 0) {
     prefetch_map(&ta0);
@@ -683,22 +733,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (tile >= nunits) break;
         if (sslot == 1 && sphase == 0) TC_TRACE(2);
-        const int split = tile / ntiles;
-        tile -= split * ntiles;
-        const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
+        const UnitInfo ui = decode_unit(sh, tile, ntiles);
+        const int kb_lo = ui.kb_lo, kb_hi = ui.kb_hi;
         int mb, nb;
-        tile_coords(tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
+        tile_coords(ui.tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
+        bool dep = sh.tsteps > 1 && ui.split > 0;   // step s-1 of this row block must be done
         const int m_row = mb * TM + rank * BM * MB;  // this CTA's A rows
         const int n_row = nb * BN + rank * (BN / 2);  // this CTA's B rows (N-half)
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
+          if (dep && kb >= sh.dep_kb) {
+            wait_ready(sh.ready + (ui.split - 1) * num_m + mb, 2u * num_n, true);
+            dep = false;
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fbar = mapa_shared(smem_u32(&full[stage]), 0);
           if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
-          const bool s1 = kb >= sh.nkb0;
-          const int kk = (s1 ? kb - sh.nkb0 : kb + sh.kb_off) * BK;
+          const bool s1 = kb >= ui.nkb0;
+          const int kk = (s1 ? kb - ui.nkb0 : kb + sh.kb_off) * BK;
           const CUtensorMap* ta = s1 ? &ta1 : &ta0;
           const CUtensorMap* tb = s1 ? &tb1 : &tb0;
-          const int za = s1 ? sh.za1 : sh.za0;
+          const int za = s1 ? ui.za1 : ui.za0;
           const int zb = s1 ? sh.zb1 : sh.zb0;
           uint8_t* a_dst = sA + stage * L::A_BYTES;
           uint8_t* b_dst = sB + stage * L::B_BYTES;
@@ -749,8 +803,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           sphase ^= 1;
         }
         if (tile >= nunits) break;
-        const int split = tile / ntiles;
-        const int kb_lo = split * nkb / nsplit, kb_hi = (split + 1) * nkb / nsplit;
+        const UnitInfo ui = decode_unit(sh, tile, ntiles);
+        const int kb_lo = ui.kb_lo, kb_hi = ui.kb_hi;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tbase + static_cast<uint32_t>(acc * 256);
@@ -809,6 +863,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int split = tile / ntiles;
       int mb, nb;
       tile_coords(tile - split * ntiles, num_m, num_n, sh.group, sh.group_n, mb, nb);
+      if (sh.tsteps > 1 && split > 0) {
+        // the epilogue reads the previous step's cell state (c / dc) of this row block
+        if (lane == 0) wait_ready(sh.ready + (split - 1) * num_m + mb, 2u * num_n, false);
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (threadIdx.x == 64 && sslot == 1 && sphase == 0) TC_TRACE(6);
@@ -824,6 +883,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      if (sh.tsteps > 1) {
+        // this CTA's half of the tile is stored: publish it to the next step (cumulative
+        // fence by one thread after the epilogue warps' barrier)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) {
+          __threadfence();
+          atomicAdd(sh.ready + split * num_m + mb, 1u);
+        }
+      }
       if (++acc == NACC) {
         acc = 0;
         acc_phase ^= 1;
@@ -1277,10 +1345,15 @@ struct EpiLstmFwd {
   float* c_out;           // C[t+1] [B][H]
   __nv_bfloat16* gates;   // G[t]   [B][4H], interleaved like the accumulator columns
   int B, H;
+  int64_t sx, sc, sg;     // multi-step launch: per-step element strides of XH, C and G
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
-                                        int split) const {
+                                        int step) const {
     static_assert(BN == 256, "cell tile holds 4 gates x 64 units");
+    __nv_bfloat16* const h_out = this->h_out + step * sx;
+    const float* const c_prev = this->c_prev + step * sc;
+    float* const c_out = this->c_out + step * sc;
+    __nv_bfloat16* const gates = this->gates + step * sg;
     const int m = m_base + row;
     const bool ok = m < B;
     const int64_t G4 = 4 * static_cast<int64_t>(H);
@@ -1357,9 +1430,14 @@ struct EpiLstmBwd {
   int first;              // 1: t = T-1, the incoming carry is zero (not read; no memset)
   int exp;                // PPO_EXPERIMENTS builds only (timing A/B, wrong results):
                           // bit0 skip the saved-activation loads, bit1 skip the stores
+  int64_t sc, sg;         // multi-step launch (step s = time T-1-s): per-step strides of C, G
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
-                                        int split) const {
+                                        int step) const {
+    __nv_bfloat16* const gz = this->gz + step * sg;
+    const float* const c_t = this->c_t + step * sc;
+    const float* const c_prev = this->c_prev + step * sc;
+    const bool first = this->first && step == 0;
     constexpr int CW = 8;  // units per chunk
     const int m = m_base + row;
     const bool ok = m < B;

@@ -122,8 +122,12 @@ int probe_die_map(DieMap& dm) {
   return PPO_OK;
 }
 
-// die-aware tile queues for the CTA-pair GEMMs (PPO_DIE_SCHED=0/1 overrides in experiment builds)
-bool die_sched() { return knob_int("PPO_DIE_SCHED", 1) != 0; }
+// Die-aware tile queues for the CTA-pair GEMMs: off.  Measured (profiles/r02_ab_die_sched2.txt,
+// same box, interleaved): each die taking a contiguous half of the raster made the step 7%
+// slower -- DRAM reads of the backward step GEMM rose from 9.6 to 14 GB per launch and the
+// cross-die (ltcfabric) traffic by 27%: both dies then stream the shared operand panels
+// separately.  PPO_DIE_SCHED=1 re-enables it in experiment builds.
+bool die_sched() { return knob_int("PPO_DIE_SCHED", 0) != 0; }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -308,7 +312,9 @@ struct WsPtrs {
   __nv_bfloat16* g;
   float* c;
   float* dc;
-  unsigned int* sched;   // this workspace's tile-scheduler counters, 2 per SchedSlot
+  unsigned int* sched;   // this workspace's tile-scheduler counters, kSchedWords per SchedSlot
+  unsigned int* ready;   // multi-step launches: [T][ceil(B / 256)] row-block ready counters
+  size_t counter_bytes;  // sched + ready
   unsigned int* slot(int k) const { return sched + kSchedWords * k; }
 };
 WsPtrs ws_ptrs(const Shape& s, int64_t B, void* ws) {
@@ -316,13 +322,29 @@ WsPtrs ws_ptrs(const Shape& s, int64_t B, void* ws) {
   uint8_t* p = static_cast<uint8_t*>(ws);
   return {reinterpret_cast<__nv_bfloat16*>(p + L.xh), reinterpret_cast<__nv_bfloat16*>(p + L.g),
           reinterpret_cast<float*>(p + L.c), reinterpret_cast<float*>(p + L.dc),
-          reinterpret_cast<unsigned int*>(p + L.sched)};
+          reinterpret_cast<unsigned int*>(p + L.sched), reinterpret_cast<unsigned int*>(p + L.ready),
+          L.ready - L.sched + (size_t)s.T * ((B + 255) / 256) * 4};
 }
 // zero the workspace's counters on the stream before its GEMMs (fresh memory is arbitrary)
 int sched_reset(const WsPtrs& P, cudaStream_t st) {
   ProfScope _prof("sched_reset", st);
-  PPO_CUDA_CHECK(cudaMemsetAsync(P.sched, 0, kSchedBytes, st));
+  PPO_CUDA_CHECK(cudaMemsetAsync(P.sched, 0, P.counter_bytes, st));
   return PPO_OK;
+}
+// The T recurrent step GEMMs as ONE persistent launch (tiles of step t+1 start as soon as
+// their row block of step t is done, instead of a launch, ramp and tail per step) when a step
+// is only a few waves of tiles (small minibatches such as the paper's B = 600); large
+// minibatches keep one launch per step (their steps are ~130 waves; nothing to overlap).
+// PPO_MULTISTEP=0/1/2 (experiment builds): off / auto / always.
+bool use_multistep(int64_t tiles_per_step, bool backward) {
+  const int k = knob_int("PPO_MULTISTEP", 1);
+  if (k == 0) return false;
+  if (k == 2) return true;
+  // the backward's A operand is almost all dz_{t+1} (only the 11 dY k-blocks are ready
+  // early), so its steps cannot overlap: measured 7% slower than per-step launches at B = 600
+  // (profiles/r02_pmb_multistep.txt); the forward's x half of K overlaps the previous step
+  if (backward) return false;
+  return tiles_per_step <= 8 * (int64_t)(num_sms() / 2);
 }
 
 }  // namespace
@@ -374,6 +396,22 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
   if ((rc = map_kmajor(&mB1, wxh, s.Kx, s.G4, s.Kx, 1, 0, 256))) return rc;
   if (pair2 && (rc = map_kmajor(&mA2, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx, 256))) return rc;
   if (pairmc && (rc = map_kmajor(&mBmc, wxh, s.Kx, s.G4, s.Kx, 1, 0, 64))) return rc;
+  const int64_t fwd_tiles = (int64_t)cdiv(B, 256) * cdiv(s.G4, 256);
+  if (pair && !pair2 && !pairmc && !x_ready && s.T > 1 && use_multistep(fwd_tiles, false)) {
+    // all T steps in one launch: step t reads XH slot t, its h k-blocks (from column D) wait
+    // for step t-1's row block; the epilogue walks XH / C / G by one slot per step
+    tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, 0, 0, 0, 0, 8, 1};
+    raster(sh, "FWD", 8, 1);
+    sh.sched = P.slot(kSchedFwd);
+    sh.tsteps = (int)s.T;
+    sh.za_step0 = 1;
+    sh.nkb0_s0 = -1;
+    sh.dep_kb = (int)(s.D / tc::BK);
+    sh.ready = P.ready;
+    tc::EpiLstmFwd epi{P.xh + B * s.Kx + s.D, s.Kx, P.c, P.c + B * s.H, P.g, (int)B, (int)s.H,
+                       B * s.Kx, B * s.H, B * s.G4};
+    if ((rc = launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st))) return rc;
+  } else
   for (int t = 0; t < s.T; ++t) {
     if (x_ready && x_ready[t]) PPO_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready[t], 0));
     tc::TileShape sh{(int)B, (int)s.G4, cdiv(s.Kx, tc::BK), 0, t, 0, 0, 0, 8, 1};
@@ -381,7 +419,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     sh.sched = P.slot(kSchedFwd);
     tc::TileShape sh1 = sh;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
-                       P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H};
+                       P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H, 0, 0, 0};
     rc = pairmc ? launch2mc("lstm_fwd_step", mA, mBmc, sh, epi, st)
          : pair2  ? launch2<false, false, tc::EpiLstmFwd, 2>("lstm_fwd_step", mA2, mA2, mB, mB, sh,
                                                            epi, st)
@@ -425,6 +463,26 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_kmajor(&a1, dY, s.A_pass, B, s.A, s.T, B * s.A, tc::BM))) return rc;
   if ((rc = map_mnmajor(&b0, wxh + s.D, s.H, s.G4, s.Kx))) return rc;
   if ((rc = map_mnmajor(&b1, wo, s.H, s.A_pass, s.Ko))) return rc;
+  const int64_t bwd_tiles = (int64_t)cdiv(B, 256) * cdiv(s.H, 256);
+  if (pair && s.T > 1 && use_multistep(bwd_tiles, true)) {
+    // all T steps in one launch, step s = time T-1-s: A = [G slot t+1 | dY slot t] (no dz part
+    // on step 0), every k-block of the dz part waits for step s-1's row block; the epilogue
+    // walks G / C back by one slot per step
+    tc::TileShape sh{(int)B, (int)s.H, cdiv(s.G4, tc::BK), cdiv(s.A_pass, tc::BK), (int)s.T,
+                     (int)s.T - 1, 0, 0, 8, 1};
+    raster(sh, "BWD", 8, 1);
+    sh.sched = P.slot(kSchedBwd);
+    sh.tsteps = (int)s.T;
+    sh.za_step0 = -1;
+    sh.za_step1 = -1;
+    sh.nkb0_s0 = 0;
+    sh.dep_kb = 0;
+    sh.ready = P.ready;
+    const int64_t t0 = s.T - 1;
+    tc::EpiLstmBwd epi{P.g + t0 * B * s.G4, P.c + (t0 + 1) * B * s.H, P.c + t0 * B * s.H, P.dc,
+                       (int)B, (int)s.H, 1, knob_int("PPO_EXP_BWD_EPI", 0), -B * s.H, -B * s.G4};
+    if ((rc = launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st))) return rc;
+  } else
   for (int t = (int)s.T - 1; t >= 0; --t) {
     const bool last = t == s.T - 1;
     tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A_pass, tc::BK),
@@ -433,7 +491,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     sh.sched = P.slot(kSchedBwd);
     tc::EpiLstmBwd epi{P.g + t * B * s.G4, P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc,
                        (int)B, (int)s.H, last ? 1 : 0,
-                       knob_int("PPO_EXP_BWD_EPI", 0)};
+                       knob_int("PPO_EXP_BWD_EPI", 0), 0, 0};
     tc::TileShape sh1 = sh;
     rc = pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
               : launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh1, epi, st);

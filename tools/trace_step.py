@@ -19,6 +19,9 @@ ap.add_argument("--B", type=int, default=32)
 ap.add_argument("--H", type=int, default=128)
 ap.add_argument("--D", type=int, default=256)
 ap.add_argument("--mhz", type=float, default=1965.0)
+ap.add_argument("--bwd", action="store_true",
+                help="trace the last backward step GEMM instead (run with PPO_VARIANT_WGRAD=1cta "
+                     "PPO_VARIANT_WGRAD_O=1cta so the weight-gradient GEMMs leave the trace alone)")
 a = ap.parse_args()
 lib = L._lib
 lib.ppo_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -27,7 +30,14 @@ opt = PPOOptimizer(a.D, a.H, a.B, 16, cfg.head_sizes, precision="bf16")
 p = synth.torch_params(cfg, 0, "cuda")
 opt.load_canonical(p["Wx"], p["Wh"], p["b"], p["Wo"], p["bo"])
 seq = synth.torch_sequences(cfg, 1, "cuda")
-batch = dict(x=seq["x"], h0=seq["h0"], c0=seq["c0"])
+batch = dict(x=seq["x"], h0=seq["h0"], c0=seq["c0"], act=seq["act"], head_on=seq["head_on"],
+             avail=seq["avail"])
+Lseg = 256 if (a.B * 16) % 256 == 0 else 160
+ro = synth.torch_rollouts(a.B * 16 // Lseg, Lseg, 1, "cuda")
+batch.update(rew=ro["rew"], val=ro["val"], done=ro["done"])
+batch["logp_old"] = opt.current_logp(batch) + seq["logp_noise"]
+if a.bwd:
+    opt.forward = lambda b: (opt.gae(b), type(opt).forward(opt, b), opt.loss(b), opt.backward())
 for _ in range(3):
     opt.forward(batch)
 torch.cuda.synchronize()
@@ -37,7 +47,7 @@ for _ in range(10):
     opt.forward(batch)
 e1.record()
 torch.cuda.synchronize()
-print(f"forward (16 step GEMMs + heads): {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
+print(f"{'gae+forward+loss+backward' if a.bwd else 'forward (16 step GEMMs + heads)'}: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
 lib.ppo_trace_clear()
 opt.forward(batch)
 torch.cuda.synchronize()
