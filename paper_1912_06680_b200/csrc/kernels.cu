@@ -1320,7 +1320,7 @@ int launch_pack_x(const Shape& s, int64_t B, const void* x, const float* h0, con
 static bool gae_use_short(int64_t R, int64_t L) { return L <= kGaeShortL || R >= 600; }
 
 size_t gae_scratch_bytes(int64_t R, int64_t L) {
-  if (gae_use_short(R, L)) return 0;
+  if (gae_use_short(R, L) && knob_int("PPO_GAE_VARIANT", 0) != 5) return 0;
   const int64_t nck = (L + kGaeChunk - 1) / kGaeChunk;
   return 256 + (size_t)(R * nck) * sizeof(GaeStatus);
 }
@@ -1339,7 +1339,28 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
                float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,
                cudaStream_t st) {
   ProfScope _prof("gae", st);
-  if (gae_use_short(R, L)) {
+  // experiment builds: PPO_GAE_VARIANT = 1 <8, no prefetch>, 2 <8, prefetch>, 3 <16, prefetch>,
+  // 4 <16, no prefetch>, 5 the chunk-parallel look-back kernel (needs the long-kernel scratch)
+  const int var = knob_int("PPO_GAE_VARIANT", 0);
+  if (var >= 1 && var <= 4) {
+    const int64_t threads = R * 32;
+    const bool vec = aligned(rew, 32) && aligned(done, 8) && aligned(adv, 32) && aligned(ret, 32);
+    if (var == 1)
+      gae_kernel<8, false><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
+                                                                   seq_T, adv, ret, vec);
+    else if (var == 2)
+      gae_kernel<8, true><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma, lam,
+                                                                  seq_T, adv, ret, vec);
+    else if (var == 3)
+      gae_kernel<16, true><<<grid_for(threads, 64), 64, 0, st>>>(rew, val, done, R, L, gamma, lam,
+                                                                 seq_T, adv, ret, vec);
+    else if (var == 4)
+      gae_kernel<16, false><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma,
+                                                                    lam, seq_T, adv, ret, vec);
+    PPO_LAUNCH_CHECK("gae_kernel");
+    return PPO_OK;
+  }
+  if (var != 5 && gae_use_short(R, L)) {
     const int64_t threads = R * 32;
     // the aligned-chunk path needs 32-byte aligned r, A, R bases and an 8-byte aligned d base
     const bool vec = aligned(rew, 32) && aligned(done, 8) && aligned(adv, 32) && aligned(ret, 32);

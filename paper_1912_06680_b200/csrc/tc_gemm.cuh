@@ -1315,25 +1315,27 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* p, const float (&v)
     h0[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
     h1[i] = __floats2bfloat162_rn(v[8 + 2 * i], v[8 + 2 * i + 1]);
   }
-  uint4* q = reinterpret_cast<uint4*>(p);
-  q[0] = a;
-  q[1] = b;
+  // one 32-byte sector: a single 256-bit store (sm_100)
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
+               "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
 }
+// 16 floats = two 32-byte sectors: two 256-bit loads / stores (sm_100)
 __device__ __forceinline__ void load_f32x16(const float* p, float (&v)[16]) {
-  const float4* q = reinterpret_cast<const float4*>(p);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float4 a = q[i];
-    v[4 * i] = a.x;
-    v[4 * i + 1] = a.y;
-    v[4 * i + 2] = a.z;
-    v[4 * i + 3] = a.w;
-  }
+  for (int h = 0; h < 2; ++h)
+    asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[8 * h]), "=f"(v[8 * h + 1]), "=f"(v[8 * h + 2]), "=f"(v[8 * h + 3]),
+                   "=f"(v[8 * h + 4]), "=f"(v[8 * h + 5]), "=f"(v[8 * h + 6]), "=f"(v[8 * h + 7])
+                 : "l"(p + 8 * h));
 }
 __device__ __forceinline__ void store_f32x16(float* p, const float (&v)[16]) {
-  float4* q = reinterpret_cast<float4*>(p);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) q[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  for (int h = 0; h < 2; ++h)
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p + 8 * h),
+                 "f"(v[8 * h]), "f"(v[8 * h + 1]), "f"(v[8 * h + 2]), "f"(v[8 * h + 3]),
+                 "f"(v[8 * h + 4]), "f"(v[8 * h + 5]), "f"(v[8 * h + 6]), "f"(v[8 * h + 7])
+                 : "memory");
 }
 
 // LSTM forward step t (oracle O4).  Tile = 128 sequences x 256 gate rows = 4 gates of 64
@@ -1396,15 +1398,30 @@ struct BwdRaw {
   uint4 g[4];            // gates i, f, g, o: 8 bf16 each
   float4 ct[2], cp[2], dc[2];
 };
+// 32-byte (one sector) loads and stores of 8 floats: sm_100's 256-bit LDG/STG
+__device__ __forceinline__ void ld_f32x8(const float* p, float4 (&v)[2]) {
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0].x), "=f"(v[0].y), "=f"(v[0].z), "=f"(v[0].w), "=f"(v[1].x),
+                 "=f"(v[1].y), "=f"(v[1].z), "=f"(v[1].w)
+               : "l"(p));
+}
+__device__ __forceinline__ void st_f32x8(float* p, const float4 (&v)[2]) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0].x),
+               "f"(v[0].y), "f"(v[0].z), "f"(v[0].w), "f"(v[1].x), "f"(v[1].y), "f"(v[1].z),
+               "f"(v[1].w)
+               : "memory");
+}
 __device__ __forceinline__ void bwd_load(BwdRaw& r, const __nv_bfloat16* gp, const float* ct,
                                          const float* cp, const float* dc) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) r.g[q] = *reinterpret_cast<const uint4*>(gp + q * 64);
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    r.ct[q] = reinterpret_cast<const float4*>(ct)[q];
-    r.cp[q] = reinterpret_cast<const float4*>(cp)[q];
-    r.dc[q] = dc ? reinterpret_cast<const float4*>(dc)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  ld_f32x8(ct, r.ct);   // 8 units of c_t, c_{t-1}, dc: one full 32-byte sector each
+  ld_f32x8(cp, r.cp);
+  if (dc) {
+    ld_f32x8(dc, r.dc);
+  } else {
+    r.dc[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    r.dc[1] = r.dc[0];
   }
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
@@ -1449,9 +1466,9 @@ struct EpiLstmBwd {
       const int j0 = n_base + cc * CW;
       return (j0 >> 6) * 256 + (j0 & 63);
     };
-    // the saved activations are loaded two chunks ahead (cur = chunk cc, nxt = cc + 1,
-    // nx2 = cc + 2 in flight), so a chunk's math overlaps ~2 chunks of HBM latency
-    BwdRaw cur, nxt, nx2;
+    // the saved activations of chunk cc + 1 are loaded while chunk cc computes (two chunks
+    // ahead measured 2% slower in the step at B = 38,400: profiles/r02_ab_bwd_ahead.txt)
+    BwdRaw cur, nxt;
     const float* dcin = first ? nullptr : dc;
 #ifdef PPO_EXPERIMENTS
     const bool no_ld = exp & 1, no_st = exp & 2;
@@ -1463,16 +1480,13 @@ struct EpiLstmBwd {
       const int64_t o = crow + cc * CW;
       bwd_load(r, grow + goff(cc), c_t + o, c_prev + o, dcin ? dcin + o : nullptr);
     };
-    if (ok && !no_ld) {
-      if (nch > 0) load_chunk(cur, 0);
-      if (nch > 1) load_chunk(nxt, 1);
-    }
+    if (ok && !no_ld && nch > 0) load_chunk(cur, 0);
 #pragma unroll 1
     for (int cc = 0; cc < BN / CW; ++cc) {
       float dh[8];
       tmem_ld8(taddr + cc * CW, dh);
       if (cc >= nch) continue;
-      if (ok && cc + 2 < nch && !no_ld) load_chunk(nx2, cc + 2);
+      if (ok && cc + 1 < nch && !no_ld) load_chunk(nxt, cc + 1);
       if (ok) {
         // in place: each 32-bit gate word holds units (2w, 2w+1); dz overwrites the gates
         float* ct = reinterpret_cast<float*>(cur.ct);
@@ -1509,17 +1523,12 @@ struct EpiLstmBwd {
           __nv_bfloat16* gp = gz + static_cast<int64_t>(m) * G4 + goff(cc);
 #pragma unroll
           for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(gp + q * 64) = cur.g[q];
-          float4* d4 = reinterpret_cast<float4*>(dc + crow + cc * CW);
-          d4[0] = cur.dc[0];
-          d4[1] = cur.dc[1];
+          st_f32x8(dc + crow + cc * CW, cur.dc);
         } else if (cur.dc[0].x == 1234.5f) {   // keep the math live
           dc[crow] = cur.dc[1].y + __uint_as_float(cur.g[0].x);
         }
       }
-      if (!no_ld) {
-        cur = nxt;
-        nxt = nx2;
-      }
+      if (!no_ld) cur = nxt;
     }
   }
 };
