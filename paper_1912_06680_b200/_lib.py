@@ -12,6 +12,9 @@ from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libppo5.so")
+# A/B timing of two builds (tools/ab_builds.sh): load another build of the same ABI
+if os.environ.get("PPO_LIB_PATH"):
+    LIB_PATH = os.environ["PPO_LIB_PATH"]
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python paper_1912_06680_b200/build.py` "
@@ -144,6 +147,8 @@ _lib_fns = dict(
 )
 EXPORTED = tuple(_lib_fns)
 for _n, (_a, _r) in _lib_fns.items():
+    if os.environ.get("PPO_LIB_PATH") and not hasattr(_lib, _n):
+        continue   # A/B against an older build: calls it lacks are unavailable
     _sig(_n, _a, _r)
 
 
