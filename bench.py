@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--H", type=int, default=4096)
     ap.add_argument("--D", type=int, default=4032)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="fused DP exchange: do not overlap W_xh's exchange with the dW_o GEMM")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seq", type=int, default=1, help="oracle sample: sequences per step")
     ap.add_argument("--aux", action="store_true",
@@ -225,6 +227,8 @@ def workload_config(args, n):
         "parallelism": f"dp{n}",
         "dp_exchange": (None if n == 1 else
                         "fused: NVLink peer-memory reduce-scatter + Adam on 1/N + bf16 all-gather"
+                        + ("" if getattr(args, "no_overlap", False) else
+                           "; W_xh's exchange overlapped with the dW_o GEMM")
                         if getattr(args, "dp", "nccl") == "fused" else
                         "fused-push: gradient shards pushed to their owners over NVLink from the "
                         "backward's epilogues + Adam on 1/N + bf16 all-gather"
@@ -677,7 +681,8 @@ def main():
     cfg = synth.Config(H=H, D=D, B=B, T=T, aux=aux)
     mk = lambda dp: PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16",  # noqa: E731
                                  device=device, comm=comm, n_buckets=8,
-                                 n_ws=1 if args.no_e2e else 2, aux=aux, dp=dp)
+                                 n_ws=1 if args.no_e2e else 2, aux=aux, dp=dp,
+                                 overlap=not args.no_overlap)
     opt = None
     if comm is not None and args.dp.startswith("fused"):
         # the peer mappings (CUDA IPC) need plain cudaMalloc'd buffers; every rank must agree

@@ -218,6 +218,12 @@ int ppo_aux_labels(const ppo_dims* dims, int64_t R, int64_t L, const uint8_t* la
 int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
                   const void* dout, int64_t B, float* grad, ppo_stream_t s);
 
+/* lstm_bptt_bwd that also records wxh_ready (a cudaEvent_t, nullable) on s as soon as the
+ * W_xh_aug gradient -- theta [0, off_wo) -- is final, before the W_o gradient GEMM, so the
+ * caller can start exchanging it while dW_o computes (ppo_dp_adam_step_range). */
+int lstm_bptt_bwd_ev(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
+                     const void* dout, int64_t B, float* grad, void* wxh_ready, ppo_stream_t s);
+
 /* NEXT-4: dL/dx for the upstream observation-processing network (the processed
  * observation vector is the LSTM input).  dx[t][b][:] = dz_t[b] W_x for all t, from the dz
  * that lstm_bptt_bwd left in ws (call it after lstm_bptt_bwd, same w, ws, B).
@@ -267,6 +273,15 @@ int ppo_dp_attach(ppo_comm* comm, float* g, float* p, uint16_t* p_bf16, size_t n
  * from this rank's staging, filled by every rank's lstm_bptt_bwd_dp of this step. */
 int ppo_dp_adam_step(ppo_comm* comm, float* m, float* v, int64_t t, double lr, double b1,
                      double b2, double eps, double clip_sigma, int32_t staged, ppo_stream_t s);
+/* The same exchange restricted to theta elements [lo, hi) (lo a multiple of 64; hi a multiple
+ * of 64 or n): each rank updates its shard's part of the range, with the same barriers.  With
+ * lstm_bptt_bwd_ev the step overlaps the exchange of W_xh_aug (theta [0, off_wo), 97% of the
+ * bytes) with the dW_o GEMM: range [0, off_wo) on a second stream once wxh_ready fires, then
+ * [off_wo, n) after the backward.  Every rank must issue the range calls in the same order
+ * (they are collective over the comm's NCCL communicator, which serialises them). */
+int ppo_dp_adam_step_range(ppo_comm* comm, float* m, float* v, int64_t t, double lr, double b1,
+                           double b2, double eps, double clip_sigma, int32_t staged, size_t lo,
+                           size_t hi, ppo_stream_t s);
 /* Push mode (staged = 1 in ppo_dp_adam_step): the backward itself delivers the gradients --
  * lstm_bptt_bwd, plus: the epilogues of the tiles that produce final weight gradients (the
  * last K-chunk of dW_xh, dW_o's split-K reduction) also store each 4-element group over

@@ -117,6 +117,10 @@ _lib_fns = dict(
     lstm_bptt_bwd_dp=([_D, c_void_p, c_void_p, c_size_t, c_void_p, c_int64, c_void_p, c_void_p,
                        c_void_p], c_int),
     ppo_dp_allgather=([c_void_p, c_void_p, c_void_p], c_int),
+    ppo_dp_adam_step_range=([c_void_p, c_void_p, c_void_p, c_int64, c_double, c_double, c_double,
+                             c_double, c_double, c_int32, c_size_t, c_size_t, c_void_p], c_int),
+    lstm_bptt_bwd_ev=([_D, c_void_p, c_void_p, c_size_t, c_void_p, c_int64, c_void_p, c_void_p,
+                       c_void_p], c_int),
     ppo_test_dp_adam=([c_int32] + [POINTER(c_void_p)] * 6 + [c_size_t, c_int64, c_double,
                       c_double, c_double, c_double, c_double, c_void_p], c_int),
     adam_step=([c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int64, c_double,
@@ -407,6 +411,20 @@ def dp_attach(comm, g, p, p_bf16, n: int):
 def dp_adam_step(comm, m, v, t, lr, b1, b2, eps, clip_sigma, staged=False, stream=None):
     _check(_lib.ppo_dp_adam_step(comm, _p(m), _p(v), t, lr, b1, b2, eps, clip_sigma,
                                  1 if staged else 0, _s(stream)))
+
+
+def dp_adam_step_range(comm, m, v, t, lr, b1, b2, eps, clip_sigma, lo, hi, staged=False,
+                       stream=None):
+    _check(_lib.ppo_dp_adam_step_range(comm, _p(m), _p(v), t, lr, b1, b2, eps, clip_sigma,
+                                       1 if staged else 0, lo, hi, _s(stream)))
+
+
+def lstm_bptt_bwd_ev(dims, w, ws, dout, B, grad, wxh_ready=None, stream=None):
+    """backward recording wxh_ready (torch.cuda.Event) once the W_xh gradient is final"""
+    _check(_lib.lstm_bptt_bwd_ev(ctypes.byref(dims), _p(w), _p(ws), ws.numel() * ws.element_size(),
+                                 _p(dout), B, _p(grad),
+                                 None if wxh_ready is None else c_void_p(wxh_ready.cuda_event),
+                                 _s(stream)))
 
 
 def lstm_bptt_bwd_dp(dims, w, ws, dout, B, grad, comm, stream=None):

@@ -437,7 +437,14 @@ int lstm_bptt_bwd_dp(const ppo_dims* dims, const void* w, void* ws, size_t ws_by
 
 int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
                   const void* dout, int64_t B, float* grad, ppo_stream_t st_) {
+  return lstm_bptt_bwd_ev(dims, w, ws, ws_bytes, dout, B, grad, nullptr, st_);
+}
+
+int lstm_bptt_bwd_ev(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes,
+                     const void* dout, int64_t B, float* grad, void* wxh_ready_ev,
+                     ppo_stream_t st_) {
   cudaStream_t st = (cudaStream_t)st_;
+  cudaEvent_t wxh_ready = static_cast<cudaEvent_t>(wxh_ready_ev);
   Shape s;
   int rc = check_dims(dims, &s);
   if (rc) return rc;
@@ -450,7 +457,7 @@ int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes
   if (ws_bytes < L.total) return fail(PPO_E_ARG, "workspace too small");
   if (s.bf16) {
     if ((rc = check_tc_device())) return rc;
-    return tc_backward(s, B, w, ws, dout, grad, st);
+    return tc_backward(s, B, w, ws, dout, grad, st, nullptr, wxh_ready);
   }
   // ---- SIMT fp32 reference path
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -490,6 +497,7 @@ int lstm_bptt_bwd(const ppo_dims* dims, const void* w, void* ws, size_t ws_bytes
     SimtOp b{{XH, nullptr}, {s.Kx, 0}, {s.Kx, 0}, {rows, 0}, rows, true};
     if ((rc = launch_simt_gemm(a, b, s.G4, s.Kx, rows, grad, s.Kx, st))) return rc;
   }
+  if (wxh_ready) PPO_CUDA_CHECK(cudaEventRecord(wxh_ready, st));
   {
     SimtOp a{{dY, nullptr}, {s.A, 0}, {s.A, 0}, {rows, 0}, rows, true};
     SimtOp b{{XH + B * s.Kx + s.D, nullptr}, {s.Kx, 0}, {s.Ko, 0}, {rows, 0}, rows, true};

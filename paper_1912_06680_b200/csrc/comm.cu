@@ -151,9 +151,9 @@ __global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int
                                                       float* __restrict__ v, ppo::AdamParams ap,
                                                       float inv_world,
                                                       const float* __restrict__ stage,
-                                                      size_t shard) {
+                                                      size_t shard, size_t shard_lo) {
   auto gsrc = [&](int j, size_t e) -> const float* {   // rank j's gradient element e
-    return stage ? stage + (size_t)j * shard + (e - lo) : pe.g[j] + e;
+    return stage ? stage + (size_t)j * shard + (e - shard_lo) : pe.g[j] + e;
   };
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t lo4 = lo / 4, hi4 = hi / 4;           // lo is a multiple of 64
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) dp_adam_kernel(DpPeers pe, int world, int
 
 int launch_dp_adam(const DpPeers& pe, int world, int rank, size_t lo, size_t hi, float* m,
                    float* v, const ppo::AdamParams& ap, const float* stage, size_t shard,
-                   cudaStream_t st) {
+                   cudaStream_t st, size_t shard_lo) {
   ppo::ProfScope _prof("dp_adam", st);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -219,7 +219,7 @@ int launch_dp_adam(const DpPeers& pe, int world, int rank, size_t lo, size_t hi,
   const size_t units = (hi - lo) / 4 + 1;
   const int grid = (int)std::min<size_t>((size_t)sms * 8, (units + 255) / 256);
   dp_adam_kernel<<<std::max(grid, 1), 256, 0, st>>>(pe, world, rank, lo, hi, m, v, ap,
-                                                    1.0f / (float)world, stage, shard);
+                                                    1.0f / (float)world, stage, shard, shard_lo);
   PPO_LAUNCH_CHECK("dp_adam_kernel");
   return PPO_OK;
 }
@@ -317,6 +317,13 @@ int ppo_dp_attach(ppo_comm* c, float* g, float* p, uint16_t* p_bf16, size_t n) {
 int ppo_dp_adam_step(ppo_comm* c, float* m, float* v, int64_t t, double lr, double b1,
                      double b2, double eps, double clip_sigma, int32_t staged, ppo_stream_t s) {
   if (!c) return ppo::fail(PPO_E_ARG, "comm is NULL");
+  return ppo_dp_adam_step_range(c, m, v, t, lr, b1, b2, eps, clip_sigma, staged, 0, c->n, s);
+}
+
+int ppo_dp_adam_step_range(ppo_comm* c, float* m, float* v, int64_t t, double lr, double b1,
+                           double b2, double eps, double clip_sigma, int32_t staged,
+                           size_t range_lo, size_t range_hi, ppo_stream_t s) {
+  if (!c) return ppo::fail(PPO_E_ARG, "comm is NULL");
   if (!c->attached) return ppo::fail(PPO_E_ARG, "ppo_dp_attach was not called on this comm");
   if (!m || !v) return ppo::fail(PPO_E_ARG, "m or v is NULL");
   if (!ppo::aligned(m, 16) || !ppo::aligned(v, 16))
@@ -324,13 +331,18 @@ int ppo_dp_adam_step(ppo_comm* c, float* m, float* v, int64_t t, double lr, doub
   if (t < 1) return ppo::fail(PPO_E_ARG, "t must be >= 1");
   if (!(b1 >= 0.0 && b1 < 1.0 && b2 >= 0.0 && b2 < 1.0)) return ppo::fail(PPO_E_ARG, "bad betas");
   const ppo::AdamParams ap = ppo::make_adam_params(t, lr, b1, b2, eps, clip_sigma);
+  if (range_lo > range_hi || range_hi > c->n || (range_lo % 64) ||
+      (range_hi % 64 && range_hi != c->n))
+    return ppo::fail(PPO_E_ARG, "range must be [lo, hi) within theta, multiples of 64 (or hi = n)");
   const size_t sh = ppo_dp_shard(c->n, c->world);
-  const size_t lo = std::min(c->n, sh * (size_t)c->rank), hi = std::min(c->n, lo + sh);
+  const size_t slo = std::min(c->n, sh * (size_t)c->rank), shi = std::min(c->n, slo + sh);
+  // this rank's shard within the range (possibly empty; the barriers still run)
+  const size_t lo = std::max(slo, range_lo), hi = std::max(lo, std::min(shi, range_hi));
   cudaStream_t st = (cudaStream_t)s;
   int rc = PPO_OK;
   if (c->world > 1 && (rc = barrier(c, st)) != PPO_OK) return rc;   // every grad is final
   rc = launch_dp_adam(c->peers, c->world, c->rank, lo, hi, m, v, ap,
-                      staged && c->world > 1 ? c->stage : nullptr, sh, st);
+                      staged && c->world > 1 ? c->stage : nullptr, sh, st, slo);
   if (rc != PPO_OK) return rc;
   // every rank's writes into this rank's theta/shadow have landed, and no rank still reads
   // this rank's grad, before the caller's next step
@@ -380,7 +392,7 @@ int ppo_test_dp_adam(int32_t world, const float* const* g, float* const* p,
     const size_t lo = std::min(n, sh * (size_t)r), hi = std::min(n, lo + sh);
     if (lo == hi) continue;
     const int rc = launch_dp_adam(pe, world, r, lo, hi, m[r], v[r], ap,
-                                  stage && world > 1 ? stage[r] : nullptr, sh, (cudaStream_t)s);
+                                  stage && world > 1 ? stage[r] : nullptr, sh, (cudaStream_t)s, lo);
     if (rc != PPO_OK) return rc;
   }
   return PPO_OK;

@@ -95,8 +95,9 @@ int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cu
 int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
                const cudaEvent_t* x_ready, cudaStream_t st);
 // dp (nullable): push the final weight gradients to the DP owners' staging (fused exchange)
+// wxh_ready (nullable): recorded on st once the W_xh gradient is final (before dW_o)
 int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
-                cudaStream_t st, const DpStage* dp = nullptr);
+                cudaStream_t st, const DpStage* dp = nullptr, cudaEvent_t wxh_ready = nullptr);
 // Standalone test GEMM (exported for tests): C = A B^T variants on bf16 inputs.
 // NEXT-4: dX = dz W_x over all T*B rows (bf16 path)
 int tc_input_grad(const Shape& s, int64_t B, const void* w, void* ws, float* dx, cudaStream_t st);

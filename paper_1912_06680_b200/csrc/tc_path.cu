@@ -455,7 +455,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
 
 // ---------------------------------------------------------------- backward (a6-a8)
 int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* dout, float* grad,
-                cudaStream_t st, const DpStage* dp) {
+                cudaStream_t st, const DpStage* dp, cudaEvent_t wxh_ready) {
   WsPtrs P = ws_ptrs(s, B, ws);
   const __nv_bfloat16* wxh = static_cast<const __nv_bfloat16*>(w);
   const __nv_bfloat16* wo = wxh + s.G4 * s.Kx;
@@ -546,6 +546,8 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
       if (rc) return rc;
     }
   }
+  // dW_xh (97% of theta) is final here: let the caller start exchanging it (overlapping dW_o)
+  if (wxh_ready) PPO_CUDA_CHECK(cudaEventRecord(wxh_ready, st));
   if ((rc = map_mnmajor(&oa, dY, s.A, rows, s.A))) return rc;
   if ((rc = map_mnmajor(&ob, P.xh + B * s.Kx + s.D, s.Ko, rows, s.Kx))) return rc;
   {

@@ -34,7 +34,7 @@ class PPOOptimizer:
     def __init__(self, D: int, H: int, B: int, T: int = 16, head_sizes=HEAD_SIZES,
                  precision: str = "bf16", device="cuda", hyper: dict | None = None,
                  comm=None, n_buckets: int = 1, n_ws: int = 1, aux=(0, 0, 0),
-                 dp: str = "allreduce"):
+                 dp: str = "allreduce", overlap: bool = True):
         self.D, self.H, self.B, self.T = D, H, B, T
         self.head_sizes = tuple(head_sizes)
         self.aux = tuple(aux)           # NEXT-4 (n_win, n_rank, n_bld) heads after the value
@@ -76,6 +76,15 @@ class PPOOptimizer:
                         and sum(self.aux) == 0)
         if self.dp == "fused":
             L.dp_attach(comm, self.grad, self.theta, self.shadow, n)
+        # pull mode at world > 1: exchange W_xh_aug (97% of theta) on a second stream while the
+        # backward's last GEMM (dW_o) still runs (lstm_bptt_bwd_ev + ppo_dp_adam_step_range)
+        self._overlap = self.dp == "fused" and world > 1 and not self.dp_push and overlap
+        if self._overlap:
+            self._comm_stream = torch.cuda.Stream(device=dev)
+            self._wxh_ev = torch.cuda.Event()
+            self._xch_done = torch.cuda.Event()
+            self._wxh_ev.record()        # (creates the events before the library records them)
+            self._xch_done.record()
         # activation workspaces; n_ws = 2 lets the next step's x be uploaded into one while
         # the current step runs in the other
         self.ws_list = [_aligned_empty(L.ws_bytes(self.dims, B), dev) for _ in range(n_ws)]
@@ -239,6 +248,10 @@ class PPOOptimizer:
             L.lstm_bptt_bwd_dp(self.dims, self.weights, self.ws, self.dout, self.B, self.grad,
                                self.comm, stream)
             return
+        if self._overlap:
+            L.lstm_bptt_bwd_ev(self.dims, self.weights, self.ws, self.dout, self.B, self.grad,
+                               self._wxh_ev, stream)
+            return
         L.lstm_bptt_bwd(self.dims, self.weights, self.ws, self.dout, self.B, self.grad, stream)
 
     def input_grad(self, dx: torch.Tensor, stream=None):
@@ -257,6 +270,20 @@ class PPOOptimizer:
         if self.device_t:
             L.adam_step_ctr(self.theta, self.shadow, self.grad, self.m, self.v, self._ctr, h["lr"],
                             h["beta1"], h["beta2"], h["adam_eps"], h["clip_sigma"], stream)
+            return
+        if self.dp == "fused" and self._overlap:
+            # W_xh_aug's shard exchange + Adam on the comm stream once its gradient is final
+            # (overlapping dW_o), then W_o_aug's on this stream; the next step waits for both
+            cs = self._comm_stream
+            main = stream or torch.cuda.current_stream(self.device)
+            off = self.layout.off_wo
+            args = (self.t, h["lr"], h["beta1"], h["beta2"], h["adam_eps"], h["clip_sigma"])
+            cs.wait_event(self._wxh_ev)
+            L.dp_adam_step_range(self.comm, self.m, self.v, *args, 0, off, stream=cs)
+            L.dp_adam_step_range(self.comm, self.m, self.v, *args, off, self.layout.n_total,
+                                 stream=main)
+            self._xch_done.record(cs)
+            main.wait_event(self._xch_done)
             return
         if self.dp == "fused":
             L.dp_adam_step(self.comm, self.m, self.v, self.t, h["lr"], h["beta1"], h["beta2"],
@@ -291,7 +318,10 @@ class PPOOptimizer:
 
     # ---------------------------------------------------------------- CUDA graphs
     def use_device_t(self):
-        """Switch Adam to the device step counter (adam_step_ctr), continuing from self.t."""
+        """Switch Adam to the device step counter (adam_step_ctr), continuing from self.t.
+        (Single rank or NCCL-allreduce exchange: the fused exchange takes t from the host.)"""
+        if self.dp == "fused":
+            raise ValueError("the device step counter needs dp='allreduce' (or one rank)")
         if not self.device_t:
             self._ctr[0] = self.t
             self.device_t = True
