@@ -217,8 +217,16 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
   if (!sh.sched) return fail(PPO_E_CUDA, "tile scheduler counter unavailable");
   const int64_t ntiles = (int64_t)((sh.M + 256 * MB - 1) / (256 * MB)) * ((sh.N + BN - 1) / BN) *
                          std::max(sh.ksplit, 1);
-  // PPO_GRID_ALL_TILES=1: one cluster per tile (hardware-ordered dispatch; experiment knob)
-  const bool all_tiles = knob_int("PPO_GRID_ALL_TILES", 0) != 0;
+  // PPO_GRID_ALL_TILES=1 (or PPO_GRID_ALL_TILES_<tag>=1): one cluster per tile, hardware-
+  // ordered dispatch instead of the persistent schedule (experiment knob)
+  bool all_tiles = knob_int("PPO_GRID_ALL_TILES", 0) != 0;
+#ifdef PPO_EXPERIMENTS
+  {
+    char n[64];
+    snprintf(n, sizeof(n), "PPO_GRID_ALL_TILES_%s", tag);
+    all_tiles = all_tiles || knob_int(n, 0) != 0;
+  }
+#endif
   const int clusters = (int)std::min<int64_t>(ntiles, all_tiles ? (int64_t)1 << 30 : num_sms() / 2);
   if (clusters <= 0) return PPO_OK;
   tc::TileShape shd = sh;

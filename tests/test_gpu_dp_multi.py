@@ -2,8 +2,9 @@
 torchrun -- N NCCL ranks on B/N sequences each against one GPU on the whole batch, for both
 gradient exchanges (NCCL allreduce + Adam; the fused NVLink peer-memory reduce-scatter +
 Adam + all-gather, in push mode -- shards delivered by the backward's epilogues -- and pull
-mode; push must equal pull bit for bit).  Tolerance: theta, the update, m and v normwise 1e-5
-(fp32 path; only the sum order differs) and 2e-2 (bf16 path) against one GPU; after step 1
+mode; push must equal pull bit for bit).  Tolerance: theta, m and v normwise 1e-5 (fp32
+path; only the sum order differs) and 2e-2 (bf16 path) against one GPU, the update 1e-4 / 2e-2
+(it is a difference of fp32 thetas: one ulp of theta is ~1e-4 of the update); after step 1
 also against the oracle on the whole batch (averaged gradient, m, and the update where the
 gradient sign is resolved): 1e-4 (fp32) / 2e-2 (bf16); replicas bit-identical after the
 exchange.  The world 2/4/8 arithmetic of the fused kernel is also checked on ONE GPU against
@@ -36,10 +37,12 @@ def test_dp_two_ranks(dp, precision):
     res = next(x for x in lines if "theta_err" in x)
     rep = next(x for x in lines if "replicas_identical" in x)
     tol = 1e-5 if precision == "fp32" else 2e-2
-    assert res["ok"], res
-    for k in ("theta_err", "m_err", "v_err", "update_err"):      # vs one GPU, whole batch
+    assert res["ok"], json.dumps(res)
+    for k in ("theta_err", "m_err", "v_err"):                    # vs one GPU, whole batch
         assert res[k] < tol, (k, res)
     otol = 1e-4 if precision == "fp32" else 2e-2                  # vs the oracle (step 1)
+    # the update vs one GPU is a difference of fp32 thetas (one ulp ~ 1e-4 of the update)
+    assert res["update_err"] < otol, res
     for k in ("oracle_m_err", "oracle_update_err", "oracle_grad_err"):
         assert res.get(k, 0.0) < otol, (k, res)
     assert res["oracle_firm_frac"] > (0.9 if precision == "fp32" else 0.8), res
