@@ -482,11 +482,6 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
   if ((rc = map_mnmajor(&b0, wxh + s.D, s.H, s.G4, s.Kx))) return rc;
   if ((rc = map_mnmajor(&b1, wo, s.H, s.A_pass, s.Ko))) return rc;
   const int64_t bwd_tiles = (int64_t)cdiv(B, 256) * cdiv(s.H, 256);
-  // Small minibatches (fewer 256 x 256 tiles than CTA pairs, e.g. the paper's B = 600: 48
-  // tiles on 74 pairs) take 256 x 128 tiles: twice the tiles, and a tile's epilogue (the
-  // cell backward, bound by its loads) overlaps the pair's next mainloop.  PPO_BWD_NARROW=0/1
-  // overrides in experiment builds.
-  const bool narrow = knob_int("PPO_BWD_NARROW", bwd_tiles < num_sms() / 2 ? 1 : 0) != 0;
   if (pair && s.T > 1 && use_multistep(bwd_tiles, true)) {
     // all T steps in one launch, step s = time T-1-s: A = [G slot t+1 | dY slot t] (no dz part
     // on step 0), every k-block of the dz part waits for step s-1's row block; the epilogue
@@ -516,9 +511,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
                        (int)B, (int)s.H, last ? 1 : 0,
                        knob_int("PPO_EXP_BWD_EPI", 0), 0, 0};
     tc::TileShape sh1 = sh;
-    rc = pair && narrow ? launch2<false, true, tc::EpiLstmBwd, 1, 128>("lstm_bwd_step", a0, a1,
-                                                                       b0, b1, sh, epi, st)
-         : pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
+    rc = pair ? launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st)
               : launch<256, false, true>("lstm_bwd_step", a0, a1, b0, b1, sh1, epi, st);
     if (rc) return rc;
   }
