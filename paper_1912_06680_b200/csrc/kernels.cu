@@ -1342,7 +1342,7 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
   // experiment builds: PPO_GAE_VARIANT = 1 <8, no prefetch>, 2 <8, prefetch>, 3 <16, prefetch>,
   // 4 <16, no prefetch>, 5 the chunk-parallel look-back kernel (needs the long-kernel scratch)
   const int var = knob_int("PPO_GAE_VARIANT", 0);
-  if ((var >= 1 && var <= 4) || var == 9 || var == 10) {
+  if (var >= 1 && var <= 4) {
     const int64_t threads = R * 32;
     const bool vec = aligned(rew, 32) && aligned(done, 8) && aligned(adv, 32) && aligned(ret, 32);
     if (var == 1)
@@ -1357,12 +1357,6 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
     else if (var == 4)
       gae_kernel<16, false><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma,
                                                                     lam, seq_T, adv, ret, vec);
-    else if (var == 9)
-      gae_kernel<8, false, 5><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma,
-                                                                      lam, seq_T, adv, ret, vec);
-    else if (var == 10)
-      gae_kernel<8, false, 6><<<grid_for(threads, 256), 256, 0, st>>>(rew, val, done, R, L, gamma,
-                                                                      lam, seq_T, adv, ret, vec);
     PPO_LAUNCH_CHECK("gae_kernel");
     return PPO_OK;
   }
