@@ -768,12 +768,15 @@ def main():
                            frac=ach / pk["hbm_gbs"])
         kernels[tag] = ent
     # DRAM traffic per launch from the committed ncu --set full capture of this config
-    traffic = {}
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            traffic = json.load(f)["kernels"]
-    except (OSError, KeyError, ValueError):
-        pass
+    traffic, traffic_src = {}, None
+    for name in ("r02_traffic.json", "r01_traffic.json"):   # the newest capture present
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                traffic = json.load(f)["kernels"]
+            traffic_src = f"profiles/{name} (ncu --set full, B=38400)"
+            break
+        except (OSError, KeyError, ValueError):
+            pass
     for tag, ent in kernels.items():
         if tag in traffic:
             ent["traffic_per_launch"] = traffic[tag]["dram_bytes_per_launch"]
@@ -785,7 +788,7 @@ def main():
     roofline = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": d["unit"], "frac": d["frac"],
                 "traffic": traffic.get(dom, {}).get("dram_bytes_per_launch") if B == 38400 else None,
-                "traffic_source": "profiles/r01_traffic.json (ncu --set full, B=38400)",
+                "traffic_source": traffic_src,
                 "kernel": dom, "launches_per_step": d["launches_per_step"],
                 "peak_source": pk["source"] + (" sustained" if d["bound"] == "tensor" else ""),
                 "step_tflops": step_flop / (ms_step / 1e3) / 1e12,

@@ -317,6 +317,222 @@ __global__ void __launch_bounds__(256, MINB) gae_kernel(const float* __restrict_
 }
 
 
+// Streams through TMA bulk copies (gae_tma_kernel).  The warp-per-stream kernels above load
+// with per-lane vector loads; with few long streams (1,000 x 10^6 steps: ~7 warps per SM) the
+// SM's outstanding-miss capacity, not the HBM, caps the bytes in flight (~64 KB per SM).  Here
+// lane 0 of each warp streams whole windows (r, V, d of 32*CH steps) into an S-deep
+// shared-memory ring with 1-D bulk copies (no per-thread miss tracking), S windows ahead across
+// stream boundaries; the lanes then run the same lane-chunk recurrence from shared memory.
+// Windows that are not entirely inside the row (the earliest window of a row, when the row is
+// not a whole number of windows) or that touch the end of an array take the per-lane load path.
+__device__ __forceinline__ uint32_t gae_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+template <int CH, int S>
+__global__ void __launch_bounds__(128) gae_tma_kernel(
+    const float* __restrict__ rew, const float* __restrict__ val, const uint8_t* __restrict__ done,
+    int64_t R, int64_t L, float gamma, float lam, int seq_T, float* __restrict__ adv,
+    float* __restrict__ ret, bool vec) {
+  constexpr int W = 32 * CH;
+  constexpr int RB = W * 4, VB = (W + 8) * 4, DB = W + 16, SB = RB + VB + DB;
+  static_assert(SB % 16 == 0, "stage alignment");
+  extern __shared__ __align__(128) uint8_t gsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* const wst = gsm + warp * (S * SB + S * 8);
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(wst + S * SB);
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gae_smem(bars + s)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float gl = gamma * lam;
+  const int64_t spr = seq_T > 0 ? L / seq_T : 0, nseq = R * spr;
+  // window [w_start, w_end) of row r; wb = its first step on the global 8-step grid
+  auto params = [&](int64_t r, int64_t w_end, int64_t& w_start, int64_t& wb, bool& tma) {
+    const int64_t g0 = r * L, sh0 = g0 & 7;
+    w_start = w_end - W;
+    if (w_start <= 0 && w_end + sh0 <= W) {
+      w_start = 0;
+    } else {
+      if (w_start < 8) w_start = 8;
+      w_start += (8 - ((g0 + w_start) & 7)) & 7;
+    }
+    wb = w_start - ((g0 + w_start) & 7);
+    tma = vec && wb == w_start && w_end - w_start == W && !(r == R - 1 && w_end + 8 > L);
+  };
+  // producer (lane 0): the next window in this warp's order, into stage `st`
+  int64_t p_r = gw, p_end = L;
+  auto produce = [&](int st) {
+    const uint32_t bar = gae_smem(bars + st);
+    bool tma = false;
+    if (p_r < R) {
+      int64_t ws, wb;
+      params(p_r, p_end, ws, wb, tma);
+      if (tma) {
+        uint8_t* s = wst + st * SB;
+        const float* rs = rew + p_r * L + wb;
+        const float* vs = val + p_r * (L + 1) + wb;
+        const uint8_t* ds = done + p_r * L + wb;
+        const float* vs_al = reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(vs) & ~uintptr_t(15));
+        const uint8_t* ds_al = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(ds) & ~uintptr_t(15));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(SB)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(gae_smem(s)), "l"(rs), "r"(RB), "r"(bar) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(gae_smem(s + RB)), "l"(vs_al), "r"(VB), "r"(bar) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(gae_smem(s + RB + VB)), "l"(ds_al), "r"(DB), "r"(bar) : "memory");
+      }
+      p_end = ws;
+      if (p_end == 0) {
+        p_r += nwarps;
+        p_end = L;
+      }
+    }
+    // windows without a copy (and past the end) still complete the stage's phase
+    if (!tma) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) produce(s);
+  }
+  uint32_t consumed = 0;
+  for (int64_t r = gw; r < R; r += nwarps) {
+    const float* rr = rew + r * L;
+    const float* vv = val + r * (L + 1);
+    const uint8_t* dd = done + r * L;
+    float carry = 0.f;
+    int64_t w_end = L;
+    while (w_end > 0) {
+      int64_t w_start, wb;
+      bool tma;
+      params(r, w_end, w_start, wb, tma);
+      const int st = (int)(consumed % S);
+      const uint32_t par = (consumed / S) & 1u;
+      {   // this window's stage phase (a bulk copy, or the producer's plain arrive)
+        const uint32_t bar = gae_smem(bars + st);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "GW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra GW;\n\t}" ::"r"(bar), "r"(par) : "memory");
+      }
+      const int64_t t0 = wb + CH * lane;
+      const int i_lo = (int)min((int64_t)CH, max((int64_t)0, w_start - t0));
+      const int i_hi = (int)max((int64_t)0, min((int64_t)CH, w_end - t0));
+      float delta[CH], cf[CH], vkeep[CH];
+      if (tma) {
+        const uint8_t* s = wst + st * SB;
+        const float* rs = reinterpret_cast<const float*>(s) + CH * lane;
+        const int vx = (int)(((reinterpret_cast<uintptr_t>(vv + wb)) & 15) >> 2);
+        const float* vsm = reinterpret_cast<const float*>(s + RB) + vx + CH * lane;
+        const int dx = (int)((reinterpret_cast<uintptr_t>(dd + wb)) & 15);
+        const uint8_t* dsm = s + RB + VB + dx + CH * lane;
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const float nd = dsm[i] ? 0.f : 1.f;
+          const float v0 = vsm[i], v1 = vsm[i + 1];
+          delta[i] = rs[i] + gamma * nd * v1 - v0;
+          cf[i] = gl * nd;
+          vkeep[i] = v0;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          if (i >= i_lo && i < i_hi) {
+            const int64_t t = t0 + i;
+            const float nd = dd[t] ? 0.f : 1.f;
+            const float vt = vv[t];
+            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vt;
+            cf[i] = gl * nd;
+            vkeep[i] = vt;
+          } else {
+            delta[i] = 0.f;
+            cf[i] = 1.f;
+            vkeep[i] = 0.f;
+          }
+        }
+      }
+      // the stage is read: refill it with the window S ahead (async-proxy write after the
+      // generic reads)
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        produce(st);
+      }
+      ++consumed;
+      float P = 0.f, Q = 1.f;
+#pragma unroll
+      for (int i = CH - 1; i >= 0; --i) {
+        P = delta[i] + cf[i] * P;
+        Q = cf[i] * Q;
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float P2 = __shfl_down_sync(0xffffffffu, P, off);
+        const float Q2 = __shfl_down_sync(0xffffffffu, Q, off);
+        if (lane + off < 32) {
+          P = P + Q * P2;
+          Q = Q * Q2;
+        }
+      }
+      const float a_first = P + Q * carry;
+      float a = __shfl_down_sync(0xffffffffu, a_first, 1);
+      if (lane == 31) a = carry;
+      float Aout[CH];
+#pragma unroll
+      for (int i = CH - 1; i >= 0; --i) {
+        a = delta[i] + cf[i] * a;
+        Aout[i] = a;
+      }
+      const bool full = tma || (vec && i_lo == 0 && i_hi == CH);
+      if (seq_T == 0 && full) {
+        float Rout[CH];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) Rout[i] = Aout[i] + vkeep[i];
+        store_floats<CH>(adv + r * L + t0, Aout);
+        store_floats<CH>(ret + r * L + t0, Rout);
+      } else {
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          if (i >= i_lo && i < i_hi) {
+            const int64_t t = t0 + i;
+            int64_t o;
+            if (seq_T > 0) {
+              const int64_t k = t / seq_T, tt = t - k * seq_T;
+              o = tt * nseq + r * spr + k;
+            } else {
+              o = r * L + t;
+            }
+            adv[o] = Aout[i];
+            ret[o] = Aout[i] + vkeep[i];
+          }
+        }
+      }
+      carry = __shfl_sync(0xffffffffu, a_first, 0);
+      w_end = w_start;
+    }
+  }
+  // drain: every stage's last phase must complete before the block exits (outstanding copies)
+  __syncwarp();
+  for (int s = 0; s < S; ++s) {
+    const uint32_t c = consumed + (uint32_t)s;
+    const uint32_t bar = gae_smem(bars + (c % S));
+    const uint32_t par = (c / S) & 1u;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "GD: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra GD;\n\t}" ::"r"(bar), "r"(par) : "memory");
+  }
+}
+
 // Long rollouts (L > kGaeShortL): chunk-parallel single pass with a decoupled look-back.
 // A block owns a chunk of kGaeChunk = 4096 steps of one stream (16 per thread, vectorised).
 // Chunks are numbered from the END of each stream and handed out in that order by a global
@@ -1335,6 +1551,25 @@ int launch_pack_state(const Shape& s, int64_t B, const float* h0, const float* c
   PPO_LAUNCH_CHECK("pack_state_kernel");
   return PPO_OK;
 }
+template <int CH, int S>
+static int launch_gae_tma(const float* rew, const float* val, const uint8_t* done, int64_t R,
+                          int64_t L, float gamma, float lam, int seq_T, float* adv, float* ret,
+                          bool vec, cudaStream_t st) {
+  constexpr int SB = 32 * CH * 4 + (32 * CH + 8) * 4 + 32 * CH + 16;
+  constexpr int smem = 4 * (S * SB + S * 8);
+  static bool configured = false;
+  if (!configured) {
+    PPO_CUDA_CHECK(cudaFuncSetAttribute(gae_tma_kernel<CH, S>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  const int64_t warps = R;
+  const int blocks = (int)std::min<int64_t>((warps + 3) / 4, (int64_t)num_sms() * 3);
+  gae_tma_kernel<CH, S><<<blocks, 128, smem, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv,
+                                                   ret, vec);
+  PPO_LAUNCH_CHECK("gae_tma_kernel");
+  return PPO_OK;
+}
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
                float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,
                cudaStream_t st) {
@@ -1359,6 +1594,13 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
                                                                     lam, seq_T, adv, ret, vec);
     PPO_LAUNCH_CHECK("gae_kernel");
     return PPO_OK;
+  }
+  if (var == 6 || var == 7) {   // TMA-streamed windows (CH 16, S = 4 / CH 8, S = 6)
+    const bool vec = aligned(rew, 32) && aligned(done, 16) && aligned(val, 16) &&
+                     aligned(adv, 32) && aligned(ret, 32);
+    if (var == 6) return launch_gae_tma<16, 4>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret,
+                                               vec, st);
+    return launch_gae_tma<8, 6>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, vec, st);
   }
   if (var != 5 && gae_use_short(R, L)) {
     const int64_t threads = R * 32;
