@@ -429,19 +429,52 @@ __global__ void __launch_bounds__(128) gae_tma_kernel(
       const int i_hi = (int)max((int64_t)0, min((int64_t)CH, w_end - t0));
       float delta[CH], cf[CH], vkeep[CH];
       if (tma) {
+        // the lane's chunk out of the stage with 16-byte shared loads (scalar loads at a
+        // 4*CH-byte lane stride would be CH-way bank conflicted): r aligned; V shifted by the
+        // window's (uniform) misalignment vx; d at byte offset dx in {0, 8}
         const uint8_t* s = wst + st * SB;
-        const float* rs = reinterpret_cast<const float*>(s) + CH * lane;
+        float rv[CH], v[CH + 1];
+        const float4* r4 = reinterpret_cast<const float4*>(s) + (CH / 4) * lane;
+#pragma unroll
+        for (int q = 0; q < CH / 4; ++q) {
+          const float4 a4 = r4[q];
+          rv[4 * q] = a4.x;
+          rv[4 * q + 1] = a4.y;
+          rv[4 * q + 2] = a4.z;
+          rv[4 * q + 3] = a4.w;
+        }
         const int vx = (int)(((reinterpret_cast<uintptr_t>(vv + wb)) & 15) >> 2);
-        const float* vsm = reinterpret_cast<const float*>(s + RB) + vx + CH * lane;
+        {
+          constexpr int NQ = CH / 4 + 1;   // CH + 1 values starting at vx < 4: NQ float4s
+          float buf[NQ * 4];
+          const float4* v4 = reinterpret_cast<const float4*>(s + RB) + (CH / 4) * lane;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) reinterpret_cast<float4*>(buf)[q] = v4[q];
+          switch (vx) {
+#define PPO_GAE_VSHIFT(M)                                                     \
+  case M:                                                                     \
+    _Pragma("unroll") for (int i = 0; i <= CH; ++i) v[i] = buf[i + M]; \
+    break;
+            PPO_GAE_VSHIFT(0)
+            PPO_GAE_VSHIFT(1)
+            PPO_GAE_VSHIFT(2)
+            PPO_GAE_VSHIFT(3)
+#undef PPO_GAE_VSHIFT
+          }
+        }
         const int dx = (int)((reinterpret_cast<uintptr_t>(dd + wb)) & 15);
-        const uint8_t* dsm = s + RB + VB + dx + CH * lane;
+        uint8_t db[CH];
+        {
+          const uint2* d2 = reinterpret_cast<const uint2*>(s + RB + VB + dx) + (CH / 8) * lane;
+#pragma unroll
+          for (int q = 0; q < CH / 8; ++q) *reinterpret_cast<uint2*>(db + 8 * q) = d2[q];
+        }
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
-          const float nd = dsm[i] ? 0.f : 1.f;
-          const float v0 = vsm[i], v1 = vsm[i + 1];
-          delta[i] = rs[i] + gamma * nd * v1 - v0;
+          const float nd = db[i] ? 0.f : 1.f;
+          delta[i] = rv[i] + gamma * nd * v[i + 1] - v[i];
           cf[i] = gl * nd;
-          vkeep[i] = v0;
+          vkeep[i] = v[i];
         }
       } else {
 #pragma unroll
@@ -1595,12 +1628,14 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
     PPO_LAUNCH_CHECK("gae_kernel");
     return PPO_OK;
   }
-  if (var == 6 || var == 7) {   // TMA-streamed windows (CH 16, S = 4 / CH 8, S = 6)
+  if (var == 6 || var == 7 || var == 8) {   // TMA-streamed windows (CH 16 S 4 / CH 8 S 6 / 8 S 10)
     const bool vec = aligned(rew, 32) && aligned(done, 16) && aligned(val, 16) &&
                      aligned(adv, 32) && aligned(ret, 32);
     if (var == 6) return launch_gae_tma<16, 4>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret,
                                                vec, st);
-    return launch_gae_tma<8, 6>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, vec, st);
+    if (var == 7) return launch_gae_tma<8, 6>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret,
+                                              vec, st);
+    return launch_gae_tma<8, 10>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, vec, st);
   }
   if (var != 5 && gae_use_short(R, L)) {
     const int64_t threads = R * 32;

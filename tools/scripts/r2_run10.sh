@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+bash tools/ab_builds.sh run 3 --steps 4 --warmup 2 > gpurun_out/r2_abb_bwd_variants.txt 2>&1
+PPO_EXPERIMENTS=1 python paper_1912_06680_b200/build.py > /dev/null 2>&1 || echo build failed
+for v in 7 8; do PPO_GAE_VARIANT=$v timeout 600 python -m pytest tests/test_gpu_kernels.py -k gae -q -p no:cacheprovider > gpurun_out/r2_gae_tma_tests$v.txt 2>&1; done
+rm -f gpurun_out/r2_gae_var5.txt
+for v in 0 6 7 8; do echo "variant $v" >> gpurun_out/r2_gae_var5.txt; PPO_GAE_VARIANT=$v timeout 300 python tools/gae_probe.py --L 256,1350,6300,20000,100000,1000000 --steps 1000000000 >> gpurun_out/r2_gae_var5.txt 2>&1; done
+python paper_1912_06680_b200/build.py > /dev/null 2>&1
+echo done
