@@ -362,7 +362,9 @@ __global__ void __launch_bounds__(128) gae_tma_kernel(
       w_start += (8 - ((g0 + w_start) & 7)) & 7;
     }
     wb = w_start - ((g0 + w_start) & 7);
-    tma = vec && wb == w_start && w_end - w_start == W && !(r == R - 1 && w_end + 8 > L);
+    // the copies cover [wb, wb + W) (+ slack): steps outside the window belong to the
+    // neighbouring rows and are masked by the lanes; only the array's tail is out of bounds
+    tma = vec && !(r == R - 1 && wb + W + 16 > L);
   };
   // producer (lane 0): the next window in this warp's order, into stage `st`
   int64_t p_r = gw, p_end = L;
@@ -471,10 +473,11 @@ __global__ void __launch_bounds__(128) gae_tma_kernel(
         }
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
+          const bool in = i >= i_lo && i < i_hi;   // steps of the window (others: identity)
           const float nd = db[i] ? 0.f : 1.f;
-          delta[i] = rv[i] + gamma * nd * v[i + 1] - v[i];
-          cf[i] = gl * nd;
-          vkeep[i] = v[i];
+          delta[i] = in ? rv[i] + gamma * nd * v[i + 1] - v[i] : 0.f;
+          cf[i] = in ? gl * nd : 1.f;
+          vkeep[i] = in ? v[i] : 0.f;
         }
       } else {
 #pragma unroll
@@ -525,7 +528,7 @@ __global__ void __launch_bounds__(128) gae_tma_kernel(
         a = delta[i] + cf[i] * a;
         Aout[i] = a;
       }
-      const bool full = tma || (vec && i_lo == 0 && i_hi == CH);
+      const bool full = vec && i_lo == 0 && i_hi == CH;
       if (seq_T == 0 && full) {
         float Rout[CH];
 #pragma unroll

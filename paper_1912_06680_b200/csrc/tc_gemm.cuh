@@ -48,8 +48,6 @@ struct TileShape {
   // takes nkb0_s0 (>= 0) source-0 k-blocks on step 0, and its k-blocks from dep_kb on wait
   // until every tile of step s-1 in the same row block has signalled ready[(s-1) num_m + mb]
   // (2 per tile: both CTAs of the pair, after their epilogue's stores).
-  int a_pol, b_pol;      // CTA-pair kernel: L2 policy of the A / B loads (0 default, 1 evict
-                         // first, 2 evict last)
   int tsteps;
   int za_step0, za_step1;
   int nkb0_s0;
@@ -258,29 +256,6 @@ __device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* map, uint32_
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
-}
-// the same with an L2 cache-eviction policy (createpolicy) for the operand's lines
-__device__ __forceinline__ void tma_load_3d_pair_hint(const CUtensorMap* map, uint32_t bar_cluster,
-                                                      void* dst, int c0, int c1, int c2,
-                                                      uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2),
-      "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-// pol: 0 = default, 1 = evict_first, 2 = evict_last
-__device__ __forceinline__ void tma_pair_pol(const CUtensorMap* map, uint32_t bar, void* dst,
-                                             int c0, int c1, int c2, int pol, uint64_t p1,
-                                             uint64_t p2) {
-  if (pol == 0) tma_load_3d_pair(map, bar, dst, c0, c1, c2);
-  else tma_load_3d_pair_hint(map, bar, dst, c0, c1, c2, pol == 1 ? p1 : p2);
 }
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd,
                                                uint32_t idesc, uint32_t accumulate) {
@@ -737,7 +712,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t sfull_f0 = mapa_shared(smem_u32(&sfull[0]), 1);
       const uint32_t ring_f0 = mapa_shared(smem_u32(&ring[0]), 1);
       const int die = sh.die_split > 0 ? sh.sm_die[smid()] : 0;
-      const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
       while (true) {
         int tile;
         if (leader) {
@@ -783,20 +757,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* a_dst = sA + stage * L::A_BYTES;
           uint8_t* b_dst = sB + stage * L::B_BYTES;
           if (!A_MN) {
-            tma_pair_pol(ta, fbar, a_dst, kk, m_row, za, sh.a_pol, pol_first, pol_last);
+            tma_load_3d_pair(ta, fbar, a_dst, kk, m_row, za);
           } else {
 #pragma unroll
             for (int p = 0; p < 2 * MB; ++p)
-              tma_pair_pol(ta, fbar, a_dst + p * (BK * 128), m_row + p * 64, kk, za, sh.a_pol,
-                           pol_first, pol_last);
+              tma_load_3d_pair(ta, fbar, a_dst + p * (BK * 128), m_row + p * 64, kk, za);
           }
           if (!B_MN) {
-            tma_pair_pol(tb, fbar, b_dst, kk, n_row, zb, sh.b_pol, pol_first, pol_last);
+            tma_load_3d_pair(tb, fbar, b_dst, kk, n_row, zb);
           } else {
 #pragma unroll
             for (int p = 0; p < BN / 128; ++p)
-              tma_pair_pol(tb, fbar, b_dst + p * (BK * 128), n_row + p * 64, kk, zb, sh.b_pol,
-                           pol_first, pol_last);
+              tma_load_3d_pair(tb, fbar, b_dst + p * (BK * 128), n_row + p * 64, kk, zb);
           }
           if (++stage == STAGES) {
             stage = 0;

@@ -230,16 +230,6 @@ int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const
   const int clusters = (int)std::min<int64_t>(ntiles, all_tiles ? (int64_t)1 << 30 : num_sms() / 2);
   if (clusters <= 0) return PPO_OK;
   tc::TileShape shd = sh;
-#ifdef PPO_EXPERIMENTS
-  {
-    // experiment builds: L2 eviction policy of the operand loads per call site tag
-    char n[64];
-    snprintf(n, sizeof(n), "PPO_EXP_APOL_%s", tag);
-    shd.a_pol = knob_int(n, sh.a_pol);
-    snprintf(n, sizeof(n), "PPO_EXP_BPOL_%s", tag);
-    shd.b_pol = knob_int(n, sh.b_pol);
-  }
-#endif
   if (die_sched()) {
     // die-aware queues: each die gets a share of the raster sequence proportional to the CTA
     // pairs it hosts (clusters are placed within one die)
