@@ -131,10 +131,12 @@ int ppo_cast_bf16(const float* src, uint16_t* dst, size_t n, ppo_stream_t s);
  * seq_T = 0: adv/ret are [R][L].  seq_T = T > 0 (L % T == 0): adv/ret are written time-major
  * for the minibatch, [T][R*L/T], sequence b = r*(L/T) + k covers steps kT..kT+T-1 (O3).
  * fp32 arithmetic.  R*L = 0 is a no-op.
- * L <= 8192 or R >= 16384: one warp per stream.  Otherwise (few long rollouts, up to the
- * paper's whole games, ~20k steps, and beyond): chunk-parallel single pass with a
- * decoupled look-back; it needs ppo_gae_scratch_bytes(R, L) bytes of caller-owned, 16-byte
- * aligned device scratch (0 -- scratch may be NULL -- when the warp-per-stream kernel runs). */
+ * L <= 8192 or R >= 600: one warp per stream (L <= 256: per-lane loads; longer streams:
+ * windows of 256 steps streamed through TMA bulk copies into a shared-memory ring, 6 windows
+ * ahead, when the bases allow it).  Otherwise (few very long rollouts, up to the paper's whole
+ * games, ~20k steps, and beyond): chunk-parallel single pass with a decoupled
+ * look-back; it needs ppo_gae_scratch_bytes(R, L) bytes of caller-owned, 16-byte aligned
+ * device scratch (0 -- scratch may be NULL -- when the warp-per-stream kernels run). */
 int ppo_gae_scratch_bytes(int64_t R, int64_t L, size_t* bytes /* host */);
 int ppo_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
             float gamma, float lam, int32_t seq_T, float* adv, float* ret, void* scratch,

@@ -1640,6 +1640,14 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
                                               vec, st);
     return launch_gae_tma<8, 10>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, vec, st);
   }
+  if (var == 0 && gae_use_short(R, L) && L > 256) {
+    // several windows per stream: stream them through TMA bulk copies (profiles/
+    // r02_gae_variants.txt: +3% at L = 1,350, +5% at 6,300, +15% at 10^5, +7% at 10^6 steps;
+    // equal at 20,000); 256-step segments keep the warp kernel below (one window each)
+    const bool tvec = aligned(rew, 32) && aligned(done, 16) && aligned(val, 16) &&
+                      aligned(adv, 32) && aligned(ret, 32);
+    if (tvec) return launch_gae_tma<8, 6>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, true, st);
+  }
   if (var != 5 && gae_use_short(R, L)) {
     const int64_t threads = R * 32;
     // the aligned-chunk path needs 32-byte aligned r, A, R bases and an 8-byte aligned d base

@@ -350,8 +350,9 @@ bool use_multistep(int64_t tiles_per_step, bool backward) {
   if (k == 2) return true;
   // the backward's A operand is almost all dz_{t+1} (only the 11 dY k-blocks are ready
   // early), so its steps cannot overlap: measured 7% slower than per-step launches at B = 600
-  // (profiles/r02_pmb_multistep.txt); the forward's x half of K overlaps the previous step
-  if (backward) return false;
+  // (profiles/r02_pmb_multistep.txt), but 21% faster in the launch-bound tiny config (one
+  // tile per step: r02_tiny_multistep.txt); the forward's x half of K overlaps the previous step
+  if (backward) return tiles_per_step <= 4;
   return tiles_per_step <= 8 * (int64_t)(num_sms() / 2);
 }
 
