@@ -1,4 +1,3 @@
-#include <type_traits>
 // kernels.cu -- HBM-bound kernels of the PPO step (GAE, loss, Adam, layout) and the SIMT
 // fp32 reference GEMM path.  See DESIGN.md for the roofline of each.
 #include <math.h>
@@ -1055,7 +1054,7 @@ constexpr int SCR = 16 * 36;     // per-warp transpose scratch of warp_sum16 (fl
 // return) is loaded into registers one row ahead.  Row r's dY is staged in its own buffer (in
 // place, once every lane holds its logits in registers).  The grid is one persistent wave
 // (SMs x MINB blocks).  Needs A % 4 == 0 and a 16-byte aligned `out` (launch_loss checks).
-template <class TD, int MINB, bool AUX>
+template <class TD, int MINB>
 __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
     const float* __restrict__ out, const int32_t* __restrict__ act,
     const uint8_t* __restrict__ head_on, const uint8_t* __restrict__ avail,
@@ -1275,7 +1274,7 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
     }
     // ---- NEXT-4 aux heads (as loss_kernel): logistic columns lane-parallel, rank softmax
     float laux = 0.f;
-    if (AUX && p.n_aux) {   // (compiled out of the paper-layout kernel without aux heads)
+    if (p.n_aux) {
       const float* lab = aux_label + row * p.n_aux;
       const int c0 = p.vcol + 1, r0 = p.n_win, r1 = p.n_win + p.n_rank;
       const float wd = w * p.inv_denom;
@@ -1306,9 +1305,9 @@ __global__ void __launch_bounds__(256, MINB) loss_fast_kernel(
       ds[p.vcol] = from_f<TD>(2.f * p.c_v * (V - Rt) * w * p.inv_denom);
       if (logp) logp[row] = lpi;
       if (w != 0.f) {
-        if (!isfinite(lrow) || (AUX && !isfinite(laux))) flags |= 1u;
+        if (!isfinite(lrow) || !isfinite(laux)) flags |= 1u;
         acc[0] += w * (lrow + laux);
-        if (AUX) acc[PPO_STAT_AUX] += w * laux;
+        acc[PPO_STAT_AUX] += w * laux;
         acc[1] += w * pg;
         acc[2] += w * vf;
         acc[3] += w * ent;
@@ -1682,7 +1681,7 @@ int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t 
   return PPO_OK;
 }
 // one persistent wave (SMs x MINB blocks), two shared-memory row buffers per warp
-template <class TD, int MINB, bool AUX>
+template <class TD, int MINB>
 static int launch_loss_fast(const LossParams& p, const float* out, const int32_t* act,
                             const uint8_t* head_on, const uint8_t* avail, const float* logp_old,
                             const float* adv, const float* ret, const uint8_t* valid,
@@ -1697,12 +1696,12 @@ static int launch_loss_fast(const LossParams& p, const float* out, const int32_t
   const size_t smem = 8 * (fastloss::NBUF * (size_t)p.A + fastloss::SCR) * sizeof(float);
   if (smem > 227 * 1024) return fail(PPO_E_SHAPE, "loss: row too wide for the fast kernel");
   if (smem > 48 * 1024)
-    PPO_CUDA_CHECK(cudaFuncSetAttribute(loss_fast_kernel<TD, MINB, AUX>,
+    PPO_CUDA_CHECK(cudaFuncSetAttribute(loss_fast_kernel<TD, MINB>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   nblk = std::min(PPO_LOSS_BLOCKS, sms * MINB);
   if (const char* g = knob("PPO_LOSS_GRID"))   // experiment knob: grid size
     nblk = std::max(1, std::min(PPO_LOSS_BLOCKS, atoi(g)));
-  loss_fast_kernel<TD, MINB, AUX><<<nblk, 256, smem, st>>>(out, act, head_on, avail, logp_old, adv,
+  loss_fast_kernel<TD, MINB><<<nblk, 256, smem, st>>>(out, act, head_on, avail, logp_old, adv,
                                                       ret, valid, aux_label, p, (TD*)dout, logp,
                                                       partials);
   PPO_LAUNCH_CHECK("loss_fast_kernel");
@@ -1724,15 +1723,12 @@ int launch_loss(const LossParams& p, bool bf16, const float* out, const int32_t*
   if (fast) {
     ProfScope _prof("loss", st);
     // 2 blocks of 8 warps per SM: 126 registers and 3 row buffers per warp, no spills
-    auto go = [&](auto td, auto aux) {
-      using TD = decltype(td);
-      return launch_loss_fast<TD, 2, decltype(aux)::value>(p, out, act, head_on, avail, logp_old,
-                                                          adv, ret, valid, aux_label, dout, logp,
-                                                          partials, nblk, st);
-    };
-    const int rc = bf16 ? (p.n_aux ? go(__nv_bfloat16{}, std::true_type{})
-                                   : go(__nv_bfloat16{}, std::false_type{}))
-                        : (p.n_aux ? go(0.f, std::true_type{}) : go(0.f, std::false_type{}));
+    const int rc = bf16 ? launch_loss_fast<__nv_bfloat16, 2>(p, out, act, head_on, avail,
+                                                            logp_old, adv, ret, valid, aux_label,
+                                                            dout, logp, partials, nblk, st)
+                        : launch_loss_fast<float, 2>(p, out, act, head_on, avail, logp_old, adv,
+                                                     ret, valid, aux_label, dout, logp, partials,
+                                                     nblk, st);
     if (rc != PPO_OK) return rc;
   } else {
   ProfScope _prof("loss", st);
