@@ -142,9 +142,9 @@ WsLayout ws_layout(const Shape& s, int64_t B) {
   L.splitk = off;  // split-K partials of dW_o (bf16 path)
   if (s.bf16) off = align_up(off + (size_t)kMaxSplitK * s.A * s.Ko * 4, 1024);
   L.sched = off;   // tile-scheduler counters of this workspace's GEMMs, then the per-step
-                   // row-block ready counters of a multi-step launch (T x ceil(B / 256))
+                   // ready counters of a multi-step launch (T x ceil(B / 256) x ready_ld(H))
   L.ready = off + kSchedBytes;
-  off = align_up(L.ready + (size_t)s.T * ((B + 255) / 256) * 4, 1024);
+  off = align_up(L.ready + ready_bytes(s.T, B, s.H), 1024);
   L.total = off;
   return L;
 }

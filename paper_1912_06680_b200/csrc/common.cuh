@@ -132,6 +132,12 @@ constexpr size_t kSchedBytes = 128;  // >= kSchedWords * 4 * max(kSchedLstmSlots
 // established; *n0 / *n1 = SMs on die 0 / 1.
 const uint8_t* sm_die_map(int* n0, int* n1);
 WsLayout ws_layout(const Shape& s, int64_t B);
+// Multi-step ready counters per (step, 256-row block): one per 64-unit block of the hidden
+// state, the row padded to 8 counters (32 bytes, polled as two 16-byte loads).
+inline int64_t ready_ld(int64_t H) { return ((std::max<int64_t>(1, (H + 63) / 64) + 7) / 8) * 8; }
+inline size_t ready_bytes(int64_t T, int64_t B, int64_t H) {
+  return (size_t)T * ((B + 255) / 256) * ready_ld(H) * 4;
+}
 
 // ---- activation storage type ---------------------------------------------------------------
 __device__ __forceinline__ float to_f(float v) { return v; }

@@ -1600,7 +1600,15 @@ static int launch_gae_tma(const float* rew, const float* val, const uint8_t* don
     configured = true;
   }
   const int64_t warps = R;
-  const int blocks = (int)std::min<int64_t>((warps + 3) / 4, (int64_t)num_sms() * 3);
+  static int occ = 0;   // resident blocks per SM at this stage depth (shared memory, registers)
+  if (occ == 0) {
+    PPO_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gae_tma_kernel<CH, S>,
+                                                                 128, smem));
+    occ = std::max(occ, 1);
+  }
+  int per_sm = occ;
+  if (const char* e = knob("PPO_GAE_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
+  const int blocks = (int)std::min<int64_t>((warps + 3) / 4, (int64_t)num_sms() * per_sm);
   gae_tma_kernel<CH, S><<<blocks, 128, smem, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv,
                                                    ret, vec);
   PPO_LAUNCH_CHECK("gae_tma_kernel");

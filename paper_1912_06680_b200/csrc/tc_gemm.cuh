@@ -53,6 +53,14 @@ struct TileShape {
   int nkb0_s0;
   int dep_kb;
   unsigned int* ready;
+  // Fine-grained dependencies (dep_fine = 1): instead of a whole row block, a unit waits only
+  // for the 64-unit blocks of the previous step it reads.  Counters ready[(s num_m + mb) dep_ld
+  // + j] count the CTAs (2 per pair) that stored hidden-unit block j of row block mb at step s;
+  // k-block kb >= dep_kb of step s reads block j = (kb - dep_kb) / dep_kpg (if j < dep_ng), and
+  // a tile's epilogue publishes its epi_q blocks one by one.
+  int dep_fine;
+  int dep_kpg, dep_ng, dep_ld, epi_q;
+  int dep_perm;
 };
 
 // One work unit of a launch: a tile and (split-K) its k-range or (multi-step) its step.
@@ -93,7 +101,43 @@ __device__ __forceinline__ void wait_ready(const unsigned int* p, unsigned int t
   }
   if (async) asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+// Fine-grained dependencies: poll the 8 counters of group j's aligned octet (two relaxed 16-byte
+// loads) until counter j reaches target; returns the octet's ready bits (bit i: counter
+// (j & ~7) + i) so the caller skips the polls of groups already seen ready.  Acquire by fence
+// after the observing load; async = then order TMA reads after it.
+__device__ __forceinline__ uint32_t wait_group(const unsigned int* row, int j, unsigned int target,
+                                               bool async) {
+  const unsigned int* p = row + (j & ~7);
+  uint32_t bits = 0;
+  uint32_t spins = 0;
+  while (true) {
+    unsigned int v[8];
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "l"(p + 4) : "memory");
+    bits = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bits |= (v[i] >= target ? 1u : 0u) << i;
+    if ((bits >> (j & 7)) & 1u) break;
+    __nanosleep(64);
+    if (++spins == (1u << 26)) asm volatile("trap;");   // watchdog
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (async) asm volatile("fence.proxy.async.global;" ::: "memory");
+  return bits;
+}
 constexpr int kSchedDepth = 4;  // tile-index ring between the fetcher and the consumers
+// Blocks of 64 hidden units a 256-column tile of an LSTM epilogue publishes under fine-grained
+// multi-step dependencies (Epi::kFineBlocks; 0 = not an LSTM step epilogue)
+template <class E, class = void>
+struct FineBlocks {
+  static constexpr int v = 0;
+};
+template <class E>
+struct FineBlocks<E, std::void_t<decltype(E::kFineBlocks)>> {
+  static constexpr int v = E::kFineBlocks;
+};
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -740,16 +784,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         bool dep = sh.tsteps > 1 && ui.split > 0;   // step s-1 of this row block must be done
         const int m_row = mb * TM + rank * BM * MB;  // this CTA's A rows
         const int n_row = nb * BN + rank * (BN / 2);  // this CTA's B rows (N-half)
+        const unsigned int* drow =
+            dep ? sh.ready + static_cast<int64_t>((ui.split - 1) * num_m + mb) * sh.dep_ld : nullptr;
+        int oct = -1;          // fine mode: octet of ready groups last polled, and its bits
+        uint32_t obits = 0;
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
-          if (dep && kb >= sh.dep_kb) {
-            wait_ready(sh.ready + (ui.split - 1) * num_m + mb, 2u * num_n, true);
-            dep = false;
+          // kx: the k-block in source order [source 0 | source 1].  dep_perm (the backward):
+          // source 1 (dy_t, no dependency) first, then source 0's blocks in the order the
+          // previous step's epilogues publish them (block q of every tile, then q + 1, ...)
+          int kx = kb;
+          if (sh.dep_perm && sh.tsteps > 1) {
+            if (kb < sh.nkb1) {
+              kx = ui.nkb0 + kb;
+            } else {
+              const int i = (kb - sh.nkb1) / sh.dep_kpg, r = (kb - sh.nkb1) % sh.dep_kpg;
+              const int tpr = sh.dep_ng / sh.epi_q;
+              kx = sh.dep_kb + ((i % tpr) * sh.epi_q + i / tpr) * sh.dep_kpg + r;
+            }
+          }
+          if (dep && kx >= sh.dep_kb && kx < ui.nkb0) {
+            if (sh.dep_fine) {
+              const int j = (kx - sh.dep_kb) / sh.dep_kpg;
+              if (j < sh.dep_ng) {
+                if ((j >> 3) != oct || !((obits >> (j & 7)) & 1u)) {
+                  obits = wait_group(drow, j, 2u, true);
+                  oct = j >> 3;
+                }
+              }
+            } else {
+              wait_ready(sh.ready + (ui.split - 1) * num_m + mb, 2u * num_n, true);
+              dep = false;
+            }
           }
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fbar = mapa_shared(smem_u32(&full[stage]), 0);
           if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
-          const bool s1 = kb >= ui.nkb0;
-          const int kk = (s1 ? kb - ui.nkb0 : kb + sh.kb_off) * BK;
+          const bool s1 = kx >= ui.nkb0;
+          const int kk = (s1 ? kx - ui.nkb0 : kx + sh.kb_off) * BK;
           const CUtensorMap* ta = s1 ? &ta1 : &ta0;
           const CUtensorMap* tb = s1 ? &tb1 : &tb0;
           const int za = s1 ? ui.za1 : ui.za0;
@@ -865,7 +936,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile - split * ntiles, num_m, num_n, sh.group, sh.group_n, mb, nb);
       if (sh.tsteps > 1 && split > 0) {
         // the epilogue reads the previous step's cell state (c / dc) of this row block
-        if (lane == 0) wait_ready(sh.ready + (split - 1) * num_m + mb, 2u * num_n, false);
+        if (lane == 0) {
+          if (sh.dep_fine) {
+            const unsigned int* drow =
+                sh.ready + static_cast<int64_t>((split - 1) * num_m + mb) * sh.dep_ld;
+            for (int q = 0; q < sh.epi_q; ++q) wait_group(drow, nb * sh.epi_q + q, 2u, false);
+          } else {
+            wait_ready(sh.ready + (split - 1) * num_m + mb, 2u * num_n, false);
+          }
+        }
         __syncwarp();
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -874,16 +953,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (lane == 0 && sslot == 1 && sphase == 0) TC_TRACE(16 + quarter);
       const uint32_t taddr =
           tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
+      bool done = false;
+      constexpr int FB = FineBlocks<Epi>::v;
+      if constexpr (MB == 1 && FB > 0) {
+        if (sh.tsteps > 1 && sh.dep_fine) {
+          // publish each block as soon as it is stored: the next step's k-blocks of that block
+          // (and the block's next-step epilogue) may start before the whole tile is done.
+          // epi_q = 1: the tile is one block (forward: 256 gate columns = 64 units); epi_q =
+          // BN / 64: 64 output columns per block (backward: dh columns = hidden units)
+          unsigned int* drow = sh.ready + static_cast<int64_t>(split * num_m + mb) * sh.dep_ld;
+          constexpr int QW = BN / FB;   // output columns per block
 #pragma unroll 1
-      for (int b = 0; b < MB; ++b)
-        epi.template apply<BN>(mb * TM + rank * BM * MB + b * BM, nb * BN, row, taddr + b * 256,
-                               split);
+          for (int q = 0; q < FB; ++q) {
+            epi.template apply<QW>(mb * TM + rank * BM, nb * BN + q * QW, row, taddr + q * QW,
+                                   split);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (threadIdx.x == 64) {
+              __threadfence();
+              atomicAdd(drow + nb * FB + q, 1u);
+            }
+          }
+          done = true;
+        }
+      }
+      if (!done) {
+#pragma unroll 1
+        for (int b = 0; b < MB; ++b)
+          epi.template apply<BN>(mb * TM + rank * BM * MB + b * BM, nb * BN, row, taddr + b * 256,
+                                 split);
+      }
       if (threadIdx.x == 64 && sslot == 1 && sphase == 0) TC_TRACE(7);
       if (lane == 0 && sslot == 1 && sphase == 0) TC_TRACE(20 + quarter);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
-      if (sh.tsteps > 1) {
+      if (sh.tsteps > 1 && !sh.dep_fine) {
         // this CTA's half of the tile is stored: publish it to the next step (cumulative
         // fence by one thread after the epilogue warps' barrier)
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -1167,6 +1271,236 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- 2 CTA pairs, A multicast
+// Weight-gradient variant: a cluster of 4 = two CTA pairs stacked along N (n-tiles 2u and
+// 2u+1 of the same 512-row M tile, MB = 2, MN-major A and B).  The pairs share the A operand
+// (the dZ panel): CTA (pair p, rank r) loads A panels {2p, 2p+1} of its 256 rows and
+// multicasts them to the same-rank CTA of the other pair, so the L2 supplies each A tile once
+// per cluster: per pair and K block 256 + 256 instead of 512 + 256 operand rows (-33% L2->SM
+// bytes per FLOP).  Barriers as tc_gemm2mc_kernel: completion counted on each destination
+// pair's leader, a stage released when both pairs' MMAs committed it.
+template <int STAGES>
+struct SmemMCA {
+  static constexpr int A_BYTES = 2 * BM * BK * 2;      // this CTA's 256 A rows (4 panels)
+  static constexpr int B_BYTES = 128 * BK * 2;         // this CTA's 128-row N-half of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4 + 2 * kSchedDepth) * 8 + 32 + 1024;
+};
+
+template <int STAGES, class Epi>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_gemm2mca_kernel(const __grid_constant__ CUtensorMap ta0,
+                       const __grid_constant__ CUtensorMap tb0, const TileShape sh,
+                       const Epi epi) {
+  constexpr int BN = 256, TM = 4 * BM;     // per-pair tile 512 x 256
+  using L = SmemMCA<STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* sfull = tempty + 2;
+  uint64_t* sempty = sfull + kSchedDepth;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + kSchedDepth);
+  int* ring = reinterpret_cast<int*>(tslot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pair = rank >> 1, prank = rank & 1, pl = rank & ~1u;
+  const int nclusters = gridDim.x >> 2;
+  const int num_m = (sh.M + TM - 1) / TM;          // 512-row tiles
+  const int num_n = (sh.N + BN - 1) / BN;
+  const int num_nu = (num_n + 1) / 2;              // units: pairs of n-tiles
+  const int nunits = num_m * num_nu;
+  const int nkb = sh.nkb0;
+
+  if (threadIdx.x == 0) {
+    prefetch_map(&ta0);
+    prefetch_map(&tb0);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);    // pair leader: one arrive.expect_tx for both CTAs' bytes
+      mbar_init(&empty[s], 2);   // one commit from each pair's MMA
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs of the pair (leader's copy)
+    }
+    for (int s = 0; s < kSchedDepth; ++s) {
+      mbar_init(&sfull[s], 1);
+      // rank 0's copy: rank0 MMA + 4 epi; ranks 1,3 producer + 4 epi; rank 2 producer + MMA
+      // + 4 epi
+      mbar_init(&sempty[s], 21);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t sempty_c0 = mapa_shared(smem_u32(&sempty[0]), 0);
+
+  auto next_unit = [&](int& sslot, uint32_t& sphase, bool arrive) -> int {
+    if (rank == 0) mbar_wait(&sfull[sslot], sphase);
+    else mbar_wait_cluster(&sfull[sslot], sphase);
+    const int u = ring[sslot];
+    if (arrive) mbar_arrive_cluster(sempty_c0 + 8 * sslot);
+    if (++sslot == kSchedDepth) {
+      sslot = 0;
+      sphase ^= 1;
+    }
+    return u;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer (all 4 CTAs); rank 0 also fetches units ==========
+      int stage = 0;
+      uint32_t phase = 0;
+      int sslot = 0;
+      uint32_t sphase = 0;
+      const uint16_t amask = (uint16_t)((1u << prank) | (1u << (prank + 2)));
+      while (true) {
+        int unit;
+        if (rank == 0) {
+          mbar_wait(&sempty[sslot], sphase ^ 1);
+          unit = sched_fetch(sh.sched, nunits, nclusters);
+          ring[sslot] = unit;
+          mbar_arrive(&sfull[sslot]);
+#pragma unroll
+          for (uint32_t r = 1; r < 4; ++r) {
+            st_shared_cluster(mapa_shared(smem_u32(&ring[sslot]), r), unit);
+            mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[sslot]), r));
+          }
+          if (++sslot == kSchedDepth) {
+            sslot = 0;
+            sphase ^= 1;
+          }
+        } else {
+          unit = next_unit(sslot, sphase, true);
+        }
+        if (unit >= nunits) break;
+        int mb, nu;
+        tile_coords(unit, num_m, num_nu, sh.group, sh.group_n, mb, nu);
+        const int m_row = mb * TM + (int)prank * 2 * BM;           // this CTA's 256 A rows
+        const int n_row = (2 * nu + (int)pair) * BN + (int)prank * 128;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fbar = mapa_shared(smem_u32(&full[stage]), pl);
+          if (prank == 0) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
+          const int kk = (kb + sh.kb_off) * BK;
+          uint8_t* a_dst = sA + stage * L::A_BYTES;
+          uint8_t* b_dst = sB + stage * L::B_BYTES;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int p = 2 * (int)pair + q;                        // my share of the panels
+            tma_load_3d_pair_mc(&ta0, fbar, a_dst + p * (BK * 128), m_row + p * 64,
+                                kk, sh.za0, amask);
+          }
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+            tma_load_3d_pair(&tb0, fbar, b_dst + p * (BK * 128), n_row + p * 64, kk, sh.zb0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int sslot = 0;
+    uint32_t sphase = 0;
+    int stage = 0;
+    uint32_t phase = 0;
+    if (prank == 0) {
+      // ===================== MMA issuer (pair leaders) =====================
+      constexpr uint32_t idesc = idesc_bf16(2 * BM, BN, true, true);
+      const uint64_t a_desc0 = sdesc(smem_u32(sA), BK * 128, 1024);
+      const uint64_t b_desc0 = sdesc(smem_u32(sB), BK * 128, 1024);
+      constexpr uint64_t a_k = 2048 >> 4, b_k = 2048 >> 4;
+      constexpr uint64_t a_blk = (BM * 128) >> 4;   // next 128-row block of A
+      const uint16_t pmask = (uint16_t)(0x3u << (2 * pair));
+      uint32_t acc_phase = 0;
+      while (true) {
+        const int unit = next_unit(sslot, sphase, lane == 0);
+        __syncwarp();
+        if (unit >= nunits) break;
+        mbar_wait(&tempty[0], acc_phase ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (L::A_BYTES >> 4));
+          const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (L::B_BYTES >> 4));
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+#pragma unroll
+              for (int b = 0; b < 2; ++b)
+                umma_bf16_pair(tbase + b * 256, ad + b * a_blk + k * a_k, bd + k * b_k, idesc,
+                               (kb | k) != 0 ? 1u : 0u);
+            umma_commit_mask(&empty[stage], (uint16_t)0xF);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit_mask(&tfull[0], pmask);
+        __syncwarp();
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5 (all CTAs) =====================
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t tempty_pl0 = mapa_shared(smem_u32(&tempty[0]), pl);
+    uint32_t acc_phase = 0;
+    int sslot = 0;
+    uint32_t sphase = 0;
+    while (true) {
+      const int unit = next_unit(sslot, sphase, lane == 0);
+      __syncwarp();
+      if (unit >= nunits) break;
+      int mb, nu;
+      tile_coords(unit, num_m, num_nu, sh.group, sh.group_n, mb, nu);
+      mbar_wait(&tfull[0], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+      for (int b = 0; b < 2; ++b)
+        epi.template apply<BN>(mb * TM + (int)prank * 2 * BM + b * BM, (2 * nu + (int)pair) * BN,
+                               row, taddr + b * 256, 0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_pl0);
+      acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
+                 : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- epilogues
 
 // Plain fp32 store: out[m*ldc + n] for m < M, n < N.
@@ -1341,6 +1675,7 @@ __device__ __forceinline__ void store_f32x16(float* p, const float (&v)[16]) {
 // LSTM forward step t (oracle O4).  Tile = 128 sequences x 256 gate rows = 4 gates of 64
 // hidden units (gate-interleaved W rows), so the whole cell update is tile-local.
 struct EpiLstmFwd {
+  static constexpr int kFineBlocks = 1;   // a tile = 4 gates x 64 units: one unit block
   __nv_bfloat16* h_out;   // XH[t+1] + D  (row stride ldxh)
   int64_t ldxh;
   const float* c_prev;    // C[t]   [B][H]
@@ -1439,6 +1774,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 }
 
 struct EpiLstmBwd {
+  static constexpr int kFineBlocks = 4;   // a tile = 256 units of dh: four unit blocks
   __nv_bfloat16* gz;      // G[t]: gates in, dz out  [B][4H]
   const float* c_t;       // C[t+1]
   const float* c_prev;    // C[t]

@@ -271,6 +271,56 @@ int launch2mc(const char* tag, const CUtensorMap& a0, const CUtensorMap& b0,
   return PPO_OK;
 }
 
+// Two CTA pairs sharing A by multicast (cluster of 4, MB = 2): 512 x 512 per cluster,
+// MN-major A and B (the weight gradient).
+template <class Epi>
+int launch2mca(const char* tag, const CUtensorMap& a0, const CUtensorMap& b0,
+               const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
+  constexpr int STAGES = 4;   // 4 x 48 KB
+  using L = tc::SmemMCA<STAGES>;
+  auto kern = tc::tc_gemm2mca_kernel<STAGES, Epi>;
+  static bool configured = false;
+  if (!configured) {
+    PPO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  if (sh.nkb0 <= 0 || sh.nkb1 != 0 || sh.ksplit > 1 || sh.tsteps > 1)
+    return fail(PPO_E_SHAPE, "multicast-A pair kernel: one K source, no split");
+  if (!sh.sched) return fail(PPO_E_CUDA, "tile scheduler counter unavailable");
+  const int64_t num_n = (sh.N + 255) / 256;
+  const int64_t units = ((sh.M + 511) / 512) * ((num_n + 1) / 2);
+  int max_clusters = num_sms() / 4;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 4;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.gridDim = dim3(4 * max_clusters);
+    cfg.blockDim = dim3(tc::kThreads);
+    cfg.dynamicSmemBytes = L::TOTAL;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0)
+      max_clusters = std::min(max_clusters, n);
+    else
+      (void)cudaGetLastError();
+  }
+  const int clusters = (int)std::min<int64_t>(units, max_clusters);
+  if (clusters <= 0) return PPO_OK;
+  ProfScope _prof(tag, st);
+  kern<<<4 * clusters, tc::kThreads, L::TOTAL, st>>>(a0, b0, sh, epi);
+  PPO_LAUNCH_CHECK("tc_gemm2mca_kernel");
+  return PPO_OK;
+}
+
+// The multicast-A kernel's units are pairs of n-tiles: halve an n-grouped raster's group.
+tc::TileShape mca_shape(tc::TileShape sh) {
+  if (sh.group_n) sh.group = std::max(1, sh.group / 2);
+  return sh;
+}
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // Split-K factor in [1, kMaxSplitK] that best fills whole waves of `sms` CTAs (each split
@@ -321,7 +371,7 @@ struct WsPtrs {
   float* c;
   float* dc;
   unsigned int* sched;   // this workspace's tile-scheduler counters, kSchedWords per SchedSlot
-  unsigned int* ready;   // multi-step launches: [T][ceil(B / 256)] row-block ready counters
+  unsigned int* ready;   // multi-step launches: [T][ceil(B / 256)][ready_ld(H)] counters
   size_t counter_bytes;  // sched + ready
   unsigned int* slot(int k) const { return sched + kSchedWords * k; }
 };
@@ -331,7 +381,7 @@ WsPtrs ws_ptrs(const Shape& s, int64_t B, void* ws) {
   return {reinterpret_cast<__nv_bfloat16*>(p + L.xh), reinterpret_cast<__nv_bfloat16*>(p + L.g),
           reinterpret_cast<float*>(p + L.c), reinterpret_cast<float*>(p + L.dc),
           reinterpret_cast<unsigned int*>(p + L.sched), reinterpret_cast<unsigned int*>(p + L.ready),
-          L.ready - L.sched + (size_t)s.T * ((B + 255) / 256) * 4};
+          L.ready - L.sched + ready_bytes(s.T, B, s.H)};
 }
 // zero the workspace's counters on the stream before its GEMMs (fresh memory is arbitrary)
 int sched_reset(const WsPtrs& P, cudaStream_t st) {
@@ -339,6 +389,28 @@ int sched_reset(const WsPtrs& P, cudaStream_t st) {
   PPO_CUDA_CHECK(cudaMemsetAsync(P.sched, 0, P.counter_bytes, st));
   return PPO_OK;
 }
+// Fine-grained multi-step dependencies (TileShape::dep_fine): the unit waits for the 64-unit
+// blocks it reads, not the whole row block.  PPO_MULTISTEP_FINE=0 (experiment builds) keeps the
+// row-block waits.
+void fine_deps(tc::TileShape& sh, const Shape& s, bool backward) {
+  if (knob_int("PPO_MULTISTEP_FINE", 1) == 0 || s.H % 64 != 0) return;
+  if (!backward && s.D % 64 != 0) return;   // h_{t-1} must start on a k-block
+  sh.dep_fine = 1;
+  sh.dep_ng = (int)(s.H / 64);
+  sh.dep_ld = (int)ready_ld(s.H);
+  if (backward) {
+    // dz_{t+1} columns of unit block j are gate-grouped: 4 k-blocks (one per gate) per block;
+    // a 256-unit tile publishes 4 blocks
+    sh.dep_kpg = 4;
+    sh.epi_q = 4;
+    sh.dep_perm = (sh.dep_ng % 4 == 0) && knob_int("PPO_MULTISTEP_PERM", 1) != 0;
+  } else {
+    // h_{t-1} columns: one k-block per 64 units; a tile (256 gate columns) is one block
+    sh.dep_kpg = 1;
+    sh.epi_q = 1;
+  }
+}
+
 // The T recurrent step GEMMs as ONE persistent launch (tiles of step t+1 start as soon as
 // their row block of step t is done, instead of a launch, ramp and tail per step) when a step
 // is only a few waves of tiles (small minibatches such as the paper's B = 600); large
@@ -417,6 +489,7 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     sh.nkb0_s0 = -1;
     sh.dep_kb = (int)(s.D / tc::BK);
     sh.ready = P.ready;
+    fine_deps(sh, s, false);
     tc::EpiLstmFwd epi{P.xh + B * s.Kx + s.D, s.Kx, P.c, P.c + B * s.H, P.g, (int)B, (int)s.H,
                        B * s.Kx, B * s.H, B * s.G4};
     if ((rc = launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st))) return rc;
@@ -487,6 +560,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     sh.nkb0_s0 = 0;
     sh.dep_kb = 0;
     sh.ready = P.ready;
+    fine_deps(sh, s, true);
     const int64_t t0 = s.T - 1;
     tc::EpiLstmBwd epi{P.g + t0 * B * s.G4, P.c + (t0 + 1) * B * s.H, P.c + t0 * B * s.H, P.dc,
                        (int)B, (int)s.H, 1, knob_int("PPO_EXP_BWD_EPI", 0), -B * s.H, -B * s.G4};
@@ -522,6 +596,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     if (const char* e = knob("PPO_WGRAD_CHUNK")) chunk_kb = std::max(1, atoi(e) / tc::BK);
     const int nchunks = std::max(1, (nkb_all + chunk_kb - 1) / chunk_kb);
     const bool pair = use_pair("WGRAD", true);
+    // experiment: PPO_VARIANT_WGRAD=pairmc -> two CTA pairs share the dZ panel by multicast
+    const char* vw = knob("PPO_VARIANT_WGRAD");
+    const bool pairmc = vw && strcmp(vw, "pairmc") == 0;
     for (int c = 0; c < nchunks; ++c) {
       const int kb0 = (int)((int64_t)nkb_all * c / nchunks);
       const int kb1 = (int)((int64_t)nkb_all * (c + 1) / nchunks);
@@ -535,12 +612,15 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
         // NVLink while the remaining tiles are still being multiplied
         tc::EpiStoreF32Dp epd{grad, s.Kx, (int)s.G4, (int)s.Kx, 0, c > 0 ? 1 : 0};
         epd.dp = *dp;
-        rc = pair ? launch2<true, true, tc::EpiStoreF32Dp, 2>("wgrad_xh", wa, wa, wb, wb, sh, epd,
-                                                             st)
-                  : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epd, st);
+        rc = pairmc ? launch2mca("wgrad_xh", wa, wb, mca_shape(sh), epd, st)
+             : pair ? launch2<true, true, tc::EpiStoreF32Dp, 2>("wgrad_xh", wa, wa, wb, wb, sh,
+                                                               epd, st)
+                    : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epd, st);
       } else {
-        rc = pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
-                  : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st);
+        rc = pairmc ? launch2mca("wgrad_xh", wa, wb, mca_shape(sh), epi, st)
+             : pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi,
+                                                             st)
+                    : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st);
       }
       if (rc) return rc;
     }
