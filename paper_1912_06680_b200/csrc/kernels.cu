@@ -1606,8 +1606,11 @@ static int launch_gae_tma(const float* rew, const float* val, const uint8_t* don
                                                                  128, smem));
     occ = std::max(occ, 1);
   }
-  int per_sm = occ;
-  if (const char* e = knob("PPO_GAE_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
+  // resident blocks: all that fit for rollouts of a few windows (L = 1,350: 4 blocks per SM
+  // 5.54 vs 3 blocks 5.09 TB/s), 3 for longer streams (L = 6,300 / 20,000: 5.70 / 5.55 vs 5.29 /
+  // 5.35 TB/s with 4; profiles/r02_gae_persm.txt)
+  int per_sm = L <= 2048 ? occ : std::min(occ, 3);
+  if (const char* e = knob("PPO_GAE_PER_SM")) per_sm = std::max(1, std::min(occ, atoi(e)));
   const int blocks = (int)std::min<int64_t>((warps + 3) / 4, (int64_t)num_sms() * per_sm);
   gae_tma_kernel<CH, S><<<blocks, 128, smem, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv,
                                                    ret, vec);

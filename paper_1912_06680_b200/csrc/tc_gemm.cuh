@@ -101,10 +101,11 @@ __device__ __forceinline__ void wait_ready(const unsigned int* p, unsigned int t
   }
   if (async) asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// Fine-grained dependencies: poll the 8 counters of group j's aligned octet (two relaxed 16-byte
+// Fine-grained dependencies: poll the 8 counters of group j's aligned octet (two acquire 16-byte
 // loads) until counter j reaches target; returns the octet's ready bits (bit i: counter
-// (j & ~7) + i) so the caller skips the polls of groups already seen ready.  Acquire by fence
-// after the observing load; async = then order TMA reads after it.
+// (j & ~7) + i) so the caller skips the polls of groups already seen ready (a full fence here
+// instead of acquire loads stalls the producer behind its own TMA loads); async = then order
+// TMA reads after it.
 __device__ __forceinline__ uint32_t wait_group(const unsigned int* row, int j, unsigned int target,
                                                bool async) {
   const unsigned int* p = row + (j & ~7);
@@ -112,9 +113,9 @@ __device__ __forceinline__ uint32_t wait_group(const unsigned int* row, int j, u
   uint32_t spins = 0;
   while (true) {
     unsigned int v[8];
-    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.acquire.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "l"(p) : "memory");
-    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.acquire.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "l"(p + 4) : "memory");
     bits = 0;
 #pragma unroll
@@ -123,7 +124,6 @@ __device__ __forceinline__ uint32_t wait_group(const unsigned int* row, int j, u
     __nanosleep(64);
     if (++spins == (1u << 26)) asm volatile("trap;");   // watchdog
   }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   if (async) asm volatile("fence.proxy.async.global;" ::: "memory");
   return bits;
 }

@@ -390,10 +390,11 @@ int sched_reset(const WsPtrs& P, cudaStream_t st) {
   return PPO_OK;
 }
 // Fine-grained multi-step dependencies (TileShape::dep_fine): the unit waits for the 64-unit
-// blocks it reads, not the whole row block.  PPO_MULTISTEP_FINE=0 (experiment builds) keeps the
-// row-block waits.
+// blocks it reads, not the whole row block.  Measured slower than the row-block waits (B = 600:
+// forward 2.53 vs 2.26 ms, backward as one launch 2.90-3.48 vs 2.44 ms per-step; tiny 575 vs
+// 555 us: profiles/r02_fine_deps_ab.txt), so off; PPO_MULTISTEP_FINE=1 (experiment builds).
 void fine_deps(tc::TileShape& sh, const Shape& s, bool backward) {
-  if (knob_int("PPO_MULTISTEP_FINE", 1) == 0 || s.H % 64 != 0) return;
+  if (knob_int("PPO_MULTISTEP_FINE", 0) == 0 || s.H % 64 != 0) return;
   if (!backward && s.D % 64 != 0) return;   // h_{t-1} must start on a k-block
   sh.dep_fine = 1;
   sh.dep_ng = (int)(s.H / 64);

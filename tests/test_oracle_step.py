@@ -81,3 +81,74 @@ def test_full_step_runs_and_moves_params():
     for k in p:
         d = newp[k] - p[k]
         assert np.all(np.abs(d) <= 5e-5 * 1.0001)
+
+
+def _gae_double_sum(r, V, d, gamma, lam):
+    """A_t = sum_l (gamma lam)^l delta_{t+l}, stopping at the first done (Q10)."""
+    L = r.shape[0]
+    delta = [r[t] + (0.0 if d[t] else gamma * V[t + 1]) - V[t] for t in range(L)]
+    A = np.zeros(L)
+    for t in range(L):
+        for l in range(L - t):
+            A[t] += (gamma * lam) ** l * delta[t + l]
+            if d[t + l]:
+                break
+    return A
+
+
+def test_ppo_step_first_update_closed_form():
+    """oracle.ppo_step end to end (GAE -> sequences -> loss gradient -> Adam), pinned by
+    pieces that share nothing with it: GAE by its double sum, the sequence layout written
+    out (sequence b = k-th T-window of the stream, time-major), the gradient of the loss by
+    central finite differences, and Adam's first step from a zero state in closed form
+    (DESIGN Q3/Q4): v = (1-b2) g^2, g_c = clip(g, +-5 sqrt(v)) = 5 sqrt(1-b2) g
+    (5 sqrt(1-b2) < 1), m = (1-b1) g_c, alpha_1 = lr sqrt(1-b2) / (1-b1), so
+        dtheta = -lr 5 (1-b2) g / (sqrt(1-b2) |g| + eps).
+    A transposed layout, a gradient of the wrong sign or shard, or Adam state mixed between
+    tensors fails it."""
+    conf = dict(gamma=oracle.gamma_from_horizon(180.0), lam=0.95, clip_eps=0.2, c_v=1.0,
+                c_e=0.01, lr=5e-5, beta1=0.9, beta2=0.999, adam_eps=1e-8, clip_sigma=5.0)
+    T = 4
+    for seed in range(5, 40):
+        cfg, p, seq, logp_old, _, _ = _setup(seed, B=4, T=T)
+        ro = synth.make_rollouts(1, 16, seed, p_done=0.15)
+        r, V, d = (np.asarray(ro[k], np.float64)[0] for k in ("r", "V", "done"))
+        A = _gae_double_sum(r, V, d, conf["gamma"], conf["lam"])
+        adv = np.zeros((T, 4))
+        ret = np.zeros((T, 4))
+        for k in range(4):
+            for t in range(T):
+                adv[t, k] = A[k * T + t]
+                ret[t, k] = A[k * T + t] + V[k * T + t]
+        lp = loss_and_grads(p, seq, logp_old, adv, ret, cfg.head_sizes)[3]["logpi"]
+        rho = np.exp(lp - logp_old.reshape(-1))
+        if np.all(np.minimum(np.abs(rho - 0.8), np.abs(rho - 1.2)) > 1e-3) and d.any():
+            break
+    conf["head_sizes"] = cfg.head_sizes
+    state = {k: (np.zeros_like(v), np.zeros_like(v)) for k, v in p.items()}
+    newp, _, rec = oracle.ppo_step(p, state, seq, ro, logp_old, conf, 1)
+    np.testing.assert_allclose(rec["adv"], adv, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(rec["ret"], ret, rtol=0, atol=1e-12)
+
+    def loss(pp):
+        return loss_and_grads(pp, seq, logp_old, adv, ret, cfg.head_sizes, 0.2, 1.0, 0.01)[0]
+
+    rng = np.random.default_rng(1)
+    b2, h = conf["beta2"], 1e-6
+    checked = 0
+    for name in ("Wx", "Wh", "b", "Wo", "bo"):
+        P = p[name]
+        for _ in range(10):
+            idx = tuple(rng.integers(0, s) for s in P.shape)
+            pp, pm = dict(p), dict(p)
+            pp[name], pm[name] = P.copy(), P.copy()
+            pp[name][idx] += h
+            pm[name][idx] -= h
+            g = (loss(pp) - loss(pm)) / (2 * h)
+            if abs(g) < 1e-6:      # finite-difference noise would decide the sign
+                continue
+            want = -conf["lr"] * 5.0 * (1 - b2) * g / (np.sqrt(1 - b2) * abs(g) + 1e-8)
+            got = newp[name][idx] - P[idx]
+            assert abs(got - want) <= 1e-4 * abs(want), (name, idx, got, want, g)
+            checked += 1
+    assert checked >= 25
