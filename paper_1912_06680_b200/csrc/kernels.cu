@@ -1,6 +1,7 @@
 // kernels.cu -- HBM-bound kernels of the PPO step (GAE, loss, Adam, layout) and the SIMT
 // fp32 reference GEMM path.  See DESIGN.md for the roofline of each.
 #include <math.h>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -325,10 +326,15 @@ __global__ void __launch_bounds__(256, MINB) gae_kernel(const float* __restrict_
 // stream boundaries; the lanes then run the same lane-chunk recurrence from shared memory.
 // Windows that are not entirely inside the row (the earliest window of a row, when the row is
 // not a whole number of windows) or that touch the end of an array take the per-lane load path.
+__device__ __forceinline__ void st_global_v8(float* p, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
 __device__ __forceinline__ uint32_t gae_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-template <int CH, int S>
+template <int CH, int S, bool FAST>
 __global__ void __launch_bounds__(128) gae_tma_kernel(
     const float* __restrict__ rew, const float* __restrict__ val, const uint8_t* __restrict__ done,
     int64_t R, int64_t L, float gamma, float lam, int seq_T, float* __restrict__ adv,
@@ -353,8 +359,14 @@ __global__ void __launch_bounds__(128) gae_tma_kernel(
   const int64_t spr = seq_T > 0 ? L / seq_T : 0, nseq = R * spr;
   // window [w_start, w_end) of row r; wb = its first step on the global 8-step grid
   auto params = [&](int64_t r, int64_t w_end, int64_t& w_start, int64_t& wb, bool& tma) {
-    const int64_t g0 = r * L, sh0 = g0 & 7;
     w_start = w_end - W;
+    if (w_end < L && w_start >= 8) {
+      // a later window's start (already on the 8-step grid) and a whole window before it
+      wb = w_start;
+      tma = vec && !(r == R - 1 && wb + W + 16 > L);
+      return;
+    }
+    const int64_t g0 = r * L, sh0 = g0 & 7;
     if (w_start <= 0 && w_end + sh0 <= W) {
       w_start = 0;
     } else {
@@ -407,18 +419,20 @@ __global__ void __launch_bounds__(128) gae_tma_kernel(
     for (int s = 0; s < S; ++s) produce(s);
   }
   uint32_t consumed = 0;
+  int st = 0;            // stage of window `consumed` (consumed % S) and its phase parity
+  uint32_t par = 0;
   for (int64_t r = gw; r < R; r += nwarps) {
     const float* rr = rew + r * L;
     const float* vv = val + r * (L + 1);
     const uint8_t* dd = done + r * L;
+    float* const ar = adv + r * L;
+    float* const rt = ret + r * L;
     float carry = 0.f;
     int64_t w_end = L;
     while (w_end > 0) {
       int64_t w_start, wb;
       bool tma;
       params(r, w_end, w_start, wb, tma);
-      const int st = (int)(consumed % S);
-      const uint32_t par = (consumed / S) & 1u;
       {   // this window's stage phase (a bulk copy, or the producer's plain arrive)
         const uint32_t bar = gae_smem(bars + st);
         asm volatile(
@@ -427,130 +441,155 @@ __global__ void __launch_bounds__(128) gae_tma_kernel(
             "@!p bra GW;\n\t}" ::"r"(bar), "r"(par) : "memory");
       }
       const int64_t t0 = wb + CH * lane;
-      const int i_lo = (int)min((int64_t)CH, max((int64_t)0, w_start - t0));
-      const int i_hi = (int)max((int64_t)0, min((int64_t)CH, w_end - t0));
-      float delta[CH], cf[CH], vkeep[CH];
-      if (tma) {
-        // the lane's chunk out of the stage with 16-byte shared loads (scalar loads at a
-        // 4*CH-byte lane stride would be CH-way bank conflicted): r aligned; V shifted by the
-        // window's (uniform) misalignment vx; d at byte offset dx in {0, 8}
-        const uint8_t* s = wst + st * SB;
-        float rv[CH], v[CH + 1];
-        const float4* r4 = reinterpret_cast<const float4*>(s) + (CH / 4) * lane;
+      // interior window (warp-uniform): every lane's CH steps are in the window and the stage
+      // holds them -- no per-step masks, vector stores
+      const bool interior = tma && w_start == wb && w_end == wb + W && vec && seq_T == 0;
+      float Aout[CH], vkeep[CH], a_first;
+      auto window = [&](auto interior_tag) {
+        constexpr bool IN = decltype(interior_tag)::value;
+        const int i_lo = IN ? 0 : (int)min((int64_t)CH, max((int64_t)0, w_start - t0));
+        const int i_hi = IN ? CH : (int)max((int64_t)0, min((int64_t)CH, w_end - t0));
+        float delta[CH], cf[CH];
+        if (IN || tma) {
+          // the lane's chunk out of the stage with 16-byte shared loads (scalar loads at a
+          // 4*CH-byte lane stride would be CH-way bank conflicted): r aligned; V shifted by
+          // the window's (uniform) misalignment vx; d at byte offset dx in {0, 8}
+          const uint8_t* s = wst + st * SB;
+          float rv[CH], v[CH + 1];
+          const float4* r4 = reinterpret_cast<const float4*>(s) + (CH / 4) * lane;
 #pragma unroll
-        for (int q = 0; q < CH / 4; ++q) {
-          const float4 a4 = r4[q];
-          rv[4 * q] = a4.x;
-          rv[4 * q + 1] = a4.y;
-          rv[4 * q + 2] = a4.z;
-          rv[4 * q + 3] = a4.w;
-        }
-        const int vx = (int)(((reinterpret_cast<uintptr_t>(vv + wb)) & 15) >> 2);
-        {
-          constexpr int NQ = CH / 4 + 1;   // CH + 1 values starting at vx < 4: NQ float4s
-          float buf[NQ * 4];
-          const float4* v4 = reinterpret_cast<const float4*>(s + RB) + (CH / 4) * lane;
+          for (int q = 0; q < CH / 4; ++q) {
+            const float4 a4 = r4[q];
+            rv[4 * q] = a4.x;
+            rv[4 * q + 1] = a4.y;
+            rv[4 * q + 2] = a4.z;
+            rv[4 * q + 3] = a4.w;
+          }
+          {
+            constexpr int NQ = CH / 4 + 1;   // CH + 1 values starting at vx < 4: NQ float4s
+            const int vx = (int)(((reinterpret_cast<uintptr_t>(vv + wb)) & 15) >> 2);
+            float buf[NQ * 4];
+            const float4* v4 = reinterpret_cast<const float4*>(s + RB) + (CH / 4) * lane;
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) reinterpret_cast<float4*>(buf)[q] = v4[q];
-          switch (vx) {
+            for (int q = 0; q < NQ; ++q) reinterpret_cast<float4*>(buf)[q] = v4[q];
+            switch (vx) {
 #define PPO_GAE_VSHIFT(M)                                                     \
   case M:                                                                     \
     _Pragma("unroll") for (int i = 0; i <= CH; ++i) v[i] = buf[i + M]; \
     break;
-            PPO_GAE_VSHIFT(0)
-            PPO_GAE_VSHIFT(1)
-            PPO_GAE_VSHIFT(2)
-            PPO_GAE_VSHIFT(3)
+              PPO_GAE_VSHIFT(0)
+              PPO_GAE_VSHIFT(1)
+              PPO_GAE_VSHIFT(2)
+              PPO_GAE_VSHIFT(3)
 #undef PPO_GAE_VSHIFT
+            }
+          }
+          const int dx = (int)((reinterpret_cast<uintptr_t>(dd + wb)) & 15);
+          uint8_t db[CH];
+          {
+            const uint2* d2 = reinterpret_cast<const uint2*>(s + RB + VB + dx) + (CH / 8) * lane;
+#pragma unroll
+            for (int q = 0; q < CH / 8; ++q) *reinterpret_cast<uint2*>(db + 8 * q) = d2[q];
+          }
+#pragma unroll
+          for (int i = 0; i < CH; ++i) {
+            const bool in = IN || (i >= i_lo && i < i_hi);   // window steps (others: identity)
+            const float nd = db[i] ? 0.f : 1.f;
+            delta[i] = in ? rv[i] + gamma * nd * v[i + 1] - v[i] : 0.f;
+            cf[i] = in ? gl * nd : 1.f;
+            vkeep[i] = in ? v[i] : 0.f;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < CH; ++i) {
+            if (i >= i_lo && i < i_hi) {
+              const int64_t t = t0 + i;
+              const float nd = dd[t] ? 0.f : 1.f;
+              const float vt = vv[t];
+              delta[i] = rr[t] + gamma * nd * vv[t + 1] - vt;
+              cf[i] = gl * nd;
+              vkeep[i] = vt;
+            } else {
+              delta[i] = 0.f;
+              cf[i] = 1.f;
+              vkeep[i] = 0.f;
+            }
           }
         }
-        const int dx = (int)((reinterpret_cast<uintptr_t>(dd + wb)) & 15);
-        uint8_t db[CH];
-        {
-          const uint2* d2 = reinterpret_cast<const uint2*>(s + RB + VB + dx) + (CH / 8) * lane;
+        // the stage is read: refill it with the window S ahead (async-proxy write after the
+        // generic reads)
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          produce(st);
+        }
+        float P = 0.f, Q = 1.f;
 #pragma unroll
-          for (int q = 0; q < CH / 8; ++q) *reinterpret_cast<uint2*>(db + 8 * q) = d2[q];
+        for (int i = CH - 1; i >= 0; --i) {
+          P = delta[i] + cf[i] * P;
+          Q = cf[i] * Q;
         }
 #pragma unroll
-        for (int i = 0; i < CH; ++i) {
-          const bool in = i >= i_lo && i < i_hi;   // steps of the window (others: identity)
-          const float nd = db[i] ? 0.f : 1.f;
-          delta[i] = in ? rv[i] + gamma * nd * v[i + 1] - v[i] : 0.f;
-          cf[i] = in ? gl * nd : 1.f;
-          vkeep[i] = in ? v[i] : 0.f;
+        for (int off = 1; off < 32; off <<= 1) {
+          const float P2 = __shfl_down_sync(0xffffffffu, P, off);
+          const float Q2 = __shfl_down_sync(0xffffffffu, Q, off);
+          if (lane + off < 32) {
+            P = P + Q * P2;
+            Q = Q * Q2;
+          }
         }
+        a_first = P + Q * carry;
+        float a = __shfl_down_sync(0xffffffffu, a_first, 1);
+        if (lane == 31) a = carry;
+#pragma unroll
+        for (int i = CH - 1; i >= 0; --i) {
+          a = delta[i] + cf[i] * a;
+          Aout[i] = a;
+        }
+        const bool full = IN || (vec && i_lo == 0 && i_hi == CH);
+        if constexpr (IN && CH == 8) {
+          // 32-byte aligned (window on the 8-step grid, vec): one 256-bit store per array
+          float Rout[CH];
+#pragma unroll
+          for (int i = 0; i < CH; ++i) Rout[i] = Aout[i] + vkeep[i];
+          st_global_v8(ar + t0, Aout);
+          st_global_v8(rt + t0, Rout);
+        } else if (IN || (seq_T == 0 && full)) {
+          float Rout[CH];
+#pragma unroll
+          for (int i = 0; i < CH; ++i) Rout[i] = Aout[i] + vkeep[i];
+          store_floats<CH>(ar + t0, Aout);
+          store_floats<CH>(rt + t0, Rout);
+        } else {
+#pragma unroll
+          for (int i = 0; i < CH; ++i) {
+            if (i >= i_lo && i < i_hi) {
+              const int64_t t = t0 + i;
+              int64_t o;
+              if (seq_T > 0) {
+                const int64_t k = t / seq_T, tt = t - k * seq_T;
+                o = tt * nseq + r * spr + k;
+              } else {
+                o = r * L + t;
+              }
+              adv[o] = Aout[i];
+              ret[o] = Aout[i] + vkeep[i];
+            }
+          }
+        }
+      };
+      // FAST (long rows): interior windows take the mask-free path; with rows of a few windows
+      // (L = 1,350) one body measured faster (3.5%: profiles/r02_gae_fast.txt)
+      if constexpr (FAST) {
+        if (interior) window(std::true_type{});
+        else window(std::false_type{});
       } else {
-#pragma unroll
-        for (int i = 0; i < CH; ++i) {
-          if (i >= i_lo && i < i_hi) {
-            const int64_t t = t0 + i;
-            const float nd = dd[t] ? 0.f : 1.f;
-            const float vt = vv[t];
-            delta[i] = rr[t] + gamma * nd * vv[t + 1] - vt;
-            cf[i] = gl * nd;
-            vkeep[i] = vt;
-          } else {
-            delta[i] = 0.f;
-            cf[i] = 1.f;
-            vkeep[i] = 0.f;
-          }
-        }
-      }
-      // the stage is read: refill it with the window S ahead (async-proxy write after the
-      // generic reads)
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        produce(st);
+        window(std::false_type{});
       }
       ++consumed;
-      float P = 0.f, Q = 1.f;
-#pragma unroll
-      for (int i = CH - 1; i >= 0; --i) {
-        P = delta[i] + cf[i] * P;
-        Q = cf[i] * Q;
-      }
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const float P2 = __shfl_down_sync(0xffffffffu, P, off);
-        const float Q2 = __shfl_down_sync(0xffffffffu, Q, off);
-        if (lane + off < 32) {
-          P = P + Q * P2;
-          Q = Q * Q2;
-        }
-      }
-      const float a_first = P + Q * carry;
-      float a = __shfl_down_sync(0xffffffffu, a_first, 1);
-      if (lane == 31) a = carry;
-      float Aout[CH];
-#pragma unroll
-      for (int i = CH - 1; i >= 0; --i) {
-        a = delta[i] + cf[i] * a;
-        Aout[i] = a;
-      }
-      const bool full = vec && i_lo == 0 && i_hi == CH;
-      if (seq_T == 0 && full) {
-        float Rout[CH];
-#pragma unroll
-        for (int i = 0; i < CH; ++i) Rout[i] = Aout[i] + vkeep[i];
-        store_floats<CH>(adv + r * L + t0, Aout);
-        store_floats<CH>(ret + r * L + t0, Rout);
-      } else {
-#pragma unroll
-        for (int i = 0; i < CH; ++i) {
-          if (i >= i_lo && i < i_hi) {
-            const int64_t t = t0 + i;
-            int64_t o;
-            if (seq_T > 0) {
-              const int64_t k = t / seq_T, tt = t - k * seq_T;
-              o = tt * nseq + r * spr + k;
-            } else {
-              o = r * L + t;
-            }
-            adv[o] = Aout[i];
-            ret[o] = Aout[i] + vkeep[i];
-          }
-        }
+      if (++st == S) {
+        st = 0;
+        par ^= 1u;
       }
       carry = __shfl_sync(0xffffffffu, a_first, 0);
       w_end = w_start;
@@ -1587,22 +1626,22 @@ int launch_pack_state(const Shape& s, int64_t B, const float* h0, const float* c
   PPO_LAUNCH_CHECK("pack_state_kernel");
   return PPO_OK;
 }
-template <int CH, int S>
-static int launch_gae_tma(const float* rew, const float* val, const uint8_t* done, int64_t R,
+template <int CH, int S, bool FAST>
+static int launch_gae_tma_t(const float* rew, const float* val, const uint8_t* done, int64_t R,
                           int64_t L, float gamma, float lam, int seq_T, float* adv, float* ret,
                           bool vec, cudaStream_t st) {
   constexpr int SB = 32 * CH * 4 + (32 * CH + 8) * 4 + 32 * CH + 16;
   constexpr int smem = 4 * (S * SB + S * 8);
   static bool configured = false;
   if (!configured) {
-    PPO_CUDA_CHECK(cudaFuncSetAttribute(gae_tma_kernel<CH, S>,
+    PPO_CUDA_CHECK(cudaFuncSetAttribute(gae_tma_kernel<CH, S, FAST>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
   const int64_t warps = R;
   static int occ = 0;   // resident blocks per SM at this stage depth (shared memory, registers)
   if (occ == 0) {
-    PPO_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gae_tma_kernel<CH, S>,
+    PPO_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gae_tma_kernel<CH, S, FAST>,
                                                                  128, smem));
     occ = std::max(occ, 1);
   }
@@ -1611,11 +1650,24 @@ static int launch_gae_tma(const float* rew, const float* val, const uint8_t* don
   // 5.35 TB/s with 4; profiles/r02_gae_persm.txt)
   int per_sm = L <= 2048 ? occ : std::min(occ, 3);
   if (const char* e = knob("PPO_GAE_PER_SM")) per_sm = std::max(1, std::min(occ, atoi(e)));
-  const int blocks = (int)std::min<int64_t>((warps + 3) / 4, (int64_t)num_sms() * per_sm);
-  gae_tma_kernel<CH, S><<<blocks, 128, smem, st>>>(rew, val, done, R, L, gamma, lam, seq_T, adv,
-                                                   ret, vec);
+  // warps per block: 4, or fewer when there are too few streams to give every SM the same
+  // number of warps in 4-warp blocks (1,000 streams: 250 blocks = 2 on 102 SMs, 1 on 46)
+  int wpb = 4;
+  if (warps < (int64_t)num_sms() * per_sm * 4) wpb = knob_int("PPO_GAE_WPB", 4);
+  const int blocks = (int)std::min<int64_t>((warps + wpb - 1) / wpb,
+                                            (int64_t)num_sms() * per_sm * (4 / wpb));
+  gae_tma_kernel<CH, S, FAST><<<blocks, 32 * wpb, smem / 4 * wpb, st>>>(rew, val, done, R, L, gamma,
+                                                                  lam, seq_T, adv, ret, vec);
   PPO_LAUNCH_CHECK("gae_tma_kernel");
   return PPO_OK;
+}
+template <int CH, int S>
+static int launch_gae_tma(const float* rew, const float* val, const uint8_t* done, int64_t R,
+                          int64_t L, float gamma, float lam, int seq_T, float* adv, float* ret,
+                          bool vec, cudaStream_t st) {
+  if (L >= 4096)
+    return launch_gae_tma_t<CH, S, true>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, vec, st);
+  return launch_gae_tma_t<CH, S, false>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, vec, st);
 }
 int launch_gae(const float* rew, const float* val, const uint8_t* done, int64_t R, int64_t L,
                float gamma, float lam, int seq_T, float* adv, float* ret, void* scratch,
