@@ -578,8 +578,8 @@ __global__ void __launch_bounds__(128) gae_tma_kernel(
           }
         }
       };
-      // FAST (long rows): interior windows take the mask-free path; with rows of a few windows
-      // (L = 1,350) one body measured faster (3.5%: profiles/r02_gae_fast.txt)
+      // FAST (long rows): interior windows take the mask-free path; with rows of fewer windows
+      // one body measured faster (profiles/r02_gae_fast.txt)
       if constexpr (FAST) {
         if (interior) window(std::true_type{});
         else window(std::false_type{});
@@ -1665,7 +1665,9 @@ template <int CH, int S>
 static int launch_gae_tma(const float* rew, const float* val, const uint8_t* done, int64_t R,
                           int64_t L, float gamma, float lam, int seq_T, float* adv, float* ret,
                           bool vec, cudaStream_t st) {
-  if (L >= 4096)
+  // the second (interior) body pays off only for rows of many windows: L = 10^6 +13%, 10^5
+  // +2%, 20,000 even, 6,300 -3.5%, 1,350 -3.5% (profiles/r02_gae_fast.txt)
+  if (L >= 65536)
     return launch_gae_tma_t<CH, S, true>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, vec, st);
   return launch_gae_tma_t<CH, S, false>(rew, val, done, R, L, gamma, lam, seq_T, adv, ret, vec, st);
 }
