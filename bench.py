@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--B", type=int, default=38400, help="sequences per GPU")
+    ap.add_argument("--small-B", type=int, default=600,
+                    help="--config paper-mb: sequences per GPU (default the paper's 600)")
     ap.add_argument("--H", type=int, default=4096)
     ap.add_argument("--D", type=int, default=4032)
     ap.add_argument("--no-e2e", action="store_true")
@@ -259,6 +261,9 @@ def algorithmic(H, D, T, B, A, nparam):
         # h0, c0 in (fp32); h0 bf16 + c0 fp32 out; the [1 | 0...] pad of T+1 slots
         "pack_state": ("byte", 8.0 * B * H + 6.0 * B * H + (T + 1) * B * 64 * 2.0),
         "input_grad": ("flop", 2.0 * rows * G4 * D),
+        # small-B backward (split-K dh GEMM + cell kernel): dh in, gates -> dz, c_t, c_{t-1},
+        # dc in/out per step (the extra split partials are implementation traffic)
+        "cell_bwd": ("byte", T * B * H * (4.0 + 2 * 8.0 + 4 * 4.0)),
     }
 
 
@@ -536,7 +541,7 @@ def run_small(args):
     if args.config == "tiny":
         H, D, B = 128, 256, 32
     else:
-        H, D, B = args.H, args.D, 600
+        H, D, B = args.H, args.D, args.small_B
     T = 16
     cfg = synth.Config(H=H, D=D, B=B, T=T)
     opt = PPOOptimizer(D, H, B, T, cfg.head_sizes, precision="bf16", device=dev)

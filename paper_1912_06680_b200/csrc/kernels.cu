@@ -1870,6 +1870,101 @@ int launch_simt_cell_fwd(const Shape& s, int64_t B, const float* z, const float*
   PPO_LAUNCH_CHECK("simt_cell_fwd_kernel");
   return PPO_OK;
 }
+// Cell backward of one recurrent step after a split-K dh GEMM (small minibatches, where the
+// step GEMM has fewer tiles than CTA pairs): dh = sum of nsplit fp32 partials (fixed order),
+// then the same cell math as the fused EpiLstmBwd epilogue (tc_math sigmoid/tanh), dz over the
+// bf16 gates in place and the dc carry.  A thread per (row, 8 units); the 8 threads of a
+// 64-unit block read each gate's 128 contiguous bytes (coalesced, unlike the epilogue's
+// row-per-thread access).
+__global__ void __launch_bounds__(256) cell_bwd_split_kernel(
+    const float* __restrict__ part, int nsplit, int64_t split_stride, __nv_bfloat16* gz,
+    const float* __restrict__ c_t, const float* __restrict__ c_prev, float* dc, int64_t B,
+    int64_t H, int first) {
+  const int64_t nch = H / 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * nch) return;
+  const int64_t m = idx / nch;
+  const int64_t j0 = (idx - m * nch) * 8;
+  const int64_t o = m * H + j0;
+  float dh[8], ct[8], cp[8], dcv[8];
+  {
+    const float4* p4 = reinterpret_cast<const float4*>(part + o);
+    float4 a = p4[0], b = p4[1];
+    for (int sp = 1; sp < nsplit; ++sp) {
+      const float4* q4 = reinterpret_cast<const float4*>(part + sp * split_stride + o);
+      const float4 x = q4[0], y = q4[1];
+      a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+      b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
+    }
+    dh[0] = a.x; dh[1] = a.y; dh[2] = a.z; dh[3] = a.w;
+    dh[4] = b.x; dh[5] = b.y; dh[6] = b.z; dh[7] = b.w;
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const float4 x = reinterpret_cast<const float4*>(c_t + o)[q];
+    const float4 y = reinterpret_cast<const float4*>(c_prev + o)[q];
+    ct[4 * q] = x.x; ct[4 * q + 1] = x.y; ct[4 * q + 2] = x.z; ct[4 * q + 3] = x.w;
+    cp[4 * q] = y.x; cp[4 * q + 1] = y.y; cp[4 * q + 2] = y.z; cp[4 * q + 3] = y.w;
+    if (first) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dcv[4 * q + i] = 0.f;
+    } else {
+      const float4 z = reinterpret_cast<const float4*>(dc + o)[q];
+      dcv[4 * q] = z.x; dcv[4 * q + 1] = z.y; dcv[4 * q + 2] = z.z; dcv[4 * q + 3] = z.w;
+    }
+  }
+  // gates of units j0..j0+7: gate q at (j0 >> 6) * 256 + q * 64 + (j0 & 63) (gate-grouped rows)
+  __nv_bfloat16* g = gz + m * 4 * H + (j0 >> 6) * 256 + (j0 & 63);
+  uint4 graw[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) graw[q] = *reinterpret_cast<const uint4*>(g + q * 64);
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    float z[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t u = reinterpret_cast<const uint32_t*>(&graw[q])[w];
+      z[q][0] = __uint_as_float(u << 16);
+      z[q][1] = __uint_as_float(u & 0xFFFF0000u);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = 2 * w + h;
+      float a, b, c, d, dn;
+      cell_bwd(dh[e], dcv[e], z[0][h], z[1][h], z[2][h], z[3][h], ct[e], cp[e], a, b, c, d, dn,
+               true);
+      z[0][h] = a;
+      z[1][h] = b;
+      z[2][h] = c;
+      z[3][h] = d;
+      dcv[e] = dn;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const __nv_bfloat162 pk = __floats2bfloat162_rn(z[q][0], z[q][1]);
+      reinterpret_cast<uint32_t*>(&graw[q])[w] = *reinterpret_cast<const uint32_t*>(&pk);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(g + q * 64) = graw[q];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    reinterpret_cast<float4*>(dc + o)[q] =
+        make_float4(dcv[4 * q], dcv[4 * q + 1], dcv[4 * q + 2], dcv[4 * q + 3]);
+}
+int launch_cell_bwd_split(const float* part, int nsplit, int64_t split_stride, void* gz,
+                          const float* c_t, const float* c_prev, float* dc, int64_t B, int64_t H,
+                          bool first, cudaStream_t st) {
+  if (H % 64 != 0) return fail(PPO_E_SHAPE, "split cell backward needs H % 64 == 0");
+  ProfScope _prof("cell_bwd", st);
+  const int64_t threads = B * (H / 8);
+  cell_bwd_split_kernel<<<grid_for(threads, 256), 256, 0, st>>>(
+      part, nsplit, split_stride, static_cast<__nv_bfloat16*>(gz), c_t, c_prev, dc, B, H,
+      first ? 1 : 0);
+  PPO_LAUNCH_CHECK("cell_bwd_split_kernel");
+  return PPO_OK;
+}
+
 int launch_simt_cell_bwd(const Shape& s, int64_t B, const float* dh, float* gz, const float* c_t,
                          const float* c_prev, float* dc, cudaStream_t st) {
   ProfScope _prof("simt_cell_bwd", st);

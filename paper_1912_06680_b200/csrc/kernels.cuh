@@ -86,6 +86,11 @@ int launch_simt_cell_fwd(const Shape& s, int64_t B, const float* z, const float*
 int launch_simt_cell_bwd(const Shape& s, int64_t B, const float* dh, float* gz, const float* c_t,
                          const float* c_prev, float* dc, cudaStream_t st);
 
+// Cell backward after a split-K dh GEMM: dh = sum of nsplit partials [nsplit][B][H] (fixed
+// order), gates -> dz in place in gz [B][4H] (gate-grouped), dc carry in/out (zero if first)
+int launch_cell_bwd_split(const float* part, int nsplit, int64_t split_stride, void* gz,
+                          const float* c_t, const float* c_prev, float* dc, int64_t B, int64_t H,
+                          bool first, cudaStream_t st);
 // out[i] = sum_{s < nsplit} part[s * n + i] in fixed order (deterministic split-K reduction)
 // dp (nullable): also push the sums to the DP owners' staging (element i = theta dp_base + i)
 int launch_splitk_reduce(const float* part, int nsplit, size_t n, float* out, cudaStream_t st,

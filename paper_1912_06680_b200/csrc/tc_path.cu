@@ -412,6 +412,22 @@ void fine_deps(tc::TileShape& sh, const Shape& s, bool backward) {
   }
 }
 
+// Split-K factor for the backward step GEMM (0 = keep the fused-epilogue launch): only when a
+// step has fewer tiles than CTA pairs, on the bf16 path (the partials use the dW_o split-K
+// region, which must hold them).  PPO_BWD_SPLIT=0 (experiment builds) keeps the fused path.
+int bwd_split(const Shape& s, int64_t B, bool pair, int64_t tiles) {
+  if (!pair || !s.bf16 || s.H % 64 != 0 || knob_int("PPO_BWD_SPLIT", 1) == 0) return 0;
+  const int clusters = num_sms() / 2;
+  if (tiles >= clusters) return 0;
+  const int nkb = (int)((s.G4 + s.A_pass + tc::BK - 1) / tc::BK);
+  int sp = pick_split((int)tiles, clusters, nkb);
+  const size_t room = (size_t)kMaxSplitK * s.A * s.Ko * 4;
+  while (sp > 1 && (size_t)sp * B * s.H * 4 > room) --sp;
+  // every split of the last step (K = the A_pass head columns only) must get a k-block
+  while (sp > 1 && (s.A_pass + tc::BK - 1) / tc::BK < sp) --sp;
+  return sp > 1 ? sp : 0;
+}
+
 // The T recurrent step GEMMs as ONE persistent launch (tiles of step t+1 start as soon as
 // their row block of step t is done, instead of a launch, ramp and tail per step) when a step
 // is only a few waves of tiles (small minibatches such as the paper's B = 600); large
@@ -566,6 +582,26 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     tc::EpiLstmBwd epi{P.g + t0 * B * s.G4, P.c + (t0 + 1) * B * s.H, P.c + t0 * B * s.H, P.dc,
                        (int)B, (int)s.H, 1, knob_int("PPO_EXP_BWD_EPI", 0), -B * s.H, -B * s.G4};
     if ((rc = launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st))) return rc;
+  } else if (const int nsplit = bwd_split(s, B, pair, bwd_tiles)) {
+    // small minibatch (fewer tiles per step than CTA pairs, e.g. the paper's B = 600: 48 tiles
+    // on 74 pairs, each running the whole K = 4H + A and then an exposed row-per-thread
+    // epilogue): split K over nsplit x tiles units (~2 full waves), fp32 partials of dh into
+    // the dW_o split-K region, then the cell backward as a coalesced elementwise kernel
+    float* part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ws_layout(s, B).splitk);
+    for (int t = (int)s.T - 1; t >= 0; --t) {
+      const bool last = t == s.T - 1;
+      tc::TileShape sh{(int)B, (int)s.H, last ? 0 : cdiv(s.G4, tc::BK), cdiv(s.A_pass, tc::BK),
+                       t + 1, t, 0, 0, 8, 1};
+      raster(sh, "BWD", 8, 1);
+      sh.ksplit = nsplit;
+      sh.sched = P.slot(kSchedBwd);
+      tc::EpiStoreF32 epi{part, s.H, (int)B, (int)s.H, B * s.H};
+      if ((rc = launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st))) return rc;
+      if ((rc = launch_cell_bwd_split(part, nsplit, B * s.H, P.g + t * B * s.G4,
+                                      P.c + (t + 1) * B * s.H, P.c + t * B * s.H, P.dc, B, s.H,
+                                      last, st)))
+        return rc;
+    }
   } else
   for (int t = (int)s.T - 1; t >= 0; --t) {
     const bool last = t == s.T - 1;

@@ -32,7 +32,7 @@ def _run(case, cfg, precision):
     return opt, batch, theta0, stats
 
 
-def _check_step(case, cfg, precision, tol_fwd, tol_grad):
+def _check_step(case, cfg, precision, tol_fwd, tol_grad, stat_floor=1e-3):
     opt, batch, theta0, stats = _run(case, cfg, precision)
     T, B, A = cfg.T, cfg.B, cfg.A
     # a1: GAE in minibatch layout
@@ -48,7 +48,7 @@ def _check_step(case, cfg, precision, tol_fwd, tol_grad):
     st = case["stats"]
     tol_s = 1e-5 if precision == "fp32" else 2e-2
     for i, k in enumerate(("loss", "pg", "vf", "ent")):
-        assert abs(stats[i] - st[k]) <= tol_s * (abs(st[k]) + 1e-3), (k, stats[i], st[k])
+        assert abs(stats[i] - st[k]) <= tol_s * (abs(st[k]) + stat_floor), (k, stats[i], st[k])
     assert stats[6] == st["n_valid"] and int(stats[7]) == 0
     # a6-a8: gradients (canonical layout)
     g = {k: v.cpu().numpy() for k, v in opt.unpack(opt.grad).items()}
@@ -118,6 +118,20 @@ def test_full_width_bf16():
     cfg = synth.Config(H=4096, D=4032, B=48)
     case = make_case(cfg, 7, pad_frac=0.1, wo_scale=5.0)
     _check_step(case, cfg, "bf16", 2e-2, 2e-2)
+
+
+def test_split_k_backward_bf16():
+    """Small minibatch (fewer backward tiles per step than CTA pairs): the backward step GEMM
+    runs split-K into fp32 partials and the cell backward as a separate coalesced kernel
+    (tc_path.cu bwd_split): H = 2048 (K = 4H + A = 139 k-blocks -> 2 splits), 2 x 8 tiles."""
+    cfg = synth.Config(H=2048, D=512, B=288)
+    # wo_scale 4: with 8 the bf16 forward alone leaves 5% of W_h's entries sign-unresolved
+    # for the split and the fused backward alike (profiles/r02_split_check.txt)
+    case = make_case(cfg, 9, pad_frac=0.1, wo_scale=4.0)
+    # pg = -mean(min(rho A, clip(rho) A)) is a cancelling mean (2.4e-3 here from terms of
+    # order |A| ~ 1): the bf16 forward (computed before and independently of the backward
+    # under test) moves it by 8.5e-5, so its absolute floor is 5e-3 x 2e-2 = 1e-4
+    _check_step(case, cfg, "bf16", 2e-2, 2e-2, stat_floor=5e-3)
 
 
 def test_determinism_bf16():
