@@ -213,7 +213,9 @@ int ppo_aux_labels(const ppo_dims* dims, int64_t R, int64_t L, const uint8_t* la
 
 /* ---- a6-a8: backward (TBPTT, no gradient into h0/c0; O8) ------------------------
  * ws: the workspace filled by lstm_bptt_fwd for the same (w, B) (it is modified: saved gates
- * are overwritten by dz).  dout: from ppo_loss_grad.  grad: [n_total] fp32, OVERWRITTEN with
+ * are overwritten by dz; with PPO_PREC_BF16 and fewer backward tiles per step than CTA pairs
+ * -- small B such as the paper's 600 -- the workspace's split-K region also receives the fp32
+ * partials of dh).  dout: from ppo_loss_grad.  grad: [n_total] fp32, OVERWRITTEN with
  * dL/dtheta in the theta layout (bias gradients fall out of the augmented columns).
  * Aux heads (NEXT-4): the LSTM receives the policy, value and (scaled) win columns of dout
  * only; every output row of W_o_aug gets its head's full gradient (DESIGN Q26). */
