@@ -61,6 +61,7 @@ struct TileShape {
   int dep_fine;
   int dep_kpg, dep_ng, dep_ld, epi_q;
   int dep_perm;
+  int src1_first;   // multi-step: take source 1's k-blocks before source 0's
 };
 
 // One work unit of a launch: a tile and (split-K) its k-range or (multi-step) its step.
@@ -793,7 +794,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // source 1 (dy_t, no dependency) first, then source 0's blocks in the order the
           // previous step's epilogues publish them (block q of every tile, then q + 1, ...)
           int kx = kb;
-          if (sh.dep_perm && sh.tsteps > 1) {
+          if (sh.src1_first && sh.tsteps > 1) {
+            // multi-step backward: source 1 (dy_t, no dependency) while the previous step's
+            // row block finishes, then source 0 (dz_{t+1})
+            kx = kb < sh.nkb1 ? ui.nkb0 + kb : kb - sh.nkb1;
+          } else if (sh.dep_perm && sh.tsteps > 1) {
             if (kb < sh.nkb1) {
               kx = ui.nkb0 + kb;
             } else {

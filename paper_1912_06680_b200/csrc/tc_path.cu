@@ -578,6 +578,8 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     sh.dep_kb = 0;
     sh.ready = P.ready;
     fine_deps(sh, s, true);
+    // the dY k-blocks (no dependency) first: they load and multiply while step s-1 finishes
+    if (!sh.dep_fine) sh.src1_first = knob_int("PPO_BWD_SRC1_FIRST", 1);
     const int64_t t0 = s.T - 1;
     tc::EpiLstmBwd epi{P.g + t0 * B * s.G4, P.c + (t0 + 1) * B * s.H, P.c + t0 * B * s.H, P.dc,
                        (int)B, (int)s.H, 1, knob_int("PPO_EXP_BWD_EPI", 0), -B * s.H, -B * s.G4};

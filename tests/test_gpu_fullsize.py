@@ -1,7 +1,8 @@
 """Parity at BASELINE.json's full size, in the launch configuration bench.py times
 (H=4096, D=4032, T=16, B=38,400 sequences, bf16 tcgen05 path), on sampled outputs -- and
 again at the maximum minibatch that fits 180 GB (B_max = 123,648 sequences, 170 GB,
-profiles/r01_sweep_B_v3.jsonl), the largest launch the library supports on one B200.
+profiles/r01_sweep_B_v3.jsonl), the largest launch the library supports on one B200, and at
+the paper's minibatch size (B = 640 ~ 600, the small-B split-K backward).
 
 The GPU runs the whole step over all 38,400 sequences.  Per-sequence quantities (GAE of a
 rollout stream, the forward pass of a sequence, the loss gradient of a row) are checked one
@@ -23,9 +24,13 @@ from oracle.step import loss_and_grads
 pytestmark = pytest.mark.gpu
 
 B_BENCH, B_MAX = 38400, 123648
+# the paper's per-GPU minibatch (600) rounded up to whole 256-step rollout streams: its
+# backward steps have fewer tiles than CTA pairs, so this runs the split-K backward path
+B_PAPER = 640
 
 
-@pytest.fixture(scope="module", params=[B_BENCH, B_MAX], ids=["B38400", "Bmax123648"])
+@pytest.fixture(scope="module", params=[B_PAPER, B_BENCH, B_MAX],
+                ids=["B640", "B38400", "Bmax123648"])
 def run(request):
     res = _run(request.param)
     yield res
@@ -39,8 +44,8 @@ def _run(B_total):
     dev = "cuda"
     cfg = synth.Config(H=4096, D=4032, B=B_total)
     # sampled sequences (first, middle, last tile); rollout streams of 256 steps (16 sequences)
-    SAMPLE_SEQ = (0, 12345, B_total - 1)
-    SAMPLE_STREAMS = (0, 771, B_total // 16 - 1)
+    SAMPLE_SEQ = (0, min(12345, B_total // 2 + 5), B_total - 1)
+    SAMPLE_STREAMS = (0, min(771, B_total // 32 + 1), B_total // 16 - 1)
     T, B, H, D = cfg.T, cfg.B, cfg.H, cfg.D
     prm = synth.torch_params(cfg, 3, dev, bo_scale=0.05)
     prm["Wo"] *= 5.0
@@ -129,7 +134,15 @@ def test_loss_rows_sampled(run):
                                          HYPER["clip_eps"], HYPER["c_v"], HYPER["c_e"],
                                          denom=float(T * B))
     d = opt.dout.view(T, B, -1)[:, sidx].float().cpu().numpy().reshape(T * len(sidx), -1)
-    assert np.all(np.abs(d - dYref) <= 2 ** -8 * np.abs(dYref) + 1e-12 * np.abs(dYref).max())
+    # one bf16 rounding of an fp32 result that meets the fp32 bar (1e-5 of |ref| + rms(ref),
+    # elementwise_ok): entries 1e-6 of their row's largest (p ~ 1e-6, cek y + c1 cancelling)
+    # carry fp32 errors that are small against the rms but not against themselves
+    rms = np.sqrt(np.mean(dYref * dYref))
+    bound = 2 ** -8 * np.abs(dYref) + 1e-5 * (np.abs(dYref) + rms)
+    bad = np.argwhere(np.abs(d - dYref) > bound)
+    rowmax = np.abs(dYref).max(axis=1)
+    assert bad.size == 0, [(int(i), int(j), float(dYref[i, j]), float(d[i, j]), float(rowmax[i]))
+                           for i, j in bad[:8]]
     lp = opt.logp.view(T, B)[:, sidx].cpu().numpy().reshape(-1)
     ok, worst = elementwise_ok(lp, lpref, 1e-5)
     assert ok, worst

@@ -4,7 +4,8 @@ device step counter of Adam that makes it replayable (adam_step_ctr).
 * Graph replays equal eager steps bit for bit: an optimizer that runs 1 eager step, captures
   the step and replays it 3 times ends with the same theta, bf16 shadow, m, v, gradient and
   loss statistics as one that runs 4 eager steps (both with the device step counter), and its
-  step count reads 4.
+  step count reads 4 -- for the multi-step launches (tiny, ragged) and the small-B split-K
+  backward (H = 2048, B = 288: split GEMM + cell kernel per step).
 * The device alpha_t equals the host one: adam_step_ctr and adam_step give the same bits for
   t = 1 ... 300 (alpha_t = lr sqrt(1 - b2^t) / (1 - b1^t) in double, rounded once to fp32 on
   either side, ppo5.h), so a graph-replayed run also equals a host-counter run.
@@ -27,8 +28,9 @@ def L():
 
 
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
-@pytest.mark.parametrize("cfg", [synth.TINY, synth.Config(H=256, D=192, B=176)],
-                         ids=["tiny", "ragged"])
+@pytest.mark.parametrize("cfg", [synth.TINY, synth.Config(H=256, D=192, B=176),
+                                 synth.Config(H=2048, D=512, B=288)],
+                         ids=["tiny", "ragged", "splitk"])
 def test_graph_replay_equals_eager(L, precision, cfg):
     from paper_1912_06680_b200 import PPOOptimizer
     case = make_case(cfg, 8, pad_frac=0.2, wo_scale=10.0)
