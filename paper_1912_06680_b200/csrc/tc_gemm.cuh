@@ -68,11 +68,12 @@ struct TileShape {
 struct UnitInfo {
   int split, tile, kb_lo, kb_hi, nkb0, za0, za1;
 };
+template <bool MS = false>
 __device__ __forceinline__ UnitInfo decode_unit(const TileShape& sh, int u, int ntiles) {
   UnitInfo r;
   r.split = u / ntiles;
   r.tile = u - r.split * ntiles;
-  if (sh.tsteps > 1) {
+  if (MS && sh.tsteps > 1) {
     r.nkb0 = (r.split == 0 && sh.nkb0_s0 >= 0) ? sh.nkb0_s0 : sh.nkb0;
     r.kb_lo = 0;
     r.kb_hi = r.nkb0 + sh.nkb1;
@@ -672,7 +673,10 @@ struct Smem2 {
   static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4 + 2 * kSchedDepth) * 8 + 32 + 1024;
 };
 
-template <bool A_MN, bool B_MN, int STAGES, int MB, int BN, class Epi>
+// MS: the persistent multi-step launch (TileShape::tsteps > 1).  Every multi-step branch is
+// compiled only into the MS instantiations: a per-k-block test in the producer loop of the
+// ordinary launches measured 7% on the backward step GEMM (profiles/r02_abb_final.txt).
+template <bool A_MN, bool B_MN, int STAGES, int MB, int BN, class Epi, bool MS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                     const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
@@ -707,7 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int ntiles = num_m * num_n;
   const int nsplit = sh.ksplit > 1 ? sh.ksplit : 1;
   // split-K: unit = split * ntiles + tile; multi-step: unit = step * ntiles + tile
-  const int nunits = ntiles * (sh.tsteps > 1 ? sh.tsteps : nsplit);
+  const int nunits = ntiles * (MS && sh.tsteps > 1 ? sh.tsteps : nsplit);
 
   if (threadIdx.x == 0) {
     prefetch_map(&ta0);
@@ -778,11 +782,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (tile >= nunits) break;
         if (sslot == 1 && sphase == 0) TC_TRACE(2);
-        const UnitInfo ui = decode_unit(sh, tile, ntiles);
+        const UnitInfo ui = decode_unit<MS>(sh, tile, ntiles);
         const int kb_lo = ui.kb_lo, kb_hi = ui.kb_hi;
         int mb, nb;
         tile_coords(ui.tile, num_m, num_n, sh.group, sh.group_n, mb, nb);
-        bool dep = sh.tsteps > 1 && ui.split > 0;   // step s-1 of this row block must be done
+        bool dep = MS && sh.tsteps > 1 && ui.split > 0;   // step s-1 of this row block must be done
         const int m_row = mb * TM + rank * BM * MB;  // this CTA's A rows
         const int n_row = nb * BN + rank * (BN / 2);  // this CTA's B rows (N-half)
         const unsigned int* drow =
@@ -794,11 +798,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // source 1 (dy_t, no dependency) first, then source 0's blocks in the order the
           // previous step's epilogues publish them (block q of every tile, then q + 1, ...)
           int kx = kb;
-          if (sh.src1_first && sh.tsteps > 1) {
+          if (MS && sh.src1_first && sh.tsteps > 1) {
             // multi-step backward: source 1 (dy_t, no dependency) while the previous step's
             // row block finishes, then source 0 (dz_{t+1})
             kx = kb < sh.nkb1 ? ui.nkb0 + kb : kb - sh.nkb1;
-          } else if (sh.dep_perm && sh.tsteps > 1) {
+          } else if (MS && sh.dep_perm && sh.tsteps > 1) {
             if (kb < sh.nkb1) {
               kx = ui.nkb0 + kb;
             } else {
@@ -879,7 +883,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           sphase ^= 1;
         }
         if (tile >= nunits) break;
-        const UnitInfo ui = decode_unit(sh, tile, ntiles);
+        const UnitInfo ui = decode_unit<MS>(sh, tile, ntiles);
         const int kb_lo = ui.kb_lo, kb_hi = ui.kb_hi;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -939,7 +943,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int split = tile / ntiles;
       int mb, nb;
       tile_coords(tile - split * ntiles, num_m, num_n, sh.group, sh.group_n, mb, nb);
-      if (sh.tsteps > 1 && split > 0) {
+      if (MS && sh.tsteps > 1 && split > 0) {
         // the epilogue reads the previous step's cell state (c / dc) of this row block
         if (lane == 0) {
           if (sh.dep_fine) {
@@ -961,7 +965,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       bool done = false;
       constexpr int FB = FineBlocks<Epi>::v;
       if constexpr (MB == 1 && FB > 0) {
-        if (sh.tsteps > 1 && sh.dep_fine) {
+        if (MS && sh.tsteps > 1 && sh.dep_fine) {
           // publish each block as soon as it is stored: the next step's k-blocks of that block
           // (and the block's next-step epilogue) may start before the whole tile is done.
           // epi_q = 1: the tile is one block (forward: 256 gate columns = 64 units); epi_q =
@@ -992,7 +996,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
-      if (sh.tsteps > 1 && !sh.dep_fine) {
+      if (MS && sh.tsteps > 1 && !sh.dep_fine) {
         // this CTA's half of the tile is stored: publish it to the next step (cumulative
         // fence by one thread after the epilogue warps' barrier)
         asm volatile("bar.sync 1, 128;" ::: "memory");

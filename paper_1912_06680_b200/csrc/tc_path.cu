@@ -202,12 +202,13 @@ int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const 
 }
 
 // CTA-pair launch: 256x256 tiles, grid = 2 x clusters (one CTA per SM, persistent).
-template <bool A_MN, bool B_MN, class Epi, int MB = 1, int BN = 256>
+template <bool A_MN, bool B_MN, class Epi, int MB = 1, int BN = 256, bool MS = false>
 int launch2(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
             const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st) {
   constexpr int STAGES = MB == 1 ? 6 : 4;
   using L = tc::Smem2<A_MN, B_MN, STAGES, MB, BN>;
-  auto kern = tc::tc_gemm2_kernel<A_MN, B_MN, STAGES, MB, BN, Epi>;
+  auto kern = tc::tc_gemm2_kernel<A_MN, B_MN, STAGES, MB, BN, Epi, MS>;
+  if ((sh.tsteps > 1) != MS) return fail(PPO_E_SHAPE, "multi-step launch without the MS kernel");
   static bool configured = false;
   if (!configured) {
     PPO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
@@ -509,7 +510,9 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     fine_deps(sh, s, false);
     tc::EpiLstmFwd epi{P.xh + B * s.Kx + s.D, s.Kx, P.c, P.c + B * s.H, P.g, (int)B, (int)s.H,
                        B * s.Kx, B * s.H, B * s.G4};
-    if ((rc = launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st))) return rc;
+    if ((rc = launch2<false, false, tc::EpiLstmFwd, 1, 256, true>("lstm_fwd_step", mA, mA, mB, mB,
+                                                                  sh, epi, st)))
+      return rc;
   } else
   for (int t = 0; t < s.T; ++t) {
     if (x_ready && x_ready[t]) PPO_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready[t], 0));
@@ -583,7 +586,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     const int64_t t0 = s.T - 1;
     tc::EpiLstmBwd epi{P.g + t0 * B * s.G4, P.c + (t0 + 1) * B * s.H, P.c + t0 * B * s.H, P.dc,
                        (int)B, (int)s.H, 1, knob_int("PPO_EXP_BWD_EPI", 0), -B * s.H, -B * s.G4};
-    if ((rc = launch2<false, true>("lstm_bwd_step", a0, a1, b0, b1, sh, epi, st))) return rc;
+    if ((rc = launch2<false, true, tc::EpiLstmBwd, 1, 256, true>("lstm_bwd_step", a0, a1, b0, b1,
+                                                                 sh, epi, st)))
+      return rc;
   } else if (const int nsplit = bwd_split(s, B, pair, bwd_tiles)) {
     // small minibatch (fewer tiles per step than CTA pairs, e.g. the paper's B = 600: 48 tiles
     // on 74 pairs, each running the whole K = 4H + A and then an exposed row-per-thread
