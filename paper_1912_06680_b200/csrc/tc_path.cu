@@ -522,11 +522,17 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     tc::TileShape sh1 = sh;
     tc::EpiLstmFwd epi{P.xh + (t + 1) * B * s.Kx + s.D, s.Kx, P.c + t * B * s.H,
                        P.c + (t + 1) * B * s.H, P.g + t * B * s.G4, (int)B, (int)s.H, 0, 0, 0};
-    rc = pairmc ? launch2mc("lstm_fwd_step", mA, mBmc, sh, epi, st)
-         : pair2  ? launch2<false, false, tc::EpiLstmFwd, 2>("lstm_fwd_step", mA2, mA2, mB, mB, sh,
-                                                           epi, st)
-         : pair ? launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st)
-                : launch<256, false, false>("lstm_fwd_step", mA, mA, mB1, mB1, sh1, epi, st);
+#ifdef PPO_EXPERIMENTS
+    if (pairmc || pair2) {
+      rc = pairmc ? launch2mc("lstm_fwd_step", mA, mBmc, sh, epi, st)
+                  : launch2<false, false, tc::EpiLstmFwd, 2>("lstm_fwd_step", mA2, mA2, mB, mB,
+                                                            sh, epi, st);
+      if (rc) return rc;
+      continue;
+    }
+#endif
+    rc = pair ? launch2<false, false>("lstm_fwd_step", mA, mA, mB, mB, sh, epi, st)
+              : launch<256, false, false>("lstm_fwd_step", mA, mA, mB1, mB1, sh1, epi, st);
     if (rc) return rc;
   }
   // heads: y = [h_t | 1] W_o_aug^T over all T*B rows (XH slots 1..T, columns D..D+Ko).
@@ -656,15 +662,20 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
         // NVLink while the remaining tiles are still being multiplied
         tc::EpiStoreF32Dp epd{grad, s.Kx, (int)s.G4, (int)s.Kx, 0, c > 0 ? 1 : 0};
         epd.dp = *dp;
-        rc = pairmc ? launch2mca("wgrad_xh", wa, wb, mca_shape(sh), epd, st)
-             : pair ? launch2<true, true, tc::EpiStoreF32Dp, 2>("wgrad_xh", wa, wa, wb, wb, sh,
-                                                               epd, st)
-                    : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epd, st);
-      } else {
-        rc = pairmc ? launch2mca("wgrad_xh", wa, wb, mca_shape(sh), epi, st)
-             : pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi,
+#ifdef PPO_EXPERIMENTS
+        if (pairmc) rc = launch2mca("wgrad_xh", wa, wb, mca_shape(sh), epd, st);
+        else
+#endif
+        rc = pair ? launch2<true, true, tc::EpiStoreF32Dp, 2>("wgrad_xh", wa, wa, wb, wb, sh, epd,
                                                              st)
-                    : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st);
+                  : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epd, st);
+      } else {
+#ifdef PPO_EXPERIMENTS
+        if (pairmc) rc = launch2mca("wgrad_xh", wa, wb, mca_shape(sh), epi, st);
+        else
+#endif
+        rc = pair ? launch2<true, true, tc::EpiStoreF32, 2>("wgrad_xh", wa, wa, wb, wb, sh, epi, st)
+                  : launch<256, true, true>("wgrad_xh", wa, wa, wb, wb, sh, epi, st);
       }
       if (rc) return rc;
     }
