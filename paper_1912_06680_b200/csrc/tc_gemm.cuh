@@ -62,6 +62,10 @@ struct TileShape {
   int dep_kpg, dep_ng, dep_ld, epi_q;
   int dep_perm;
   int src1_first;   // multi-step: take source 1's k-blocks before source 0's
+  // multi-step, one 256-row tile: the A maps are 4-D row-interleaved views {k, i, q, z} of
+  // [rows][k] (row = 4 i + q), so TMEM lane 32 q + i of a CTA holds its row 4 i + q and the
+  // valid rows of a small batch spread over all four epilogue warps (Epi::ilv maps back)
+  int a_ilv;
 };
 
 // One work unit of a launch: a tile and (split-K) its k-range or (multi-step) its step.
@@ -303,6 +307,14 @@ __device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* map, uint32_
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* map, uint32_t bar_cluster,
+                                                 void* dst, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd,
                                                uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -385,6 +397,11 @@ __device__ __forceinline__ void tc_trace(int i, long long t0) {
   g_tc_trace[blockIdx.x][i] = (unsigned long long)(clock64() - t0);
 }
 #define TC_TRACE(i) tc_trace((i), trace_t0)
+#ifdef PPO_TRACE_UNIT   // trace the unit with this index (multi-step: step s of tile 0 = s)
+#define TC_SEL(u, first) ((u) == PPO_TRACE_UNIT)
+#else                   // trace the CTA's first unit
+#define TC_SEL(u, first) (first)
+#endif
 #define TC_TRACE_BEGIN()                                                 \
   const long long trace_t0 = clock64();                                  \
   if (threadIdx.x == 0) g_tc_trace[blockIdx.x][0] = globaltimer_ns()
@@ -392,6 +409,7 @@ __device__ __forceinline__ void tc_trace(int i, long long t0) {
 #define TC_TRACE(i) \
   do {              \
   } while (0)
+#define TC_SEL(u, first) false
 #define TC_TRACE_BEGIN() \
   do {                   \
   } while (0)
@@ -781,7 +799,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           sphase ^= 1;
         }
         if (tile >= nunits) break;
-        if (sslot == 1 && sphase == 0) TC_TRACE(2);
+        if (TC_SEL(tile, sslot == 1 && sphase == 0)) TC_TRACE(2);
         const UnitInfo ui = decode_unit<MS>(sh, tile, ntiles);
         const int kb_lo = ui.kb_lo, kb_hi = ui.kb_hi;
         int mb, nb;
@@ -822,6 +840,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             } else {
               wait_ready(sh.ready + (ui.split - 1) * num_m + mb, 2u * num_n, true);
+              if (TC_SEL(tile, false)) TC_TRACE(3);
               dep = false;
             }
           }
@@ -837,7 +856,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* a_dst = sA + stage * L::A_BYTES;
           uint8_t* b_dst = sB + stage * L::B_BYTES;
           if (!A_MN) {
-            tma_load_3d_pair(ta, fbar, a_dst, kk, m_row, za);
+            if (MS && sh.a_ilv) tma_load_4d_pair(ta, fbar, a_dst, kk, m_row >> 2, 0, za);
+            else tma_load_3d_pair(ta, fbar, a_dst, kk, m_row, za);
           } else {
 #pragma unroll
             for (int p = 0; p < 2 * MB; ++p)
@@ -891,7 +911,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          if (lane == 0 && kb == kb_lo && sslot == 1 && sphase == 0) TC_TRACE(4);
+          if (lane == 0 && kb == kb_lo && TC_SEL(tile, sslot == 1 && sphase == 0)) TC_TRACE(4);
           const uint64_t ad = a_desc0 + static_cast<uint64_t>(stage * (L::A_BYTES >> 4));
           const uint64_t bd = b_desc0 + static_cast<uint64_t>(stage * (L::B_BYTES >> 4));
           if (elect_one()) {
@@ -911,7 +931,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) umma_commit_pair(&tfull[acc]);
         __syncwarp();
-        if (lane == 0 && sslot == 1 && sphase == 0) TC_TRACE(5);
+        if (lane == 0 && TC_SEL(tile, sslot == 1 && sphase == 0)) TC_TRACE(5);
         if (++acc == NACC) {
           acc = 0;
           acc_phase ^= 1;
@@ -958,8 +978,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (threadIdx.x == 64 && sslot == 1 && sphase == 0) TC_TRACE(6);
-      if (lane == 0 && sslot == 1 && sphase == 0) TC_TRACE(16 + quarter);
+      if (threadIdx.x == 64 && TC_SEL(tile, sslot == 1 && sphase == 0)) TC_TRACE(6);
+      if (lane == 0 && TC_SEL(tile, sslot == 1 && sphase == 0)) TC_TRACE(16 + quarter);
       const uint32_t taddr =
           tbase + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * 256);
       bool done = false;
@@ -991,8 +1011,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           epi.template apply<BN>(mb * TM + rank * BM * MB + b * BM, nb * BN, row, taddr + b * 256,
                                  split);
       }
-      if (threadIdx.x == 64 && sslot == 1 && sphase == 0) TC_TRACE(7);
-      if (lane == 0 && sslot == 1 && sphase == 0) TC_TRACE(20 + quarter);
+      if (threadIdx.x == 64 && TC_SEL(tile, sslot == 1 && sphase == 0)) TC_TRACE(7);
+      if (lane == 0 && TC_SEL(tile, sslot == 1 && sphase == 0)) TC_TRACE(20 + quarter);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
@@ -1692,6 +1712,7 @@ struct EpiLstmFwd {
   __nv_bfloat16* gates;   // G[t]   [B][4H], interleaved like the accumulator columns
   int B, H;
   int64_t sx, sc, sg;     // multi-step launch: per-step element strides of XH, C and G
+  int ilv;                // TMEM lane r holds row 4 (r % 32) + r / 32 (TileShape::a_ilv)
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int step) const {
@@ -1700,7 +1721,7 @@ struct EpiLstmFwd {
     const float* const c_prev = this->c_prev + step * sc;
     float* const c_out = this->c_out + step * sc;
     __nv_bfloat16* const gates = this->gates + step * sg;
-    const int m = m_base + row;
+    const int m = m_base + (ilv ? (row & 31) * 4 + (row >> 5) : row);
     const bool ok = m < B;
     const int64_t G4 = 4 * static_cast<int64_t>(H);
 #pragma unroll 1
@@ -1793,6 +1814,7 @@ struct EpiLstmBwd {
   int exp;                // PPO_EXPERIMENTS builds only (timing A/B, wrong results):
                           // bit0 skip the saved-activation loads, bit1 skip the stores
   int64_t sc, sg;         // multi-step launch (step s = time T-1-s): per-step strides of C, G
+  int ilv;                // TMEM lane r holds row 4 (r % 32) + r / 32 (TileShape::a_ilv)
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int step) const {
@@ -1801,7 +1823,7 @@ struct EpiLstmBwd {
     const float* const c_prev = this->c_prev + step * sc;
     const bool first = this->first && step == 0;
     constexpr int CW = 8;  // units per chunk
-    const int m = m_base + row;
+    const int m = m_base + (ilv ? (row & 31) * 4 + (row >> 5) : row);
     const bool ok = m < B;
     const int64_t G4 = 4 * static_cast<int64_t>(H);
     const int nch = max(0, min(BN, H - n_base)) / CW;

@@ -172,6 +172,33 @@ int map_mnmajor(CUtensorMap* m, const void* base, uint64_t MN, uint64_t K, uint6
   return make_map(m, base, MN, K, 1, ld_elems * 2, 0, 64, tc::BK);
 }
 
+// Row-interleaved K-major view for single-tile multi-step launches (TileShape::a_ilv):
+// dims {K, rows / 4 (i), 4 (q), Z} with strides {4 ld, ld, zstride}: a {64, 32, 4, 1} box puts
+// row 4 i + q of a 128-row block at smem row 32 q + i.
+int map_kmajor_ilv(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint64_t ld_elems,
+                   uint64_t Z, uint64_t zstride_elems) {
+  auto fn = encode_fn();
+  if (!fn) return fail(PPO_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (rows % 4 != 0) return fail(PPO_E_SHAPE, "interleaved map needs rows % 4 == 0");
+  const cuuint64_t dims[4] = {K, rows / 4, 4, Z};
+  const cuuint64_t strides[3] = {4 * ld_elems * 2, ld_elems * 2,
+                                 (Z > 1 ? zstride_elems : rows * ld_elems) * 2};
+  const cuuint32_t box[4] = {64, 32, 4, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(PPO_E_CUDA, "cuTensorMapEncodeTiled (interleaved) failed (code " +
+                                std::to_string((int)r) + ")");
+  return PPO_OK;
+}
+// Single 256-row tile per step (B <= 256, B % 4 == 0): interleave the rows over the four TMEM
+// lane quarters so a small batch's epilogue runs on all four epilogue warps (the backward's:
+// tiny config 311 -> 287 us, profiles/r02_ilv_tiny.txt).  PPO_ILV=0 (experiment builds) keeps
+// the natural order.
+bool use_ilv(int64_t B) { return B <= 256 && B % 4 == 0 && knob_int("PPO_ILV", 1) != 0; }
+
 template <int BN, bool A_MN, bool B_MN, class Epi, int STAGES = 4>
 int launch(const char* tag, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
            const CUtensorMap& b1, const tc::TileShape& sh, const Epi& epi, cudaStream_t st,
@@ -510,8 +537,17 @@ int tc_forward(const Shape& s, int64_t B, const void* w, void* ws, float* out,
     fine_deps(sh, s, false);
     tc::EpiLstmFwd epi{P.xh + B * s.Kx + s.D, s.Kx, P.c, P.c + B * s.H, P.g, (int)B, (int)s.H,
                        B * s.Kx, B * s.H, B * s.G4};
-    if ((rc = launch2<false, false, tc::EpiLstmFwd, 1, 256, true>("lstm_fwd_step", mA, mA, mB, mB,
-                                                                  sh, epi, st)))
+    CUtensorMap mAi;
+    // (the interleaved rows measured 4% slower for the forward's light epilogue:
+    // profiles/r02_ilv_tiny.txt; PPO_ILV_FWD=1 in experiment builds)
+    if (use_ilv(B) && knob_int("PPO_ILV_FWD", 0) != 0) {
+      if ((rc = map_kmajor_ilv(&mAi, P.xh, s.Kx, B, s.Kx, s.T + 1, B * s.Kx))) return rc;
+      sh.a_ilv = 1;
+      epi.ilv = 1;
+    }
+    const CUtensorMap& mAx = sh.a_ilv ? mAi : mA;
+    if ((rc = launch2<false, false, tc::EpiLstmFwd, 1, 256, true>("lstm_fwd_step", mAx, mAx, mB,
+                                                                  mB, sh, epi, st)))
       return rc;
   } else
   for (int t = 0; t < s.T; ++t) {
@@ -592,8 +628,15 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     const int64_t t0 = s.T - 1;
     tc::EpiLstmBwd epi{P.g + t0 * B * s.G4, P.c + (t0 + 1) * B * s.H, P.c + t0 * B * s.H, P.dc,
                        (int)B, (int)s.H, 1, knob_int("PPO_EXP_BWD_EPI", 0), -B * s.H, -B * s.G4};
-    if ((rc = launch2<false, true, tc::EpiLstmBwd, 1, 256, true>("lstm_bwd_step", a0, a1, b0, b1,
-                                                                 sh, epi, st)))
+    CUtensorMap a0i, a1i;
+    if (use_ilv(B)) {
+      if ((rc = map_kmajor_ilv(&a0i, P.g, s.G4, B, s.G4, s.T, B * s.G4))) return rc;
+      if ((rc = map_kmajor_ilv(&a1i, dY, s.A_pass, B, s.A, s.T, B * s.A))) return rc;
+      sh.a_ilv = 1;
+      epi.ilv = 1;
+    }
+    if ((rc = launch2<false, true, tc::EpiLstmBwd, 1, 256, true>(
+             "lstm_bwd_step", sh.a_ilv ? a0i : a0, sh.a_ilv ? a1i : a1, b0, b1, sh, epi, st)))
       return rc;
   } else if (const int nsplit = bwd_split(s, B, pair, bwd_tiles)) {
     // small minibatch (fewer tiles per step than CTA pairs, e.g. the paper's B = 600: 48 tiles

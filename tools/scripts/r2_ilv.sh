@@ -1,0 +1,13 @@
+cd $GRAFT_REPO_ROOT
+PPO_EXPERIMENTS=1 python paper_1912_06680_b200/build.py > /dev/null 2>&1 || echo build failed
+timeout 900 python -m pytest tests/test_gpu_step.py tests/test_gpu_graph.py tests/test_gpu_aux.py -q -x -p no:cacheprovider > gpurun_out/r2_ilv_tests.txt 2>&1
+echo "tests rc=$?" >> gpurun_out/r2_ilv_tests.txt
+rm -f gpurun_out/r2_ilv_tiny.txt
+for r in 1 2; do for v in 0 1; do
+  echo "== PPO_ILV=$v" >> gpurun_out/r2_ilv_tiny.txt
+  PPO_ILV=$v timeout 300 python bench.py --config tiny --steps 200 --warmup 20 --no-cpu-baseline 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1]); k=d['kernels']
+print(round(d['value'],1), 'us/step graph; eager', round(d['eager']['ms_per_step']*1e3,1), 'fwd', round(k['lstm_fwd_step']['us_per_step'],1), 'bwd', round(k['lstm_bwd_step']['us_per_step'],1))" >> gpurun_out/r2_ilv_tiny.txt 2>&1
+done; done
+echo done
