@@ -23,7 +23,7 @@ def main(dst, reps):
                      "tools/profile_step.py --B 38400 (round-2 tree)", "kernels": {}}
     lines = []
     for p in reps:
-        tag = os.path.basename(p)[len("r2_tr_"):-len(".ncu-rep")]
+        tag = os.path.basename(p).split("_tr_", 1)[1][:-len(".ncu-rep")]
         txt = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv", "--metrics", ",".join(M)],
                              capture_output=True, text=True).stdout
         r = list(csv.reader(io.StringIO(txt)))
