@@ -1815,48 +1815,6 @@ struct EpiLstmBwd {
                           // bit0 skip the saved-activation loads, bit1 skip the stores
   int64_t sc, sg;         // multi-step launch (step s = time T-1-s): per-step strides of C, G
   int ilv;                // TMEM lane r holds row 4 (r % 32) + r / 32 (TileShape::a_ilv)
-  // one chunk of CW = 8 units of one row: the cell backward in place over the gate words
-  // (each 32-bit word holds units (2w, 2w+1); dz overwrites the gates), then the stores
-  __device__ __forceinline__ void chunk(BwdRaw& cur, const float (&dh)[8], __nv_bfloat16* gp,
-                                        float* dcp, bool no_st) const {
-    float* ct = reinterpret_cast<float*>(cur.ct);
-    float* cp = reinterpret_cast<float*>(cur.cp);
-    float* dcv = reinterpret_cast<float*>(cur.dc);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      float z[4][2];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t u = reinterpret_cast<const uint32_t*>(&cur.g[q])[w];
-        z[q][0] = __uint_as_float(u << 16);
-        z[q][1] = __uint_as_float(u & 0xFFFF0000u);
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int e = 2 * w + h;
-        float a, b, c, d, dn;
-        cell_bwd(dh[e], dcv[e], z[0][h], z[1][h], z[2][h], z[3][h], ct[e], cp[e], a, b, c, d,
-                 dn, true);
-        z[0][h] = a;
-        z[1][h] = b;
-        z[2][h] = c;
-        z[3][h] = d;
-        dcv[e] = dn;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const __nv_bfloat162 pk = __floats2bfloat162_rn(z[q][0], z[q][1]);
-        reinterpret_cast<uint32_t*>(&cur.g[q])[w] = *reinterpret_cast<const uint32_t*>(&pk);
-      }
-    }
-    if (!no_st) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(gp + q * 64) = cur.g[q];
-      st_f32x8(dcp, cur.dc);
-    } else if (cur.dc[0].x == 1234.5f) {   // keep the math live
-      *dcp = cur.dc[1].y + __uint_as_float(cur.g[0].x);
-    }
-  }
   template <int BN>
   __device__ __forceinline__ void apply(int m_base, int n_base, int row, uint32_t taddr,
                                         int step) const {
@@ -1865,56 +1823,25 @@ struct EpiLstmBwd {
     const float* const c_prev = this->c_prev + step * sc;
     const bool first = this->first && step == 0;
     constexpr int CW = 8;  // units per chunk
+    const int m = m_base + (ilv ? (row & 31) * 4 + (row >> 5) : row);
+    const bool ok = m < B;
     const int64_t G4 = 4 * static_cast<int64_t>(H);
     const int nch = max(0, min(BN, H - n_base)) / CW;
+    const __nv_bfloat16* grow = gz + static_cast<int64_t>(m) * G4;
+    const int64_t crow = static_cast<int64_t>(m) * H + n_base;
     auto goff = [&](int cc) {
       const int j0 = n_base + cc * CW;
       return (j0 >> 6) * 256 + (j0 & 63);
     };
+    // the saved activations of chunk cc + 1 are loaded while chunk cc computes (two chunks
+    // ahead measured 2% slower in the step at B = 38,400: profiles/r02_ab_bwd_ahead.txt)
+    BwdRaw cur, nxt;
     const float* dcin = first ? nullptr : dc;
 #ifdef PPO_EXPERIMENTS
     const bool no_ld = exp & 1, no_st = exp & 2;
 #else
     constexpr bool no_ld = false, no_st = false;
 #endif
-    if (ilv) {
-      // interleaved rows: lane i of quarter q holds row 4 i + q.  When at most 8 lanes of
-      // the warp hold rows of the batch (a small batch), every lane takes a quarter of one
-      // valid row's chunks: row lane & 7, chunks cc = lane >> 3 (mod 4), its dh shuffled
-      // from the owning lane -- four short dependent-load chains instead of one long one
-      const int lane = row & 31, quarter = row >> 5;
-      const int V = min(32, max(0, (B - m_base - quarter + 3) / 4));   // lanes with rows < B
-      if (V <= 8) {
-        const int src = lane & 7, part = lane >> 3;
-        const int ms = m_base + 4 * src + quarter;
-        const bool has = src < V;
-        const __nv_bfloat16* grow = gz + static_cast<int64_t>(ms) * G4;
-        const int64_t crow = static_cast<int64_t>(ms) * H + n_base;
-#pragma unroll 1
-        for (int cc = 0; cc < BN / CW; ++cc) {
-          float dh[8];
-          tmem_ld8(taddr + cc * CW, dh);
-          if (cc >= nch) continue;
-          float d[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) d[j] = __shfl_sync(0xffffffffu, dh[j], src);
-          if (!has || (cc & 3) != part) continue;
-          BwdRaw cur;
-          const int64_t o = crow + cc * CW;
-          if (no_ld) cur = BwdRaw{};
-          else bwd_load(cur, grow + goff(cc), c_t + o, c_prev + o, dcin ? dcin + o : nullptr);
-          chunk(cur, d, gz + static_cast<int64_t>(ms) * G4 + goff(cc), dc + o, no_st);
-        }
-        return;
-      }
-    }
-    const int m = m_base + (ilv ? (row & 31) * 4 + (row >> 5) : row);
-    const bool ok = m < B;
-    const __nv_bfloat16* grow = gz + static_cast<int64_t>(m) * G4;
-    const int64_t crow = static_cast<int64_t>(m) * H + n_base;
-    // the saved activations of chunk cc + 1 are loaded while chunk cc computes (two chunks
-    // ahead measured 2% slower in the step at B = 38,400: profiles/r02_ab_bwd_ahead.txt)
-    BwdRaw cur, nxt;
     if (no_ld) cur = BwdRaw{};
     auto load_chunk = [&](BwdRaw& r, int cc) {
       const int64_t o = crow + cc * CW;
@@ -1927,8 +1854,47 @@ struct EpiLstmBwd {
       tmem_ld8(taddr + cc * CW, dh);
       if (cc >= nch) continue;
       if (ok && cc + 1 < nch && !no_ld) load_chunk(nxt, cc + 1);
-      if (ok)
-        chunk(cur, dh, gz + static_cast<int64_t>(m) * G4 + goff(cc), dc + crow + cc * CW, no_st);
+      if (ok) {
+        // in place: each 32-bit gate word holds units (2w, 2w+1); dz overwrites the gates
+        float* ct = reinterpret_cast<float*>(cur.ct);
+        float* cp = reinterpret_cast<float*>(cur.cp);
+        float* dcv = reinterpret_cast<float*>(cur.dc);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          float z[4][2];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t u = reinterpret_cast<const uint32_t*>(&cur.g[q])[w];
+            z[q][0] = __uint_as_float(u << 16);
+            z[q][1] = __uint_as_float(u & 0xFFFF0000u);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = 2 * w + h;
+            float a, b, c, d, dn;
+            cell_bwd(dh[e], dcv[e], z[0][h], z[1][h], z[2][h], z[3][h], ct[e], cp[e], a, b, c,
+                     d, dn, true);
+            z[0][h] = a;
+            z[1][h] = b;
+            z[2][h] = c;
+            z[3][h] = d;
+            dcv[e] = dn;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162 pk = __floats2bfloat162_rn(z[q][0], z[q][1]);
+            reinterpret_cast<uint32_t*>(&cur.g[q])[w] = *reinterpret_cast<const uint32_t*>(&pk);
+          }
+        }
+        if (!no_st) {
+          __nv_bfloat16* gp = gz + static_cast<int64_t>(m) * G4 + goff(cc);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(gp + q * 64) = cur.g[q];
+          st_f32x8(dc + crow + cc * CW, cur.dc);
+        } else if (cur.dc[0].x == 1234.5f) {   // keep the math live
+          dc[crow] = cur.dc[1].y + __uint_as_float(cur.g[0].x);
+        }
+      }
       if (!no_ld) cur = nxt;
     }
   }
