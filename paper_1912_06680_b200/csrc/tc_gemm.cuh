@@ -1848,11 +1848,11 @@ struct EpiLstmBwd {
       bwd_load(r, grow + goff(cc), c_t + o, c_prev + o, dcin ? dcin + o : nullptr);
     };
     if (ok && !no_ld && nch > 0) load_chunk(cur, 0);
+    // chunks past H (a last N tile wider than the hidden state) are never loaded from TMEM
 #pragma unroll 1
-    for (int cc = 0; cc < BN / CW; ++cc) {
+    for (int cc = 0; cc < nch; ++cc) {
       float dh[8];
       tmem_ld8(taddr + cc * CW, dh);
-      if (cc >= nch) continue;
       if (ok && cc + 1 < nch && !no_ld) load_chunk(nxt, cc + 1);
       if (ok) {
         // in place: each 32-bit gate word holds units (2w, 2w+1); dz overwrites the gates
