@@ -1849,8 +1849,11 @@ struct EpiLstmBwd {
     };
     if (ok && !no_ld && nch > 0) load_chunk(cur, 0);
     // chunks past H (a last N tile wider than the hidden state) are never loaded from TMEM
+    // (a break under the constant trip count: bounding the loop by nch itself cost the
+    // backward step GEMM 3% at B = 38,400, profiles/r02_nch_ab.txt)
 #pragma unroll 1
-    for (int cc = 0; cc < nch; ++cc) {
+    for (int cc = 0; cc < BN / CW; ++cc) {
+      if (cc >= nch) break;
       float dh[8];
       tmem_ld8(taddr + cc * CW, dh);
       if (ok && cc + 1 < nch && !no_ld) load_chunk(nxt, cc + 1);
