@@ -1803,7 +1803,11 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-struct EpiLstmBwd {
+// TAIL: stop at the last chunk inside H (no TMEM loads of a last N tile's columns past H) --
+// only in the multi-step instantiation: any change to this loop in the per-step kernel moved
+// the backward step GEMM at B = 38,400 by 2-3% (profiles/r02_nch_ab.txt, r02_nch2_ab.txt)
+template <bool TAIL>
+struct EpiLstmBwdT {
   static constexpr int kFineBlocks = 4;   // a tile = 256 units of dh: four unit blocks
   __nv_bfloat16* gz;      // G[t]: gates in, dz out  [B][4H]
   const float* c_t;       // C[t+1]
@@ -1848,14 +1852,16 @@ struct EpiLstmBwd {
       bwd_load(r, grow + goff(cc), c_t + o, c_prev + o, dcin ? dcin + o : nullptr);
     };
     if (ok && !no_ld && nch > 0) load_chunk(cur, 0);
-    // chunks past H (a last N tile wider than the hidden state) are never loaded from TMEM
-    // (a break under the constant trip count: bounding the loop by nch itself cost the
-    // backward step GEMM 3% at B = 38,400, profiles/r02_nch_ab.txt)
 #pragma unroll 1
     for (int cc = 0; cc < BN / CW; ++cc) {
-      if (cc >= nch) break;
+      if constexpr (TAIL) {
+        if (cc >= nch) break;
+      }
       float dh[8];
       tmem_ld8(taddr + cc * CW, dh);
+      if constexpr (!TAIL) {
+        if (cc >= nch) continue;
+      }
       if (ok && cc + 1 < nch && !no_ld) load_chunk(nxt, cc + 1);
       if (ok) {
         // in place: each 32-bit gate word holds units (2w, 2w+1); dz overwrites the gates
@@ -1902,6 +1908,8 @@ struct EpiLstmBwd {
     }
   }
 };
+using EpiLstmBwd = EpiLstmBwdT<false>;
+using EpiLstmBwdTail = EpiLstmBwdT<true>;
 
 }  // namespace tc
 }  // namespace ppo

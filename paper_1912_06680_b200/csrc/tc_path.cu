@@ -626,8 +626,9 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
     // the dY k-blocks (no dependency) first: they load and multiply while step s-1 finishes
     if (!sh.dep_fine) sh.src1_first = knob_int("PPO_BWD_SRC1_FIRST", 1);
     const int64_t t0 = s.T - 1;
-    tc::EpiLstmBwd epi{P.g + t0 * B * s.G4, P.c + (t0 + 1) * B * s.H, P.c + t0 * B * s.H, P.dc,
-                       (int)B, (int)s.H, 1, knob_int("PPO_EXP_BWD_EPI", 0), -B * s.H, -B * s.G4};
+    tc::EpiLstmBwdTail epi{P.g + t0 * B * s.G4, P.c + (t0 + 1) * B * s.H, P.c + t0 * B * s.H,
+                           P.dc, (int)B, (int)s.H, 1, knob_int("PPO_EXP_BWD_EPI", 0), -B * s.H,
+                           -B * s.G4};
     CUtensorMap a0i, a1i;
     if (use_ilv(B)) {
       if ((rc = map_kmajor_ilv(&a0i, P.g, s.G4, B, s.G4, s.T, B * s.G4))) return rc;
@@ -635,7 +636,7 @@ int tc_backward(const Shape& s, int64_t B, const void* w, void* ws, const void* 
       sh.a_ilv = 1;
       epi.ilv = 1;
     }
-    if ((rc = launch2<false, true, tc::EpiLstmBwd, 1, 256, true>(
+    if ((rc = launch2<false, true, tc::EpiLstmBwdTail, 1, 256, true>(
              "lstm_bwd_step", sh.a_ilv ? a0i : a0, sh.a_ilv ? a1i : a1, b0, b1, sh, epi, st)))
       return rc;
   } else if (const int nsplit = bwd_split(s, B, pair, bwd_tiles)) {
